@@ -1,0 +1,99 @@
+/*
+ * b200k.h — C ABI of the B200 execution backend for staircase tapes.
+ *
+ * The reference executes loop nests on the CPU through its engine protocol:
+ * staircase.interp.machine.run() calls  eng.run_tape(program, code, regs,
+ * tally, ctx)  (reference pkg/src/staircase/interp/machine.py:105-112), whose
+ * implementations are the pure and compiled evaluators
+ * (interp/_evalpy.py:81-331, interp/_evalcy.pyx:74-344).  The Python engine
+ * module paper_2307_16080_b200.engine keeps that protocol and lowers every
+ * loop-nest region of the tape onto the entry points below.  Each entry point
+ * replaces the part of run_tape named in its comment.
+ *
+ * Conventions: all data pointers are DEVICE pointers (the host side owns the
+ * allocations); `stream` is a cudaStream_t passed as void*; every call only
+ * enqueues work on `stream` (no host synchronisation) and returns 0 on
+ * success or a negative b200_status on a launch/configuration error.
+ * Runtime faults of the executed program (OutOfBounds, InvalidBound) are
+ * reported through the device-side b200_vm_error record.
+ */
+#ifndef B200K_H
+#define B200K_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum b200_status {
+  B200_OK = 0,
+  B200_EINVAL = -1,     /* bad shape / argument */
+  B200_ELAUNCH = -2,    /* CUDA launch or attribute error */
+  B200_EUNSUPPORTED = -3
+};
+
+/* dtype codes shared by all entry points (reference interp/buffer.py:16) */
+enum b200_dtype { B200_F32 = 0, B200_F64 = 1, B200_I32 = 2, B200_I64 = 3 };
+
+/* A memref argument: dense row-major storage (reference interp/buffer.py:34-131). */
+typedef struct {
+  void *ptr;            /* device pointer */
+  int32_t dtype;        /* b200_dtype */
+  int32_t rank;
+  int64_t shape[8];
+  int64_t strides[8];   /* in elements */
+} b200_buffer;
+
+/* First fault of a checked VM run (reference interp/_evalpy.py:74-78,149-153). */
+typedef struct {
+  int32_t code;         /* 0 none, 1 OutOfBounds, 2 InvalidBound (loop), 3 InvalidBound (parallel) */
+  int32_t slot;         /* buffer slot of the faulting access */
+  int64_t index;        /* offending index value */
+  int64_t extent;       /* extent of the faulting dimension */
+  int64_t loc;          /* location id of the faulting op */
+} b200_vm_error;
+
+/*
+ * Tape VM: executes a region of a tape, one band point per GPU thread.
+ * Replaces run_tape's interpretation of loops, parallel loops, launches,
+ * branches, loads/stores and arithmetic (interp/_evalpy.py:81-232,
+ * _run_parallel :244-273, _run_launch :303-331) for the region.
+ *
+ *   prog/n_words     encoded per-thread program (paper_2307_16080_b200/vmcode.py)
+ *   init_regs/vals   registers preloaded before the program runs
+ *   n_regs           register file size (<= 256)
+ *   bufs/n_bufs      DEVICE array of b200_buffer
+ *   band_*           nd band dimensions: register, lower bound, step, trip count
+ *   count            1: accumulate tally counters into `tally` (25 x uint64, device)
+ *   err              DEVICE b200_vm_error, must be zeroed by the caller
+ */
+int b200_vm_run(const int32_t *prog, int32_t n_words, const int32_t *init_regs,
+                const int64_t *init_vals, int32_t n_init, int32_t n_regs,
+                const b200_buffer *bufs, int32_t n_bufs, int32_t nd,
+                const int32_t *band_regs, const int64_t *band_lb,
+                const int64_t *band_step, const int64_t *band_trip, int32_t count,
+                unsigned long long *tally, b200_vm_error *err, void *stream);
+
+/*
+ * Exact fp32 contraction C[m,n] = C[m,n] (+) sum_k A[m,k]*B[k,n], every
+ * product and sum individually rounded (__fmul_rn/__fadd_rn), k ascending:
+ * bit-identical to the reference's matmul nests (reference
+ * tests/kernels.py:24-38; interp/_evalpy.py:115-127 rounding).
+ * Replaces run_tape on a recognised matmul/Linear nest.  Strides in elements,
+ * any sign.  init: 0 = accumulate into C, 1 = start from `init_value`.
+ * bias (nullable): out[m,n] = out + bias[n*bias_stride] after the chain
+ * (the Linear lowering's bias nest).
+ */
+int b200_gemm_f32_exact(const float *A, int64_t sAm, int64_t sAk,
+                        const float *B, int64_t sBk, int64_t sBn,
+                        float *C, int64_t sCm, int64_t sCn,
+                        int64_t M, int64_t N, int64_t K,
+                        int32_t init, float init_value,
+                        const float *bias, int64_t bias_stride, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* B200K_H */

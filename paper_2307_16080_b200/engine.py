@@ -1,0 +1,305 @@
+"""The B200 engine: a drop-in for staircase's CPU tape evaluators.
+
+Plug-in point (reference pkg/src/staircase/interp/machine.py:26-34,105-112):
+
+    eng = engine or _engine
+    ctx = eng.ExecContext(mode, workers)
+    rets = eng.run_tape(program, tape.code, regs, tally, ctx)
+
+This module provides ``ExecContext`` and ``run_tape`` with the same
+signatures, ownership and error behaviour as ``_evalpy``/``_evalcy``
+(interp/_evalpy.py:61-232): memref Buffers are mutated in place, ``tally``
+is incremented exactly as the reference increments it, and faults raise
+``staircase.errors`` types with the reference's messages.
+
+Execution model: the top level of the entry tape is walked on the host —
+that is only scalar bookkeeping (constants, index arithmetic, branches on
+scalars, calls, returns) and single-element loads/stores.  Every loop nest,
+``scf.parallel`` and ``gpu.launch_func`` found there is a *region*: it is
+lifted (lift.py), analysed (analysis.py), matched against the kernel
+templates (templates.py) and executed on the GPU, either by a specialised
+kernel or by the device tape VM (csrc/vm.cu).  Nothing in a region runs on
+the CPU; there is no fallback.
+
+Install globally (the tuner calls run() without engine=, search.py:170,190):
+
+    import paper_2307_16080_b200 as b2
+    b2.install()          # sets staircase.interp.machine._engine
+"""
+from __future__ import annotations
+
+import math
+
+from . import analysis, templates, vmcode
+from .host import errors as _errors
+from .lift import (ALLOC, BINF, BINI, BOOKKEEPING, CALL, CAST, CMPF, CMPI, CONST,
+                   DEALLOC, IF_FALSE, JUMP, LAUNCH, LOAD, LOOP_INIT_A, LOOP_INIT_S,
+                   PARALLEL, RETURN, RETURN_GPU, STORE, Launch, Unsupported,
+                   evaluate, lift_region)
+from .runtime import DeviceBackend
+
+ENGINE_NAME = "b200"
+
+# kernel choice statistics of the last run (tests and bench inspect these)
+last_plan = []
+
+
+class ExecContext:
+    """Per-run execution knobs (same slots as interp/_evalpy.py:61-71)."""
+
+    __slots__ = ("mode", "workers", "recorder", "gpu_ids", "depth")
+
+    def __init__(self, mode="sequential", workers=1, recorder=None):
+        self.mode = mode
+        self.workers = workers
+        self.recorder = recorder
+        self.gpu_ids = None
+        self.depth = 0
+
+
+def _to_f32(x):
+    import struct
+
+    try:
+        return struct.unpack("<f", struct.pack("<f", x))[0]
+    except OverflowError:
+        return math.copysign(math.inf, x)
+
+
+def _wrap(v, dtype):
+    span, half = (1 << 32, 1 << 31) if dtype == "i32" else (1 << 64, 1 << 63)
+    return (int(v) + half) % span - half
+
+
+def _where(loc):
+    return f" at {loc.file}:{loc.line}" if loc else ""
+
+
+class _Run:
+    """One run() call: host walk of the entry tape + device regions."""
+
+    def __init__(self, program, ctx, backend=None):
+        self.program = program
+        self.ctx = ctx
+        self.be = backend if backend is not None else DeviceBackend()
+        self.plan = []
+
+    # -- host walk (mirrors interp/_evalpy.py:81-232 for top-level scalars) --
+    def exec_tape(self, code, regs, tally):
+        E = _errors()
+        n = len(code)
+        pc = 0
+        while pc < n:
+            ins = code[pc]
+            op = ins[0]
+            if op in (LOOP_INIT_S, LOOP_INIT_A):
+                end = code[pc + 1][3]
+                self.region(code, pc, end, regs, tally)
+                pc = end
+                continue
+            if op in (PARALLEL, LAUNCH):
+                self.region(code, pc, pc + 1, regs, tally)
+                pc += 1
+                continue
+            tally[op] += 1
+            if op == CONST:
+                regs[ins[1]] = ins[2]
+            elif op == BINF:
+                a, b, f = regs[ins[3]], regs[ins[4]], ins[2]
+                if f == 0:
+                    r = a + b
+                elif f == 1:
+                    r = a - b
+                elif f == 2:
+                    r = a * b
+                else:
+                    r = _fdiv(a, b)
+                regs[ins[1]] = _to_f32(r) if ins[5] else r
+            elif op == BINI:
+                a, b, f = regs[ins[3]], regs[ins[4]], ins[2]
+                r = a + b if f == 0 else (a - b if f == 1 else a * b)
+                regs[ins[1]] = _wrap(r, ins[5])
+            elif op == CMPF:
+                regs[ins[1]] = _cmpf(ins[2], regs[ins[3]], regs[ins[4]])
+            elif op == CMPI:
+                regs[ins[1]] = _cmpi(ins[2], regs[ins[3]], regs[ins[4]])
+            elif op == CAST:
+                v = regs[ins[2]]
+                regs[ins[1]] = _wrap(v, "i32") if ins[3] == "i32" else v
+            elif op == LOAD:
+                buf = regs[ins[2]]
+                off = self._offset(buf, [regs[r] for r in ins[3]], ins[4], E)
+                regs[ins[1]] = self.be.read(buf, off)
+            elif op == STORE:
+                buf = regs[ins[2]]
+                off = self._offset(buf, [regs[r] for r in ins[3]], ins[4], E)
+                v = regs[ins[1]]
+                if buf.dtype[0] == "i":
+                    v = _wrap(v, buf.dtype)
+                self.be.write(buf, off, v)
+            elif op == ALLOC:
+                from staircase.interp.buffer import Buffer
+
+                regs[ins[1]] = Buffer(ins[2], ins[3])
+            elif op == DEALLOC:
+                pass
+            elif op == IF_FALSE:
+                if not regs[ins[1]]:
+                    pc = ins[2]
+                    continue
+            elif op == JUMP:
+                pc = ins[1]
+                continue
+            elif op == CALL:
+                callee = self.program.funcs[ins[2]]
+                sub = [None] * callee.n_regs
+                for dst, src in zip(callee.arg_regs, ins[3]):
+                    sub[dst] = regs[src]
+                rets = self.exec_tape(callee.code, sub, tally)
+                for dst, v in zip(ins[1], rets or ()):
+                    regs[dst] = v
+            elif op in (RETURN, RETURN_GPU):
+                return tuple(regs[r] for r in ins[1])
+            else:
+                raise E.UnknownOperation(f"opcode {op} at the top level of a tape")
+            pc += 1
+        return None
+
+    @staticmethod
+    def _offset(buf, idx, loc, E):
+        off = 0
+        for i, extent, stride in zip(idx, buf.shape, buf.strides):
+            if i < 0 or i >= extent:
+                raise E.OutOfBounds(
+                    f"index {i} out of bounds for extent {extent} of {buf!r}{_where(loc)}")
+            off += i * stride
+        return off
+
+    # -- regions ---------------------------------------------------------------
+    def region(self, code, start, end, regs, tally):
+        E = _errors()
+        try:
+            r = lift_region(self.program, code, start, end, regs)
+            evaluate(r)
+        except Unsupported as exc:
+            raise E.ModeUnsupported(f"b200 engine: {exc}") from None
+        if r.has_launch and self.ctx.mode != "gpu_emulated":
+            loc = _first_launch_loc(r.tree)
+            raise E.ModeUnsupported(
+                f"gpu.launch_func needs gpu_emulated mode, not {self.ctx.mode!r}{_where(loc)}")
+        try:
+            accesses = analysis.collect_accesses(r)
+        except Unsupported as exc:
+            raise E.ModeUnsupported(f"b200 engine: {exc}") from None
+        links, remainder = analysis.chain_of(r)
+        safe = analysis.statically_in_bounds(r, accesses) and not analysis.invalid_steps(r)
+        band = analysis.choose_band(r, links, accesses) if safe else []
+        st = analysis.static_tally(r.tree)
+        written = {a.slot for a in accesses if a.write}
+        for slot in written:
+            self.be.mark_dirty(r.buffers[slot])
+
+        if safe and st is not None:
+            g = templates.match_gemm(r, links, remainder, accesses)
+            if g is not None:
+                self.be.gemm(g)
+                _add(tally, st)
+                self.plan.append(("gemm_f32_exact", g.M, g.N, g.K))
+                return
+
+        count = st is None
+        try:
+            prog = vmcode.encode(r, links, remainder, band, count, checked=not safe)
+        except Unsupported as exc:
+            raise E.ModeUnsupported(f"b200 engine: {exc}") from None
+        dev_tally, fault = self.be.vm(r, prog, checked=not safe)
+        if fault is not None:
+            self.be.flush()
+            self.raise_fault(r, prog, fault)
+        if count:
+            chain, _ = analysis.chain_tally(links)
+            _add(tally, chain)
+            _add(tally, dev_tally)
+        else:
+            _add(tally, st)
+        self.plan.append(("vm", len(band), "checked" if not safe else "unchecked",
+                          "count" if count else "static"))
+
+    def raise_fault(self, r, prog, fault):
+        code, slot, index, extent, loc = fault
+        E = _errors()
+        if code == 1:
+            loc = prog.locs[loc] if loc >= 0 else None
+            raise E.OutOfBounds(
+                f"index {index} out of bounds for extent {extent} of "
+                f"{r.buffers[slot]!r}{_where(loc)}")
+        if code == 2:
+            raise E.InvalidBound("loop step must be positive at runtime")
+        raise E.InvalidBound("scf.parallel steps must be positive at runtime")
+
+
+def _first_launch_loc(nodes):
+    from .analysis import _iter_nodes
+
+    for n in _iter_nodes(nodes):
+        if isinstance(n, Launch):
+            return n.loc
+    return None
+
+
+def _add(tally, extra):
+    for i, v in enumerate(extra):
+        tally[i] += v
+
+
+def _fdiv(a, b):
+    if b == 0.0:
+        if a != a or a == 0.0:
+            return math.nan
+        return math.copysign(math.inf, a) * math.copysign(1.0, b)
+    return a / b
+
+
+def _cmpf(p, a, b):
+    if p == 0:
+        return a == b
+    if p == 1:
+        return a == a and b == b and a != b
+    return (a < b, a <= b, a > b, a >= b)[p - 2]
+
+
+def _cmpi(p, a, b):
+    return (a == b, a != b, a < b, a <= b, a > b, a >= b)[p]
+
+
+def run_tape(program, code, regs, tally, ctx, backend=None):
+    """Engine-protocol entry point (machine.py:112)."""
+    global last_plan
+    run = _Run(program, ctx, backend)
+    try:
+        rets = run.exec_tape(code, regs, tally)
+    except BaseException:
+        try:
+            run.be.flush()
+        finally:
+            last_plan = run.plan
+        raise
+    run.be.flush()
+    last_plan = run.plan
+    return rets
+
+
+def install():
+    """Make this engine the default of staircase.interp.machine.run()."""
+    from .host import ensure_staircase
+
+    ensure_staircase()
+    import sys
+
+    from staircase.interp import machine
+
+    machine._engine = sys.modules[__name__]
+    return machine
+
+
+__all__ = ["ExecContext", "run_tape", "install", "ENGINE_NAME"]

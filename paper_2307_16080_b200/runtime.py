@@ -1,0 +1,225 @@
+"""Device runtime: the libb200k.so binding and per-run buffer staging.
+
+PyTorch is used only as the device allocator / stream provider.  All
+compute goes through the C ABI in include/b200k.h, loaded with ctypes from
+the in-tree shared object built by paper_2307_16080_b200/build.py.  There is
+no CPU fallback: if the library or a GPU is missing, every entry point
+raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libb200k.so")
+
+_lib = None
+
+
+class BackendUnavailable(RuntimeError):
+    """The CUDA backend cannot run here (no library or no B200)."""
+
+
+class B200Buffer(ctypes.Structure):
+    _fields_ = [("ptr", ctypes.c_void_p), ("dtype", ctypes.c_int32),
+                ("rank", ctypes.c_int32), ("shape", ctypes.c_int64 * 8),
+                ("strides", ctypes.c_int64 * 8)]
+
+
+class B200VmError(ctypes.Structure):
+    _fields_ = [("code", ctypes.c_int32), ("slot", ctypes.c_int32),
+                ("index", ctypes.c_int64), ("extent", ctypes.c_int64),
+                ("loc", ctypes.c_int64)]
+
+
+_P = ctypes.c_void_p
+_I32 = ctypes.c_int32
+_I64 = ctypes.c_int64
+_F32 = ctypes.c_float
+
+SIGNATURES = {
+    "b200_vm_run": [_P, _I32, _P, _P, _I32, _I32, _P, _I32, _I32, _P, _P, _P, _P,
+                    _I32, _P, _P, _P],
+    "b200_gemm_f32_exact": [_P, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64, _I64,
+                            _I64, _I64, _I32, _F32, _P, _I64, _P],
+}
+
+
+def load_library(path=LIB_PATH):
+    """Load libb200k.so and declare every exported C-ABI symbol."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise BackendUnavailable(
+            f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; "
+            f"g.build()'` (nvcc, sm_100a)")
+    lib = ctypes.CDLL(path)
+    for name, argtypes in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = argtypes
+        fn.restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def torch_mod():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise BackendUnavailable("no CUDA device: the B200 engine has no CPU fallback")
+    return torch
+
+
+def check(rc, what):
+    if rc != 0:
+        raise RuntimeError(f"{what} failed with status {rc}")
+
+
+_TORCH_DT = {"f32": "float32", "f64": "float64", "i32": "int32", "i64": "int64"}
+DT_CODE = {"f32": 0, "f64": 1, "i32": 2, "i64": 3}
+
+
+class Staging:
+    """Device copies of the host Buffers touched by one run.
+
+    Memref arguments are mutated in place in the reference (SPEC: memref
+    reference semantics), so every buffer a region writes is copied back
+    into the caller's ``array.array`` when the run ends (or faults).
+    """
+
+    def __init__(self):
+        self.torch = torch_mod()
+        self.lib = load_library()
+        self.dev = {}        # id(Buffer) -> (Buffer, tensor)
+        self.dirty = set()
+        self.stream = self.torch.cuda.current_stream()
+
+    @property
+    def stream_ptr(self):
+        return ctypes.c_void_p(self.stream.cuda_stream)
+
+    def tensor(self, buf):
+        ent = self.dev.get(id(buf))
+        if ent is None:
+            torch = self.torch
+            dt = getattr(torch, _TORCH_DT[buf.dtype])
+            host = torch.frombuffer(buf.data, dtype=dt)
+            t = host.to("cuda", non_blocking=False)
+            ent = (buf, t)
+            self.dev[id(buf)] = ent
+        return ent[1]
+
+    def mark_dirty(self, buf):
+        self.dirty.add(id(buf))
+
+    def flush(self):
+        torch = self.torch
+        for key in list(self.dirty):
+            buf, t = self.dev[key]
+            dt = getattr(torch, _TORCH_DT[buf.dtype])
+            host = torch.frombuffer(buf.data, dtype=dt)
+            host.copy_(t)
+        self.dirty.clear()
+        torch.cuda.current_stream().synchronize()
+
+    def buffer_table(self, buffers):
+        """A device array of b200_buffer for the given host Buffers."""
+        table = (B200Buffer * len(buffers))()
+        for k, b in enumerate(buffers):
+            t = self.tensor(b)
+            table[k].ptr = t.data_ptr()
+            table[k].dtype = DT_CODE[b.dtype]
+            table[k].rank = len(b.shape)
+            for d, (s, st) in enumerate(zip(b.shape, b.strides)):
+                table[k].shape[d] = s
+                table[k].strides[d] = st
+        return self.upload_bytes(bytes(table))
+
+    def upload_bytes(self, blob):
+        torch = self.torch
+        host = torch.frombuffer(bytearray(blob), dtype=torch.uint8) if blob else \
+            torch.zeros(1, dtype=torch.uint8)
+        return host.to("cuda", non_blocking=False)
+
+    def upload_i32(self, values):
+        return self.upload_bytes(np.asarray(values, dtype=np.int32).tobytes())
+
+    def upload_i64(self, values):
+        return self.upload_bytes(np.asarray(values, dtype=np.int64).tobytes())
+
+
+class DeviceBackend:
+    """Executes region plans on the B200 through libb200k.so."""
+
+    def __init__(self):
+        self.stage = Staging()
+        self._keep = None
+
+    def read(self, buf, off):
+        v = self.stage.tensor(buf)[off].item()
+        return float(v) if buf.dtype[0] == "f" else int(v)
+
+    def write(self, buf, off, v):
+        self.stage.tensor(buf)[off] = v
+        self.stage.mark_dirty(buf)
+
+    def mark_dirty(self, buf):
+        self.stage.mark_dirty(buf)
+
+    def flush(self):
+        self.stage.flush()
+
+    def gemm(self, g):
+        s = self.stage
+        tA, tB, tC = s.tensor(g.A), s.tensor(g.B), s.tensor(g.C)
+
+        def fp(t, off):
+            return ctypes.c_void_p(t.data_ptr() + 4 * off)
+
+        rc = s.lib.b200_gemm_f32_exact(
+            fp(tA, g.offA), g.sA[0], g.sA[1], fp(tB, g.offB), g.sB[0], g.sB[1],
+            fp(tC, g.offC), g.sC[0], g.sC[1], g.M, g.N, g.K, 0, 0.0, None, 0,
+            s.stream_ptr)
+        check(rc, "b200_gemm_f32_exact")
+
+    def vm(self, r, prog, checked):
+        """Run a VM program; returns (device tally | None, fault | None)."""
+        s = self.stage
+        torch = s.torch
+        table = s.buffer_table(r.buffers)
+        words = s.upload_i32(prog.words)
+        iregs = s.upload_i32(prog.init_regs or [0])
+        ivals = s.upload_i64(prog.init_vals or [0])
+        nd = len(prog.band)
+        breg = s.upload_i32([b[0] for b in prog.band] or [0])
+        blb = s.upload_i64([b[1] for b in prog.band] or [0])
+        bst = s.upload_i64([b[2] for b in prog.band] or [0])
+        btr = s.upload_i64([b[3] for b in prog.band] or [0])
+        dtally = torch.zeros(25, dtype=torch.int64, device="cuda")
+        err = torch.zeros(ctypes.sizeof(B200VmError), dtype=torch.uint8, device="cuda")
+        P = ctypes.c_void_p
+        rc = s.lib.b200_vm_run(
+            P(words.data_ptr()), len(prog.words), P(iregs.data_ptr()),
+            P(ivals.data_ptr()), len(prog.init_regs), prog.n_regs,
+            P(table.data_ptr()), len(r.buffers), nd, P(breg.data_ptr()),
+            P(blb.data_ptr()), P(bst.data_ptr()), P(btr.data_ptr()),
+            1 if prog.count else 0, P(dtally.data_ptr()), P(err.data_ptr()),
+            s.stream_ptr)
+        check(rc, "b200_vm_run")
+        # the uploads must outlive the (asynchronous) kernel
+        self._keep = (table, words, iregs, ivals, breg, blb, bst, btr, dtally, err)
+        fault = None
+        if checked:
+            e = B200VmError.from_buffer_copy(bytes(err.cpu().numpy()))
+            if e.code:
+                fault = (e.code, e.slot, e.index, e.extent, e.loc)
+        dev_tally = [int(x) for x in dtally.cpu().tolist()] if prog.count else None
+        return dev_tally, fault
+
+
+__all__ = ["load_library", "Staging", "DeviceBackend", "BackendUnavailable", "B200Buffer",
+           "B200VmError", "LIB_PATH", "SIGNATURES"]

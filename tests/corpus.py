@@ -229,3 +229,36 @@ def ewise_gpu(A: MemRef[(4, 4), F32], B: MemRef[(4, 4), F32],
 ALL = [oob_kernel, matmul_affine, matmul_96, matmul_par, linear32, conv2d_desk, conv_small,
        conv_rows, conv_f32, saxpy, saxpy_f32, strided, ewise_ops, int_ops,
        cond_body, triangle, prefix, scalar_args, ewise_gpu]
+
+
+# -- larger shapes for the GPU parity tests (edges not multiples of the tiles)
+
+
+@staged(range_ctor="affine_for")
+def matmul_odd(A: MemRef[(130, 150), F32], B: MemRef[(150, 70), F32],
+               C: MemRef[(130, 70), F32]):
+    for i in range(130):
+        for j in range(150):
+            for k in range(70):
+                C[i, k] = C[i, k] + A[i, j] * B[j, k]
+
+
+@staged
+def matmul_t(A: MemRef[(96, 160), F32], Bt: MemRef[(200, 160), F32],
+             C: MemRef[(96, 200), F32]):
+    for i, n in parallel((0, 0), (96, 200)):
+        for k in range(160):
+            C[i, n] = C[i, n] + A[i, k] * Bt[n, k]
+
+
+@staged
+def conv_mid(inp: MemRef[(4, 16, 34, 34), F32], ker: MemRef[(8, 16, 3, 3), F32],
+             out: MemRef[(4, 8, 32, 32), F32]):
+    for n, co, ho, wo in parallel((0, 0, 0, 0), (4, 8, 32, 32)):
+        for ci in range(0, 16):
+            for ki in range(0, 3):
+                for kj in range(0, 3):
+                    out[n, co, ho, wo] += inp[n, ci, ho + ki, wo + kj] * ker[co, ci, ki, kj]
+
+
+BIG = [matmul_odd, matmul_t, conv_mid]
