@@ -64,7 +64,8 @@ typedef struct {
  *   init_regs/vals   registers preloaded before the program runs
  *   n_regs           register file size (<= 256)
  *   bufs/n_bufs      DEVICE array of b200_buffer
- *   band_*           nd band dimensions: register, lower bound, step, trip count
+ *   band_*           HOST arrays, nd band dimensions: register, lower bound, step,
+ *                    trip count (copied into the kernel parameters)
  *   count            1: accumulate tally counters into `tally` (25 x uint64, device)
  *   err              DEVICE b200_vm_error, must be zeroed by the caller
  */

@@ -195,18 +195,18 @@ class DeviceBackend:
         iregs = s.upload_i32(prog.init_regs or [0])
         ivals = s.upload_i64(prog.init_vals or [0])
         nd = len(prog.band)
-        breg = s.upload_i32([b[0] for b in prog.band] or [0])
-        blb = s.upload_i64([b[1] for b in prog.band] or [0])
-        bst = s.upload_i64([b[2] for b in prog.band] or [0])
-        btr = s.upload_i64([b[3] for b in prog.band] or [0])
+        # band arrays are read on the host (they become kernel parameters)
+        breg = (ctypes.c_int32 * max(1, nd))(*[b[0] for b in prog.band])
+        blb = (ctypes.c_int64 * max(1, nd))(*[b[1] for b in prog.band])
+        bst = (ctypes.c_int64 * max(1, nd))(*[b[2] for b in prog.band])
+        btr = (ctypes.c_int64 * max(1, nd))(*[b[3] for b in prog.band])
         dtally = torch.zeros(25, dtype=torch.int64, device="cuda")
         err = torch.zeros(ctypes.sizeof(B200VmError), dtype=torch.uint8, device="cuda")
         P = ctypes.c_void_p
         rc = s.lib.b200_vm_run(
             P(words.data_ptr()), len(prog.words), P(iregs.data_ptr()),
             P(ivals.data_ptr()), len(prog.init_regs), prog.n_regs,
-            P(table.data_ptr()), len(r.buffers), nd, P(breg.data_ptr()),
-            P(blb.data_ptr()), P(bst.data_ptr()), P(btr.data_ptr()),
+            P(table.data_ptr()), len(r.buffers), nd, breg, blb, bst, btr,
             1 if prog.count else 0, P(dtally.data_ptr()), P(err.data_ptr()),
             s.stream_ptr)
         check(rc, "b200_vm_run")
