@@ -1,29 +1,35 @@
 """Benchmark: GFLOP/s of the B200 backend on BASELINE.json's matmul config.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--precision exact]
+                    [--precision bf16|tf32|exact]
 
 Workload (BASELINE.json configs[1]): ``linalg.matmul`` 4096x4096x4096, the
 reference's matmul nest (reference tests/kernels.py:24-38) at full size:
-C[i,k] += A[i,j] * B[j,k] in f32.  A step is one pass of the hot path over
-one batch: one C += A.B contraction.  Data: U(-1,1) f32 from
-torch.Generator().manual_seed(arg index).
+C[i,k] += A[i,j] * B[j,k] on f32 Buffers.  A step is one pass of the hot
+path over one batch: one C += A.B contraction, including the operand
+packing the tensor-core path needs (f32 -> bf16/tf32, B transposed to
+K-major).  Data: U(-1,1) f32 from torch.Generator().manual_seed(arg index)
+(SURVEY.md §8d).
 
-* ``value``  — device-resident: the C-ABI kernel on HBM tensors, timed with
-  CUDA events on the launch stream, inputs (3 x 64 MiB) larger than L2.
+* ``value``  — device-resident: the C-ABI sequence (pack, pack, tcgen05
+  GEMM) on HBM tensors, timed with CUDA events on the launch stream; inputs
+  (3 x 64 MiB f32) are larger than the 126 MB L2.
+* ``roofline`` — the dominant kernel (b200_gemm_tc) alone: algorithmic
+  2*M*N*K flops per launch / its average CUDA-event duration inside the
+  timed region, against MEASURED_PEAKS.json bf16 (tf32: half of it).
 * ``e2e``    — through the reference-facing plugin: staircase's own
   ``machine.run(module, "mm", [A, B, C], engine=b200)`` with host Buffers;
   the H2D of A, B, C and the D2H of C are inside the timed region.
 * ``cpu_baseline`` — the reference executor itself (baseline/_ref, compiled
   _evalcy engine) on a 1x4096x256 slice of the same nest (same loop
-  structure and reduction length), 1 core; its rate extrapolates to the
-  full matmul.
+  structure and reduction length), 1 core; its rate extrapolates.
 * ``--impl reference`` — rank 0 times that reference CPU path per step.
 
 Multi-GPU (torchrun): every rank runs its own 4096^3 matmul (weak scaling,
 no data-path collective); time is the max over ranks.
 """
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -116,7 +122,6 @@ class Clocks:
         except OSError:
             self.proc = None
             return
-        # wait for the sampler's first line so the timed region is covered
         t0 = time.time()
         while time.time() - t0 < 5.0:
             if os.path.exists(self.path) and os.path.getsize(self.path) > 0:
@@ -148,7 +153,7 @@ class Clocks:
                 "samples": len(sm)}
 
 
-def dist_setup(n_gpus):
+def dist_setup():
     import torch
 
     rank = int(os.environ.get("RANK", "0"))
@@ -186,7 +191,15 @@ def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
         return json.load(open(path)), "measured"
-    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def load_traffic(precision):
+    """dram bytes per GEMM launch from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(path):
+        return json.load(open(path)).get(f"gemm_{precision}")
+    return None
 
 
 def run_reference(args, rank, world):
@@ -202,12 +215,12 @@ def run_reference(args, rank, world):
     wall = time.perf_counter() - t0
     value = statistics.median(rates)
     line = {
-        "impl": "reference", "metric": "GFLOP/s (matmul 4096^3 f32)", "value": value,
+        "impl": "reference", "metric": "GFLOP/s (matmul 4096^3)", "value": value,
         "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "matmul 4096x4096x4096 f32 (reference executor on a "
-                               "1x4096x256 slice, rate extrapolates)"},
+        "config": {"workload": "linalg.matmul 4096x4096x4096 (reference CPU executor on a "
+                               "1x4096x256 slice of the nest, rate extrapolates)"},
         "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": 1, "kind": "reference",
                          "sample": "1x4096x256 slice of the 4096^3 matmul nest, "
                                    "staircase _evalcy, median of 3 runs per step"},
@@ -218,8 +231,6 @@ def run_reference(args, rank, world):
 
 
 def run_ours(args, rank, world, local):
-    import ctypes
-
     import torch
 
     import paper_2307_16080_b200 as b2
@@ -235,15 +246,38 @@ def run_ours(args, rank, world, local):
     A, B, C = tens
     stream = torch.cuda.current_stream()
     sp = ctypes.c_void_p(stream.cuda_stream)
+    prec = args.precision
+    tc = runtime.tc_supported(prec, K)
+    kind = 0 if prec == "bf16" else 1
+    elt = torch.bfloat16 if prec == "bf16" else torch.float32
+    Ap = torch.empty(M, K, dtype=elt, device=dev)
+    Bp = torch.empty(N, K, dtype=elt, device=dev)
     P = ctypes.c_void_p
+    gemm_ms = []
 
-    def step():
-        rc = lib.b200_gemm_f32_exact(P(A.data_ptr()), K, 1, P(B.data_ptr()), N, 1,
-                                     P(C.data_ptr()), N, 1, M, N, K, 0, 0.0, None, 0, sp)
+    def step(timed):
+        if tc:
+            assert lib.b200_pack_operand(kind, P(A.data_ptr()), K, 1, P(Ap.data_ptr()),
+                                         M, K, sp) == 0
+            assert lib.b200_pack_operand(kind, P(B.data_ptr()), 1, N, P(Bp.data_ptr()),
+                                         N, K, sp) == 0
+        if timed:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        if tc:
+            rc = lib.b200_gemm_tc(kind, P(Ap.data_ptr()), P(Bp.data_ptr()), P(C.data_ptr()),
+                                  N, 1, M, N, K, 0, 0.0, None, 0, 0, sp)
+        else:
+            rc = lib.b200_gemm_f32_exact(P(A.data_ptr()), K, 1, P(B.data_ptr()), N, 1,
+                                         P(C.data_ptr()), N, 1, M, N, K, 0, 0.0, None, 0, sp)
         assert rc == 0
+        if timed:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record(stream)
+            gemm_ms.append((e0, e1))
 
     for _ in range(args.warmup):
-        step()
+        step(False)
     torch.cuda.synchronize()
     barrier(world)
     clocks = Clocks(local)
@@ -252,19 +286,23 @@ def run_ours(args, rank, world, local):
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for _ in range(args.steps):
-        step()
+        step(True)
     ev1.record(stream)
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.steps
+    kernel_ms = statistics.mean(a.elapsed_time(b) for a, b in gemm_ms)
     clk = clocks.stop()
     barrier(world)
     ms = max_over_ranks(ms, world)
+    kernel_ms = max_over_ranks(kernel_ms, world)
     value = world * FLOP / (ms * 1e-3) / 1e9
+    launches_per_step = 3 if tc else 1
 
     # e2e through the plugin: host Buffers, H2D + D2H inside the timed region
+    b2.configure(precision=prec)
     e2e_steps = max(1, min(args.steps, 3))
     host = host_inputs([(M, K), (K, N), (M, N)])
-    machine.run(mm.module, "mm", host, engine=b2.engine)   # warm (lift cache, alloc)
+    machine.run(mm.module, "mm", host, engine=b2.engine)   # warm
     torch.cuda.synchronize()
     barrier(world)
     t0 = time.perf_counter()
@@ -278,21 +316,32 @@ def run_ours(args, rank, world, local):
     if rank != 0:
         return
     peaks, src = load_peaks()
-    fp32_peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-    achieved_tf = FLOP / (ms * 1e-3) / 1e12
+    if tc:
+        peak = peaks["bf16_tflops"] * (1.0 if prec == "bf16" else 0.5)
+        bound = "tensor"
+        peak_source = (f"{src} bf16 dense (MEASURED_PEAKS.json)" if prec == "bf16" else
+                       f"{src} bf16 x 0.5 (tf32 = half rate, derived)")
+    else:
+        peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        bound = "fp32-simt"
+        peak_source = "derived: 148 SM x 128 FP32 lanes x 2 x sm_max_mhz"
+    achieved = FLOP / (kernel_ms * 1e-3) / 1e12
     cpu_rate, cpu_t = reference_slice_rate()
+    dtype = {"bf16": "bf16 (fp32 accumulate)", "tf32": "tf32 (fp32 accumulate)",
+             "exact": "f32"}[prec]
     line = {
-        "metric": "GFLOP/s (matmul 4096^3 f32)", "value": value, "unit": "GFLOP/s",
+        "metric": "GFLOP/s (matmul 4096^3)", "value": value, "unit": "GFLOP/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype,
         "data": "synthetic",
-        "config": {"workload": "linalg.matmul 4096x4096x4096 (C += A.B), exact fp32 path",
-                   "precision": "exact (per-op IEEE f32, bit-identical to reference)",
-                   "l2": "inputs 192 MiB > 126 MB L2", "parallelism": f"replica x{world}"},
-        "roofline": {"bound": "fp32-simt", "achieved": achieved_tf, "peak": fp32_peak,
-                     "unit": "TFLOP/s", "frac": achieved_tf / fp32_peak,
-                     "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x sm_max_mhz",
-                     "traffic": None},
+        "config": {"workload": "linalg.matmul 4096x4096x4096, C += A.B on f32 buffers "
+                               "(step = operand pack + contraction)",
+                   "precision": prec, "l2": "inputs 192 MiB f32 > 126 MB L2 (no flush)",
+                   "parallelism": f"replica x{world}"},
+        "roofline": {"bound": bound, "kernel": "b200_gemm_tc" if tc else "b200_gemm_f32_exact",
+                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "peak_source": peak_source,
+                     "kernel_ms": kernel_ms, "traffic": load_traffic(prec)},
         "e2e": {"value": FLOP / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s",
                 "ms_per_step": e2e_ms, "h2d_bytes_per_step": 3 * M * N * 4,
                 "d2h_bytes_per_step": M * N * 4, "plan": [list(p) for p in plan]},
@@ -300,7 +349,7 @@ def run_ours(args, rank, world, local):
                          "kind": "reference",
                          "sample": f"1x4096x256 slice of the matmul nest via staircase _evalcy "
                                    f"({cpu_t:.2f} s); host cores {len(os.sched_getaffinity(0))}"},
-        "clocks": clk, "gpu_launches": args.steps,
+        "clocks": clk, "gpu_launches": launches_per_step * args.steps,
     }
     print(json.dumps(line), flush=True)
 
@@ -308,11 +357,12 @@ def run_ours(args, rank, world, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "tf32", "exact"])
     args = ap.parse_args()
-    rank, world, local = dist_setup(args.gpus)
+    rank, world, local = dist_setup()
     if args.impl == "reference":
         run_reference(args, rank, world)
     else:

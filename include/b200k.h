@@ -93,6 +93,31 @@ int b200_gemm_f32_exact(const float *A, int64_t sAm, int64_t sAk,
                         int32_t init, float init_value,
                         const float *bias, int64_t bias_stride, void *stream);
 
+/*
+ * Operand packing for the tensor-core contraction: dst[r][c] (dense
+ * row-major, i.e. K-major for the GEMM) = round(src[r*s_row + c*s_col]),
+ * kind 0 -> bf16 (RN), kind 1 -> tf32 held in f32 (RN, low 13 bits zero).
+ * Used to stage A (rows = M) and B^T (rows = N) of a recognised matmul nest,
+ * whatever the nest's index maps (reference tests/kernels.py:24-38).
+ */
+int b200_pack_operand(int32_t kind, const float *src, int64_t s_row, int64_t s_col,
+                      void *dst, int64_t rows, int64_t cols, void *stream);
+
+/*
+ * Tensor-core contraction (tcgen05.mma, TMEM accumulators, TMA operand
+ * loads): C[m*sCm + n*sCn] = (init ? init_value : C[...]) + sum_k A[m,k]*Bt[n,k]
+ * (+ bias[n*bias_stride]), fp32 accumulate.  kind 0: bf16 operands
+ * (kind::f16), kind 1: tf32 operands (kind::tf32).  A is M x K and Bt is
+ * N x K, dense K-major (b200_pack_operand output).  Replaces run_tape on a
+ * recognised matmul / Linear contraction when the engine precision is bf16
+ * or tf32 (accumulation-order tolerance).  max_ctas <= 0 uses
+ * one persistent CTA per SM.
+ */
+int b200_gemm_tc(int32_t kind, const void *A, const void *Bt, float *C, int64_t sCm,
+                 int64_t sCn, int64_t M, int64_t N, int64_t K, int32_t init,
+                 float init_value, const float *bias, int64_t bias_stride,
+                 int32_t max_ctas, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -14,6 +14,6 @@ from .host import ensure_staircase
 ensure_staircase()
 
 from . import engine  # noqa: E402
-from .engine import ENGINE_NAME, ExecContext, install, run_tape  # noqa: E402
+from .engine import ENGINE_NAME, ExecContext, configure, install, run_tape  # noqa: E402
 
-__all__ = ["engine", "install", "run_tape", "ExecContext", "ENGINE_NAME"]
+__all__ = ["engine", "install", "configure", "run_tape", "ExecContext", "ENGINE_NAME"]

@@ -29,6 +29,7 @@ Install globally (the tuner calls run() without engine=, search.py:170,190):
 from __future__ import annotations
 
 import math
+import os
 
 from . import analysis, templates, vmcode
 from .host import errors as _errors
@@ -39,6 +40,22 @@ from .lift import (ALLOC, BINF, BINI, BOOKKEEPING, CALL, CAST, CMPF, CMPI, CONST
 from .runtime import DeviceBackend
 
 ENGINE_NAME = "b200"
+
+# Contraction precision.  "exact" (default): fp32 per-op rounding on the FP32
+# pipes, bit-identical to the reference.  "tf32" / "bf16": operands rounded to
+# tf32 / bf16 and contracted on the tcgen05 tensor cores with fp32
+# accumulation (tolerance: DESIGN.md, tests/test_gpu_tc.py).
+PRECISION = os.environ.get("B200_PRECISION", "exact")
+
+
+def configure(precision=None):
+    """Select the contraction precision for subsequent runs."""
+    global PRECISION
+    if precision is not None:
+        if precision not in ("exact", "tf32", "bf16"):
+            raise ValueError(f"unknown precision {precision!r}")
+        PRECISION = precision
+    return {"precision": PRECISION}
 
 # kernel choice statistics of the last run (tests and bench inspect these)
 last_plan = []
@@ -202,9 +219,9 @@ class _Run:
         if safe and st is not None:
             g = templates.match_gemm(r, links, remainder, accesses)
             if g is not None:
-                self.be.gemm(g)
+                kernels = self.be.gemm(g, PRECISION) or ["gemm_f32_exact"]
                 _add(tally, st)
-                self.plan.append(("gemm_f32_exact", g.M, g.N, g.K))
+                self.plan.append((kernels[-1], g.M, g.N, g.K))
                 return
 
         count = st is None

@@ -45,6 +45,9 @@ SIGNATURES = {
                     _I32, _P, _P, _P],
     "b200_gemm_f32_exact": [_P, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64, _I64,
                             _I64, _I64, _I32, _F32, _P, _I64, _P],
+    "b200_pack_operand": [_I32, _P, _I64, _I64, _P, _I64, _I64, _P],
+    "b200_gemm_tc": [_I32, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I32, _F32, _P,
+                     _I64, _I32, _P],
 }
 
 
@@ -152,6 +155,56 @@ class Staging:
         return self.upload_bytes(np.asarray(values, dtype=np.int64).tobytes())
 
 
+PRECISIONS = ("exact", "tf32", "bf16")
+_WORKSPACE = {}
+
+
+def workspace(slot, dtype, rows, cols):
+    """Cached device scratch for packed tensor-core operands."""
+    torch = torch_mod()
+    key = (slot, dtype, rows, cols, torch.cuda.current_device())
+    t = _WORKSPACE.get(key)
+    if t is None:
+        t = torch.empty(rows, cols, dtype=getattr(torch, dtype), device="cuda")
+        _WORKSPACE[key] = t
+    return t
+
+
+def tc_supported(precision, K):
+    """tcgen05 path needs 16-byte TMA rows of packed K (bf16: K%8, tf32: K%4)."""
+    return precision in ("bf16", "tf32") and K > 0 and \
+        (K * (2 if precision == "bf16" else 4)) % 16 == 0
+
+
+def launch_gemm(lib, precision, a_ptr, sA, b_ptr, sB, c_ptr, sC, M, N, K, stream,
+                init=0, init_value=0.0, bias_ptr=None, bias_stride=0, max_ctas=0):
+    """Enqueue C (+)= A.B with the kernel chosen by ``precision``.
+
+    Returns the list of kernel names launched (for the launch count).
+    exact -> b200_gemm_f32_exact (bit-identical to the reference);
+    bf16/tf32 -> b200_pack_operand x2 + b200_gemm_tc (tcgen05).
+    """
+    P = ctypes.c_void_p
+    if not tc_supported(precision, K):
+        check(lib.b200_gemm_f32_exact(P(a_ptr), sA[0], sA[1], P(b_ptr), sB[0], sB[1],
+                                      P(c_ptr), sC[0], sC[1], M, N, K, init, init_value,
+                                      P(bias_ptr) if bias_ptr else None, bias_stride,
+                                      stream), "b200_gemm_f32_exact")
+        return ["gemm_f32_exact"]
+    kind = 0 if precision == "bf16" else 1
+    dt = "bfloat16" if kind == 0 else "float32"
+    Ap = workspace(0, dt, M, K)
+    Bp = workspace(1, dt, N, K)
+    check(lib.b200_pack_operand(kind, P(a_ptr), sA[0], sA[1], P(Ap.data_ptr()), M, K,
+                                stream), "b200_pack_operand")
+    check(lib.b200_pack_operand(kind, P(b_ptr), sB[1], sB[0], P(Bp.data_ptr()), N, K,
+                                stream), "b200_pack_operand")
+    check(lib.b200_gemm_tc(kind, P(Ap.data_ptr()), P(Bp.data_ptr()), P(c_ptr), sC[0], sC[1],
+                           M, N, K, init, init_value, P(bias_ptr) if bias_ptr else None,
+                           bias_stride, max_ctas, stream), "b200_gemm_tc")
+    return ["pack_operand", "pack_operand", f"gemm_tc_{precision}"]
+
+
 class DeviceBackend:
     """Executes region plans on the B200 through libb200k.so."""
 
@@ -173,18 +226,12 @@ class DeviceBackend:
     def flush(self):
         self.stage.flush()
 
-    def gemm(self, g):
+    def gemm(self, g, precision="exact"):
         s = self.stage
         tA, tB, tC = s.tensor(g.A), s.tensor(g.B), s.tensor(g.C)
-
-        def fp(t, off):
-            return ctypes.c_void_p(t.data_ptr() + 4 * off)
-
-        rc = s.lib.b200_gemm_f32_exact(
-            fp(tA, g.offA), g.sA[0], g.sA[1], fp(tB, g.offB), g.sB[0], g.sB[1],
-            fp(tC, g.offC), g.sC[0], g.sC[1], g.M, g.N, g.K, 0, 0.0, None, 0,
-            s.stream_ptr)
-        check(rc, "b200_gemm_f32_exact")
+        return launch_gemm(s.lib, precision, tA.data_ptr() + 4 * g.offA, g.sA,
+                           tB.data_ptr() + 4 * g.offB, g.sB, tC.data_ptr() + 4 * g.offC,
+                           g.sC, g.M, g.N, g.K, s.stream_ptr)
 
     def vm(self, r, prog, checked):
         """Run a VM program; returns (device tally | None, fault | None)."""

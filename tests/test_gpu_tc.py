@@ -1,0 +1,104 @@
+"""Tensor-core contraction (b200_gemm_tc, tcgen05) on a real B200.
+
+Inputs are pre-rounded to the kernel's operand type (bf16 / tf32) so every
+product is exact in fp32 and the only deviation from the reference's
+sequential per-op-rounded f32 chain is accumulation rounding.  Tolerance
+(stated here and in DESIGN.md):
+
+    |got - want| <= 2 * K * 2^-24 * sum_k |a_mk * b_kn|  + 1e-30
+
+per output, where ``want`` is the exact (float64) sum of the same rounded
+products plus the initial C.  This is the standard γ_K bound for any fp32
+summation order (the reference's own chain obeys it too).
+"""
+import ctypes
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _round(t, kind):
+    import torch
+
+    if kind == 0:
+        return t.to(torch.bfloat16).to(torch.float32)
+    u = t.view(torch.int32)
+    u = (u + 0xFFF + ((u >> 13) & 1)) & ~0x1FFF
+    return u.view(torch.float32)
+
+
+def _run(kind, M, N, K, init=0, bias=False, trans_b=False, seed=0, max_ctas=0):
+    import torch
+
+    from paper_2307_16080_b200 import runtime
+
+    lib = runtime.load_library()
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    A = _round(torch.rand(M, K, device="cuda", generator=g) * 2 - 1, kind)
+    if trans_b:
+        Bsrc = _round(torch.rand(N, K, device="cuda", generator=g) * 2 - 1, kind)
+        sBk, sBn = 1, K
+        B = Bsrc.t()
+    else:
+        Bsrc = _round(torch.rand(K, N, device="cuda", generator=g) * 2 - 1, kind)
+        sBk, sBn = N, 1
+        B = Bsrc
+    C = torch.rand(M, N, device="cuda", generator=g) * 2 - 1
+    bvec = torch.rand(N, device="cuda", generator=g) if bias else None
+    C0 = C.clone()
+    elt = torch.bfloat16 if kind == 0 else torch.float32
+    Ap = torch.empty(M, K, dtype=elt, device="cuda")
+    Bp = torch.empty(N, K, dtype=elt, device="cuda")
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    P = ctypes.c_void_p
+    assert lib.b200_pack_operand(kind, P(A.data_ptr()), K, 1, P(Ap.data_ptr()), M, K, s) == 0
+    assert lib.b200_pack_operand(kind, P(Bsrc.data_ptr()), sBn, sBk, P(Bp.data_ptr()),
+                                 N, K, s) == 0
+    rc = lib.b200_gemm_tc(kind, P(Ap.data_ptr()), P(Bp.data_ptr()), P(C.data_ptr()), N, 1,
+                          M, N, K, init, 0.5, P(bvec.data_ptr()) if bias else None, 1,
+                          max_ctas, s)
+    assert rc == 0
+    torch.cuda.synchronize()
+    Ad, Bd = A.double(), B.double()
+    want = Ad @ Bd + (0.5 if init else C0.double())
+    if bias:
+        want = want + bvec.double()[None, :]
+    mag = Ad.abs() @ Bd.abs()
+    err = (C.double() - want).abs()
+    bound = 2 * K * 2.0 ** -24 * mag + 4 * 2.0 ** -24 * want.abs() + 1e-30
+    return err, bound, Ap, Bp, A, Bsrc
+
+
+@pytest.mark.parametrize("kind", [0, 1], ids=["bf16", "tf32"])
+@pytest.mark.parametrize("shape", [(128, 256, 64), (256, 512, 256), (300, 520, 200),
+                                   (1024, 1024, 1024)])
+def test_gemm_tc_accuracy(kind, shape):
+    M, N, K = shape
+    if kind == 0 and K % 8:
+        pytest.skip("bf16 TMA rows need K % 8 == 0")
+    err, bound, *_ = _run(kind, M, N, K)
+    bad = (err > bound).sum().item()
+    assert bad == 0, f"{bad} outputs outside the bound; max err {err.max().item()}"
+
+
+@pytest.mark.parametrize("kind", [0, 1], ids=["bf16", "tf32"])
+def test_gemm_tc_epilogue_modes(kind):
+    err, bound, *_ = _run(kind, 256, 256, 128, init=1, bias=True, trans_b=True)
+    assert (err > bound).sum().item() == 0
+
+
+def test_pack_rounding_exact():
+    import torch
+
+    err, bound, Ap, Bp, A, Bsrc = _run(0, 128, 256, 64)
+    assert torch.equal(Ap.float(), A)
+    err, bound, Ap, Bp, A, Bsrc = _run(1, 128, 256, 64)
+    assert torch.equal(Ap, A)
+    assert torch.equal(Bp, Bsrc.t().contiguous())
+
+
+def test_gemm_tc_few_ctas_persistent_loop():
+    # fewer CTAs than tiles: every CTA loops over several tiles (TMEM ping-pong)
+    err, bound, *_ = _run(0, 512, 1024, 256, max_ctas=3)
+    assert (err > bound).sum().item() == 0

@@ -63,7 +63,8 @@ class SimBackend:
             np.frombuffer(buf.data, dtype=_NP[buf.dtype])[:] = a
         self.dirty.clear()
 
-    def gemm(self, g):
+    def gemm(self, g, precision="exact"):
+        assert precision == "exact", "the simulator models the exact path only"
         self.launches.append("gemm")
         A, B, C = self.arr(g.A), self.arr(g.B), self.arr(g.C)
         m = np.arange(g.M)[:, None]
