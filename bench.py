@@ -266,7 +266,7 @@ def run_ours(args, rank, world, local):
             e0.record(stream)
         if tc:
             rc = lib.b200_gemm_tc(kind, P(Ap.data_ptr()), P(Bp.data_ptr()), P(C.data_ptr()),
-                                  N, 1, M, N, K, 0, 0.0, None, 0, 0, sp)
+                                  N, 1, M, N, K, 0, 0.0, None, 0, 0, args.variant, sp)
         else:
             rc = lib.b200_gemm_f32_exact(P(A.data_ptr()), K, 1, P(B.data_ptr()), N, 1,
                                          P(C.data_ptr()), N, 1, M, N, K, 0, 0.0, None, 0, sp)
@@ -361,6 +361,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="bf16", choices=["bf16", "tf32", "exact"])
+    ap.add_argument("--variant", type=int, default=0,
+                    help="tcgen05 schedule: 0 auto, 1 single-CTA, 2 CTA pair")
     args = ap.parse_args()
     rank, world, local = dist_setup()
     if args.impl == "reference":

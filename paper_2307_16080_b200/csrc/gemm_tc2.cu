@@ -1,0 +1,186 @@
+// 2-SM tensor-core contraction: a CTA pair (cluster of 2) computes a 256x256
+// output tile with tcgen05.mma.cta_group::2 (UMMA M=256, N=256).
+//
+// Each CTA stages its own half of the operands — 128 rows of A and 128 rows of
+// B^T per 128-byte K slice — so per SM the shared-memory traffic per MMA is
+// half of the single-CTA 128x256 kernel's (TMA writes 64 B/clk + UMMA reads
+// 64 B/clk at full tensor rate instead of 96 + 96).  Only the leader CTA
+// (cluster rank 0) issues MMAs; both CTAs' TMA loads complete on the leader's
+// full-barrier, MMA commits are multicast to both CTAs' empty / tmem-full
+// barriers, and both CTAs' epilogues release the accumulator buffer on the
+// leader's tmem-empty barrier.  Each CTA's TMEM holds its 128 rows x 256
+// columns of the fp32 accumulator (2 buffers = 512 columns).
+//
+// Replaces run_tape on a recognised matmul / Linear contraction nest
+// (reference tests/kernels.py:24-38) at bf16/tf32 precision.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/b200k.h"
+#include "tc_common.cuh"
+
+namespace b200tc {
+
+namespace {
+
+constexpr int PSTAGES = 6;
+constexpr int PA = 128 * 128;   // A half: 128 rows x 128 B
+constexpr int PB = 128 * 128;   // B half: 128 rows x 128 B
+constexpr int PTHREADS = 256;
+constexpr size_t PSMEM = 1024 + PSTAGES * (PA + PB) + 256;
+
+template <int KIND>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tma_a,
+                    const __grid_constant__ CUtensorMap tma_b, Epi ep, int64_t M, int64_t N,
+                    int64_t K) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  unsigned char *gbase = smem_raw + (base - smem_u32(smem_raw));
+  const uint32_t sA = base;
+  const uint32_t sB = base + PSTAGES * PA;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + PSTAGES * (PA + PB));
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * PSTAGES + 4);
+  const uint32_t bar0 = smem_u32(bars);
+  auto full = [&](int s) { return bar0 + 8u * s; };
+  auto empty = [&](int s) { return bar0 + 8u * (PSTAGES + s); };
+  auto tfull = [&](int a) { return bar0 + 8u * (2 * PSTAGES + a); };
+  auto tempty = [&](int a) { return bar0 + 8u * (2 * PSTAGES + 2 + a); };
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  constexpr int ELEM = KIND == 0 ? 2 : 4;
+  constexpr int BK = 128 / ELEM;
+  constexpr int UK = 32 / ELEM;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < PSTAGES; ++s) {
+      mbar_init(full(s), 1);
+      mbar_init(empty(s), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull(a), 1);
+      mbar_init(tempty(a), 256);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int64_t mt = (M + 255) / 256, nt = (N + 255) / 256;
+  const int64_t tiles = mt * nt;
+  const int64_t kb_total = (K + BK - 1) / BK;
+  const int64_t cid = blockIdx.x / 2, ncl = gridDim.x / 2;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t t = cid; t < tiles; t += ncl) {
+        const int32_t m0 = (int32_t)((t / nt) * 256 + rank * 128);
+        const int32_t n0 = (int32_t)((t % nt) * 256 + rank * 128);
+        for (int64_t kb = 0; kb < kb_total; ++kb) {
+          mbar_wait(empty(s), ph ^ 1);
+          if (leader) mbar_expect_tx(full(s), 2 * (PA + PB));
+          const uint32_t lf = map_to_rank(full(s), 0);
+          tma_load_2d_pair(&tma_a, lf, sA + s * PA, (int32_t)(kb * BK), m0);
+          tma_load_2d_pair(&tma_b, lf, sB + s * PB, (int32_t)(kb * BK), n0);
+          if (++s == PSTAGES) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = make_idesc(KIND, 256, 256);
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      for (int64_t t = cid; t < tiles; t += ncl) {
+        mbar_wait_cluster(tempty(acc), aph ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + (uint32_t)(acc * 256);
+        for (int64_t kb = 0; kb < kb_total; ++kb) {
+          mbar_wait(full(s), ph);
+          tc_fence_after();
+          const uint32_t a_addr = sA + s * PA, b_addr = sB + s * PB;
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k)
+            umma<KIND, 2>(tmem_d, smem_desc(a_addr + 32 * k), smem_desc(b_addr + 32 * k), idesc,
+                          (kb | k) != 0);
+          umma_commit_pair(empty(s), 0x3);
+          if (++s == PSTAGES) { s = 0; ph ^= 1; }
+        }
+        umma_commit_pair(tfull(acc), 0x3);
+        if (++acc == 2) { acc = 0; aph ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp - 4;
+    int acc = 0;
+    uint32_t aph = 0;
+    const uint32_t lead_tempty0 = map_to_rank(tempty(0), 0);
+    const uint32_t lead_tempty1 = map_to_rank(tempty(1), 0);
+    for (int64_t t = cid; t < tiles; t += ncl) {
+      const int64_t m = (t / nt) * 256 + rank * 128 + q * 32 + lane;
+      const int64_t n0 = (t % nt) * 256;
+      mbar_wait_cluster(tfull(acc), aph);
+      tc_fence_after();
+      const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 256);
+#pragma unroll 1
+      for (int c = 0; c < 8; ++c) {
+        uint32_t r[32];
+        tmem_ld32(trow + (uint32_t)(c * 32), r);
+        epilogue_row32(ep, m, n0 + c * 32, M, N, r);
+      }
+      tc_fence_before();
+      mbar_arrive_cluster(acc == 0 ? lead_tempty0 : lead_tempty1);
+      if (++acc == 2) { acc = 0; aph ^= 1; }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(512));
+  }
+}
+
+}  // namespace
+
+int launch_gemm_tc2(int kind, const void *A, const void *Bt, const Epi &ep, int64_t M, int64_t N,
+                    int64_t K, int max_clusters, cudaStream_t s) {
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, kind, A, M, K, 128) || !make_map(&mb, kind, Bt, N, K, 128))
+    return B200_ELAUNCH;
+  const int64_t tiles = ((M + 255) / 256) * ((N + 255) / 256);
+  int clusters = num_sms() / 2;
+  if (max_clusters > 0 && max_clusters < clusters) clusters = max_clusters;
+  if (tiles < clusters) clusters = (int)tiles;
+  if (kind == 0) {
+    cudaFuncSetAttribute(gemm_tc2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)PSMEM);
+    gemm_tc2_kernel<0><<<2 * clusters, PTHREADS, PSMEM, s>>>(ma, mb, ep, M, N, K);
+  } else {
+    cudaFuncSetAttribute(gemm_tc2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)PSMEM);
+    gemm_tc2_kernel<1><<<2 * clusters, PTHREADS, PSMEM, s>>>(ma, mb, ep, M, N, K);
+  }
+  return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
+}
+
+}  // namespace b200tc

@@ -47,7 +47,7 @@ SIGNATURES = {
                             _I64, _I64, _I32, _F32, _P, _I64, _P],
     "b200_pack_operand": [_I32, _P, _I64, _I64, _P, _I64, _I64, _P],
     "b200_gemm_tc": [_I32, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I32, _F32, _P,
-                     _I64, _I32, _P],
+                     _I64, _I32, _I32, _P],
 }
 
 
@@ -177,7 +177,8 @@ def tc_supported(precision, K):
 
 
 def launch_gemm(lib, precision, a_ptr, sA, b_ptr, sB, c_ptr, sC, M, N, K, stream,
-                init=0, init_value=0.0, bias_ptr=None, bias_stride=0, max_ctas=0):
+                init=0, init_value=0.0, bias_ptr=None, bias_stride=0, max_ctas=0,
+                variant=0):
     """Enqueue C (+)= A.B with the kernel chosen by ``precision``.
 
     Returns the list of kernel names launched (for the launch count).
@@ -201,7 +202,7 @@ def launch_gemm(lib, precision, a_ptr, sA, b_ptr, sB, c_ptr, sC, M, N, K, stream
                                 stream), "b200_pack_operand")
     check(lib.b200_gemm_tc(kind, P(Ap.data_ptr()), P(Bp.data_ptr()), P(c_ptr), sC[0], sC[1],
                            M, N, K, init, init_value, P(bias_ptr) if bias_ptr else None,
-                           bias_stride, max_ctas, stream), "b200_gemm_tc")
+                           bias_stride, max_ctas, variant, stream), "b200_gemm_tc")
     return ["pack_operand", "pack_operand", f"gemm_tc_{precision}"]
 
 

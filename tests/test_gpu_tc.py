@@ -28,7 +28,7 @@ def _round(t, kind):
     return u.view(torch.float32)
 
 
-def _run(kind, M, N, K, init=0, bias=False, trans_b=False, seed=0, max_ctas=0):
+def _run(kind, M, N, K, init=0, bias=False, trans_b=False, seed=0, max_ctas=0, variant=0):
     import torch
 
     from paper_2307_16080_b200 import runtime
@@ -57,7 +57,7 @@ def _run(kind, M, N, K, init=0, bias=False, trans_b=False, seed=0, max_ctas=0):
                                  N, K, s) == 0
     rc = lib.b200_gemm_tc(kind, P(Ap.data_ptr()), P(Bp.data_ptr()), P(C.data_ptr()), N, 1,
                           M, N, K, init, 0.5, P(bvec.data_ptr()) if bias else None, 1,
-                          max_ctas, s)
+                          max_ctas, variant, s)
     assert rc == 0
     torch.cuda.synchronize()
     Ad, Bd = A.double(), B.double()
@@ -70,21 +70,24 @@ def _run(kind, M, N, K, init=0, bias=False, trans_b=False, seed=0, max_ctas=0):
     return err, bound, Ap, Bp, A, Bsrc
 
 
+@pytest.mark.parametrize("variant", [1, 2], ids=["cta1", "cta2"])
 @pytest.mark.parametrize("kind", [0, 1], ids=["bf16", "tf32"])
 @pytest.mark.parametrize("shape", [(128, 256, 64), (256, 512, 256), (300, 520, 200),
-                                   (1024, 1024, 1024)])
-def test_gemm_tc_accuracy(kind, shape):
+                                   (1024, 1024, 1024), (2048, 1536, 512)])
+def test_gemm_tc_accuracy(kind, shape, variant):
     M, N, K = shape
     if kind == 0 and K % 8:
         pytest.skip("bf16 TMA rows need K % 8 == 0")
-    err, bound, *_ = _run(kind, M, N, K)
+    err, bound, *_ = _run(kind, M, N, K, variant=variant)
     bad = (err > bound).sum().item()
     assert bad == 0, f"{bad} outputs outside the bound; max err {err.max().item()}"
 
 
+@pytest.mark.parametrize("variant", [1, 2], ids=["cta1", "cta2"])
 @pytest.mark.parametrize("kind", [0, 1], ids=["bf16", "tf32"])
-def test_gemm_tc_epilogue_modes(kind):
-    err, bound, *_ = _run(kind, 256, 256, 128, init=1, bias=True, trans_b=True)
+def test_gemm_tc_epilogue_modes(kind, variant):
+    err, bound, *_ = _run(kind, 512, 512, 128, init=1, bias=True, trans_b=True,
+                          variant=variant)
     assert (err > bound).sum().item() == 0
 
 
@@ -98,7 +101,31 @@ def test_pack_rounding_exact():
     assert torch.equal(Bp, Bsrc.t().contiguous())
 
 
-def test_gemm_tc_few_ctas_persistent_loop():
+@pytest.mark.parametrize("variant", [1, 2], ids=["cta1", "cta2"])
+def test_gemm_tc_few_ctas_persistent_loop(variant):
     # fewer CTAs than tiles: every CTA loops over several tiles (TMEM ping-pong)
-    err, bound, *_ = _run(0, 512, 1024, 256, max_ctas=3)
+    err, bound, *_ = _run(0, 1024, 1024, 256, max_ctas=4, variant=variant)
     assert (err > bound).sum().item() == 0
+
+
+@pytest.mark.parametrize("kind", [0, 1], ids=["bf16", "tf32"])
+def test_pack_paths(kind):
+    """row-contiguous, transposed and general-stride packs agree with torch."""
+    import torch
+
+    from paper_2307_16080_b200 import runtime
+
+    lib = runtime.load_library()
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    P = ctypes.c_void_p
+    src = torch.randn(300, 264, device="cuda")
+    elt = torch.bfloat16 if kind == 0 else torch.float32
+    for rows, cols, s_row, s_col in [(300, 264, 264, 1), (264, 300, 1, 264),
+                                     (150, 132, 528, 2)]:
+        dst = torch.empty(rows, cols, dtype=elt, device="cuda")
+        assert lib.b200_pack_operand(kind, P(src.data_ptr()), s_row, s_col,
+                                     P(dst.data_ptr()), rows, cols, s) == 0
+        torch.cuda.synchronize()
+        view = torch.as_strided(src, (rows, cols), (s_row, s_col))
+        want = _round(view.contiguous(), kind)
+        assert torch.equal(dst.float(), want), (rows, cols, s_row, s_col)
