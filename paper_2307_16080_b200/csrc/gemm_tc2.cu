@@ -2,14 +2,21 @@
 // output tile with tcgen05.mma.cta_group::2 (UMMA M=256, N=256).
 //
 // Each CTA stages its own half of the operands — 128 rows of A and 128 rows of
-// B^T per 128-byte K slice — so per SM the shared-memory traffic per MMA is
-// half of the single-CTA 128x256 kernel's (TMA writes 64 B/clk + UMMA reads
-// 64 B/clk at full tensor rate instead of 96 + 96).  Only the leader CTA
-// (cluster rank 0) issues MMAs; both CTAs' TMA loads complete on the leader's
-// full-barrier, MMA commits are multicast to both CTAs' empty / tmem-full
-// barriers, and both CTAs' epilogues release the accumulator buffer on the
-// leader's tmem-empty barrier.  Each CTA's TMEM holds its 128 rows x 256
-// columns of the fp32 accumulator (2 buffers = 512 columns).
+// B^T per 128-byte K slice — so per SM the TMA traffic per MMA is half of the
+// single-CTA 128x256 kernel's.  Only the leader CTA (cluster rank 0) issues
+// MMAs; both CTAs' TMA loads complete on the leader's full-barrier, MMA
+// commits are multicast to both CTAs' empty / tmem-full barriers, and both
+// CTAs' epilogues release the accumulator buffer on the leader's tmem-empty
+// barrier.  Each CTA's TMEM holds its 128 rows x 256 columns of the fp32
+// accumulator (2 buffers = 512 columns, epilogue of tile i overlaps the MMAs
+// of tile i+1).
+//
+// Epilogue (C = C + acc [+ bias]): C is staged through shared memory in
+// 128-row x 32-column chunks by TMA (128B swizzle, 4 buffers): the loads of
+// upcoming chunks — including the next tile's — are issued ahead, each thread
+// adds its TMEM row in place, and a TMA bulk store writes the chunk back.  All
+// global traffic of the epilogue is coalesced bulk copies.  (Strided C falls
+// back to per-row 128-bit stores.)
 //
 // Replaces run_tape on a recognised matmul / Linear contraction nest
 // (reference tests/kernels.py:24-38) at bf16/tf32 precision.
@@ -24,29 +31,35 @@ namespace b200tc {
 
 namespace {
 
-constexpr int PSTAGES = 6;
+constexpr int PSTAGES = 5;
 constexpr int PA = 128 * 128;   // A half: 128 rows x 128 B
 constexpr int PB = 128 * 128;   // B half: 128 rows x 128 B
+constexpr int CBUF = 128 * 128; // C chunk: 128 rows x 32 fp32
+constexpr int NCBUF = 4;
 constexpr int PTHREADS = 256;
-constexpr size_t PSMEM = 1024 + PSTAGES * (PA + PB) + 256;
+constexpr size_t PSMEM = 1024 + PSTAGES * (PA + PB) + NCBUF * CBUF + 256;
 
 template <int KIND>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tma_a,
-                    const __grid_constant__ CUtensorMap tma_b, Epi ep, int64_t M, int64_t N,
-                    int64_t K) {
+                    const __grid_constant__ CUtensorMap tma_b,
+                    const __grid_constant__ CUtensorMap tma_c, int use_tma_c, Epi ep, int64_t M,
+                    int64_t N, int64_t K) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   unsigned char *gbase = smem_raw + (base - smem_u32(smem_raw));
   const uint32_t sA = base;
   const uint32_t sB = base + PSTAGES * PA;
-  uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + PSTAGES * (PA + PB));
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * PSTAGES + 4);
+  const uint32_t sC = base + PSTAGES * (PA + PB);
+  unsigned char *gC = gbase + PSTAGES * (PA + PB);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + PSTAGES * (PA + PB) + NCBUF * CBUF);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * PSTAGES + 4 + NCBUF);
   const uint32_t bar0 = smem_u32(bars);
   auto full = [&](int s) { return bar0 + 8u * s; };
   auto empty = [&](int s) { return bar0 + 8u * (PSTAGES + s); };
   auto tfull = [&](int a) { return bar0 + 8u * (2 * PSTAGES + a); };
   auto tempty = [&](int a) { return bar0 + 8u * (2 * PSTAGES + 2 + a); };
+  auto cbar = [&](int b) { return bar0 + 8u * (2 * PSTAGES + 4 + b); };
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -65,6 +78,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
       mbar_init(tfull(a), 1);
       mbar_init(tempty(a), 256);
     }
+    for (int b = 0; b < NCBUF; ++b) mbar_init(cbar(b), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
@@ -129,27 +143,71 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
       }
     }
   } else if (warp >= 4) {
+    const int et = threadIdx.x - 128;  // TMEM lane / row within the CTA's 128 rows
     const int q = warp - 4;
+    const bool lead_t = et == 0;
+    const bool load_c = use_tma_c && !ep.init;
+    // chunk g of this CTA: tile k = g / 8 of its tile list, columns (g % 8) * 32
+    auto chunk_coords = [&](int64_t g, int32_t &col, int32_t &row) -> bool {
+      const int64_t t = cid + (g / 8) * ncl;
+      if (t >= tiles) return false;
+      row = (int32_t)((t / nt) * 256 + rank * 128);
+      col = (int32_t)((t % nt) * 256 + (g % 8) * 32);
+      return true;
+    };
+    auto issue_load = [&](int64_t g) {
+      int32_t col, row;
+      if (!chunk_coords(g, col, row)) return;
+      const int b = (int)(g % NCBUF);
+      mbar_expect_tx(cbar(b), CBUF);
+      tma_load_2d(&tma_c, cbar(b), sC + b * CBUF, col, row);
+    };
+    if (load_c && lead_t)
+      for (int64_t g = 0; g < NCBUF - 1; ++g) issue_load(g);
     int acc = 0;
     uint32_t aph = 0;
+    int64_t g = 0;
     const uint32_t lead_tempty0 = map_to_rank(tempty(0), 0);
     const uint32_t lead_tempty1 = map_to_rank(tempty(1), 0);
     for (int64_t t = cid; t < tiles; t += ncl) {
-      const int64_t m = (t / nt) * 256 + rank * 128 + q * 32 + lane;
+      const int64_t m_base = (t / nt) * 256 + rank * 128;
       const int64_t n0 = (t % nt) * 256;
       mbar_wait_cluster(tfull(acc), aph);
       tc_fence_after();
       const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 256);
 #pragma unroll 1
-      for (int c = 0; c < 8; ++c) {
+      for (int c = 0; c < 8; ++c, ++g) {
         uint32_t r[32];
         tmem_ld32(trow + (uint32_t)(c * 32), r);
-        epilogue_row32(ep, m, n0 + c * 32, M, N, r);
+        if (use_tma_c) {
+          const int b = (int)(g % NCBUF);
+          if (load_c) {
+            mbar_wait(cbar(b), (uint32_t)((g / NCBUF) & 1));
+          } else {
+            // no C load: make sure the store of chunk g-4 has left this buffer
+            if (lead_t) bulk_wait_read<NCBUF - 1>();
+            named_bar_sync(1, 128);
+          }
+          epilogue_chunk_smem(gC + b * CBUF, et, n0 + c * 32, N, ep, r);
+          fence_proxy_async();
+          named_bar_sync(1, 128);
+          if (lead_t) {
+            tma_store_2d(&tma_c, sC + b * CBUF, (int32_t)(n0 + c * 32), (int32_t)m_base);
+            bulk_commit();
+            if (load_c) {
+              bulk_wait_read<1>();  // store of chunk g-1 has read buffer (g+3) % 4
+              issue_load(g + NCBUF - 1);
+            }
+          }
+        } else {
+          epilogue_row32(ep, m_base + et, n0 + c * 32, M, N, r);
+        }
       }
       tc_fence_before();
       mbar_arrive_cluster(acc == 0 ? lead_tempty0 : lead_tempty1);
       if (++acc == 2) { acc = 0; aph ^= 1; }
     }
+    if (lead_t && use_tma_c) bulk_wait_all();
   }
   tc_fence_before();
   cluster_sync();
@@ -164,9 +222,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
 
 int launch_gemm_tc2(int kind, const void *A, const void *Bt, const Epi &ep, int64_t M, int64_t N,
                     int64_t K, int max_clusters, cudaStream_t s) {
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mc;
   if (!make_map(&ma, kind, A, M, K, 128) || !make_map(&mb, kind, Bt, N, K, 128))
     return B200_ELAUNCH;
+  // staged epilogue needs unit column stride and 16-byte aligned rows
+  int use_tma_c = ep.sCn == 1 && (ep.sCm * 4) % 16 == 0 &&
+                  (reinterpret_cast<uintptr_t>(ep.C) & 15) == 0 && ep.sCm >= N;
+  if (use_tma_c && !make_map_c(&mc, ep.C, M, N, ep.sCm, 128)) use_tma_c = 0;
+  if (!use_tma_c) mc = ma;  // unused placeholder
   const int64_t tiles = ((M + 255) / 256) * ((N + 255) / 256);
   int clusters = num_sms() / 2;
   if (max_clusters > 0 && max_clusters < clusters) clusters = max_clusters;
@@ -174,11 +237,11 @@ int launch_gemm_tc2(int kind, const void *A, const void *Bt, const Epi &ep, int6
   if (kind == 0) {
     cudaFuncSetAttribute(gemm_tc2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)PSMEM);
-    gemm_tc2_kernel<0><<<2 * clusters, PTHREADS, PSMEM, s>>>(ma, mb, ep, M, N, K);
+    gemm_tc2_kernel<0><<<2 * clusters, PTHREADS, PSMEM, s>>>(ma, mb, mc, use_tma_c, ep, M, N, K);
   } else {
     cudaFuncSetAttribute(gemm_tc2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)PSMEM);
-    gemm_tc2_kernel<1><<<2 * clusters, PTHREADS, PSMEM, s>>>(ma, mb, ep, M, N, K);
+    gemm_tc2_kernel<1><<<2 * clusters, PTHREADS, PSMEM, s>>>(ma, mb, mc, use_tma_c, ep, M, N, K);
   }
   return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
 }

@@ -87,6 +87,37 @@ __device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap *map, uint32_
       : "memory");
 }
 
+// TMA store (bulk group) from local smem to global, OOB elements clipped.
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, uint32_t src, int32_t c0,
+                                             int32_t c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+// make generic-proxy shared-memory writes visible to the async (TMA) proxy
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// 2-D fp32 tensor map over C (row-major, unit column stride) with boxes of
+// 32 columns (128 B, swizzled) x box_rows rows, for the staged epilogue.
+inline bool make_map_c(CUtensorMap *map, const float *C, int64_t rows, int64_t cols,
+                       int64_t row_stride, uint32_t box_rows);
+
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -247,6 +278,48 @@ inline bool make_map(CUtensorMap *map, int kind, const void *ptr, int64_t rows, 
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+inline bool make_map_c(CUtensorMap *map, const float *C, int64_t rows, int64_t cols,
+                       int64_t row_stride, uint32_t box_rows) {
+  EncodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(row_stride * 4)};
+  cuuint32_t box[2] = {32, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(C), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// Epilogue over one 32-column chunk staged in shared memory by TMA with the
+// 128B swizzle: row r's 16-byte unit j lives at unit j ^ (r & 7).  The
+// thread owning row r adds its accumulator (and bias) in place.
+__device__ __forceinline__ void epilogue_chunk_smem(unsigned char *chunk, int r, int64_t nb,
+                                                    int64_t N, const Epi &ep,
+                                                    const uint32_t (&acc)[32]) {
+  float4 *row = reinterpret_cast<float4 *>(chunk + r * 128);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    float4 *p = row + (j ^ (r & 7));
+    float4 o = ep.init ? make_float4(ep.init_value, ep.init_value, ep.init_value, ep.init_value)
+                       : *p;
+    o.x += __uint_as_float(acc[4 * j + 0]);
+    o.y += __uint_as_float(acc[4 * j + 1]);
+    o.z += __uint_as_float(acc[4 * j + 2]);
+    o.w += __uint_as_float(acc[4 * j + 3]);
+    if (ep.bias) {
+      const int64_t n = nb + 4 * j;
+      const float *b = ep.bias + n * ep.bias_stride;
+      o.x += n + 0 < N ? __ldg(b) : 0.f;
+      o.y += n + 1 < N ? __ldg(b + ep.bias_stride) : 0.f;
+      o.z += n + 2 < N ? __ldg(b + 2 * ep.bias_stride) : 0.f;
+      o.w += n + 3 < N ? __ldg(b + 3 * ep.bias_stride) : 0.f;
+    }
+    *p = o;
+  }
 }
 
 inline int num_sms() {
