@@ -129,3 +129,16 @@ def test_pack_paths(kind):
         view = torch.as_strided(src, (rows, cols), (s_row, s_col))
         want = _round(view.contiguous(), kind)
         assert torch.equal(dst.float(), want), (rows, cols, s_row, s_col)
+
+
+@pytest.mark.parametrize("kind", [0, 1], ids=["bf16", "tf32"])
+@pytest.mark.parametrize("shape,clusters", [((4096, 4096, 512), 74), ((2560, 2304, 640), 20),
+                                            ((1280, 1280, 1024), 7)])
+def test_gemm_tc2_split_tail(kind, shape, clusters):
+    """partial last wave split along K; run twice to check ticket reset and
+    that results are deterministic (bit-identical across launches)."""
+    M, N, K = shape
+    err, bound, *_ = _run(kind, M, N, K, variant=2, max_ctas=2 * clusters, seed=3)
+    assert (err > bound).sum().item() == 0
+    err2, _, *_ = _run(kind, M, N, K, variant=2, max_ctas=2 * clusters, seed=3)
+    assert (err2 == err).all().item()
