@@ -13,9 +13,9 @@
 //
 // Work schedule: persistent clusters walk full tiles round-robin; the tiles of
 // the last, partial wave are split S = floor(clusters / remaining) ways along
-// K so the tail wave is balanced.  Split parts write fp32 partials to a
-// workspace and take a ticket; the last part to finish combines
-// C + P_0 + ... + P_{S-1} in fixed order (deterministic, no inter-CTA waits).
+// N into 256 x (256/S) sub-tiles (UMMA N = 256/S, same efficiency per flop),
+// so the tail wave is balanced while every output keeps one full-K chain
+// (deterministic, no partial sums, no workspace).
 //
 // Epilogue (C = C + acc [+ bias]): C is staged through shared memory in
 // 128-row x 32-column chunks by TMA (128B swizzle, 4 buffers): the loads of
@@ -48,50 +48,38 @@ struct Sched {
   int64_t tiles, nt, kb_total, ncl;
   int64_t waves;   // full waves of whole tiles
   int64_t rem;     // tiles in the partial wave
-  int64_t split;   // parts per tail tile (1 = no split)
+  int64_t split;   // N sub-tiles per tail tile (1, 2, 4 or 8)
 };
 
 struct Item {
-  int64_t t;       // tile index
-  int64_t kb0, kb1;
-  int part;        // -1 whole tile, else split part
-  int64_t tail;    // tail tile ordinal (split items)
+  int64_t m0, n0;  // pair tile origin
+  int ncols;       // 256 or 256 / split
 };
 
 __device__ __forceinline__ bool get_item(const Sched &s, int64_t cid, int64_t i, Item &it) {
+  int64_t t, sub = 0;
   if (i < s.waves) {
-    it.t = cid + i * s.ncl;
-    it.kb0 = 0;
-    it.kb1 = s.kb_total;
-    it.part = -1;
-    it.tail = -1;
-    return true;
+    t = cid + i * s.ncl;
+    it.ncols = 256;
+  } else if (i == s.waves && cid < s.rem * s.split) {
+    t = s.waves * s.ncl + cid / s.split;
+    sub = cid % s.split;
+    it.ncols = (int)(256 / s.split);
+  } else {
+    return false;
   }
-  if (i == s.waves && cid < s.rem * s.split) {
-    const int64_t tt = cid / s.split;
-    it.t = s.waves * s.ncl + tt;
-    if (s.split == 1) {
-      it.kb0 = 0;
-      it.kb1 = s.kb_total;
-      it.part = -1;
-      it.tail = -1;
-    } else {
-      it.part = (int)(cid % s.split);
-      it.tail = tt;
-      it.kb0 = it.part * s.kb_total / s.split;
-      it.kb1 = (it.part + 1) * s.kb_total / s.split;
-    }
-    return true;
-  }
-  return false;
+  it.m0 = (t / s.nt) * 256;
+  it.n0 = (t % s.nt) * 256 + sub * it.ncols;
+  return true;
 }
 
 template <int KIND>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tma_a,
                     const __grid_constant__ CUtensorMap tma_b,
+                    const __grid_constant__ CUtensorMap tma_bs,
                     const __grid_constant__ CUtensorMap tma_c, int use_tma_c, Epi ep, int64_t M,
-                    int64_t N, Sched sch, float *ws, int *ws_cnt) {
+                    int64_t N, Sched sch) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   unsigned char *gbase = smem_raw + (base - smem_u32(smem_raw));
@@ -101,7 +89,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
   unsigned char *gC = gbase + PSTAGES * (PA + PB);
   uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + PSTAGES * (PA + PB) + NCBUF * CBUF);
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * PSTAGES + 4 + NCBUF);
-  int *ticket_slot = reinterpret_cast<int *>(tmem_slot + 1);
   const uint32_t bar0 = smem_u32(bars);
   auto full = [&](int s) { return bar0 + 8u * s; };
   auto empty = [&](int s) { return bar0 + 8u * (PSTAGES + s); };
@@ -116,6 +103,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
   constexpr int ELEM = KIND == 0 ? 2 : 4;
   constexpr int BK = 128 / ELEM;
   constexpr int UK = 32 / ELEM;
+  const int64_t kb_total = sch.kb_total;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < PSTAGES; ++s) {
@@ -142,7 +130,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int64_t cid = blockIdx.x / 2;
-  const int64_t nt = sch.nt;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -150,38 +137,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
       uint32_t ph = 0;
       Item it;
       for (int64_t i = 0; get_item(sch, cid, i, it); ++i) {
-        const int32_t m0 = (int32_t)((it.t / nt) * 256 + rank * 128);
-        const int32_t n0 = (int32_t)((it.t % nt) * 256 + rank * 128);
-        for (int64_t kb = it.kb0; kb < it.kb1; ++kb) {
+        // each CTA stages half of the item's columns of B^T
+        const int brows = it.ncols / 2;
+        const CUtensorMap *mb = brows == 128 ? &tma_b : &tma_bs;
+        const uint32_t bytes = 2u * (PA + brows * 128);
+        const int32_t m0 = (int32_t)(it.m0 + rank * 128);
+        const int32_t n0 = (int32_t)(it.n0 + rank * brows);
+        for (int64_t kb = 0; kb < kb_total; ++kb) {
           mbar_wait(empty(s), ph ^ 1);
-          if (leader) mbar_expect_tx(full(s), 2 * (PA + PB));
+          if (leader) mbar_expect_tx(full(s), bytes);
           const uint32_t lf = map_to_rank(full(s), 0);
           tma_load_2d_pair(&tma_a, lf, sA + s * PA, (int32_t)(kb * BK), m0);
-          tma_load_2d_pair(&tma_b, lf, sB + s * PB, (int32_t)(kb * BK), n0);
+          tma_load_2d_pair(mb, lf, sB + s * PB, (int32_t)(kb * BK), n0);
           if (++s == PSTAGES) { s = 0; ph ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     if (leader && lane == 0) {
-      constexpr uint32_t idesc = make_idesc(KIND, 256, 256);
       int s = 0;
       uint32_t ph = 0;
       int acc = 0;
       uint32_t aph = 0;
       Item it;
       for (int64_t i = 0; get_item(sch, cid, i, it); ++i) {
+        const uint32_t idesc = make_idesc(KIND, 256, it.ncols);
         mbar_wait_cluster(tempty(acc), aph ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + (uint32_t)(acc * 256);
-        for (int64_t kb = it.kb0; kb < it.kb1; ++kb) {
+        for (int64_t kb = 0; kb < kb_total; ++kb) {
           mbar_wait(full(s), ph);
           tc_fence_after();
           const uint32_t a_addr = sA + s * PA, b_addr = sB + s * PB;
 #pragma unroll
           for (int k = 0; k < BK / UK; ++k)
             umma<KIND, 2>(tmem_d, smem_desc(a_addr + 32 * k), smem_desc(b_addr + 32 * k), idesc,
-                          (kb != it.kb0 || k != 0));
+                          (kb | k) != 0);
           umma_commit_pair(empty(s), 0x3);
           if (++s == PSTAGES) { s = 0; ph ^= 1; }
         }
@@ -194,12 +185,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
     const int q = warp - 4;
     const bool lead_t = et == 0;
     const bool load_c = use_tma_c && !ep.init;
-    // chunk g of this CTA: work item g / 8, columns (g % 8) * 32 (whole tiles only)
+    // chunk g of this CTA: work item g / 8, columns (g % 8) * 32 of the item
     auto chunk_coords = [&](int64_t g, int32_t &col, int32_t &row) -> bool {
       Item ci;
-      if (!get_item(sch, cid, g / 8, ci) || ci.part >= 0) return false;
-      row = (int32_t)((ci.t / nt) * 256 + rank * 128);
-      col = (int32_t)((ci.t % nt) * 256 + (g % 8) * 32);
+      if (!get_item(sch, cid, g / 8, ci) || (g % 8) * 32 >= ci.ncols) return false;
+      row = (int32_t)(ci.m0 + rank * 128);
+      col = (int32_t)(ci.n0 + (g % 8) * 32);
       return true;
     };
     auto issue_load = [&](int64_t g) {
@@ -218,90 +209,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
     const uint32_t lead_tempty1 = map_to_rank(tempty(1), 0);
     Item it;
     for (int64_t i = 0; get_item(sch, cid, i, it); ++i) {
-      const int64_t m_base = (it.t / nt) * 256 + rank * 128;
-      const int64_t n0 = (it.t % nt) * 256;
+      const int64_t m_base = it.m0 + rank * 128;
       mbar_wait_cluster(tfull(acc), aph);
       tc_fence_after();
       const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 256);
-      if (it.part >= 0) {
-        // split part: fp32 partial of this CTA's 128 x 256 block -> workspace
-        float *P = ws + ((it.tail * sch.split + it.part) * 2 + rank) * (128 * 256);
+      const int nchunks = it.ncols / 32;
 #pragma unroll 1
-        for (int c = 0; c < 8; ++c) {
-          uint32_t r[32];
-          tmem_ld32(trow + (uint32_t)(c * 32), r);
-          float4 *dst = reinterpret_cast<float4 *>(P + et * 256 + c * 32);
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                 __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
-        }
-        g += 8;
-        tc_fence_before();
-        mbar_arrive_cluster(acc == 0 ? lead_tempty0 : lead_tempty1);
-        __threadfence();
-        named_bar_sync(1, 128);
-        if (lead_t) *ticket_slot = atomicAdd(&ws_cnt[it.tail * 2 + rank], 1);
-        named_bar_sync(1, 128);
-        if (*ticket_slot == sch.split - 1) {
-          // last part: C = C + P_0 + ... + P_{S-1} in part order
-          __threadfence();
-          const int64_t m = m_base + et;
-          if (m < M) {
-            for (int c = 0; c < 256; c += 4) {
-              float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-              for (int p = 0; p < sch.split; ++p) {
-                // L2 (coherent) loads: the partials were written by other SMs
-                const float4 w = __ldcg(reinterpret_cast<const float4 *>(
-                    ws + ((it.tail * sch.split + p) * 2 + rank) * (128 * 256) + et * 256 + c));
-                v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
-              }
-              for (int j = 0; j < 4; ++j) {
-                const int64_t n = n0 + c + j;
-                if (n >= N) break;
-                float *dst = ep.C + m * ep.sCm + n * ep.sCn;
-                float o = ep.init ? ep.init_value : *dst;
-                o += (&v.x)[j];
-                if (ep.bias) o += ep.bias[n * ep.bias_stride];
-                *dst = o;
-              }
-            }
-          }
-          named_bar_sync(1, 128);
-          if (lead_t) ws_cnt[it.tail * 2 + rank] = 0;  // reset for the next launch
-        }
-      } else {
-#pragma unroll 1
-        for (int c = 0; c < 8; ++c, ++g) {
-          uint32_t r[32];
-          tmem_ld32(trow + (uint32_t)(c * 32), r);
-          if (use_tma_c) {
-            const int b = (int)(g % NCBUF);
-            if (load_c) {
-              mbar_wait(cbar(b), (uint32_t)((g / NCBUF) & 1));
-            } else {
-              // no C load: make sure the store of chunk g-4 has left this buffer
-              if (lead_t) bulk_wait_read<NCBUF - 1>();
-              named_bar_sync(1, 128);
-            }
-            epilogue_chunk_smem(gC + b * CBUF, et, n0 + c * 32, N, ep, r);
-            fence_proxy_async();
-            named_bar_sync(1, 128);
-            if (lead_t) {
-              tma_store_2d(&tma_c, sC + b * CBUF, (int32_t)(n0 + c * 32), (int32_t)m_base);
-              bulk_commit();
-              if (load_c) {
-                bulk_wait_read<1>();  // store of chunk g-1 has read buffer (g+3) % 4
-                issue_load(g + NCBUF - 1);
-              }
-            }
+      for (int c = 0; c < nchunks; ++c, ++g) {
+        uint32_t r[32];
+        tmem_ld32(trow + (uint32_t)(c * 32), r);
+        const int64_t nb = it.n0 + c * 32;
+        if (use_tma_c) {
+          const int b = (int)(g % NCBUF);
+          if (load_c) {
+            mbar_wait(cbar(b), (uint32_t)((g / NCBUF) & 1));
           } else {
-            epilogue_row32(ep, m_base + et, n0 + c * 32, M, N, r);
+            // no C load: make sure the store of chunk g-4 has left this buffer
+            if (lead_t) bulk_wait_read<NCBUF - 1>();
+            named_bar_sync(1, 128);
           }
+          epilogue_chunk_smem(gC + b * CBUF, et, nb, N, ep, r);
+          fence_proxy_async();
+          named_bar_sync(1, 128);
+          if (lead_t) {
+            tma_store_2d(&tma_c, sC + b * CBUF, (int32_t)nb, (int32_t)m_base);
+            bulk_commit();
+            if (load_c) {
+              bulk_wait_read<1>();  // store of chunk g-1 has read buffer (g+3) % 4
+              issue_load(g + NCBUF - 1);
+            }
+          }
+        } else {
+          epilogue_row32(ep, m_base + et, nb, M, N, r);
         }
-        tc_fence_before();
-        mbar_arrive_cluster(acc == 0 ? lead_tempty0 : lead_tempty1);
       }
+      g += 8 - nchunks;  // keep one 8-chunk slot per item (only the last item is narrower)
+      tc_fence_before();
+      mbar_arrive_cluster(acc == 0 ? lead_tempty0 : lead_tempty1);
       if (++acc == 2) { acc = 0; aph ^= 1; }
     }
     if (lead_t && use_tma_c) bulk_wait_all();
@@ -315,47 +259,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
   }
 }
 
-// split-K workspace: fp32 partials + per-(tail tile, rank) tickets (zeroed
-// once; the last part of every tile resets its ticket).  One launch at a time.
-float *g_ws = nullptr;
-int *g_cnt = nullptr;
-size_t g_ws_floats = 0, g_cnt_n = 0;
-
-bool ensure_ws(size_t floats, size_t cnt, cudaStream_t s) {
-  if (floats > g_ws_floats) {
-    if (g_ws) cudaFree(g_ws);
-    if (cudaMalloc(&g_ws, floats * sizeof(float)) != cudaSuccess) {
-      g_ws = nullptr;
-      g_ws_floats = 0;
-      return false;
-    }
-    g_ws_floats = floats;
-  }
-  if (cnt > g_cnt_n) {
-    if (g_cnt) cudaFree(g_cnt);
-    if (cudaMalloc(&g_cnt, cnt * sizeof(int)) != cudaSuccess) {
-      g_cnt = nullptr;
-      g_cnt_n = 0;
-      return false;
-    }
-    cudaMemsetAsync(g_cnt, 0, cnt * sizeof(int), s);
-    g_cnt_n = cnt;
-  }
-  return true;
-}
-
 }  // namespace
 
 int launch_gemm_tc2(int kind, const void *A, const void *Bt, const Epi &ep, int64_t M, int64_t N,
                     int64_t K, int max_clusters, cudaStream_t s) {
-  CUtensorMap ma, mb, mc;
-  if (!make_map(&ma, kind, A, M, K, 128) || !make_map(&mb, kind, Bt, N, K, 128))
-    return B200_ELAUNCH;
-  // staged epilogue needs unit column stride and 16-byte aligned rows
-  int use_tma_c = ep.sCn == 1 && (ep.sCm * 4) % 16 == 0 &&
-                  (reinterpret_cast<uintptr_t>(ep.C) & 15) == 0 && ep.sCm >= N;
-  if (use_tma_c && !make_map_c(&mc, ep.C, M, N, ep.sCm, 128)) use_tma_c = 0;
-  if (!use_tma_c) mc = ma;  // unused placeholder
   Sched sch;
   sch.nt = (N + 255) / 256;
   sch.tiles = ((M + 255) / 256) * sch.nt;
@@ -368,24 +275,28 @@ int launch_gemm_tc2(int kind, const void *A, const void *Bt, const Epi &ep, int6
   sch.rem = sch.tiles - sch.waves * clusters;
   sch.split = 1;
   if (sch.rem > 0) {
-    int64_t S = clusters / sch.rem;
-    if (S > sch.kb_total) S = sch.kb_total;
-    if (S > 8) S = 8;
-    if (S >= 2) sch.split = S;
+    const int64_t S = clusters / sch.rem;
+    sch.split = S >= 8 ? 8 : (S >= 4 ? 4 : (S >= 2 ? 2 : 1));
   }
-  if (sch.split > 1 &&
-      !ensure_ws((size_t)sch.rem * sch.split * 2 * 128 * 256, (size_t)sch.rem * 2, s))
-    sch.split = 1;
+  CUtensorMap ma, mb, mbs, mc;
+  if (!make_map(&ma, kind, A, M, K, 128) || !make_map(&mb, kind, Bt, N, K, 128) ||
+      !make_map(&mbs, kind, Bt, N, K, (uint32_t)(128 / sch.split)))
+    return B200_ELAUNCH;
+  // staged epilogue needs unit column stride and 16-byte aligned rows
+  int use_tma_c = ep.sCn == 1 && (ep.sCm * 4) % 16 == 0 &&
+                  (reinterpret_cast<uintptr_t>(ep.C) & 15) == 0 && ep.sCm >= N;
+  if (use_tma_c && !make_map_c(&mc, ep.C, M, N, ep.sCm, 128)) use_tma_c = 0;
+  if (!use_tma_c) mc = ma;  // unused placeholder
   if (kind == 0) {
     cudaFuncSetAttribute(gemm_tc2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)PSMEM);
-    gemm_tc2_kernel<0><<<2 * clusters, PTHREADS, PSMEM, s>>>(ma, mb, mc, use_tma_c, ep, M, N, sch,
-                                                            g_ws, g_cnt);
+    gemm_tc2_kernel<0><<<2 * clusters, PTHREADS, PSMEM, s>>>(ma, mb, mbs, mc, use_tma_c, ep, M, N,
+                                                            sch);
   } else {
     cudaFuncSetAttribute(gemm_tc2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)PSMEM);
-    gemm_tc2_kernel<1><<<2 * clusters, PTHREADS, PSMEM, s>>>(ma, mb, mc, use_tma_c, ep, M, N, sch,
-                                                            g_ws, g_cnt);
+    gemm_tc2_kernel<1><<<2 * clusters, PTHREADS, PSMEM, s>>>(ma, mb, mbs, mc, use_tma_c, ep, M, N,
+                                                            sch);
   }
   return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
 }
