@@ -28,6 +28,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/b200k.h"
 #include "tc_common.cuh"
@@ -68,8 +69,16 @@ __device__ __forceinline__ bool get_item(const Sched &s, int64_t cid, int64_t i,
   } else {
     return false;
   }
-  it.m0 = (t / s.nt) * 256;
-  it.n0 = (t % s.nt) * 256 + sub * it.ncols;
+  // grouped raster: GROUP_M consecutive M-blocks walk N together, so one wave
+  // of tiles touches ~GROUP_M A panels and ~waves/GROUP_M B panels (L2 reuse)
+  constexpr int64_t GROUP_M = 8;
+  const int64_t mt = s.tiles / s.nt;
+  const int64_t group = t / (GROUP_M * s.nt);
+  const int64_t first_m = group * GROUP_M;
+  const int64_t gm = (mt - first_m) < GROUP_M ? (mt - first_m) : GROUP_M;
+  const int64_t tin = t - group * GROUP_M * s.nt;
+  it.m0 = (first_m + tin % gm) * 256;
+  it.n0 = (tin / gm) * 256 + sub * it.ncols;
   return true;
 }
 
@@ -274,7 +283,8 @@ int launch_gemm_tc2(int kind, const void *A, const void *Bt, const Epi &ep, int6
   sch.waves = sch.tiles / clusters;
   sch.rem = sch.tiles - sch.waves * clusters;
   sch.split = 1;
-  if (sch.rem > 0) {
+  const char *env = getenv("B200_TC2_SPLIT");
+  if (sch.rem > 0 && !(env && env[0] == '0')) {
     const int64_t S = clusters / sch.rem;
     sch.split = S >= 8 ? 8 : (S >= 4 ? 4 : (S >= 2 ? 2 : 1));
   }

@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--init", type=int, nargs="+", default=[0, 1])
     ap.add_argument("--mnk", type=int, nargs=3, default=[4096, 4096, 4096])
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--cublas", action="store_true", help="also time torch.mm (cuBLAS) bf16")
     a = ap.parse_args()
     import torch
 
@@ -30,6 +31,24 @@ def main():
     s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
     P = ctypes.c_void_p
     C = torch.zeros(M, N, device="cuda")
+    if a.cublas:
+        for dt in (torch.bfloat16,):
+            X = torch.randn(M, K, device="cuda").to(dt)
+            Y = torch.randn(K, N, device="cuda").to(dt)
+            Z = torch.empty(M, N, device="cuda", dtype=dt)
+            for _ in range(3):
+                torch.mm(X, Y, out=Z)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(a.iters):
+                torch.mm(X, Y, out=Z)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / a.iters
+            print(f"cublas {dt} M={M} N={N} K={K} ms={ms:.4f} TFLOP/s={2*M*N*K/ms/1e9:.1f}",
+                  flush=True)
     for kind in a.kind:
         elt = torch.bfloat16 if kind == 0 else torch.float32
         A = torch.randn(M, K, device="cuda").to(elt)
