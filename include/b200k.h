@@ -94,6 +94,23 @@ int b200_gemm_f32_exact(const float *A, int64_t sAm, int64_t sAk,
                         const float *bias, int64_t bias_stride, void *stream);
 
 /*
+ * Exact separable contraction (f32 or f64, per-op rounding, K in nest order):
+ *   C[c_m[m] + c_n[n]] = (init ? init_value : C[..]) +
+ *                        sum_k A[a_m[m] + a_k[k]] * B[b_k[k] + b_n[n]]  (+ bias)
+ * with int64 element-offset tables (DEVICE arrays).  Replaces run_tape on any
+ * contraction nest whose index maps split into output-row (M), output-column
+ * (N) and reduction (K) variable groups — e.g. the NCHW/FCHW conv nest
+ * (reference tests/kernels.py:50-64) as an implicit GEMM
+ * M = (n, ho, wo), N = co, K = (ci, ki, kj).  a_k_fast / b_n_fast pick the
+ * coalesced loader orientation.  Bit-identical to the reference.
+ */
+int b200_contract_exact(int32_t dtype, const void *A, const int64_t *a_m, const int64_t *a_k,
+                        const void *B, const int64_t *b_k, const int64_t *b_n, void *C,
+                        const int64_t *c_m, const int64_t *c_n, int64_t M, int64_t N, int64_t K,
+                        int32_t a_k_fast, int32_t b_n_fast, int32_t init, double init_value,
+                        const void *bias, int64_t bias_stride, void *stream);
+
+/*
  * Operand packing for the tensor-core contraction: dst[r][c] (dense
  * row-major, i.e. K-major for the GEMM) = round(src[r*s_row + c*s_col]),
  * kind 0 -> bf16 (RN), kind 1 -> tf32 held in f32 (RN, low 13 bits zero).

@@ -32,9 +32,14 @@ from __future__ import annotations
 
 from .lift import (BOOKKEEPING, CAST, CMPF, CMPI, CONST, BINF, BINI, GPUID, JUMP,
                    IF_FALSE, LAUNCH, LOAD, LOOP_INIT_A, LOOP_INIT_S, LOOP_NEXT_I,
-                   LOOP_NEXT_R, LOOP_TEST_I, LOOP_TEST_R, N_OPCODES, PARALLEL,
+                   LOOP_NEXT_R, LOOP_TEST_I, LOOP_TEST_R, N_OPCODES, PARALLEL, RETURN_GPU,
                    PURE_OPS, STORE, EMPTY, Aff, If, Ins, Launch, Loop, Par,
                    aff_range, prod, var_range)
+
+
+# leaves allowed beside a chain loop: pure scalar ops and the kernel's
+# gpu.return (a no-op for memory; counted in the tally like any leaf)
+CHAIN_LEAVES = PURE_OPS | {RETURN_GPU}
 
 
 class Access:
@@ -119,7 +124,7 @@ def chain_of(region):
     while True:
         loops = [n for n in seq if not isinstance(n, Ins)]
         leaves = [n for n in seq if isinstance(n, Ins)]
-        if len(loops) != 1 or any(x.op not in PURE_OPS for x in leaves):
+        if len(loops) != 1 or any(x.op not in CHAIN_LEAVES for x in leaves):
             break
         node = loops[0]
         if isinstance(node, Loop):

@@ -1,22 +1,27 @@
-// Bit-exact fp32 contraction on the FP32 pipes of sm_100a.
+// Bit-exact contraction on the FP32/FP64 pipes of sm_100a.
 //
 // The reference computes every f32 product and sum in double and rounds it
 // back to f32 (reference pkg/src/staircase/interp/_evalpy.py:115-127 and
 // interp/_evalcy.pyx:122-136).  Double rounding is innocuous for + - * /
 // (53 >= 2*24+2), so each op equals one IEEE f32 op; there is no FMA and the
-// reduction runs k-ascending.  This kernel performs exactly that chain per
-// output — __fmul_rn/__fadd_rn cannot be contracted — so results are
-// bit-identical to the reference for every shape, stride and tile config.
+// reduction runs in nest order.  These kernels perform exactly that chain per
+// output — __fmul_rn/__fadd_rn (__dmul_rn/__dadd_rn for f64) cannot be
+// contracted — so results are bit-identical to the reference for every shape,
+// stride and tile config.
 //
-// Tiling: 128x128 CTA tile, BK = 16, 256 threads each owning an 8x8 register
-// micro-tile (split as 2x2 blocks of 4x4 so shared-memory reads are
-// conflict-free float4 broadcasts); global->shared staging is register
-// double-buffered so the next k-tile's loads overlap the current tile's math.
-// Operands are arbitrary-strided (the recogniser hands over the affine index
-// maps of the nest), loads are coalesced along whichever dimension has unit
-// stride.  Epilogue: optional init value (the fill/copy nests of the Linear
-// lowering) and optional bias add,
-// each a separately rounded f32 op in reference order.
+// Two operand addressings share one tiled core:
+//   * strided (b200_gemm_f32_exact): A[m*sAm + k*sAk] etc. — matmul nests;
+//   * separable tables (b200_contract_exact): A[a_m[m] + a_k[k]],
+//     B[b_k[k] + b_n[n]], C[c_m[m] + c_n[n]] — any contraction whose index
+//     maps split into output-row / output-column / reduction variable groups,
+//     e.g. the NCHW/FCHW convolution (reference tests/kernels.py:50-64) as an
+//     implicit GEMM with M = (n, ho, wo), N = co, K = (ci, ki, kj) in nest
+//     order.
+// Tiling: 128x128 (f32) / 64x64 (f64) CTA tile, BK = 16, 256 threads with an
+// 8x8 / 4x4 register micro-tile (2x2 blocks of 4x4 so shared-memory reads are
+// float4 broadcasts); global->shared staging is register double-buffered so
+// the next k-tile's loads overlap the current tile's math; loads are
+// coalesced along whichever operand dimension has unit stride.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -24,143 +29,179 @@
 
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16, TM = 8, TN = 8;
+constexpr int BK = 16;
 constexpr int kThreads = 256;
-constexpr int APAD = 4;   // As row padding: conflict-light transposed stores
 
-struct GemmArgs {
-  const float *A, *B;
-  float *C;
-  const float *bias;
-  int64_t sAm, sAk, sBk, sBn, sCm, sCn, bias_stride;
-  int64_t M, N, K;
-  int init;
-  float init_value;
+template <typename T>
+struct Cfg;
+template <>
+struct Cfg<float> {
+  static constexpr int BM = 128, BN = 128, TM = 8, TN = 8, PAD = 4;
+};
+template <>
+struct Cfg<double> {
+  static constexpr int BM = 64, BN = 64, TM = 4, TN = 4, PAD = 2;
 };
 
-// Each thread stages 8 A elements and 8 B elements per k-tile.
-__device__ __forceinline__ void load_tile(const GemmArgs &g, int64_t m0, int64_t n0, int64_t k0,
-                                          float (&ra)[8], float (&rb)[8]) {
-  const int t = threadIdx.x;
-  // A tile: BM x BK = 2048 elements.  If A is k-contiguous walk k fastest.
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    int e = t + i * kThreads;
-    int mm, kk;
-    if (g.sAk == 1) { kk = e % BK; mm = e / BK; } else { mm = e % BM; kk = e / BM; }
-    int64_t m = m0 + mm, k = k0 + kk;
-    ra[i] = (m < g.M && k < g.K) ? __ldg(g.A + m * g.sAm + k * g.sAk) : 0.0f;
-  }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    int e = t + i * kThreads;
-    int nn, kk;
-    if (g.sBn == 1) { nn = e % BN; kk = e / BN; } else { kk = e % BK; nn = e / BK; }
-    int64_t n = n0 + nn, k = k0 + kk;
-    rb[i] = (n < g.N && k < g.K) ? __ldg(g.B + k * g.sBk + n * g.sBn) : 0.0f;
-  }
-}
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
 
-__device__ __forceinline__ void store_tile(const GemmArgs &g, float (*As)[BM + APAD], float (*Bs)[BN],
-                                           const float (&ra)[8], const float (&rb)[8]) {
-  const int t = threadIdx.x;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    int e = t + i * kThreads;
-    int mm, kk;
-    if (g.sAk == 1) { kk = e % BK; mm = e / BK; } else { mm = e % BM; kk = e / BM; }
-    As[kk][mm] = ra[i];
-  }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    int e = t + i * kThreads;
-    int nn, kk;
-    if (g.sBn == 1) { nn = e % BN; kk = e / BN; } else { kk = e % BK; nn = e / BK; }
-    Bs[kk][nn] = rb[i];
-  }
-}
+// Operand addressing.  a(m,k), b(k,n), c(m,n) return element offsets.
+struct Strided {
+  int64_t sAm, sAk, sBk, sBn, sCm, sCn;
+  bool a_k_fast, b_n_fast;
+  __device__ __forceinline__ int64_t a(int64_t m, int64_t k) const { return m * sAm + k * sAk; }
+  __device__ __forceinline__ int64_t b(int64_t k, int64_t n) const { return k * sBk + n * sBn; }
+  __device__ __forceinline__ int64_t c(int64_t m, int64_t n) const { return m * sCm + n * sCn; }
+};
+struct Tables {
+  const int64_t *a_m, *a_k, *b_k, *b_n, *c_m, *c_n;
+  bool a_k_fast, b_n_fast;
+  __device__ __forceinline__ int64_t a(int64_t m, int64_t k) const { return __ldg(a_m + m) + __ldg(a_k + k); }
+  __device__ __forceinline__ int64_t b(int64_t k, int64_t n) const { return __ldg(b_k + k) + __ldg(b_n + n); }
+  __device__ __forceinline__ int64_t c(int64_t m, int64_t n) const { return __ldg(c_m + m) + __ldg(c_n + n); }
+};
 
-__global__ void __launch_bounds__(kThreads) gemm_exact_kernel(GemmArgs g) {
-  __shared__ __align__(16) float As[2][BK][BM + APAD];
-  __shared__ __align__(16) float Bs[2][BK][BN];
+template <typename T, typename Addr>
+struct Args {
+  const T *A, *B;
+  T *C;
+  const T *bias;
+  int64_t bias_stride;
+  int64_t M, N, K;
+  int init;
+  T init_value;
+  Addr ad;
+};
+
+template <typename T, typename Addr>
+__global__ void __launch_bounds__(kThreads) contract_exact_kernel(Args<T, Addr> g) {
+  using C_ = Cfg<T>;
+  constexpr int BM = C_::BM, BN = C_::BN, TM = C_::TM, TN = C_::TN;
+  constexpr int LA = BM * BK / kThreads;  // A elements staged per thread
+  constexpr int LB = BN * BK / kThreads;
+  constexpr int HM = TM / 2, HN = TN / 2;  // micro-tile halves
+  constexpr int TX = BN / TN;              // threads along n
+  __shared__ __align__(16) T As[2][BK][BM + C_::PAD];
+  __shared__ __align__(16) T Bs[2][BK][BN];
 
   const int64_t m0 = (int64_t)blockIdx.y * BM;
   const int64_t n0 = (int64_t)blockIdx.x * BN;
-  const int tx = threadIdx.x % 16;   // n direction
-  const int ty = threadIdx.x / 16;   // m direction
-  // micro-tile rows: ty*4 + {0..3} and 64 + ty*4 + {0..3}; cols likewise.
-  float acc[TM][TN];
+  const int tx = threadIdx.x % TX;
+  const int ty = threadIdx.x / TX;
+  auto row_of = [&](int i) { return i < HM ? ty * HM + i : BM / 2 + ty * HM + (i - HM); };
+  auto col_of = [&](int j) { return j < HN ? tx * HN + j : BN / 2 + tx * HN + (j - HN); };
+
+  T acc[TM][TN];
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
-    int64_t m = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+    const int64_t m = m0 + row_of(i);
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
-      int64_t n = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
-      float v = g.init_value;
-      if (!g.init && m < g.M && n < g.N) v = g.C[m * g.sCm + n * g.sCn];
+      const int64_t n = n0 + col_of(j);
+      T v = g.init_value;
+      if (!g.init && m < g.M && n < g.N) v = g.C[g.ad.c(m, n)];
       acc[i][j] = v;
     }
   }
 
-  float ra[8], rb[8];
-  const int64_t ktiles = (g.K + BK - 1) / BK;
-  load_tile(g, m0, n0, 0, ra, rb);
-  store_tile(g, As[0], Bs[0], ra, rb);
-  __syncthreads();
+  T ra[LA], rb[LB];
+  auto load = [&](int64_t k0) {
+#pragma unroll
+    for (int i = 0; i < LA; ++i) {
+      const int e = threadIdx.x + i * kThreads;
+      int mm, kk;
+      if (g.ad.a_k_fast) { kk = e % BK; mm = e / BK; } else { mm = e % BM; kk = e / BM; }
+      const int64_t m = m0 + mm, k = k0 + kk;
+      ra[i] = (m < g.M && k < g.K) ? __ldg(g.A + g.ad.a(m, k)) : T(0);
+    }
+#pragma unroll
+    for (int i = 0; i < LB; ++i) {
+      const int e = threadIdx.x + i * kThreads;
+      int nn, kk;
+      if (g.ad.b_n_fast) { nn = e % BN; kk = e / BN; } else { kk = e % BK; nn = e / BK; }
+      const int64_t n = n0 + nn, k = k0 + kk;
+      rb[i] = (n < g.N && k < g.K) ? __ldg(g.B + g.ad.b(k, n)) : T(0);
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < LA; ++i) {
+      const int e = threadIdx.x + i * kThreads;
+      int mm, kk;
+      if (g.ad.a_k_fast) { kk = e % BK; mm = e / BK; } else { mm = e % BM; kk = e / BM; }
+      As[buf][kk][mm] = ra[i];
+    }
+#pragma unroll
+    for (int i = 0; i < LB; ++i) {
+      const int e = threadIdx.x + i * kThreads;
+      int nn, kk;
+      if (g.ad.b_n_fast) { nn = e % BN; kk = e / BN; } else { kk = e % BK; nn = e / BK; }
+      Bs[buf][kk][nn] = rb[i];
+    }
+  };
 
+  const int64_t ktiles = (g.K + BK - 1) / BK;
+  if (ktiles > 0) {
+    load(0);
+    store(0);
+  }
+  __syncthreads();
   for (int64_t kt = 0; kt < ktiles; ++kt) {
     const int cur = kt & 1;
-    if (kt + 1 < ktiles) load_tile(g, m0, n0, (kt + 1) * BK, ra, rb);
+    if (kt + 1 < ktiles) load((kt + 1) * BK);
     const int64_t krem = g.K - kt * BK;
-    if (krem >= BK) {
+    const int kn = krem >= BK ? BK : (int)krem;
+#pragma unroll 4
+    for (int kk = 0; kk < kn; ++kk) {
+      T av[TM], bv[TN];
 #pragma unroll
-      for (int kk = 0; kk < BK; ++kk) {
-        float4 a0 = *reinterpret_cast<const float4 *>(&As[cur][kk][ty * 4]);
-        float4 a1 = *reinterpret_cast<const float4 *>(&As[cur][kk][64 + ty * 4]);
-        float4 b0 = *reinterpret_cast<const float4 *>(&Bs[cur][kk][tx * 4]);
-        float4 b1 = *reinterpret_cast<const float4 *>(&Bs[cur][kk][64 + tx * 4]);
-        const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-        const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-#pragma unroll
-        for (int i = 0; i < TM; ++i)
-#pragma unroll
-          for (int j = 0; j < TN; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(av[i], bv[j]));
+      for (int i = 0; i < HM; ++i) {
+        av[i] = As[cur][kk][ty * HM + i];
+        av[HM + i] = As[cur][kk][BM / 2 + ty * HM + i];
       }
-    } else {
-      for (int kk = 0; kk < krem; ++kk) {
-        float av[8], bv[8];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          av[i] = As[cur][kk][ty * 4 + i];
-          av[4 + i] = As[cur][kk][64 + ty * 4 + i];
-          bv[i] = Bs[cur][kk][tx * 4 + i];
-          bv[4 + i] = Bs[cur][kk][64 + tx * 4 + i];
-        }
-#pragma unroll
-        for (int i = 0; i < TM; ++i)
-#pragma unroll
-          for (int j = 0; j < TN; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(av[i], bv[j]));
+      for (int j = 0; j < HN; ++j) {
+        bv[j] = Bs[cur][kk][tx * HN + j];
+        bv[HN + j] = Bs[cur][kk][BN / 2 + tx * HN + j];
       }
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = add_rn(acc[i][j], mul_rn(av[i], bv[j]));
     }
     if (kt + 1 < ktiles) {
-      store_tile(g, As[cur ^ 1], Bs[cur ^ 1], ra, rb);
+      store(cur ^ 1);
       __syncthreads();
     }
   }
 
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
-    int64_t m = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+    const int64_t m = m0 + row_of(i);
     if (m >= g.M) continue;
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
-      int64_t n = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
+      const int64_t n = n0 + col_of(j);
       if (n >= g.N) continue;
-      float v = acc[i][j];
-      if (g.bias) v = __fadd_rn(v, __ldg(g.bias + n * g.bias_stride));
-      g.C[m * g.sCm + n * g.sCn] = v;
+      T v = acc[i][j];
+      if (g.bias) v = add_rn(v, __ldg(g.bias + n * g.bias_stride));
+      g.C[g.ad.c(m, n)] = v;
     }
   }
+}
+
+template <typename T, typename Addr>
+int launch(const Args<T, Addr> &g, void *stream) {
+  using C_ = Cfg<T>;
+  if (g.M < 0 || g.N < 0 || g.K < 0) return B200_EINVAL;
+  if (g.M == 0 || g.N == 0) return B200_OK;
+  dim3 grid((unsigned)((g.N + C_::BN - 1) / C_::BN), (unsigned)((g.M + C_::BM - 1) / C_::BM));
+  if (grid.y > 65535u) return B200_EINVAL;
+  contract_exact_kernel<T, Addr><<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(g);
+  return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
 }
 
 }  // namespace
@@ -170,11 +211,30 @@ extern "C" int b200_gemm_f32_exact(const float *A, int64_t sAm, int64_t sAk, con
                                    int64_t M, int64_t N, int64_t K, int32_t init,
                                    float init_value, const float *bias, int64_t bias_stride,
                                    void *stream) {
-  if (M < 0 || N < 0 || K < 0) return B200_EINVAL;
-  if (M == 0 || N == 0) return B200_OK;
-  GemmArgs g{A, B, C, bias, sAm, sAk, sBk, sBn, sCm, sCn, bias_stride, M, N, K, init, init_value};
-  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
-  if (grid.y > 65535) return B200_EINVAL;
-  gemm_exact_kernel<<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(g);
-  return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
+  Args<float, Strided> g{A, B, C, bias, bias_stride, M, N, K, init, init_value,
+                         Strided{sAm, sAk, sBk, sBn, sCm, sCn, sAk == 1, sBn == 1}};
+  return launch(g, stream);
+}
+
+extern "C" int b200_contract_exact(int32_t dtype, const void *A, const int64_t *a_m,
+                                   const int64_t *a_k, const void *B, const int64_t *b_k,
+                                   const int64_t *b_n, void *C, const int64_t *c_m,
+                                   const int64_t *c_n, int64_t M, int64_t N, int64_t K,
+                                   int32_t a_k_fast, int32_t b_n_fast, int32_t init,
+                                   double init_value, const void *bias, int64_t bias_stride,
+                                   void *stream) {
+  Tables t{a_m, a_k, b_k, b_n, c_m, c_n, a_k_fast != 0, b_n_fast != 0};
+  if (dtype == B200_F32) {
+    Args<float, Tables> g{static_cast<const float *>(A), static_cast<const float *>(B),
+                          static_cast<float *>(C), static_cast<const float *>(bias), bias_stride,
+                          M, N, K, init, (float)init_value, t};
+    return launch(g, stream);
+  }
+  if (dtype == B200_F64) {
+    Args<double, Tables> g{static_cast<const double *>(A), static_cast<const double *>(B),
+                           static_cast<double *>(C), static_cast<const double *>(bias),
+                           bias_stride, M, N, K, init, init_value, t};
+    return launch(g, stream);
+  }
+  return B200_EUNSUPPORTED;
 }

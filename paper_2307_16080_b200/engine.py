@@ -217,9 +217,9 @@ class _Run:
             self.be.mark_dirty(r.buffers[slot])
 
         if safe and st is not None:
-            g = templates.match_gemm(r, links, remainder, accesses)
+            g = templates.match_contraction(r, links, remainder, accesses)
             if g is not None:
-                kernels = self.be.gemm(g, PRECISION) or ["gemm_f32_exact"]
+                kernels = self.be.contract(g, PRECISION)
                 _add(tally, st)
                 self.plan.append((kernels[-1], g.M, g.N, g.K))
                 return

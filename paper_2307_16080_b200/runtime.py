@@ -45,6 +45,8 @@ SIGNATURES = {
                     _I32, _P, _P, _P],
     "b200_gemm_f32_exact": [_P, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64, _I64,
                             _I64, _I64, _I32, _F32, _P, _I64, _P],
+    "b200_contract_exact": [_I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64,
+                            _I32, _I32, _I32, ctypes.c_double, _P, _I64, _P],
     "b200_pack_operand": [_I32, _P, _I64, _I64, _P, _I64, _I64, _P],
     "b200_gemm_tc": [_I32, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I32, _F32, _P,
                      _I64, _I32, _I32, _P],
@@ -227,12 +229,28 @@ class DeviceBackend:
     def flush(self):
         self.stage.flush()
 
-    def gemm(self, g, precision="exact"):
+    def contract(self, g, precision="exact"):
+        """Run a templates.ContractMatch; returns the kernel names launched."""
         s = self.stage
         tA, tB, tC = s.tensor(g.A), s.tensor(g.B), s.tensor(g.C)
-        return launch_gemm(s.lib, precision, tA.data_ptr() + 4 * g.offA, g.sA,
-                           tB.data_ptr() + 4 * g.offB, g.sB, tC.data_ptr() + 4 * g.offC,
-                           g.sC, g.M, g.N, g.K, s.stream_ptr)
+        if g.strided and g.dtype == "f32":
+            return launch_gemm(s.lib, precision, tA.data_ptr() + 4 * g.offA, g.sA,
+                               tB.data_ptr() + 4 * g.offB, g.sB, tC.data_ptr() + 4 * g.offC,
+                               g.sC, g.M, g.N, g.K, s.stream_ptr)
+        torch = s.torch
+        tabs = [torch.from_numpy(t).to("cuda") for t in g.tables]
+        a_m, a_k, b_k, b_n, c_m, c_n = g.tables
+        a_k_fast = int(len(a_k) > 1 and a_k[1] - a_k[0] == 1)
+        b_n_fast = int(len(b_n) > 1 and b_n[1] - b_n[0] == 1)
+        P = ctypes.c_void_p
+        check(s.lib.b200_contract_exact(
+            DT_CODE[g.dtype], P(tA.data_ptr()), P(tabs[0].data_ptr()), P(tabs[1].data_ptr()),
+            P(tB.data_ptr()), P(tabs[2].data_ptr()), P(tabs[3].data_ptr()),
+            P(tC.data_ptr()), P(tabs[4].data_ptr()), P(tabs[5].data_ptr()),
+            g.M, g.N, g.K, a_k_fast, b_n_fast, 0, 0.0, None, 0, s.stream_ptr),
+            "b200_contract_exact")
+        self._keep = tabs   # tables must outlive the asynchronous kernel
+        return ["contract_exact"]
 
     def vm(self, r, prog, checked):
         """Run a VM program; returns (device tally | None, fault | None)."""

@@ -1,42 +1,67 @@
 """Recognise dense contractions in lifted regions and map them to kernels.
 
 The reference's matmul nests (reference tests/kernels.py:24-38, PAPER.md
-143-191) and the contraction nest of the Linear lowering (PAPER.md 443-454)
-all have the shape
+143-191), the contraction nest of the Linear lowering (PAPER.md 443-454) and
+the NCHW/FCHW convolution (tests/kernels.py:50-64, PAPER.md 1048-1068) all
+have the shape
 
-    for <vars in any order>:            # static bounds
-        a = A[fA(m, k)]; b = B[fB(k, n)]; c = C[fC(m, n)]
-        C[fC(m, n)] = c + a * b         # f32, each op rounded
+    for <vars, any nesting / parallel / launch mix, static bounds>:
+        a = A[fA(vars)]; b = B[fB(vars)]; c = C[fC(vars)]
+        C[fC(vars)] = c + a * b            # f32 or f64, each op rounded
 
-with affine index maps.  Every variable plays exactly one role: M (in C and
-A), N (in C and B) or K (in A and B only — the reduction, executed in
-ascending order per output), or is a trip-1 variable.  Such a region is a
-GEMM ``C[m,n] = C[m,n] + sum_k A[m,k] B[k,n]`` over element strides read
-off the affine maps, whatever the loop order or parallel/for mix.
+with affine index maps.  Every variable with trip > 1 must play exactly one
+role: M (appears in C and A), N (C and B) or K (A and B only — a reduction,
+executed per output in nest order, i.e. lexicographically over the K
+variables in nesting order).  Trip-1 variables are constants.  Then
+
+    C[cM(m) + cN(n)] = C[..] + sum_k A[aM(m) + aK(k)] * B[bK(k) + bN(n)]
+
+where each offset function is a per-group table (mixed-radix enumeration of
+that group's variables).  A contraction with exactly one variable per group
+is a plain strided GEMM (and can use the tensor-core path); anything else
+(conv = implicit GEMM with M = (n, ho, wo), N = co, K = (ci, ki, kj), tiled
+nests whose M/N dims are origin + offset pairs, ...) uses offset tables.
 """
 from __future__ import annotations
 
+import numpy as np
+
 from .analysis import _mixed_radix_injective
-from .lift import BINF, LOAD, STORE, PURE_OPS, Aff, Ins
+from .lift import BINF, LOAD, PURE_OPS, RETURN_GPU, STORE, Ins
+
+_IGNORED = PURE_OPS | {RETURN_GPU}
 
 
-class GemmMatch:
-    __slots__ = ("A", "B", "C", "offA", "offB", "offC", "sA", "sB", "sC", "M", "N", "K")
+class ContractMatch:
+    """A recognised contraction: operands, groups and addressing."""
+
+    __slots__ = ("A", "B", "C", "dtype", "M", "N", "K", "m_vars", "n_vars", "k_vars",
+                 "tables", "strided", "offA", "offB", "offC", "sA", "sB", "sC")
 
     def __repr__(self):
-        return (f"GemmMatch(M={self.M}, N={self.N}, K={self.K}, sA={self.sA}, "
-                f"sB={self.sB}, sC={self.sC})")
+        return (f"ContractMatch({self.dtype}, M={self.M}, N={self.N}, K={self.K}, "
+                f"strided={self.strided})")
 
 
 def _straight_line(nodes):
     return all(isinstance(n, Ins) for n in nodes)
 
 
-def match_gemm(region, links, remainder, accesses):
-    """Return a GemmMatch for a fp32 C += A*B nest, else None."""
+def _table(region, vars_, off):
+    """Element offsets of one operand over the mixed-radix enumeration of vars_."""
+    t = np.zeros(1, dtype=np.int64)
+    for v in vars_:
+        lb, st, trip = v.static()
+        vals = off.t.get(v.id, 0) * (lb + st * np.arange(trip, dtype=np.int64))
+        t = (t[:, None] + vals[None, :]).reshape(-1)
+    return t
+
+
+def match_contraction(region, links, remainder, accesses):
+    """Return a ContractMatch for a C (+)= A*B nest, else None."""
     if not links or not _straight_line(remainder):
         return None
-    body = [n for n in remainder if n.op not in PURE_OPS or n.op == BINF]
+    body = [n for n in remainder if n.op not in _IGNORED or n.op == BINF]
     loads = [n for n in body if n.op == LOAD]
     binf = [n for n in body if n.op == BINF]
     stores = [n for n in body if n.op == STORE]
@@ -44,69 +69,99 @@ def match_gemm(region, links, remainder, accesses):
         return None
     st = stores[0]
     add = next((n for n in binf if n.dst == st.a), None)
-    if add is None or add.sub != 0 or not add.f32:
+    if add is None or add.sub != 0:
         return None
     mul = next((n for n in binf if n is not add), None)
-    if mul.sub != 2 or not mul.f32 or mul.dst not in (add.a, add.b):
+    if mul.sub != 2 or mul.f32 != add.f32 or mul.dst not in (add.a, add.b):
         return None
     load_of = {n.dst: n for n in loads}
     c_reg = add.b if mul.dst == add.a else add.a
     if c_reg not in load_of or mul.a not in load_of or mul.b not in load_of:
         return None
     lc, la, lb = load_of[c_reg], load_of[mul.a], load_of[mul.b]
+    # the C load must precede nothing that writes C: only one store exists and
+    # it consumes `add`, so the chain is c -> c + a*b.
     acc = {id(a.node): a for a in accesses}
     aS, aC, aA, aB = acc[id(st)], acc[id(lc)], acc[id(la)], acc[id(lb)]
     bufs = region.buffers
     if aS.slot != aC.slot or aS.offset is None or aS.offset != aC.offset:
         return None
-    if aA.offset is None or aB.offset is None:
+    if aA.offset is None or aB.offset is None or aA.slot == aS.slot or aB.slot == aS.slot:
         return None
-    C = bufs[aS.slot]
-    A, B = bufs[aA.slot], bufs[aB.slot]
-    if any(x.dtype != "f32" for x in (A, B, C)) or aA.slot == aS.slot or aB.slot == aS.slot:
+    C, A, B = bufs[aS.slot], bufs[aA.slot], bufs[aB.slot]
+    dtype = C.dtype
+    if dtype not in ("f32", "f64") or A.dtype != dtype or B.dtype != dtype:
         return None
+    if add.f32 != (dtype == "f32"):
+        return None
+
     vars_ = [v for link in links for v in link.vars]
-    roles = {"m": [], "n": [], "k": []}
+    groups = {"m": [], "n": [], "k": []}
     for v in vars_:
-        lb, step, trip = v.static()
+        lb_, step, trip = v.static()
         cc, ca, cb = (aS.offset.t.get(v.id, 0), aA.offset.t.get(v.id, 0),
                       aB.offset.t.get(v.id, 0))
-        if trip == 1 and not (cc or ca or cb):
-            continue
+        if trip == 1:
+            continue   # a constant: folded into the tables below
         if cc and ca and not cb:
-            roles["m"].append(v)
+            groups["m"].append(v)
         elif cc and cb and not ca:
-            roles["n"].append(v)
+            groups["n"].append(v)
         elif ca and cb and not cc:
-            roles["k"].append(v)
-        elif trip == 1:
-            continue
+            groups["k"].append(v)
         else:
-            return None
-    # an A-only / B-only operand pairing is symmetric: swap so A carries m
-    if any(len(r) != 1 for r in roles.values()):
+            return None   # batch dims, reductions into C, or unused loop vars
+    if not groups["k"]:
         return None
-    (vm,), (vn,), (vk,) = roles["m"], roles["n"], roles["k"]
-    g = GemmMatch()
+    # M / N: order by decreasing |C stride| so the last (fastest) index is the
+    # most contiguous in C; K: nest order (the reference's reduction order).
+    for key in ("m", "n"):
+        groups[key].sort(key=lambda v: -abs(aS.offset.t.get(v.id, 0) * v.static()[1]))
 
-    def stride(off, v):
-        return off.t.get(v.id, 0) * v.static()[1]
+    g = ContractMatch()
+    g.A, g.B, g.C, g.dtype = A, B, C, dtype
+    g.m_vars, g.n_vars, g.k_vars = groups["m"], groups["n"], groups["k"]
+    prod = lambda vs: int(np.prod([v.static()[2] for v in vs])) if vs else 1  # noqa: E731
+    g.M, g.N, g.K = prod(g.m_vars), prod(g.n_vars), prod(g.k_vars)
 
-    def base(off):
-        b = off.c
-        for vid, c in off.t.items():
-            b += c * region.vars[vid].static()[0]
-        return b
+    def const(off, used):
+        c = off.c
+        for vid, coef in off.t.items():
+            if vid not in used:
+                c += coef * region.vars[vid].static()[0]   # trip-1 vars
+        return c
 
-    g.A, g.B, g.C = A, B, C
-    g.sA = (stride(aA.offset, vm), stride(aA.offset, vk))
-    g.sB = (stride(aB.offset, vk), stride(aB.offset, vn))
-    g.sC = (stride(aS.offset, vm), stride(aS.offset, vn))
-    g.M, g.N, g.K = vm.static()[2], vn.static()[2], vk.static()[2]
-    g.offA, g.offB, g.offC = base(aA.offset), base(aB.offset), base(aS.offset)
-    if not _mixed_radix_injective([(abs(g.sC[0]), g.M), (abs(g.sC[1]), g.N)], 0):
+    used = {v.id for v in vars_ if v.static()[2] > 1}
+    cA, cB, cC = const(aA.offset, used), const(aB.offset, used), const(aS.offset, used)
+    a_m = _table(region, g.m_vars, aA.offset) + cA
+    a_k = _table(region, g.k_vars, aA.offset)
+    b_k = _table(region, g.k_vars, aB.offset) + cB
+    b_n = _table(region, g.n_vars, aB.offset)
+    c_m = _table(region, g.m_vars, aS.offset) + cC
+    c_n = _table(region, g.n_vars, aS.offset)
+    g.tables = (a_m, a_k, b_k, b_n, c_m, c_n)
+    # outputs must be distinct (writes of different (m, n) never collide)
+    terms = [(abs(aS.offset.t.get(v.id, 0) * v.static()[1]), v.static()[2])
+             for v in g.m_vars + g.n_vars]
+    if not _mixed_radix_injective(terms, 0):
+        return None
+    g.strided = len(g.m_vars) <= 1 and len(g.n_vars) <= 1 and len(g.k_vars) == 1
+    if g.strided:
+        def stride(off, vs):
+            return off.t.get(vs[0].id, 0) * vs[0].static()[1] if vs else 0
+        g.sA = (stride(aA.offset, g.m_vars), stride(aA.offset, g.k_vars))
+        g.sB = (stride(aB.offset, g.k_vars), stride(aB.offset, g.n_vars))
+        g.sC = (stride(aS.offset, g.m_vars), stride(aS.offset, g.n_vars))
+        g.offA, g.offB, g.offC = int(a_m[0] + a_k[0]), int(b_k[0] + b_n[0]), int(c_m[0] + c_n[0])
+    return g
+
+
+def match_gemm(region, links, remainder, accesses):
+    """Back-compat: a strided fp32 contraction only."""
+    g = match_contraction(region, links, remainder, accesses)
+    if g is None or not g.strided or g.dtype != "f32":
         return None
     return g
 
 
-__all__ = ["match_gemm", "GemmMatch"]
+__all__ = ["match_contraction", "match_gemm", "ContractMatch"]

@@ -63,19 +63,20 @@ class SimBackend:
             np.frombuffer(buf.data, dtype=_NP[buf.dtype])[:] = a
         self.dirty.clear()
 
-    def gemm(self, g, precision="exact"):
+    def contract(self, g, precision="exact"):
         assert precision == "exact", "the simulator models the exact path only"
-        self.launches.append("gemm")
+        self.launches.append("contract")
         A, B, C = self.arr(g.A), self.arr(g.B), self.arr(g.C)
-        m = np.arange(g.M)[:, None]
-        n = np.arange(g.N)[None, :]
-        coff = g.offC + m * g.sC[0] + n * g.sC[1]
-        acc = C[coff].astype(np.float32)
+        a_m, a_k, b_k, b_n, c_m, c_n = g.tables
+        dt = np.float32 if g.dtype == "f32" else np.float64
+        coff = c_m[:, None] + c_n[None, :]
+        acc = C[coff].astype(dt)
         for k in range(g.K):
-            a = A[g.offA + m * g.sA[0] + k * g.sA[1]].astype(np.float32)
-            b = B[g.offB + k * g.sB[0] + n * g.sB[1]].astype(np.float32)
-            acc = (acc + (a * b).astype(np.float32)).astype(np.float32)
+            a = A[a_m + a_k[k]].astype(dt)[:, None]
+            b = B[b_k[k] + b_n].astype(dt)[None, :]
+            acc = (acc + (a * b).astype(dt)).astype(dt)
         C[coff] = acc
+        return ["contract_exact"]
 
     def vm(self, r, prog, checked):
         self.launches.append(("vm", len(prog.band), checked))
