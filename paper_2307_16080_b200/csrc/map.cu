@@ -1,0 +1,144 @@
+// Pointwise nests on the B200: fill / copy / elementwise / broadcast-bias.
+//
+// Replaces run_tape on a region whose every loop variable is distributed
+// (the whole iteration box is race-free, analysis.choose_band) and whose body
+// is straight-line f32 code: loads, constants, add/sub/mul/div, stores
+// (reference interp/_evalpy.py:90-127; nests such as PAPER.md:431-441 fill /
+// copy, PAPER.md:455-462 bias, benchmarks/bench_interp.py:46-49 saxpy).
+//
+// Each operand is addressed affinely over the box: off = base + sum_d coef_d*i_d.
+// Vector path: the innermost box dimension is split into groups of 4 and every
+// operand is either contiguous (coef 1, 16-byte aligned) or broadcast (coef 0)
+// along it, so each thread moves 128-bit vectors; otherwise one element per
+// thread.  The per-element program runs in reference order with each f32 op
+// individually rounded (__f*_rn), so results are bit-identical to the
+// reference.  Grid: persistent, 148 SMs x 8 CTAs x 256 threads, grid-stride.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/b200k.h"
+
+namespace {
+
+constexpr int kMaxDims = 8;
+constexpr int kMaxOps = 8;
+constexpr int kMaxRegs = 8;
+constexpr int kMaxProg = 64;   // words
+constexpr int kMaxConst = 16;
+
+enum { M_LD = 0, M_CF = 1, M_BF = 2, M_ST = 3 };
+
+struct MapParams {
+  float *ptr[kMaxOps];
+  int64_t coef[kMaxOps][kMaxDims];
+  int64_t trip[kMaxDims];
+  int32_t prog[kMaxProg];
+  float consts[kMaxConst];
+  int32_t nd, nops, nwords;
+  int64_t total;   // work items (vectors or elements)
+};
+
+__device__ __forceinline__ float fop(int f, float a, float b) {
+  return f == 0 ? __fadd_rn(a, b) : f == 1 ? __fsub_rn(a, b) : f == 2 ? __fmul_rn(a, b)
+                                                                   : __fdiv_rn(a, b);
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(256) map_kernel(const __grid_constant__ MapParams p) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < p.total; w += stride) {
+    // decompose the work index over the box (innermost dim in vectors of 4)
+    int64_t rem = w;
+    int64_t off[kMaxOps];
+#pragma unroll
+    for (int k = 0; k < kMaxOps; ++k) off[k] = 0;
+    for (int d = p.nd - 1; d >= 0; --d) {
+      const int64_t trip = (VEC && d == p.nd - 1) ? p.trip[d] / 4 : p.trip[d];
+      int64_t i = rem % trip;
+      rem /= trip;
+      if (VEC && d == p.nd - 1) i *= 4;
+#pragma unroll
+      for (int k = 0; k < kMaxOps; ++k)
+        if (k < p.nops) off[k] += p.coef[k][d] * i;
+    }
+    float4 r[kMaxRegs];
+    for (int pc = 0; pc < p.nwords;) {
+      const int32_t w0 = p.prog[pc];
+      const int op = w0 & 0xff, dst = (w0 >> 8) & 0xff, a = (w0 >> 16) & 0xff,
+                b = (w0 >> 24) & 0xff;
+      switch (op) {
+        case M_LD: {
+          const float *src = p.ptr[a] + off[a];
+          if (VEC) {
+            if (p.coef[a][p.nd - 1] == 1) r[dst] = *reinterpret_cast<const float4 *>(src);
+            else { const float v = *src; r[dst] = make_float4(v, v, v, v); }
+          } else {
+            r[dst].x = *src;
+          }
+          pc += 1;
+          break;
+        }
+        case M_CF: {
+          const float c = p.consts[a];
+          r[dst] = make_float4(c, c, c, c);
+          pc += 1;
+          break;
+        }
+        case M_BF: {
+          const int f = p.prog[pc + 1];
+          const float4 x = r[a], y = r[b];
+          if (VEC) r[dst] = make_float4(fop(f, x.x, y.x), fop(f, x.y, y.y), fop(f, x.z, y.z),
+                                        fop(f, x.w, y.w));
+          else r[dst].x = fop(f, x.x, y.x);
+          pc += 2;
+          break;
+        }
+        default: {  // M_ST: operand a <- register dst
+          float *d = p.ptr[a] + off[a];
+          if (VEC) *reinterpret_cast<float4 *>(d) = r[dst];
+          else *d = r[dst].x;
+          pc += 1;
+          break;
+        }
+      }
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" int b200_map_f32(const int32_t *prog, int32_t n_words, const float *consts,
+                            int32_t n_consts, float *const *ptrs, const int64_t *coefs,
+                            int32_t n_ops, const int64_t *trips, int32_t nd, int32_t vector,
+                            void *stream) {
+  if (nd < 1 || nd > kMaxDims || n_ops < 1 || n_ops > kMaxOps || n_words > kMaxProg ||
+      n_consts > kMaxConst)
+    return B200_EINVAL;
+  MapParams p{};
+  int64_t total = 1;
+  for (int d = 0; d < nd; ++d) {
+    p.trip[d] = trips[d];
+    total *= trips[d];
+  }
+  if (total == 0) return B200_OK;
+  for (int k = 0; k < n_ops; ++k) {
+    p.ptr[k] = ptrs[k];
+    for (int d = 0; d < nd; ++d) p.coef[k][d] = coefs[k * nd + d];
+  }
+  for (int i = 0; i < n_words; ++i) p.prog[i] = prog[i];
+  for (int i = 0; i < n_consts; ++i) p.consts[i] = consts[i];
+  p.nd = nd;
+  p.nops = n_ops;
+  p.nwords = n_words;
+  if (vector) {
+    if (trips[nd - 1] % 4) return B200_EINVAL;
+    total /= 4;
+  }
+  p.total = total;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (vector) map_kernel<true><<<(unsigned)blocks, 256, 0, s>>>(p);
+  else map_kernel<false><<<(unsigned)blocks, 256, 0, s>>>(p);
+  return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
+}

@@ -18,8 +18,12 @@ scalars, calls, returns) and single-element loads/stores.  Every loop nest,
 ``scf.parallel`` and ``gpu.launch_func`` found there is a *region*: it is
 lifted (lift.py), analysed (analysis.py), matched against the kernel
 templates (templates.py) and executed on the GPU, either by a specialised
-kernel or by the device tape VM (csrc/vm.cu).  Nothing in a region runs on
-the CPU; there is no fallback.
+kernel (contraction, pointwise map) or by the device tape VM (csrc/vm.cu).
+Specialised plans are queued while only pure host scalar work separates
+them and are fused across regions (fusion.py) before launch — e.g. the
+Linear lowering's fill/copy/contraction/bias become one GEMM with an init
+value and a bias epilogue.  Nothing in a region runs on the CPU; there is
+no fallback.
 
 Install globally (the tuner calls run() without engine=, search.py:170,190):
 
@@ -31,12 +35,11 @@ from __future__ import annotations
 import math
 import os
 
-from . import analysis, templates, vmcode
+from . import analysis, fusion, templates, vmcode
 from .host import errors as _errors
-from .lift import (ALLOC, BINF, BINI, BOOKKEEPING, CALL, CAST, CMPF, CMPI, CONST,
-                   DEALLOC, IF_FALSE, JUMP, LAUNCH, LOAD, LOOP_INIT_A, LOOP_INIT_S,
-                   PARALLEL, RETURN, RETURN_GPU, STORE, Launch, Unsupported,
-                   evaluate, lift_region)
+from .lift import (ALLOC, BINF, BINI, CALL, CAST, CMPF, CMPI, CONST, DEALLOC, IF_FALSE,
+                   JUMP, LAUNCH, LOAD, LOOP_INIT_A, LOOP_INIT_S, PARALLEL, RETURN,
+                   RETURN_GPU, STORE, Launch, Unsupported, evaluate, lift_region)
 from .runtime import DeviceBackend
 
 ENGINE_NAME = "b200"
@@ -46,19 +49,23 @@ ENGINE_NAME = "b200"
 # tf32 / bf16 and contracted on the tcgen05 tensor cores with fp32
 # accumulation (tolerance: DESIGN.md, tests/test_gpu_tc.py).
 PRECISION = os.environ.get("B200_PRECISION", "exact")
+# Cross-region fusion of queued plans (B200_FUSE=0 disables, for A/B tests).
+FUSE = os.environ.get("B200_FUSE", "1") != "0"
+
+# kernel choice of the last run (tests and bench inspect these)
+last_plan = []
 
 
-def configure(precision=None):
-    """Select the contraction precision for subsequent runs."""
-    global PRECISION
+def configure(precision=None, fuse=None):
+    """Select the contraction precision / fusion for subsequent runs."""
+    global PRECISION, FUSE
     if precision is not None:
         if precision not in ("exact", "tf32", "bf16"):
             raise ValueError(f"unknown precision {precision!r}")
         PRECISION = precision
-    return {"precision": PRECISION}
-
-# kernel choice statistics of the last run (tests and bench inspect these)
-last_plan = []
+    if fuse is not None:
+        FUSE = bool(fuse)
+    return {"precision": PRECISION, "fuse": FUSE}
 
 
 class ExecContext:
@@ -100,6 +107,7 @@ class _Run:
         self.ctx = ctx
         self.be = backend if backend is not None else DeviceBackend()
         self.plan = []
+        self.pending = []     # queued MapItem / ContractItem, program order
 
     # -- host walk (mirrors interp/_evalpy.py:81-232 for top-level scalars) --
     def exec_tape(self, code, regs, tally):
@@ -118,6 +126,8 @@ class _Run:
                 self.region(code, pc, pc + 1, regs, tally)
                 pc += 1
                 continue
+            if op in (LOAD, STORE):
+                self.flush_pending()   # the host touches device data
             tally[op] += 1
             if op == CONST:
                 regs[ins[1]] = ins[2]
@@ -199,14 +209,17 @@ class _Run:
             r = lift_region(self.program, code, start, end, regs)
             evaluate(r)
         except Unsupported as exc:
+            self.flush_pending()
             raise E.ModeUnsupported(f"b200 engine: {exc}") from None
         if r.has_launch and self.ctx.mode != "gpu_emulated":
+            self.flush_pending()
             loc = _first_launch_loc(r.tree)
             raise E.ModeUnsupported(
                 f"gpu.launch_func needs gpu_emulated mode, not {self.ctx.mode!r}{_where(loc)}")
         try:
             accesses = analysis.collect_accesses(r)
         except Unsupported as exc:
+            self.flush_pending()
             raise E.ModeUnsupported(f"b200 engine: {exc}") from None
         links, remainder = analysis.chain_of(r)
         safe = analysis.statically_in_bounds(r, accesses) and not analysis.invalid_steps(r)
@@ -219,11 +232,17 @@ class _Run:
         if safe and st is not None:
             g = templates.match_contraction(r, links, remainder, accesses)
             if g is not None:
-                kernels = self.be.contract(g, PRECISION)
                 _add(tally, st)
-                self.plan.append((kernels[-1], g.M, g.N, g.K))
+                self.pending.append(fusion.ContractItem(g))
+                return
+            mm = templates.match_map(r, links, remainder, accesses, band)
+            if mm is not None:
+                _add(tally, st)
+                self.pending.append(fusion.MapItem(mm))
                 return
 
+        # generic tier: the device tape VM (runs in order after queued plans)
+        self.flush_pending()
         count = st is None
         try:
             prog = vmcode.encode(r, links, remainder, band, count, checked=not safe)
@@ -241,6 +260,26 @@ class _Run:
             _add(tally, st)
         self.plan.append(("vm", len(band), "checked" if not safe else "unchecked",
                           "count" if count else "static"))
+
+    def flush_pending(self):
+        if not self.pending:
+            return
+        items = fusion.fuse(self.pending) if FUSE else self.pending
+        self.pending = []
+        for it in items:
+            if isinstance(it, fusion.ContractItem):
+                kernels = self.be.contract(it.g, PRECISION, init=it.init,
+                                           init_value=it.init_value, bias=it.bias,
+                                           bias_base=it.bias_base,
+                                           bias_stride=it.bias_stride)
+                g = it.g
+                self.plan.append((kernels[-1], g.M, g.N, g.K) +
+                                 ((tuple(it.fused),) if it.fused else ()))
+            else:
+                m = it.m
+                self.be.map(m)
+                self.plan.append(("map_" + m.kind, tuple(m.trips),
+                                  "vec4" if m.vector else "scalar"))
 
     def raise_fault(self, r, prog, fault):
         code, slot, index, extent, loc = fault
@@ -295,8 +334,10 @@ def run_tape(program, code, regs, tally, ctx, backend=None):
     run = _Run(program, ctx, backend)
     try:
         rets = run.exec_tape(code, regs, tally)
+        run.flush_pending()
     except BaseException:
         try:
+            run.flush_pending()
             run.be.flush()
         finally:
             last_plan = run.plan
@@ -319,4 +360,4 @@ def install():
     return machine
 
 
-__all__ = ["ExecContext", "run_tape", "install", "ENGINE_NAME"]
+__all__ = ["ExecContext", "run_tape", "install", "configure", "ENGINE_NAME"]

@@ -1,0 +1,156 @@
+"""Cross-region fusion of queued kernel plans (the Linear lowering and friends).
+
+The Linear(32,32) lowering is four top-level nests:
+
+    fill  tmp[i,j] = 0.0                          (map, kind "fill")
+    copy  out[i,j] = tmp[i,j]                      (map, kind "copy")
+    mm    out[i,j] = out[i,j] + x[i,k] * wt[k,j]   (contraction)
+    bias  out[i,j] = out[i,j] + bias[j]            (map, kind "ewise")
+
+Executed naively that is four launches and three extra passes over `out`.
+Because each of these nests is race-free and fully covers its output, their
+composition is exactly
+
+    tmp = fill(0.0);  out[i,j] = ((0.0 + x.w chain in k order) + bias[j])
+
+so the copy disappears, the fill value becomes the contraction's initial
+value and the bias becomes its epilogue — every f32 op still individually
+rounded in reference order (init -> k-ascending chain -> + bias), hence
+bit-identical on the exact path.  `tmp` is still filled because it is a
+live (observable) buffer.  A fill immediately overwritten by a covering
+contraction (fill(out); mm(out)) is dropped entirely.
+"""
+from __future__ import annotations
+
+import math
+
+
+class MapItem:
+    __slots__ = ("m", "tally")
+
+    def __init__(self, m):
+        self.m = m
+
+
+class ContractItem:
+    __slots__ = ("g", "init", "init_value", "bias", "bias_base", "bias_stride", "fused")
+
+    def __init__(self, g):
+        self.g = g
+        self.init = 0
+        self.init_value = 0.0
+        self.bias = None
+        self.bias_base = 0
+        self.bias_stride = 0
+        self.fused = []
+
+
+def _size(buf):
+    return math.prod(buf.shape)
+
+
+def _covers(m, buf):
+    """The map's store writes every element of buf exactly once."""
+    return math.prod(m.trips) == _size(buf)
+
+
+def _fill(item):
+    """(buffer, value) if item is a full-buffer constant fill."""
+    if isinstance(item, MapItem) and item.m.kind == "fill" and len(item.m.buffers) == 1:
+        buf = item.m.buffers[0]
+        if _covers(item.m, buf):
+            return buf, item.m.consts[0]
+    return None
+
+
+def _copy(item):
+    """(dst, src) if item is a full-buffer copy."""
+    if isinstance(item, MapItem) and item.m.kind == "copy" and len(item.m.buffers) == 2:
+        src, dst = item.m.buffers
+        if _covers(item.m, dst) and src is not dst:
+            return dst, src
+    return None
+
+
+def _contract_covers(item, buf):
+    g = item.g
+    return g.C is buf and g.M * g.N == _size(buf)
+
+
+def _bias(citem, item):
+    """(bias buffer, base, stride) if item adds a per-column vector to the
+    strided GEMM output of citem over the whole output."""
+    g = citem.g
+    if not isinstance(item, MapItem) or item.m.kind != "ewise" or not g.strided:
+        return None
+    m = item.m
+    if len(m.buffers) != 3 or len(m.trips) != 2:
+        return None
+    o_ld, b_ld, o_st = m.buffers
+    prog = m.prog
+    # LD r0<-op0 ; LD r1<-op1 ; BF add r2 = r0+r1 | r1+r0 ; ST op2<-r2
+    if len(prog) != 5 or prog[0] & 0xFF != 0 or prog[1] & 0xFF != 0 or \
+            prog[2] & 0xFF != 2 or prog[3] != 0 or prog[4] & 0xFF != 3:
+        return None
+    if o_ld is not g.C or o_st is not g.C or b_ld is g.C:
+        return None
+    if m.bases[0] != m.bases[2] or m.coefs[0] != m.coefs[2] or not _covers(m, g.C):
+        return None
+    if b_ld.dtype != g.C.dtype:
+        return None
+    # identify the map dims with the GEMM's m / n by their stride in C
+    (ci, cj), (ti, tj) = m.coefs[0], m.trips
+    if (ci, ti, cj, tj) == (g.sC[0], g.M, g.sC[1], g.N):
+        m_dim, n_dim = 0, 1
+    elif (cj, tj, ci, ti) == (g.sC[0], g.M, g.sC[1], g.N):
+        m_dim, n_dim = 1, 0
+    else:
+        return None
+    if m.bases[0] != g.offC or m.coefs[1][m_dim] != 0:
+        return None
+    return b_ld, m.bases[1], m.coefs[1][n_dim]
+
+
+def fuse(items):
+    """Peephole-fuse a queue of MapItem / ContractItem in program order."""
+    out = []
+    i = 0
+    n = len(items)
+    while i < n:
+        it = items[i]
+        f = _fill(it)
+        # fill(T); copy(O <- T); contract(O)  ->  fill(T); contract(O, init)
+        if f is not None and i + 2 < n:
+            c = _copy(items[i + 1])
+            nxt = items[i + 2]
+            if c is not None and c[1] is f[0] and isinstance(nxt, ContractItem) and \
+                    _contract_covers(nxt, c[0]) and nxt.g.dtype == "f32":
+                out.append(it)
+                nxt.init, nxt.init_value = 1, f[1]
+                nxt.fused += ["copy", "init"]
+                items[i + 2] = nxt
+                i += 2
+                continue
+        # fill(O); contract(O)  ->  contract(O, init)
+        if f is not None and i + 1 < n and isinstance(items[i + 1], ContractItem) and \
+                _contract_covers(items[i + 1], f[0]) and items[i + 1].g.dtype == "f32":
+            nxt = items[i + 1]
+            nxt.init, nxt.init_value = 1, f[1]
+            nxt.fused += ["fill"]
+            i += 1
+            continue
+        # contract(O); bias(O)  ->  contract(O, bias)
+        if isinstance(it, ContractItem) and it.bias is None and i + 1 < n:
+            b = _bias(it, items[i + 1])
+            if b is not None:
+                it.bias, it.bias_base, it.bias_stride = b
+                it.fused += ["bias"]
+                out.append(it)
+                i += 2
+                continue
+        out.append(it)
+        i += 1
+    return out
+
+
+__all__ = ["MapItem", "ContractItem", "fuse"]

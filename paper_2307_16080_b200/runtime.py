@@ -48,6 +48,7 @@ SIGNATURES = {
     "b200_contract_exact": [_I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64,
                             _I32, _I32, _I32, ctypes.c_double, _P, _I64, _P],
     "b200_pack_operand": [_I32, _P, _I64, _I64, _P, _I64, _I64, _P],
+    "b200_map_f32": [_P, _I32, _P, _I32, _P, _P, _I32, _P, _I32, _I32, _P],
     "b200_gemm_tc": [_I32, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I32, _F32, _P,
                      _I64, _I32, _I32, _P],
 }
@@ -229,14 +230,19 @@ class DeviceBackend:
     def flush(self):
         self.stage.flush()
 
-    def contract(self, g, precision="exact"):
-        """Run a templates.ContractMatch; returns the kernel names launched."""
+    def contract(self, g, precision="exact", init=0, init_value=0.0, bias=None, bias_base=0,
+                 bias_stride=0):
+        """Run a templates.ContractMatch (+ fused init / bias); returns kernel names."""
         s = self.stage
         tA, tB, tC = s.tensor(g.A), s.tensor(g.B), s.tensor(g.C)
+        esz = 4 if g.dtype == "f32" else 8
+        bias_ptr = s.tensor(bias).data_ptr() + esz * bias_base if bias is not None else None
         if g.strided and g.dtype == "f32":
             return launch_gemm(s.lib, precision, tA.data_ptr() + 4 * g.offA, g.sA,
                                tB.data_ptr() + 4 * g.offB, g.sB, tC.data_ptr() + 4 * g.offC,
-                               g.sC, g.M, g.N, g.K, s.stream_ptr)
+                               g.sC, g.M, g.N, g.K, s.stream_ptr, init=init,
+                               init_value=init_value, bias_ptr=bias_ptr,
+                               bias_stride=bias_stride)
         torch = s.torch
         tabs = [torch.from_numpy(t).to("cuda") for t in g.tables]
         a_m, a_k, b_k, b_n, c_m, c_n = g.tables
@@ -247,10 +253,25 @@ class DeviceBackend:
             DT_CODE[g.dtype], P(tA.data_ptr()), P(tabs[0].data_ptr()), P(tabs[1].data_ptr()),
             P(tB.data_ptr()), P(tabs[2].data_ptr()), P(tabs[3].data_ptr()),
             P(tC.data_ptr()), P(tabs[4].data_ptr()), P(tabs[5].data_ptr()),
-            g.M, g.N, g.K, a_k_fast, b_n_fast, 0, 0.0, None, 0, s.stream_ptr),
+            g.M, g.N, g.K, a_k_fast, b_n_fast, init, init_value,
+            P(bias_ptr) if bias_ptr else None, bias_stride, s.stream_ptr),
             "b200_contract_exact")
         self._keep = tabs   # tables must outlive the asynchronous kernel
         return ["contract_exact"]
+
+    def map(self, m):
+        """Run a templates.MapMatch through b200_map_f32."""
+        s = self.stage
+        nd, nops = len(m.trips), len(m.buffers)
+        ptrs = (ctypes.c_void_p * nops)(*[s.tensor(b).data_ptr() + 4 * base
+                                          for b, base in zip(m.buffers, m.bases)])
+        coefs = (ctypes.c_int64 * (nops * nd))(*[c for row in m.coefs for c in row])
+        trips = (ctypes.c_int64 * nd)(*m.trips)
+        prog = (ctypes.c_int32 * len(m.prog))(*m.prog)
+        consts = (ctypes.c_float * max(1, len(m.consts)))(*m.consts)
+        check(s.lib.b200_map_f32(prog, len(m.prog), consts, len(m.consts), ptrs, coefs, nops,
+                                 trips, nd, int(m.vector), s.stream_ptr), "b200_map_f32")
+        return ["map_f32"]
 
     def vm(self, r, prog, checked):
         """Run a VM program; returns (device tally | None, fault | None)."""

@@ -156,6 +156,104 @@ def match_contraction(region, links, remainder, accesses):
     return g
 
 
+class MapMatch:
+    """A pointwise f32 nest: box dims, operands, straight-line program."""
+
+    __slots__ = ("trips", "buffers", "bases", "coefs", "prog", "consts", "vector", "kind")
+
+    def __repr__(self):
+        return f"MapMatch({self.kind}, trips={self.trips}, ops={len(self.buffers)})"
+
+
+M_LD, M_CF, M_BF, M_ST = 0, 1, 2, 3
+
+
+def match_map(region, links, remainder, accesses, band):
+    """Straight-line f32 body over a fully distributed static box."""
+    from .lift import CONST
+
+    if not links or not _straight_line(remainder):
+        return None
+    box = [v for link in links for v in link.vars]
+    if set(band) != {v.id for v in box}:
+        return None
+    dims = [v for v in box if v.static()[2] > 1]
+    if not dims or len(dims) > 8:
+        return None
+    acc_of = {id(a.node): a for a in accesses}
+    m = MapMatch()
+    m.trips = [v.static()[2] for v in dims]
+    m.buffers, m.bases, m.coefs, m.prog, m.consts = [], [], [], [], []
+    regs = {}
+
+    def reg_of(v):
+        return regs.get(v)
+
+    def new_reg(v):
+        if len(regs) >= 8:
+            raise ValueError
+        regs[v] = len(regs)
+        return regs[v]
+
+    def operand(a):
+        buf = region.buffers[a.slot]
+        if buf.dtype != "f32" or a.offset is None or len(m.buffers) >= 8:
+            raise ValueError
+        base = a.offset.c
+        for vid, c in a.offset.t.items():
+            base += c * region.vars[vid].static()[0]
+        m.buffers.append(buf)
+        m.bases.append(base)
+        m.coefs.append([a.offset.t.get(v.id, 0) * v.static()[1] for v in dims])
+        return len(m.buffers) - 1
+
+    n_mem = 0
+    try:
+        for n in remainder:
+            if n.op == LOAD:
+                k = operand(acc_of[id(n)])
+                m.prog.append(M_LD | (new_reg(n.dst) << 8) | (k << 16))
+                n_mem += 1
+            elif n.op == STORE:
+                k = operand(acc_of[id(n)])
+                r = reg_of(n.a)
+                if r is None:
+                    return None
+                m.prog.append(M_ST | (r << 8) | (k << 16))
+                n_mem += 1
+            elif n.op == CONST and isinstance(n.value, float):
+                if len(m.consts) >= 16:
+                    return None
+                m.consts.append(n.value)
+                m.prog.append(M_CF | (new_reg(n.dst) << 8) | ((len(m.consts) - 1) << 16))
+            elif n.op == BINF:
+                a, b = reg_of(n.a), reg_of(n.b)
+                if a is None or b is None or not n.f32:
+                    return None
+                m.prog.append(M_BF | (new_reg(n.dst) << 8) | (a << 16) | (b << 24))
+                m.prog.append(n.sub)
+            elif n.op in _IGNORED:
+                continue   # index arithmetic: folded into the affine operands
+            else:
+                return None
+    except ValueError:
+        return None
+    ops_seq, pc = [], 0
+    while pc < len(m.prog):
+        op = m.prog[pc] & 0xFF
+        ops_seq.append(op)
+        pc += 2 if op == M_BF else 1
+    if M_ST not in ops_seq or len(m.prog) > 64:
+        return None
+    inner = len(dims) - 1
+    m.vector = m.trips[inner] % 4 == 0 and all(
+        c[inner] in (0, 1) and (c[inner] == 0 or (b % 4 == 0 and all(x % 4 == 0 for x in c[:inner])))
+        for b, c in zip(m.bases, m.coefs))
+    m.kind = ("fill" if ops_seq == [M_CF, M_ST] else
+              "copy" if ops_seq == [M_LD, M_ST] else "ewise")
+    return m
+
+
 def match_gemm(region, links, remainder, accesses):
     """Back-compat: a strided fp32 contraction only."""
     g = match_contraction(region, links, remainder, accesses)
@@ -164,4 +262,4 @@ def match_gemm(region, links, remainder, accesses):
     return g
 
 
-__all__ = ["match_contraction", "match_gemm", "ContractMatch"]
+__all__ = ["match_contraction", "match_gemm", "match_map", "ContractMatch", "MapMatch"]

@@ -63,20 +63,53 @@ class SimBackend:
             np.frombuffer(buf.data, dtype=_NP[buf.dtype])[:] = a
         self.dirty.clear()
 
-    def contract(self, g, precision="exact"):
+    def contract(self, g, precision="exact", init=0, init_value=0.0, bias=None, bias_base=0,
+                 bias_stride=0):
         assert precision == "exact", "the simulator models the exact path only"
         self.launches.append("contract")
         A, B, C = self.arr(g.A), self.arr(g.B), self.arr(g.C)
         a_m, a_k, b_k, b_n, c_m, c_n = g.tables
         dt = np.float32 if g.dtype == "f32" else np.float64
         coff = c_m[:, None] + c_n[None, :]
-        acc = C[coff].astype(dt)
+        acc = np.full(coff.shape, init_value, dtype=dt) if init else C[coff].astype(dt)
         for k in range(g.K):
             a = A[a_m + a_k[k]].astype(dt)[:, None]
             b = B[b_k[k] + b_n].astype(dt)[None, :]
             acc = (acc + (a * b).astype(dt)).astype(dt)
+        if bias is not None:
+            bv = self.arr(bias)[bias_base + bias_stride * np.arange(g.N)].astype(dt)
+            acc = (acc + bv[None, :]).astype(dt)
         C[coff] = acc
         return ["contract_exact"]
+
+    def map(self, m):
+        """b200_map_f32 semantics: every box point runs the program in order."""
+        self.launches.append(("map", m.kind, m.vector))
+        arrs = [self.arr(b) for b in m.buffers]
+        grids = np.meshgrid(*[np.arange(t) for t in m.trips], indexing="ij")
+        offs = [base + sum(c * g.reshape(-1) for c, g in zip(coefs, grids))
+                for base, coefs in zip(m.bases, m.coefs)]
+        regs = {}
+        pc = 0
+        with np.errstate(all="ignore"):
+            while pc < len(m.prog):
+                w = m.prog[pc]
+                op, dst, a, b = w & 0xFF, (w >> 8) & 0xFF, (w >> 16) & 0xFF, (w >> 24) & 0xFF
+                if op == 0:
+                    regs[dst] = arrs[a][offs[a]].astype(np.float32)
+                    pc += 1
+                elif op == 1:
+                    regs[dst] = np.float32(m.consts[a])
+                    pc += 1
+                elif op == 2:
+                    f = m.prog[pc + 1]
+                    x, y = np.float32(regs[a]), np.float32(regs[b])
+                    regs[dst] = [x + y, x - y, x * y, x / y][f].astype(np.float32)
+                    pc += 2
+                else:
+                    arrs[a][offs[a]] = regs[dst]
+                    pc += 1
+        return ["map_f32"]
 
     def vm(self, r, prog, checked):
         self.launches.append(("vm", len(prog.band), checked))
