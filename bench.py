@@ -1,36 +1,43 @@
-"""Benchmark: GFLOP/s of the B200 backend on BASELINE.json's matmul config.
+"""Benchmark: GFLOP/s of the B200 backend on BASELINE.json's configs.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--precision bf16|tf32|exact]
+                    [--workload mm|conv|ls|linear32|ewise] [--precision bf16|tf32|exact]
 
-Workload (BASELINE.json configs[1]): ``linalg.matmul`` 4096x4096x4096, the
-reference's matmul nest (reference tests/kernels.py:24-38) at full size:
-C[i,k] += A[i,j] * B[j,k] on f32 Buffers.  A step is one pass of the hot
-path over one batch: one C += A.B contraction, including the operand
-packing the tensor-core path needs (f32 -> bf16/tf32, B transposed to
-K-major).  Data: U(-1,1) f32 from torch.Generator().manual_seed(arg index)
-(SURVEY.md §8d).
+Default workload (BASELINE.json configs[1]): ``linalg.matmul`` 4096x4096x4096
+— the reference's matmul nest (reference tests/kernels.py:24-38) at full
+size, C[i,k] += A[i,j] * B[j,k] on f32 Buffers, bf16 tensor-core precision.
+Other workloads (configs[0], [2], [3]): ``linear32`` (Linear(32,32) lowering),
+``conv`` (conv_2d_nchw_fchw N=256 C=F=64 56x56 3x3, batch-sharded),
+``ls`` (Linear stack 65536x1024->4096->1024, batch-sharded), ``ewise``
+(y = y + 2x over 4096x4096 f32).
 
-* ``value``  — device-resident: the C-ABI sequence (pack, pack, tcgen05
-  GEMM) on HBM tensors, timed with CUDA events on the launch stream; inputs
-  (3 x 64 MiB f32) are larger than the 126 MB L2.
-* ``roofline`` — the dominant kernel (b200_gemm_tc) alone: algorithmic
-  2*M*N*K flops per launch / its average CUDA-event duration inside the
-  timed region, against MEASURED_PEAKS.json bf16 (tf32: half of it).
+A step is one pass of the hot path over one batch: one run of the nest.
+Data: U(-1,1) f32 from torch.Generator().manual_seed(arg index).
+
+* ``value``  — device-resident: the engine's own launch sequence for the
+  nest (recorded once by paper_2307_16080_b200.Session, then replayed),
+  timed with CUDA events on the launch stream; every workload except
+  linear32 has inputs larger than the 126 MB L2.
+* ``roofline`` — the dominant kernel family of that sequence, timed per
+  launch with CUDA events inside an instrumented replay: algorithmic flops
+  (or bytes) / time, against MEASURED_PEAKS.json.
 * ``e2e``    — through the reference-facing plugin: staircase's own
-  ``machine.run(module, "mm", [A, B, C], engine=b200)`` with host Buffers;
-  the H2D of A, B, C and the D2H of C are inside the timed region.
+  ``machine.run(module, name, host_buffers, engine=b200)``; the H2D of every
+  argument and the D2H of every written buffer are in the timed region.
 * ``cpu_baseline`` — the reference executor itself (baseline/_ref, compiled
-  _evalcy engine) on a 1x4096x256 slice of the same nest (same loop
-  structure and reduction length), 1 core; its rate extrapolates.
+  _evalcy engine) on a thin slice of the same nest (same loop structure and
+  reduction length), 1 core; its rate extrapolates to the full size.
 * ``--impl reference`` — rank 0 times that reference CPU path per step.
 
-Multi-GPU (torchrun): every rank runs its own 4096^3 matmul (weak scaling,
-no data-path collective); time is the max over ranks.
+Multi-GPU (torchrun): mm / linear32 / ewise run one replica per rank (weak
+scaling); conv and ls shard the batch (strong scaling, contiguous ranges as
+in worksharing, interp/_evalpy.py:279).  No data-path collective: one NCCL
+all_gather of per-rank output checksums after timing.  Time = max over ranks.
 """
 import argparse
 import ctypes
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -44,65 +51,92 @@ from paper_2307_16080_b200.host import ensure_staircase  # noqa: E402
 
 ensure_staircase()
 
-from staircase import F32, MemRef, staged  # noqa: E402
-
-M = N = K = 4096
-FLOP = 2.0 * M * N * K
+import bench_kernels as bk  # noqa: E402
 
 
-@staged(range_ctor="affine_for")
-def mm(A: MemRef[(4096, 4096), F32], B: MemRef[(4096, 4096), F32],
-       C: MemRef[(4096, 4096), F32]):
-    for i in range(4096):
-        for j in range(4096):
-            for k in range(4096):
-                a = A[i, j]
-                b = B[j, k]
-                c = C[i, k]
-                d = a * b
-                e = c + d
-                C[i, k] = e
+# -- workloads -------------------------------------------------------------------
+
+class Workload:
+    def __init__(self, name, world):
+        self.name = name
+        self.world = world
+        if name == "mm":
+            self.fn = bk.mm4096
+            self.flops = 2.0 * 4096 ** 3
+            self.scaling = "weak"
+            self.desc = "linalg.matmul 4096x4096x4096, C += A.B on f32 buffers"
+            self.slice = (bk.mm_slice, 2.0 * 4096 * 256, "1x4096x256 slice of the matmul nest")
+            self.default_precision = "bf16"
+        elif name == "conv":
+            nb = 256 // world
+            self.fn = bk.make_conv(nb)
+            self.flops = 2.0 * nb * 64 * 56 * 56 * 64 * 9
+            self.scaling = "strong"
+            self.desc = (f"conv_2d_nchw_fchw N=256 (this rank: {nb}) C=F=64 58x58 pre-padded "
+                         f"-> 56x56, 3x3, f32")
+            self.slice = (bk.conv_slice, 2.0 * 2 * 8 * 56 * 64 * 9,
+                          "1x2x8x56 outputs of the conv nest (C=64, 3x3)")
+            self.default_precision = "exact"
+        elif name == "ls":
+            rows = 65536 // world
+            self.fn = bk.make_linear_stack(rows)
+            self.flops = 2.0 * rows * (1024 * 4096 * 2) + 2.0 * rows * (4096 + 1024)
+            self.scaling = "strong"
+            self.desc = (f"Linear stack 65536 (this rank: {rows}) x 1024 -> 4096 -> 1024, "
+                         f"fill + contraction + bias nests")
+            self.slice = (bk.make_linear_stack(1), 2.0 * (1024 * 4096 * 2),
+                          "1 row through both Linear lowerings")
+            self.default_precision = "bf16"
+        elif name == "linear32":
+            self.fn = bk.linear32
+            self.flops = 2.0 * 32 ** 3 + 32 * 32
+            self.scaling = "weak"
+            self.desc = "torch.nn.Linear(32,32) lowering: fill + copy + 32^3 contraction + bias"
+            self.slice = (bk.linear32, self.flops, "the full Linear(32,32) lowering")
+            self.default_precision = "exact"
+        elif name == "ewise":
+            self.fn = bk.saxpy4k
+            self.flops = 2.0 * 4096 * 4096
+            self.bytes = 3 * 4096 * 4096 * 4
+            self.scaling = "weak"
+            self.desc = "elementwise y = y + 2x over 4096x4096 f32"
+            self.slice = (bk.saxpy_slice, 2.0 * 16 * 4096, "16x4096 rows of the same nest")
+            self.default_precision = "exact"
+        else:
+            raise SystemExit(f"unknown workload {name!r}")
+
+    def shapes(self):
+        return [tuple(a.type.shape) for a in self.fn.func_op.body().args]
 
 
-@staged(range_ctor="affine_for")
-def mm_slice(A: MemRef[(1, 4096), F32], B: MemRef[(4096, 256), F32],
-             C: MemRef[(1, 256), F32]):
-    for i in range(1):
-        for j in range(4096):
-            for k in range(256):
-                a = A[i, j]
-                b = B[j, k]
-                c = C[i, k]
-                d = a * b
-                e = c + d
-                C[i, k] = e
-
-
-def host_inputs(shapes, dtype="f32"):
+def host_inputs(fn, seed_base=0):
     import torch
     from staircase.interp import Buffer
 
     out = []
-    for seed, shape in enumerate(shapes):
-        g = torch.Generator().manual_seed(seed)
+    for i, a in enumerate(fn.func_op.body().args):
+        shape = tuple(a.type.shape)
+        g = torch.Generator().manual_seed(seed_base + i)
         t = torch.rand(shape, generator=g, dtype=torch.float32) * 2 - 1
-        out.append(Buffer(shape, dtype, t.numpy().tobytes()))
+        out.append(Buffer(shape, "f32", t.numpy().tobytes()))
     return out
 
 
-def reference_slice_rate():
-    """GFLOP/s of the reference's compiled executor on the 1x4096x256 slice."""
+def reference_rate(wl, repeats=3):
+    """GFLOP/s of the reference's compiled executor on the workload's slice."""
     from staircase.interp import _evalcy, machine
 
+    fn, flops, _ = wl.slice
     times = []
-    for _ in range(3):
-        args = host_inputs([(1, 4096), (4096, 256), (1, 256)])
-        _, stats = machine.run(mm_slice.module, "mm_slice", args, engine=_evalcy)
+    for _ in range(repeats):
+        args = host_inputs(fn)
+        _, stats = machine.run(fn.module, fn.__name__, args, engine=_evalcy)
         times.append(stats.wall_time)
     t = statistics.median(times)
-    flops = 2.0 * 1 * 4096 * 256
     return flops / t / 1e9, t
 
+
+# -- measurement helpers ----------------------------------------------------------
 
 class Clocks:
     """nvidia-smi sampler for the timed region (B200_PROFILING.md recipe)."""
@@ -187,6 +221,19 @@ def max_over_ranks(x, world):
     return float(t.item())
 
 
+def gather_checksums(value, world):
+    """The only collective: one NCCL all_gather of per-rank result checksums."""
+    if world == 1:
+        return [value]
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    out = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(out, t)
+    return [float(x.item()) for x in out]
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -194,36 +241,43 @@ def load_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
-def load_traffic(precision):
-    """dram bytes per GEMM launch from the committed ncu --set full summary."""
+def load_traffic(key):
+    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(path):
-        return json.load(open(path)).get(f"gemm_{precision}")
+        return json.load(open(path)).get(key)
     return None
 
+
+KERNEL_OF = {"b200_gemm_tc": "gemm", "b200_gemm_f32_exact": "gemm",
+             "b200_contract_exact": "contract", "b200_map_f32": "map", "b200_vm_run": "vm",
+             "b200_pack_operand": "pack"}
+
+
+# -- arms ----------------------------------------------------------------------------
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    rates = []
+    wl = Workload(args.workload, 1)
     for _ in range(args.warmup):
-        reference_slice_rate()
+        reference_rate(wl, repeats=1)
+    rates = []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        rate, _ = reference_slice_rate()
+        rate, _ = reference_rate(wl, repeats=1)
         rates.append(rate)
     wall = time.perf_counter() - t0
     value = statistics.median(rates)
     line = {
-        "impl": "reference", "metric": "GFLOP/s (matmul 4096^3)", "value": value,
+        "impl": "reference", "metric": f"GFLOP/s ({args.workload})", "value": value,
         "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "linalg.matmul 4096x4096x4096 (reference CPU executor on a "
-                               "1x4096x256 slice of the nest, rate extrapolates)"},
+        "scaling": wl.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": wl.desc + " (reference CPU executor on a slice; "
+                                         "rate extrapolates)"},
         "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": 1, "kind": "reference",
-                         "sample": "1x4096x256 slice of the 4096^3 matmul nest, "
-                                   "staircase _evalcy, median of 3 runs per step"},
+                         "sample": wl.slice[2] + ", staircase _evalcy, one run per step"},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -238,118 +292,123 @@ def run_ours(args, rank, world, local):
     from staircase.interp import machine
 
     lib = runtime.load_library()
-    dev = torch.device("cuda", local)
-    tens = []
-    for seed, shape in enumerate([(M, K), (K, N), (M, N)]):
-        g = torch.Generator().manual_seed(seed)
-        tens.append((torch.rand(shape, generator=g) * 2 - 1).to(dev))
-    A, B, C = tens
+    wl = Workload(args.workload, world)
+    prec = args.precision or wl.default_precision
+    b2.configure(precision=prec)
+    fn = wl.fn
+    name = fn.__name__
+
+    # device-resident: record the engine's plan once, replay it
+    sess = b2.Session()
+    dev_args = host_inputs(fn, seed_base=100 * rank)
+    rec = sess.record(fn.module, name, dev_args)
+    plan = list(sess.plan)
+    torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
-    sp = ctypes.c_void_p(stream.cuda_stream)
-    prec = args.precision
-    tc = runtime.tc_supported(prec, K)
-    kind = 0 if prec == "bf16" else 1
-    elt = torch.bfloat16 if prec == "bf16" else torch.float32
-    Ap = torch.empty(M, K, dtype=elt, device=dev)
-    Bp = torch.empty(N, K, dtype=elt, device=dev)
-    P = ctypes.c_void_p
-    gemm_ms = []
-
-    def step(timed):
-        if tc:
-            assert lib.b200_pack_operand(kind, P(A.data_ptr()), K, 1, P(Ap.data_ptr()),
-                                         M, K, sp) == 0
-            assert lib.b200_pack_operand(kind, P(B.data_ptr()), 1, N, P(Bp.data_ptr()),
-                                         N, K, sp) == 0
-        if timed:
-            e0 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-        if tc:
-            rc = lib.b200_gemm_tc(kind, P(Ap.data_ptr()), P(Bp.data_ptr()), P(C.data_ptr()),
-                                  N, 1, M, N, K, 0, 0.0, None, 0, 0, args.variant, sp)
-        else:
-            rc = lib.b200_gemm_f32_exact(P(A.data_ptr()), K, 1, P(B.data_ptr()), N, 1,
-                                         P(C.data_ptr()), N, 1, M, N, K, 0, 0.0, None, 0, sp)
-        assert rc == 0
-        if timed:
-            e1 = torch.cuda.Event(enable_timing=True)
-            e1.record(stream)
-            gemm_ms.append((e0, e1))
-
     for _ in range(args.warmup):
-        step(False)
+        rec.replay(lib)
     torch.cuda.synchronize()
     barrier(world)
     clocks = Clocks(local)
-    torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
     ev0.record(stream)
     for _ in range(args.steps):
-        step(True)
+        rec.replay(lib)
     ev1.record(stream)
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.steps
-    kernel_ms = statistics.mean(a.elapsed_time(b) for a, b in gemm_ms)
     clk = clocks.stop()
+    # per-launch timing (instrumented replay): kernel family shares
+    fam_ms = {}
+    reps = max(1, min(args.steps, 5))
+    for _ in range(reps):
+        for cname, cargs in rec.calls:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            runtime.check(getattr(lib, cname)(*cargs[:-1],
+                                              ctypes.c_void_p(stream.cuda_stream)),
+                          cname)
+            e1.record(stream)
+            fam_ms.setdefault(cname, []).append((e0, e1))
+    torch.cuda.synchronize()
+    fam = {k: sum(a.elapsed_time(b) for a, b in v) / reps for k, v in fam_ms.items()}
     barrier(world)
     ms = max_over_ranks(ms, world)
-    kernel_ms = max_over_ranks(kernel_ms, world)
-    value = world * FLOP / (ms * 1e-3) / 1e9
-    launches_per_step = 3 if tc else 1
+    value = world * wl.flops / (ms * 1e-3) / 1e9
+    out_sum = float(sess.tensor(dev_args[-1]).double().sum().item())
+    sums = gather_checksums(out_sum, world)
 
     # e2e through the plugin: host Buffers, H2D + D2H inside the timed region
-    b2.configure(precision=prec)
-    e2e_steps = max(1, min(args.steps, 3))
-    host = host_inputs([(M, K), (K, N), (M, N)])
-    machine.run(mm.module, "mm", host, engine=b2.engine)   # warm
+    host = host_inputs(fn, seed_base=100 * rank)
+    machine.run(fn.module, name, host, engine=b2.engine)   # warm
     torch.cuda.synchronize()
     barrier(world)
+    e2e_steps = max(1, min(args.steps, 3))
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        machine.run(mm.module, "mm", host, engine=b2.engine)
+        machine.run(fn.module, name, host, engine=b2.engine)
     torch.cuda.synchronize()
     e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
     e2e_ms = max_over_ranks(e2e_ms, world)
-    plan = list(b2.engine.last_plan)
+    h2d = sum(len(b.data) * b.data.itemsize for b in host)
+    d2h = sum(len(b.data) * b.data.itemsize for b in host[-1:])
+    if wl.name == "ls":
+        d2h = sum(len(b.data) * b.data.itemsize for b in (host[3], host[6]))
+    elif wl.name == "linear32":
+        d2h = sum(len(b.data) * b.data.itemsize for b in (host[3], host[4]))
 
     if rank != 0:
         return
     peaks, src = load_peaks()
-    if tc:
+    dom = max(fam, key=fam.get)
+    dom_ms = fam[dom]
+    family = KERNEL_OF.get(dom, dom)
+    if wl.name == "ewise":
+        achieved = wl.bytes / (dom_ms * 1e-3) / 1e9
+        peak, unit, bound = peaks["hbm_gbs"], "GB/s", "hbm"
+        peak_source = f"{src} HBM copy bandwidth (MEASURED_PEAKS.json)"
+    elif dom == "b200_gemm_tc":
+        achieved = wl.flops / (dom_ms * 1e-3) / 1e12
         peak = peaks["bf16_tflops"] * (1.0 if prec == "bf16" else 0.5)
-        bound = "tensor"
+        unit, bound = "TFLOP/s", "tensor"
         peak_source = (f"{src} bf16 dense (MEASURED_PEAKS.json)" if prec == "bf16" else
                        f"{src} bf16 x 0.5 (tf32 = half rate, derived)")
     else:
+        achieved = wl.flops / (dom_ms * 1e-3) / 1e12
         peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-        bound = "fp32-simt"
+        unit, bound = "TFLOP/s", "fp32-simt"
         peak_source = "derived: 148 SM x 128 FP32 lanes x 2 x sm_max_mhz"
-    achieved = FLOP / (kernel_ms * 1e-3) / 1e12
-    cpu_rate, cpu_t = reference_slice_rate()
+    cpu_rate, cpu_t = reference_rate(wl)
     dtype = {"bf16": "bf16 (fp32 accumulate)", "tf32": "tf32 (fp32 accumulate)",
              "exact": "f32"}[prec]
+    big = wl.name != "linear32"
     line = {
-        "metric": "GFLOP/s (matmul 4096^3)", "value": value, "unit": "GFLOP/s",
+        "metric": f"GFLOP/s ({wl.name})", "value": value, "unit": "GFLOP/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype,
+        "higher_is_better": True, "scaling": wl.scaling, "vs_baseline": None, "dtype": dtype,
         "data": "synthetic",
-        "config": {"workload": "linalg.matmul 4096x4096x4096, C += A.B on f32 buffers "
-                               "(step = operand pack + contraction)",
-                   "precision": prec, "l2": "inputs 192 MiB f32 > 126 MB L2 (no flush)",
-                   "parallelism": f"replica x{world}"},
-        "roofline": {"bound": bound, "kernel": "b200_gemm_tc" if tc else "b200_gemm_f32_exact",
-                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "peak_source": peak_source,
-                     "kernel_ms": kernel_ms, "traffic": load_traffic(prec)},
-        "e2e": {"value": FLOP / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s",
-                "ms_per_step": e2e_ms, "h2d_bytes_per_step": 3 * M * N * 4,
-                "d2h_bytes_per_step": M * N * 4, "plan": [list(p) for p in plan]},
+        "config": {"workload": wl.desc, "precision": prec,
+                   "l2": "inputs larger than the 126 MB L2 (no flush)" if big else
+                         "L2-resident, latency-bound config",
+                   "parallelism": f"{'replica' if wl.scaling == 'weak' else 'batch-shard'} "
+                                  f"x{world}",
+                   "plan": [list(map(str, p)) for p in plan]},
+        "roofline": {"bound": bound, "kernel": dom, "achieved": achieved, "peak": peak,
+                     "unit": unit, "frac": achieved / peak, "peak_source": peak_source,
+                     "kernel_ms": dom_ms,
+                     "share_of_step": sum(fam.values()) and dom_ms / sum(fam.values()),
+                     "traffic": load_traffic(f"{wl.name}_{family}_{prec}")},
+        "e2e": {"value": wl.flops / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s",
+                "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "cpu_baseline": {"value": cpu_rate, "unit": "GFLOP/s", "cores": 1,
                          "kind": "reference",
-                         "sample": f"1x4096x256 slice of the matmul nest via staircase _evalcy "
-                                   f"({cpu_t:.2f} s); host cores {len(os.sched_getaffinity(0))}"},
-        "clocks": clk, "gpu_launches": launches_per_step * args.steps,
+                         "sample": f"{wl.slice[2]} via staircase _evalcy ({cpu_t:.2f} s); "
+                                   f"host cores {len(os.sched_getaffinity(0))}"},
+        "clocks": clk, "gpu_launches": rec.launches * args.steps,
+        "checksums": sums,
     }
     print(json.dumps(line), flush=True)
 
@@ -360,9 +419,9 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--precision", default="bf16", choices=["bf16", "tf32", "exact"])
-    ap.add_argument("--variant", type=int, default=0,
-                    help="tcgen05 schedule: 0 auto, 1 single-CTA, 2 CTA pair")
+    ap.add_argument("--workload", default="mm", choices=["mm", "conv", "ls", "linear32",
+                                                         "ewise"])
+    ap.add_argument("--precision", default=None, choices=["bf16", "tf32", "exact"])
     args = ap.parse_args()
     rank, world, local = dist_setup()
     if args.impl == "reference":

@@ -14,6 +14,8 @@ from .host import ensure_staircase
 ensure_staircase()
 
 from . import engine  # noqa: E402
-from .engine import ENGINE_NAME, ExecContext, configure, install, run_tape  # noqa: E402
+from .engine import (ENGINE_NAME, ExecContext, Session, configure, install,  # noqa: E402
+                     run_tape)
 
-__all__ = ["engine", "install", "configure", "run_tape", "ExecContext", "ENGINE_NAME"]
+__all__ = ["engine", "install", "configure", "run_tape", "ExecContext", "Session",
+           "ENGINE_NAME"]

@@ -347,6 +347,69 @@ def run_tape(program, code, regs, tally, ctx, backend=None):
     return rets
 
 
+class Session:
+    """Device-resident execution of staircase modules on the B200.
+
+    ``run()`` has the signature and results of ``machine.run`` but Buffers
+    stay in HBM between runs (uploaded on first use, no write-back until
+    ``sync()``), so chains of runs on the same data — or repeated timing
+    runs — move no host data.  ``record()`` runs a module once and returns
+    the exact launch sequence the engine chose (runtime.Recording), which
+    ``replay()``s without re-planning; it can be captured in a CUDA graph.
+    Host data changed after the first upload is not re-read (call
+    ``forget(buf)``).
+    """
+
+    def __init__(self):
+        self.be = DeviceBackend()
+        self.plan = []
+
+    def _engine(self):
+        sess = self
+
+        class _Eng:
+            ExecContext = globals()["ExecContext"]
+
+            @staticmethod
+            def run_tape(program, code, regs, tally, ctx):
+                run = _Run(program, ctx, sess.be)
+                try:
+                    rets = run.exec_tape(code, regs, tally)
+                finally:
+                    run.flush_pending()
+                    sess.plan = run.plan
+                return rets
+
+        return _Eng
+
+    def run(self, module, func, args, mode="sequential", workers=1):
+        from staircase.interp import machine
+
+        return machine.run(module, func, args, mode=mode, workers=workers,
+                           engine=self._engine())
+
+    def record(self, module, func, args, mode="sequential", workers=1):
+        from .runtime import Recording
+
+        self.be.recording = Recording()
+        try:
+            self.run(module, func, args, mode=mode, workers=workers)
+        finally:
+            rec, self.be.recording = self.be.recording, None
+        return rec
+
+    def tensor(self, buf):
+        """The device tensor backing a Buffer in this session."""
+        return self.be.stage.tensor(buf)
+
+    def forget(self, buf):
+        self.be.stage.dev.pop(id(buf), None)
+
+    def sync(self):
+        """Write every buffer the session's runs modified back to the host."""
+        self.be.flush()
+
+
 def install():
     """Make this engine the default of staircase.interp.machine.run()."""
     from .host import ensure_staircase

@@ -1,10 +1,15 @@
-"""Device runtime: the libb200k.so binding and per-run buffer staging.
+"""Device runtime: the libb200k.so binding, buffer staging, launch recording.
 
 PyTorch is used only as the device allocator / stream provider.  All
 compute goes through the C ABI in include/b200k.h, loaded with ctypes from
 the in-tree shared object built by paper_2307_16080_b200/build.py.  There is
 no CPU fallback: if the library or a GPU is missing, every entry point
 raises.
+
+Every C-ABI launch goes through ``DeviceBackend.call`` so a run can be
+*recorded* (the exact launch sequence the engine chose for a module, with
+its device pointers) and replayed — directly or as a CUDA graph — without
+re-planning; bench.py uses this for device-resident timing.
 """
 from __future__ import annotations
 
@@ -90,7 +95,7 @@ DT_CODE = {"f32": 0, "f64": 1, "i32": 2, "i64": 3}
 
 
 class Staging:
-    """Device copies of the host Buffers touched by one run.
+    """Device copies of the host Buffers touched by a run (or a Session).
 
     Memref arguments are mutated in place in the reference (SPEC: memref
     reference semantics), so every buffer a region writes is copied back
@@ -106,11 +111,11 @@ class Staging:
 
     @property
     def stream_ptr(self):
-        return ctypes.c_void_p(self.stream.cuda_stream)
+        return ctypes.c_void_p(self.torch.cuda.current_stream().cuda_stream)
 
     def tensor(self, buf):
         ent = self.dev.get(id(buf))
-        if ent is None:
+        if ent is None or ent[0] is not buf:
             torch = self.torch
             dt = getattr(torch, _TORCH_DT[buf.dtype])
             host = torch.frombuffer(buf.data, dtype=dt)
@@ -179,42 +184,80 @@ def tc_supported(precision, K):
         (K * (2 if precision == "bf16" else 4)) % 16 == 0
 
 
+def _direct_call(lib):
+    def call(name, *args):
+        check(getattr(lib, name)(*args), name)
+    return call
+
+
 def launch_gemm(lib, precision, a_ptr, sA, b_ptr, sB, c_ptr, sC, M, N, K, stream,
                 init=0, init_value=0.0, bias_ptr=None, bias_stride=0, max_ctas=0,
-                variant=0):
+                variant=0, call=None):
     """Enqueue C (+)= A.B with the kernel chosen by ``precision``.
 
     Returns the list of kernel names launched (for the launch count).
     exact -> b200_gemm_f32_exact (bit-identical to the reference);
     bf16/tf32 -> b200_pack_operand x2 + b200_gemm_tc (tcgen05).
     """
+    call = call or _direct_call(lib)
     P = ctypes.c_void_p
     if not tc_supported(precision, K):
-        check(lib.b200_gemm_f32_exact(P(a_ptr), sA[0], sA[1], P(b_ptr), sB[0], sB[1],
-                                      P(c_ptr), sC[0], sC[1], M, N, K, init, init_value,
-                                      P(bias_ptr) if bias_ptr else None, bias_stride,
-                                      stream), "b200_gemm_f32_exact")
+        call("b200_gemm_f32_exact", P(a_ptr), sA[0], sA[1], P(b_ptr), sB[0], sB[1],
+             P(c_ptr), sC[0], sC[1], M, N, K, init, init_value,
+             P(bias_ptr) if bias_ptr else None, bias_stride, stream)
         return ["gemm_f32_exact"]
     kind = 0 if precision == "bf16" else 1
     dt = "bfloat16" if kind == 0 else "float32"
     Ap = workspace(0, dt, M, K)
     Bp = workspace(1, dt, N, K)
-    check(lib.b200_pack_operand(kind, P(a_ptr), sA[0], sA[1], P(Ap.data_ptr()), M, K,
-                                stream), "b200_pack_operand")
-    check(lib.b200_pack_operand(kind, P(b_ptr), sB[1], sB[0], P(Bp.data_ptr()), N, K,
-                                stream), "b200_pack_operand")
-    check(lib.b200_gemm_tc(kind, P(Ap.data_ptr()), P(Bp.data_ptr()), P(c_ptr), sC[0], sC[1],
-                           M, N, K, init, init_value, P(bias_ptr) if bias_ptr else None,
-                           bias_stride, max_ctas, variant, stream), "b200_gemm_tc")
+    call("b200_pack_operand", kind, P(a_ptr), sA[0], sA[1], P(Ap.data_ptr()), M, K, stream)
+    call("b200_pack_operand", kind, P(b_ptr), sB[1], sB[0], P(Bp.data_ptr()), N, K, stream)
+    call("b200_gemm_tc", kind, P(Ap.data_ptr()), P(Bp.data_ptr()), P(c_ptr), sC[0], sC[1],
+         M, N, K, init, init_value, P(bias_ptr) if bias_ptr else None, bias_stride,
+         max_ctas, variant, stream)
     return ["pack_operand", "pack_operand", f"gemm_tc_{precision}"]
+
+
+class Recording:
+    """A recorded launch sequence: replayable on the current stream."""
+
+    def __init__(self):
+        self.calls = []      # (name, args)
+        self.keep = []       # device uploads the recorded args point into
+
+    def replay(self, lib=None):
+        lib = lib or load_library()
+        torch = torch_mod()
+        stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        for name, args in self.calls:
+            # the stream is always the last argument of a C-ABI entry point
+            check(getattr(lib, name)(*args[:-1], stream), name)
+
+    @property
+    def launches(self):
+        return len(self.calls)
+
+    def names(self):
+        return [n for n, _ in self.calls]
 
 
 class DeviceBackend:
     """Executes region plans on the B200 through libb200k.so."""
 
-    def __init__(self):
-        self.stage = Staging()
+    def __init__(self, staging=None):
+        self.stage = staging or Staging()
         self._keep = None
+        self.recording = None    # Recording while recording
+
+    def call(self, name, *args):
+        check(getattr(self.stage.lib, name)(*args), name)
+        if self.recording is not None:
+            self.recording.calls.append((name, args))
+
+    def keep(self, *objs):
+        self._keep = objs
+        if self.recording is not None:
+            self.recording.keep.append(objs)
 
     def read(self, buf, off):
         v = self.stage.tensor(buf)[off].item()
@@ -242,21 +285,20 @@ class DeviceBackend:
                                tB.data_ptr() + 4 * g.offB, g.sB, tC.data_ptr() + 4 * g.offC,
                                g.sC, g.M, g.N, g.K, s.stream_ptr, init=init,
                                init_value=init_value, bias_ptr=bias_ptr,
-                               bias_stride=bias_stride)
+                               bias_stride=bias_stride, call=self.call)
         torch = s.torch
         tabs = [torch.from_numpy(t).to("cuda") for t in g.tables]
         a_m, a_k, b_k, b_n, c_m, c_n = g.tables
         a_k_fast = int(len(a_k) > 1 and a_k[1] - a_k[0] == 1)
         b_n_fast = int(len(b_n) > 1 and b_n[1] - b_n[0] == 1)
         P = ctypes.c_void_p
-        check(s.lib.b200_contract_exact(
-            DT_CODE[g.dtype], P(tA.data_ptr()), P(tabs[0].data_ptr()), P(tabs[1].data_ptr()),
-            P(tB.data_ptr()), P(tabs[2].data_ptr()), P(tabs[3].data_ptr()),
-            P(tC.data_ptr()), P(tabs[4].data_ptr()), P(tabs[5].data_ptr()),
-            g.M, g.N, g.K, a_k_fast, b_n_fast, init, init_value,
-            P(bias_ptr) if bias_ptr else None, bias_stride, s.stream_ptr),
-            "b200_contract_exact")
-        self._keep = tabs   # tables must outlive the asynchronous kernel
+        self.keep(*tabs)   # tables must outlive the asynchronous kernel
+        self.call("b200_contract_exact",
+                  DT_CODE[g.dtype], P(tA.data_ptr()), P(tabs[0].data_ptr()),
+                  P(tabs[1].data_ptr()), P(tB.data_ptr()), P(tabs[2].data_ptr()),
+                  P(tabs[3].data_ptr()), P(tC.data_ptr()), P(tabs[4].data_ptr()),
+                  P(tabs[5].data_ptr()), g.M, g.N, g.K, a_k_fast, b_n_fast, init, init_value,
+                  P(bias_ptr) if bias_ptr else None, bias_stride, s.stream_ptr)
         return ["contract_exact"]
 
     def map(self, m):
@@ -269,8 +311,8 @@ class DeviceBackend:
         trips = (ctypes.c_int64 * nd)(*m.trips)
         prog = (ctypes.c_int32 * len(m.prog))(*m.prog)
         consts = (ctypes.c_float * max(1, len(m.consts)))(*m.consts)
-        check(s.lib.b200_map_f32(prog, len(m.prog), consts, len(m.consts), ptrs, coefs, nops,
-                                 trips, nd, int(m.vector), s.stream_ptr), "b200_map_f32")
+        self.call("b200_map_f32", prog, len(m.prog), consts, len(m.consts), ptrs, coefs, nops,
+                  trips, nd, int(m.vector), s.stream_ptr)
         return ["map_f32"]
 
     def vm(self, r, prog, checked):
@@ -290,15 +332,14 @@ class DeviceBackend:
         dtally = torch.zeros(25, dtype=torch.int64, device="cuda")
         err = torch.zeros(ctypes.sizeof(B200VmError), dtype=torch.uint8, device="cuda")
         P = ctypes.c_void_p
-        rc = s.lib.b200_vm_run(
-            P(words.data_ptr()), len(prog.words), P(iregs.data_ptr()),
-            P(ivals.data_ptr()), len(prog.init_regs), prog.n_regs,
-            P(table.data_ptr()), len(r.buffers), nd, breg, blb, bst, btr,
-            1 if prog.count else 0, P(dtally.data_ptr()), P(err.data_ptr()),
-            s.stream_ptr)
-        check(rc, "b200_vm_run")
         # the uploads must outlive the (asynchronous) kernel
-        self._keep = (table, words, iregs, ivals, breg, blb, bst, btr, dtally, err)
+        self.keep(table, words, iregs, ivals, dtally, err)
+        self.call("b200_vm_run",
+                  P(words.data_ptr()), len(prog.words), P(iregs.data_ptr()),
+                  P(ivals.data_ptr()), len(prog.init_regs), prog.n_regs,
+                  P(table.data_ptr()), len(r.buffers), nd, breg, blb, bst, btr,
+                  1 if prog.count else 0, P(dtally.data_ptr()), P(err.data_ptr()),
+                  s.stream_ptr)
         fault = None
         if checked:
             e = B200VmError.from_buffer_copy(bytes(err.cpu().numpy()))
@@ -308,5 +349,6 @@ class DeviceBackend:
         return dev_tally, fault
 
 
-__all__ = ["load_library", "Staging", "DeviceBackend", "BackendUnavailable", "B200Buffer",
-           "B200VmError", "LIB_PATH", "SIGNATURES"]
+__all__ = ["load_library", "Staging", "DeviceBackend", "Recording", "BackendUnavailable",
+           "B200Buffer", "B200VmError", "LIB_PATH", "SIGNATURES", "launch_gemm",
+           "tc_supported", "workspace"]
