@@ -221,6 +221,28 @@ def max_over_ranks(x, world):
     return float(t.item())
 
 
+def capture_graph(fn):
+    """Capture fn's launches (on the current stream) into a CUDA graph."""
+    import torch
+
+    try:
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            fn()   # warm-up on a side stream, as torch requires before capture
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        torch.cuda.synchronize()
+        return g
+    except Exception as exc:  # graph capture is an optimisation of the timing only
+        print(f"# graph capture failed ({exc}); timing eager replays", file=sys.stderr)
+        torch.cuda.synchronize()
+        return None
+
+
 def gather_checksums(value, world):
     """The only collective: one NCCL all_gather of per-rank result checksums."""
     if world == 1:
@@ -308,6 +330,13 @@ def run_ours(args, rank, world, local):
     for _ in range(args.warmup):
         rec.replay(lib)
     torch.cuda.synchronize()
+    # the recorded launch sequence as one CUDA graph: device time per step
+    # without host enqueue gaps between the (possibly tiny) kernels
+    step_graph = capture_graph(lambda: rec.replay(lib))
+    run_step = step_graph.replay if step_graph is not None else (lambda: rec.replay(lib))
+    for _ in range(args.warmup):
+        run_step()
+    torch.cuda.synchronize()
     barrier(world)
     clocks = Clocks(local)
     ev0 = torch.cuda.Event(enable_timing=True)
@@ -315,26 +344,28 @@ def run_ours(args, rank, world, local):
     torch.cuda.synchronize()
     ev0.record(stream)
     for _ in range(args.steps):
-        rec.replay(lib)
+        run_step()
     ev1.record(stream)
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.steps
     clk = clocks.stop()
-    # per-launch timing (instrumented replay): kernel family shares
-    fam_ms = {}
-    reps = max(1, min(args.steps, 5))
-    for _ in range(reps):
-        for cname, cargs in rec.calls:
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            runtime.check(getattr(lib, cname)(*cargs[:-1],
-                                              ctypes.c_void_p(stream.cuda_stream)),
-                          cname)
-            e1.record(stream)
-            fam_ms.setdefault(cname, []).append((e0, e1))
-    torch.cuda.synchronize()
-    fam = {k: sum(a.elapsed_time(b) for a, b in v) / reps for k, v in fam_ms.items()}
+    # per-launch device time of each recorded call: a graph of R back-to-back
+    # repeats of that one launch, timed with events, / R
+    fam = {}
+    reps = 20 if ms < 1.0 else 3
+    for cname, cargs in rec.calls:
+        def one(cname=cname, cargs=cargs):
+            s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+            for _ in range(reps):
+                runtime.check(getattr(lib, cname)(*cargs[:-1], s), cname)
+        gph = capture_graph(one)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        gph.replay() if gph is not None else one()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        fam[cname] = fam.get(cname, 0.0) + e0.elapsed_time(e1) / reps
     barrier(world)
     ms = max_over_ranks(ms, world)
     value = world * wl.flops / (ms * 1e-3) / 1e9

@@ -9,19 +9,20 @@
 // contracted — so results are bit-identical to the reference for every shape,
 // stride and tile config.
 //
-// Two operand addressings share one tiled core:
+// Two operand addressings share one tiled core, both separable
+// (offset = row part + column part):
 //   * strided (b200_gemm_f32_exact): A[m*sAm + k*sAk] etc. — matmul nests;
-//   * separable tables (b200_contract_exact): A[a_m[m] + a_k[k]],
-//     B[b_k[k] + b_n[n]], C[c_m[m] + c_n[n]] — any contraction whose index
-//     maps split into output-row / output-column / reduction variable groups,
-//     e.g. the NCHW/FCHW convolution (reference tests/kernels.py:50-64) as an
-//     implicit GEMM with M = (n, ho, wo), N = co, K = (ci, ki, kj) in nest
-//     order.
-// Tiling: 128x128 (f32) / 64x64 (f64) CTA tile, BK = 16, 256 threads with an
-// 8x8 / 4x4 register micro-tile (2x2 blocks of 4x4 so shared-memory reads are
-// float4 broadcasts); global->shared staging is register double-buffered so
-// the next k-tile's loads overlap the current tile's math; loads are
-// coalesced along whichever operand dimension has unit stride.
+//   * tables (b200_contract_exact): A[a_m[m] + a_k[k]], B[b_k[k] + b_n[n]],
+//     C[c_m[m] + c_n[n]] — any contraction whose index maps split into
+//     output-row / output-column / reduction variable groups, e.g. the
+//     NCHW/FCHW convolution (reference tests/kernels.py:50-64) as an implicit
+//     GEMM with M = (n, ho, wo), N = co, K = (ci, ki, kj) in nest order.
+// Tiles (256 threads, register micro-tiles as 2x2 blocks of TM/2 x TN/2 so
+// shared-memory reads are vector broadcasts): f32 128x128 (8x8) or, for
+// narrow N (conv's F = 64), 256x64 (8x8); f64 64x64 (4x4).  BK = 16 with
+// register double-buffered global->shared staging; loads are coalesced along
+// whichever operand dimension has unit stride, and each thread's fixed row
+// offset (the separable half) is looked up once per CTA.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -32,36 +33,31 @@ namespace {
 constexpr int BK = 16;
 constexpr int kThreads = 256;
 
-template <typename T>
-struct Cfg;
-template <>
-struct Cfg<float> {
-  static constexpr int BM = 128, BN = 128, TM = 8, TN = 8, PAD = 4;
-};
-template <>
-struct Cfg<double> {
-  static constexpr int BM = 64, BN = 64, TM = 4, TN = 4, PAD = 2;
-};
-
 __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
 
-// Operand addressing.  a(m,k), b(k,n), c(m,n) return element offsets.
+// Separable operand addressing: a(m,k) = am(m) + ak(k), etc.
 struct Strided {
   int64_t sAm, sAk, sBk, sBn, sCm, sCn;
   bool a_k_fast, b_n_fast;
-  __device__ __forceinline__ int64_t a(int64_t m, int64_t k) const { return m * sAm + k * sAk; }
-  __device__ __forceinline__ int64_t b(int64_t k, int64_t n) const { return k * sBk + n * sBn; }
+  __device__ __forceinline__ int64_t am(int64_t m) const { return m * sAm; }
+  __device__ __forceinline__ int64_t ak(int64_t k) const { return k * sAk; }
+  __device__ __forceinline__ int64_t bk(int64_t k) const { return k * sBk; }
+  __device__ __forceinline__ int64_t bn(int64_t n) const { return n * sBn; }
   __device__ __forceinline__ int64_t c(int64_t m, int64_t n) const { return m * sCm + n * sCn; }
 };
 struct Tables {
   const int64_t *a_m, *a_k, *b_k, *b_n, *c_m, *c_n;
   bool a_k_fast, b_n_fast;
-  __device__ __forceinline__ int64_t a(int64_t m, int64_t k) const { return __ldg(a_m + m) + __ldg(a_k + k); }
-  __device__ __forceinline__ int64_t b(int64_t k, int64_t n) const { return __ldg(b_k + k) + __ldg(b_n + n); }
-  __device__ __forceinline__ int64_t c(int64_t m, int64_t n) const { return __ldg(c_m + m) + __ldg(c_n + n); }
+  __device__ __forceinline__ int64_t am(int64_t m) const { return __ldg(a_m + m); }
+  __device__ __forceinline__ int64_t ak(int64_t k) const { return __ldg(a_k + k); }
+  __device__ __forceinline__ int64_t bk(int64_t k) const { return __ldg(b_k + k); }
+  __device__ __forceinline__ int64_t bn(int64_t n) const { return __ldg(b_n + n); }
+  __device__ __forceinline__ int64_t c(int64_t m, int64_t n) const {
+    return __ldg(c_m + m) + __ldg(c_n + n);
+  }
 };
 
 template <typename T, typename Addr>
@@ -76,21 +72,23 @@ struct Args {
   Addr ad;
 };
 
-template <typename T, typename Addr>
+template <typename T, typename Addr, int BM, int BN, int TM, int TN>
 __global__ void __launch_bounds__(kThreads) contract_exact_kernel(Args<T, Addr> g) {
-  using C_ = Cfg<T>;
-  constexpr int BM = C_::BM, BN = C_::BN, TM = C_::TM, TN = C_::TN;
+  constexpr int PAD = 16 / sizeof(T);
   constexpr int LA = BM * BK / kThreads;  // A elements staged per thread
   constexpr int LB = BN * BK / kThreads;
   constexpr int HM = TM / 2, HN = TN / 2;  // micro-tile halves
   constexpr int TX = BN / TN;              // threads along n
-  __shared__ __align__(16) T As[2][BK][BM + C_::PAD];
+  static_assert((BM / TM) * (BN / TN) == kThreads, "tile / thread mismatch");
+  static_assert(kThreads % BM == 0 && kThreads % BN == 0, "fixed-row staging");
+  __shared__ __align__(16) T As[2][BK][BM + PAD];
   __shared__ __align__(16) T Bs[2][BK][BN];
 
   const int64_t m0 = (int64_t)blockIdx.y * BM;
   const int64_t n0 = (int64_t)blockIdx.x * BN;
-  const int tx = threadIdx.x % TX;
-  const int ty = threadIdx.x / TX;
+  const int t = threadIdx.x;
+  const int tx = t % TX;
+  const int ty = t / TX;
   auto row_of = [&](int i) { return i < HM ? ty * HM + i : BM / 2 + ty * HM + (i - HM); };
   auto col_of = [&](int j) { return j < HN ? tx * HN + j : BN / 2 + tx * HN + (j - HN); };
 
@@ -107,39 +105,55 @@ __global__ void __launch_bounds__(kThreads) contract_exact_kernel(Args<T, Addr> 
     }
   }
 
+  // staging geometry.  m-fast A: this thread always stages row mm_fix and
+  // k rows kk0 + i * (kThreads / BM); k-fast A: column kk_fix, rows vary.
+  const bool afast = g.ad.a_k_fast, bfast = g.ad.b_n_fast;
+  const int mm_fix = t % BM;
+  const int kk_fix_a = t % BK;
+  const int nn_fix = t % BN;
+  const int kk_fix_b = t % BK;
+  const int64_t m_fix = m0 + mm_fix;
+  const int64_t n_fix = n0 + nn_fix;
+  const int64_t arow_fix = (!afast && m_fix < g.M) ? g.ad.am(m_fix) : 0;
+  const int64_t bcol_fix = (bfast && n_fix < g.N) ? g.ad.bn(n_fix) : 0;
+
   T ra[LA], rb[LB];
   auto load = [&](int64_t k0) {
 #pragma unroll
     for (int i = 0; i < LA; ++i) {
-      const int e = threadIdx.x + i * kThreads;
-      int mm, kk;
-      if (g.ad.a_k_fast) { kk = e % BK; mm = e / BK; } else { mm = e % BM; kk = e / BM; }
-      const int64_t m = m0 + mm, k = k0 + kk;
-      ra[i] = (m < g.M && k < g.K) ? __ldg(g.A + g.ad.a(m, k)) : T(0);
+      const int e = t + i * kThreads;
+      if (afast) {
+        const int64_t m = m0 + e / BK, k = k0 + kk_fix_a;
+        ra[i] = (m < g.M && k < g.K) ? __ldg(g.A + g.ad.am(m) + g.ad.ak(k)) : T(0);
+      } else {
+        const int64_t k = k0 + e / BM;
+        ra[i] = (m_fix < g.M && k < g.K) ? __ldg(g.A + arow_fix + g.ad.ak(k)) : T(0);
+      }
     }
 #pragma unroll
     for (int i = 0; i < LB; ++i) {
-      const int e = threadIdx.x + i * kThreads;
-      int nn, kk;
-      if (g.ad.b_n_fast) { nn = e % BN; kk = e / BN; } else { kk = e % BK; nn = e / BK; }
-      const int64_t n = n0 + nn, k = k0 + kk;
-      rb[i] = (n < g.N && k < g.K) ? __ldg(g.B + g.ad.b(k, n)) : T(0);
+      const int e = t + i * kThreads;
+      if (bfast) {
+        const int64_t k = k0 + e / BN;
+        rb[i] = (n_fix < g.N && k < g.K) ? __ldg(g.B + g.ad.bk(k) + bcol_fix) : T(0);
+      } else {
+        const int64_t n = n0 + e / BK, k = k0 + kk_fix_b;
+        rb[i] = (n < g.N && k < g.K) ? __ldg(g.B + g.ad.bk(k) + g.ad.bn(n)) : T(0);
+      }
     }
   };
   auto store = [&](int buf) {
 #pragma unroll
     for (int i = 0; i < LA; ++i) {
-      const int e = threadIdx.x + i * kThreads;
-      int mm, kk;
-      if (g.ad.a_k_fast) { kk = e % BK; mm = e / BK; } else { mm = e % BM; kk = e / BM; }
-      As[buf][kk][mm] = ra[i];
+      const int e = t + i * kThreads;
+      if (afast) As[buf][kk_fix_a][e / BK] = ra[i];
+      else As[buf][e / BM][mm_fix] = ra[i];
     }
 #pragma unroll
     for (int i = 0; i < LB; ++i) {
-      const int e = threadIdx.x + i * kThreads;
-      int nn, kk;
-      if (g.ad.b_n_fast) { nn = e % BN; kk = e / BN; } else { kk = e % BK; nn = e / BK; }
-      Bs[buf][kk][nn] = rb[i];
+      const int e = t + i * kThreads;
+      if (bfast) Bs[buf][e / BN][nn_fix] = rb[i];
+      else Bs[buf][kk_fix_b][e / BK] = rb[i];
     }
   };
 
@@ -173,7 +187,7 @@ __global__ void __launch_bounds__(kThreads) contract_exact_kernel(Args<T, Addr> 
         for (int j = 0; j < TN; ++j) acc[i][j] = add_rn(acc[i][j], mul_rn(av[i], bv[j]));
     }
     if (kt + 1 < ktiles) {
-      store(cur ^ 1);
+      store(cur ^ 1);   // cur^1 was last read before the previous barrier
       __syncthreads();
     }
   }
@@ -193,15 +207,28 @@ __global__ void __launch_bounds__(kThreads) contract_exact_kernel(Args<T, Addr> 
   }
 }
 
-template <typename T, typename Addr>
-int launch(const Args<T, Addr> &g, void *stream) {
-  using C_ = Cfg<T>;
+template <typename T, typename Addr, int BM, int BN, int TM, int TN>
+int launch_tile(const Args<T, Addr> &g, void *stream) {
+  dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM));
+  if (grid.y > 65535u) return B200_EINVAL;
+  contract_exact_kernel<T, Addr, BM, BN, TM, TN>
+      <<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(g);
+  return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
+}
+
+template <typename Addr>
+int launch(const Args<float, Addr> &g, void *stream) {
   if (g.M < 0 || g.N < 0 || g.K < 0) return B200_EINVAL;
   if (g.M == 0 || g.N == 0) return B200_OK;
-  dim3 grid((unsigned)((g.N + C_::BN - 1) / C_::BN), (unsigned)((g.M + C_::BM - 1) / C_::BM));
-  if (grid.y > 65535u) return B200_EINVAL;
-  contract_exact_kernel<T, Addr><<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(g);
-  return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
+  if (g.N <= 64) return launch_tile<float, Addr, 256, 64, 8, 8>(g, stream);
+  return launch_tile<float, Addr, 128, 128, 8, 8>(g, stream);
+}
+
+template <typename Addr>
+int launch(const Args<double, Addr> &g, void *stream) {
+  if (g.M < 0 || g.N < 0 || g.K < 0) return B200_EINVAL;
+  if (g.M == 0 || g.N == 0) return B200_OK;
+  return launch_tile<double, Addr, 64, 64, 4, 4>(g, stream);
 }
 
 }  // namespace

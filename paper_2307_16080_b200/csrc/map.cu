@@ -43,23 +43,30 @@ __device__ __forceinline__ float fop(int f, float a, float b) {
                                                                    : __fdiv_rn(a, b);
 }
 
-template <bool VEC>
+template <bool VEC, bool ONE_D>
 __global__ void __launch_bounds__(256) map_kernel(const __grid_constant__ MapParams p) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < p.total; w += stride) {
     // decompose the work index over the box (innermost dim in vectors of 4)
-    int64_t rem = w;
     int64_t off[kMaxOps];
+    if (ONE_D) {
+      // dims merged on the host: a dense 1-D walk, no division
+      const int64_t i = VEC ? w * 4 : w;
 #pragma unroll
-    for (int k = 0; k < kMaxOps; ++k) off[k] = 0;
-    for (int d = p.nd - 1; d >= 0; --d) {
-      const int64_t trip = (VEC && d == p.nd - 1) ? p.trip[d] / 4 : p.trip[d];
-      int64_t i = rem % trip;
-      rem /= trip;
-      if (VEC && d == p.nd - 1) i *= 4;
+      for (int k = 0; k < kMaxOps; ++k) off[k] = k < p.nops ? p.coef[k][0] * i : 0;
+    } else {
+      int64_t rem = w;
 #pragma unroll
-      for (int k = 0; k < kMaxOps; ++k)
-        if (k < p.nops) off[k] += p.coef[k][d] * i;
+      for (int k = 0; k < kMaxOps; ++k) off[k] = 0;
+      for (int d = p.nd - 1; d >= 0; --d) {
+        const int64_t trip = (VEC && d == p.nd - 1) ? p.trip[d] / 4 : p.trip[d];
+        int64_t i = rem % trip;
+        rem /= trip;
+        if (VEC && d == p.nd - 1) i *= 4;
+#pragma unroll
+        for (int k = 0; k < kMaxOps; ++k)
+          if (k < p.nops) off[k] += p.coef[k][d] * i;
+      }
     }
     float4 r[kMaxRegs];
     for (int pc = 0; pc < p.nwords;) {
@@ -138,7 +145,12 @@ extern "C" int b200_map_f32(const int32_t *prog, int32_t n_words, const float *c
   int64_t blocks = (total + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (vector) map_kernel<true><<<(unsigned)blocks, 256, 0, s>>>(p);
-  else map_kernel<false><<<(unsigned)blocks, 256, 0, s>>>(p);
+  if (nd == 1) {
+    if (vector) map_kernel<true, true><<<(unsigned)blocks, 256, 0, s>>>(p);
+    else map_kernel<false, true><<<(unsigned)blocks, 256, 0, s>>>(p);
+  } else {
+    if (vector) map_kernel<true, false><<<(unsigned)blocks, 256, 0, s>>>(p);
+    else map_kernel<false, false><<<(unsigned)blocks, 256, 0, s>>>(p);
+  }
   return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
 }

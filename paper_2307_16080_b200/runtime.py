@@ -130,6 +130,8 @@ class Staging:
     def flush(self):
         torch = self.torch
         for key in list(self.dirty):
+            if key not in self.dev:
+                continue   # marked but never staged: the device never touched it
             buf, t = self.dev[key]
             dt = getattr(torch, _TORCH_DT[buf.dtype])
             host = torch.frombuffer(buf.data, dtype=dt)

@@ -238,6 +238,7 @@ def match_map(region, links, remainder, accesses, band):
                 return None
     except ValueError:
         return None
+    _merge_dims(m)
     ops_seq, pc = [], 0
     while pc < len(m.prog):
         op = m.prog[pc] & 0xFF
@@ -245,13 +246,27 @@ def match_map(region, links, remainder, accesses, band):
         pc += 2 if op == M_BF else 1
     if M_ST not in ops_seq or len(m.prog) > 64:
         return None
-    inner = len(dims) - 1
+    inner = len(m.trips) - 1
     m.vector = m.trips[inner] % 4 == 0 and all(
         c[inner] in (0, 1) and (c[inner] == 0 or (b % 4 == 0 and all(x % 4 == 0 for x in c[:inner])))
         for b, c in zip(m.bases, m.coefs))
     m.kind = ("fill" if ops_seq == [M_CF, M_ST] else
               "copy" if ops_seq == [M_LD, M_ST] else "ewise")
     return m
+
+
+def _merge_dims(m):
+    """Collapse adjacent box dims that every operand walks contiguously
+    (coef[d] == coef[d+1] * trip[d+1]); a dense row-major box becomes 1-D."""
+    d = len(m.trips) - 2
+    while d >= 0:
+        t_in = m.trips[d + 1]
+        if all(c[d] == c[d + 1] * t_in for c in m.coefs):
+            m.trips[d] = m.trips[d] * t_in
+            del m.trips[d + 1]
+            for c in m.coefs:
+                del c[d]          # the merged dim keeps coef[d+1]
+        d -= 1
 
 
 def match_gemm(region, links, remainder, accesses):

@@ -59,6 +59,8 @@ class SimBackend:
 
     def flush(self):
         for k in list(self.dirty):
+            if k not in self.dev:
+                continue
             buf, a = self.dev[k]
             np.frombuffer(buf.data, dtype=_NP[buf.dtype])[:] = a
         self.dirty.clear()
