@@ -111,6 +111,22 @@ int b200_contract_exact(int32_t dtype, const void *A, const int64_t *a_m, const 
                         const void *bias, int64_t bias_stride, void *stream);
 
 /*
+ * Pointwise f32 nest (fill / copy / elementwise / broadcast bias): every point
+ * of the nd-dim box runs the straight-line program `prog` (map.cu encoding:
+ * LD/CF/BF/ST over 8 registers) on n_ops operands addressed
+ * ptrs[k] + sum_d coefs[k*nd + d] * i_d.  Replaces run_tape on race-free
+ * straight-line nests (reference interp/_evalpy.py:90-127; PAPER.md:431-441,
+ * 455-462 fill/copy/bias nests).  Per-op IEEE f32 rounding (bit-exact).
+ * ptrs/coefs/trips/prog/consts are HOST arrays (copied into the kernel
+ * parameters).  vector: 128-bit path (innermost trip % 4 == 0, operands
+ * contiguous or broadcast along it); nload: number of leading LD words
+ * whose loads may be issued together (0..4).
+ */
+int b200_map_f32(const int32_t *prog, int32_t n_words, const float *consts, int32_t n_consts,
+                 float *const *ptrs, const int64_t *coefs, int32_t n_ops, const int64_t *trips,
+                 int32_t nd, int32_t vector, int32_t nload, void *stream);
+
+/*
  * Operand packing for the tensor-core contraction: dst[r][c] (dense
  * row-major, i.e. K-major for the GEMM) = round(src[r*s_row + c*s_col]),
  * kind 0 -> bf16 (RN), kind 1 -> tf32 held in f32 (RN, low 13 bits zero).

@@ -43,7 +43,7 @@ __device__ __forceinline__ float fop(int f, float a, float b) {
                                                                    : __fdiv_rn(a, b);
 }
 
-template <bool VEC, bool ONE_D>
+template <bool VEC, bool ONE_D, int NL>
 __global__ void __launch_bounds__(256) map_kernel(const __grid_constant__ MapParams p) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < p.total; w += stride) {
@@ -69,7 +69,22 @@ __global__ void __launch_bounds__(256) map_kernel(const __grid_constant__ MapPar
       }
     }
     float4 r[kMaxRegs];
-    for (int pc = 0; pc < p.nwords;) {
+    // hoisted loads: operand q feeds the q-th leading LD word; compile-time q
+    // keeps them in registers, all NL loads in flight together
+    float4 L[NL > 0 ? NL : 1];
+#pragma unroll
+    for (int q = 0; q < NL; ++q) {
+      const float *src = p.ptr[q] + off[q];
+      if (VEC) {
+        if (p.coef[q][p.nd - 1] == 1) L[q] = *reinterpret_cast<const float4 *>(src);
+        else { const float v = *src; L[q] = make_float4(v, v, v, v); }
+      } else {
+        L[q].x = *src;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NL; ++q) r[(p.prog[q] >> 8) & 0xff] = L[q];
+    for (int pc = NL; pc < p.nwords;) {
       const int32_t w0 = p.prog[pc];
       const int op = w0 & 0xff, dst = (w0 >> 8) & 0xff, a = (w0 >> 16) & 0xff,
                 b = (w0 >> 24) & 0xff;
@@ -112,12 +127,31 @@ __global__ void __launch_bounds__(256) map_kernel(const __grid_constant__ MapPar
   }
 }
 
+template <bool VEC, bool ONE_D>
+void dispatch_vec(const MapParams &p, int nload, unsigned blocks, cudaStream_t s) {
+  switch (nload) {
+    case 1: map_kernel<VEC, ONE_D, 1><<<blocks, 256, 0, s>>>(p); break;
+    case 2: map_kernel<VEC, ONE_D, 2><<<blocks, 256, 0, s>>>(p); break;
+    case 3: map_kernel<VEC, ONE_D, 3><<<blocks, 256, 0, s>>>(p); break;
+    case 4: map_kernel<VEC, ONE_D, 4><<<blocks, 256, 0, s>>>(p); break;
+    default: map_kernel<VEC, ONE_D, 0><<<blocks, 256, 0, s>>>(p); break;
+  }
+}
+
+void dispatch_nl(const MapParams &p, bool vec, bool one_d, int nload, unsigned blocks,
+                 cudaStream_t s) {
+  if (vec && one_d) dispatch_vec<true, true>(p, nload, blocks, s);
+  else if (vec) dispatch_vec<true, false>(p, nload, blocks, s);
+  else if (one_d) dispatch_vec<false, true>(p, nload, blocks, s);
+  else dispatch_vec<false, false>(p, nload, blocks, s);
+}
+
 }  // namespace
 
 extern "C" int b200_map_f32(const int32_t *prog, int32_t n_words, const float *consts,
                             int32_t n_consts, float *const *ptrs, const int64_t *coefs,
                             int32_t n_ops, const int64_t *trips, int32_t nd, int32_t vector,
-                            void *stream) {
+                            int32_t nload, void *stream) {
   if (nd < 1 || nd > kMaxDims || n_ops < 1 || n_ops > kMaxOps || n_words > kMaxProg ||
       n_consts > kMaxConst)
     return B200_EINVAL;
@@ -145,12 +179,6 @@ extern "C" int b200_map_f32(const int32_t *prog, int32_t n_words, const float *c
   int64_t blocks = (total + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (nd == 1) {
-    if (vector) map_kernel<true, true><<<(unsigned)blocks, 256, 0, s>>>(p);
-    else map_kernel<false, true><<<(unsigned)blocks, 256, 0, s>>>(p);
-  } else {
-    if (vector) map_kernel<true, false><<<(unsigned)blocks, 256, 0, s>>>(p);
-    else map_kernel<false, false><<<(unsigned)blocks, 256, 0, s>>>(p);
-  }
+  dispatch_nl(p, vector != 0, nd == 1, nload, (unsigned)blocks, s);
   return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
 }

@@ -53,7 +53,7 @@ SIGNATURES = {
     "b200_contract_exact": [_I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64,
                             _I32, _I32, _I32, ctypes.c_double, _P, _I64, _P],
     "b200_pack_operand": [_I32, _P, _I64, _I64, _P, _I64, _I64, _P],
-    "b200_map_f32": [_P, _I32, _P, _I32, _P, _P, _I32, _P, _I32, _I32, _P],
+    "b200_map_f32": [_P, _I32, _P, _I32, _P, _P, _I32, _P, _I32, _I32, _I32, _P],
     "b200_gemm_tc": [_I32, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I32, _F32, _P,
                      _I64, _I32, _I32, _P],
 }
@@ -314,7 +314,7 @@ class DeviceBackend:
         prog = (ctypes.c_int32 * len(m.prog))(*m.prog)
         consts = (ctypes.c_float * max(1, len(m.consts)))(*m.consts)
         self.call("b200_map_f32", prog, len(m.prog), consts, len(m.consts), ptrs, coefs, nops,
-                  trips, nd, int(m.vector), s.stream_ptr)
+                  trips, nd, int(m.vector), m.nload, s.stream_ptr)
         return ["map_f32"]
 
     def vm(self, r, prog, checked):

@@ -159,7 +159,8 @@ def match_contraction(region, links, remainder, accesses):
 class MapMatch:
     """A pointwise f32 nest: box dims, operands, straight-line program."""
 
-    __slots__ = ("trips", "buffers", "bases", "coefs", "prog", "consts", "vector", "kind")
+    __slots__ = ("trips", "buffers", "bases", "coefs", "prog", "consts", "vector", "kind",
+                 "nload")
 
     def __repr__(self):
         return f"MapMatch({self.kind}, trips={self.trips}, ops={len(self.buffers)})"
@@ -239,6 +240,7 @@ def match_map(region, links, remainder, accesses, band):
     except ValueError:
         return None
     _merge_dims(m)
+    _hoist_loads(m)
     ops_seq, pc = [], 0
     while pc < len(m.prog):
         op = m.prog[pc] & 0xFF
@@ -253,6 +255,37 @@ def match_map(region, links, remainder, accesses, band):
     m.kind = ("fill" if ops_seq == [M_CF, M_ST] else
               "copy" if ops_seq == [M_LD, M_ST] else "ewise")
     return m
+
+
+def _hoist_loads(m):
+    """Move every load to the front of the program (loads only depend on
+    affine addresses) unless a load follows a store — then a read-after-
+    write through memory inside one point could exist and order is kept.
+    m.nload = number of leading loads (the kernel issues them together)."""
+    words, pc, seen_store = [], 0, False
+    loads, rest = [], []
+    hoistable = True
+    while pc < len(m.prog):
+        w = m.prog[pc]
+        op = w & 0xFF
+        if op == M_BF:
+            rest.append([w, m.prog[pc + 1]])
+            pc += 2
+            continue
+        if op == M_ST:
+            seen_store = True
+        if op == M_LD:
+            if seen_store:
+                hoistable = False
+            loads.append([w])
+        else:
+            rest.append([w])
+        pc += 1
+    if hoistable and len(loads) <= 4:
+        m.prog = [x for ins in loads + rest for x in ins]
+        m.nload = len(loads)
+    else:
+        m.nload = 0
 
 
 def _merge_dims(m):
