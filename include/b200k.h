@@ -152,6 +152,20 @@ int b200_gemm_tc(int32_t kind, const void *A, const void *Bt, float *C, int64_t 
                  float init_value, const float *bias, int64_t bias_stride,
                  int32_t max_ctas, int32_t variant, void *stream);
 
+/*
+ * Runtime specialisation (NVRTC, sm_100a): compile generated CUDA C `src`
+ * and return the kernel `kernel` as an opaque handle in *fn.  The engine
+ * generates straight-line kernels for region shapes whose generic execution
+ * would be interpretive (pointwise nests: reference interp/_evalpy.py:90-127
+ * per point).  b200_jit_log() returns the last compiler log.
+ */
+int b200_jit_compile(const char *src, const char *kernel, void **fn);
+const char *b200_jit_log(void);
+
+/* Launch a b200_jit_compile kernel; args = array of pointers to argument values. */
+int b200_jit_launch(void *fn, uint32_t gx, uint32_t gy, uint32_t gz, uint32_t bx, uint32_t by,
+                    uint32_t bz, uint32_t smem, void **args, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -52,7 +52,7 @@ def build(force=False, verbose=False):
             fh.write(res.stderr)
         objs.append(obj)
     cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
-           "-cudart", "static", "-o", OUT, *objs]
+           "-cudart", "static", "-o", OUT, *objs, "-ldl"]
     subprocess.run(cmd, check=True)
     return OUT
 

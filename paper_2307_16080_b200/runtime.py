@@ -56,6 +56,10 @@ SIGNATURES = {
     "b200_map_f32": [_P, _I32, _P, _I32, _P, _P, _I32, _P, _I32, _I32, _I32, _P],
     "b200_gemm_tc": [_I32, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I32, _F32, _P,
                      _I64, _I32, _I32, _P],
+    "b200_jit_compile": [ctypes.c_char_p, ctypes.c_char_p, _P],
+    "b200_jit_launch": [_P, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+                        ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+                        _P, _P],
 }
 
 
@@ -73,6 +77,8 @@ def load_library(path=LIB_PATH):
         fn = getattr(lib, name)
         fn.argtypes = argtypes
         fn.restype = ctypes.c_int
+    lib.b200_jit_log.argtypes = []
+    lib.b200_jit_log.restype = ctypes.c_char_p
     _lib = lib
     return lib
 
@@ -304,8 +310,20 @@ class DeviceBackend:
         return ["contract_exact"]
 
     def map(self, m):
-        """Run a templates.MapMatch through b200_map_f32."""
+        """Run a templates.MapMatch: an NVRTC-specialised kernel when the JIT
+        is available (straight-line native code), else b200_map_f32."""
         s = self.stage
+        from . import jit
+
+        if jit.available():
+            ptrs = [s.tensor(b).data_ptr() + 4 * base for b, base in zip(m.buffers, m.bases)]
+            ln = jit.map_launch(m, ptrs)
+            self.keep(ln)
+            if self.recording is not None:
+                self.recording.keep.append(ln)
+            self.call("b200_jit_launch", ctypes.c_void_p(ln.fn), ln.grid, 1, 1, 256, 1, 1, 0,
+                      ln.argv, s.stream_ptr)
+            return ["map_jit"]
         nd, nops = len(m.trips), len(m.buffers)
         ptrs = (ctypes.c_void_p * nops)(*[s.tensor(b).data_ptr() + 4 * base
                                           for b, base in zip(m.buffers, m.bases)])
