@@ -220,6 +220,12 @@ template <typename Addr>
 int launch(const Args<float, Addr> &g, void *stream) {
   if (g.M < 0 || g.N < 0 || g.K < 0) return B200_EINVAL;
   if (g.M == 0 || g.N == 0) return B200_OK;
+  // tile choice: big tiles amortise staging; when they would leave most SMs
+  // idle (or compute mostly padding) use smaller ones — each output's
+  // k-chain is identical for every tile shape, so results do not change.
+  const int64_t big_ctas = ((g.M + 127) / 128) * ((g.N + 127) / 128);
+  if (g.M * g.N <= 64 * 64) return launch_tile<float, Addr, 32, 32, 2, 2>(g, stream);
+  if (big_ctas < 148) return launch_tile<float, Addr, 64, 64, 4, 4>(g, stream);
   if (g.N <= 64) return launch_tile<float, Addr, 256, 64, 8, 8>(g, stream);
   return launch_tile<float, Addr, 128, 128, 8, 8>(g, stream);
 }
