@@ -21,10 +21,10 @@
 namespace {
 
 constexpr int kMaxDims = 8;
-constexpr int kMaxOps = 8;
-constexpr int kMaxRegs = 8;
-constexpr int kMaxProg = 64;   // words
-constexpr int kMaxConst = 16;
+constexpr int kMaxOps = 16;
+constexpr int kMaxRegs = 32;
+constexpr int kMaxProg = 256;  // words
+constexpr int kMaxConst = 32;
 
 enum { M_LD = 0, M_CF = 1, M_BF = 2, M_ST = 3 };
 

@@ -47,25 +47,23 @@ def _straight_line(nodes):
     return all(isinstance(n, Ins) for n in nodes)
 
 
-def _table(region, vars_, off):
+
+def _table(region, vars_, off, stat):
     """Element offsets of one operand over the mixed-radix enumeration of vars_."""
     t = np.zeros(1, dtype=np.int64)
     for v in vars_:
-        lb, st, trip = v.static()
+        lb, st, trip = stat(v)
         vals = off.t.get(v.id, 0) * (lb + st * np.arange(trip, dtype=np.int64))
         t = (t[:, None] + vals[None, :]).reshape(-1)
     return t
 
 
-def match_contraction(region, links, remainder, accesses):
-    """Return a ContractMatch for a C (+)= A*B nest, else None."""
-    if not links or not _straight_line(remainder):
-        return None
-    body = [n for n in remainder if n.op not in _IGNORED or n.op == BINF]
-    loads = [n for n in body if n.op == LOAD]
-    binf = [n for n in body if n.op == BINF]
-    stores = [n for n in body if n.op == STORE]
-    if len(loads) != 3 or len(binf) != 2 or len(stores) != 1 or len(body) != 6:
+def _statement(ops, acc):
+    """Match one `C[f] = C[f] + A[a] * B[b]` statement: (aS, aA, aB, f32)."""
+    loads = [n for n in ops if n.op == LOAD]
+    binf = [n for n in ops if n.op == BINF]
+    stores = [n for n in ops if n.op == STORE]
+    if len(loads) != 3 or len(binf) != 2 or len(stores) != 1 or len(ops) != 6:
         return None
     st = stores[0]
     add = next((n for n in binf if n.dst == st.a), None)
@@ -79,26 +77,88 @@ def match_contraction(region, links, remainder, accesses):
     if c_reg not in load_of or mul.a not in load_of or mul.b not in load_of:
         return None
     lc, la, lb = load_of[c_reg], load_of[mul.a], load_of[mul.b]
-    # the C load must precede nothing that writes C: only one store exists and
-    # it consumes `add`, so the chain is c -> c + a*b.
-    acc = {id(a.node): a for a in accesses}
     aS, aC, aA, aB = acc[id(st)], acc[id(lc)], acc[id(la)], acc[id(lb)]
-    bufs = region.buffers
     if aS.slot != aC.slot or aS.offset is None or aS.offset != aC.offset:
         return None
     if aA.offset is None or aB.offset is None or aA.slot == aS.slot or aB.slot == aS.slot:
         return None
+    return aS, aA, aB, add.f32
+
+
+def _reroll(stmts, vars_):
+    """U unrolled clones of one contraction statement -> the rolled loop.
+
+    loop-unroll (reference passes/unroll.py:42-56) multiplies the innermost
+    step by U and clones the body with iv + u*step: clone u reads A/B at a
+    constant offset u*delta from clone 0 and accumulates into the same C
+    element, so the clones are exactly the next U iterations of the
+    reduction.  Returns {var id: (lb, step, trip)} overriding the unrolled
+    variable, or None if the clones are not such a progression.
+    """
+    s0 = stmts[0]
+    U = len(stmts)
+    dS = [s[0].offset.c - s0[0].offset.c for s in stmts]
+    dA = [s[1].offset.c - s0[1].offset.c for s in stmts]
+    dB = [s[2].offset.c - s0[2].offset.c for s in stmts]
+    for s in stmts:
+        if (s[0].slot, s[1].slot, s[2].slot) != (s0[0].slot, s0[1].slot, s0[2].slot) or \
+                s[0].offset.t != s0[0].offset.t or s[1].offset.t != s0[1].offset.t or \
+                s[2].offset.t != s0[2].offset.t or s[3] != s0[3]:
+            return None
+    # the unrolled variable may be a reduction (same C, shifted A/B: the next
+    # U steps of each chain) or an output dimension (shifted C: U distinct
+    # outputs whose chains are interleaved but individually unchanged)
+    for v in vars_:
+        lb, step, trip = v.static()
+        cs, ca, cb = (s0[0].offset.t.get(v.id, 0), s0[1].offset.t.get(v.id, 0),
+                      s0[2].offset.t.get(v.id, 0))
+        if not (cs or ca or cb) or step % U:
+            continue
+        sub = step // U
+        if all(dS[u] == u * cs * sub and dA[u] == u * ca * sub and dB[u] == u * cb * sub
+               for u in range(U)):
+            return {v.id: (lb, sub, trip * U)}
+    return None
+
+
+def match_contraction(region, links, remainder, accesses):
+    """Return a ContractMatch for a C (+)= A*B nest (possibly unrolled), else None."""
+    if not links or not _straight_line(remainder):
+        return None
+    body = [n for n in remainder if n.op not in _IGNORED or n.op == BINF]
+    acc = {id(a.node): a for a in accesses}
+    stmts, cur = [], []
+    for n in body:
+        cur.append(n)
+        if n.op == STORE:
+            s = _statement(cur, acc)
+            if s is None:
+                return None
+            stmts.append(s)
+            cur = []
+    if cur or not stmts:
+        return None
+    vars_ = [v for link in links for v in link.vars]
+    ovr = {}
+    if len(stmts) > 1:
+        ovr = _reroll(stmts, vars_)
+        if ovr is None:
+            return None
+    aS, aA, aB, f32 = stmts[0]
+    bufs = region.buffers
     C, A, B = bufs[aS.slot], bufs[aA.slot], bufs[aB.slot]
     dtype = C.dtype
     if dtype not in ("f32", "f64") or A.dtype != dtype or B.dtype != dtype:
         return None
-    if add.f32 != (dtype == "f32"):
+    if f32 != (dtype == "f32"):
         return None
 
-    vars_ = [v for link in links for v in link.vars]
+    def stat(v):
+        return ovr.get(v.id) or v.static()
+
     groups = {"m": [], "n": [], "k": []}
     for v in vars_:
-        lb_, step, trip = v.static()
+        lb_, step, trip = stat(v)
         cc, ca, cb = (aS.offset.t.get(v.id, 0), aA.offset.t.get(v.id, 0),
                       aB.offset.t.get(v.id, 0))
         if trip == 1:
@@ -116,12 +176,12 @@ def match_contraction(region, links, remainder, accesses):
     # M / N: order by decreasing |C stride| so the last (fastest) index is the
     # most contiguous in C; K: nest order (the reference's reduction order).
     for key in ("m", "n"):
-        groups[key].sort(key=lambda v: -abs(aS.offset.t.get(v.id, 0) * v.static()[1]))
+        groups[key].sort(key=lambda v: -abs(aS.offset.t.get(v.id, 0) * stat(v)[1]))
 
     g = ContractMatch()
     g.A, g.B, g.C, g.dtype = A, B, C, dtype
     g.m_vars, g.n_vars, g.k_vars = groups["m"], groups["n"], groups["k"]
-    prod = lambda vs: int(np.prod([v.static()[2] for v in vs])) if vs else 1  # noqa: E731
+    prod = lambda vs: int(np.prod([stat(v)[2] for v in vs])) if vs else 1  # noqa: E731
     g.M, g.N, g.K = prod(g.m_vars), prod(g.n_vars), prod(g.k_vars)
 
     def const(off, used):
@@ -131,29 +191,30 @@ def match_contraction(region, links, remainder, accesses):
                 c += coef * region.vars[vid].static()[0]   # trip-1 vars
         return c
 
-    used = {v.id for v in vars_ if v.static()[2] > 1}
+    used = {v.id for v in vars_ if stat(v)[2] > 1}
     cA, cB, cC = const(aA.offset, used), const(aB.offset, used), const(aS.offset, used)
-    a_m = _table(region, g.m_vars, aA.offset) + cA
-    a_k = _table(region, g.k_vars, aA.offset)
-    b_k = _table(region, g.k_vars, aB.offset) + cB
-    b_n = _table(region, g.n_vars, aB.offset)
-    c_m = _table(region, g.m_vars, aS.offset) + cC
-    c_n = _table(region, g.n_vars, aS.offset)
+    a_m = _table(region, g.m_vars, aA.offset, stat) + cA
+    a_k = _table(region, g.k_vars, aA.offset, stat)
+    b_k = _table(region, g.k_vars, aB.offset, stat) + cB
+    b_n = _table(region, g.n_vars, aB.offset, stat)
+    c_m = _table(region, g.m_vars, aS.offset, stat) + cC
+    c_n = _table(region, g.n_vars, aS.offset, stat)
     g.tables = (a_m, a_k, b_k, b_n, c_m, c_n)
     # outputs must be distinct (writes of different (m, n) never collide)
-    terms = [(abs(aS.offset.t.get(v.id, 0) * v.static()[1]), v.static()[2])
+    terms = [(abs(aS.offset.t.get(v.id, 0) * stat(v)[1]), stat(v)[2])
              for v in g.m_vars + g.n_vars]
     if not _mixed_radix_injective(terms, 0):
         return None
     g.strided = len(g.m_vars) <= 1 and len(g.n_vars) <= 1 and len(g.k_vars) == 1
     if g.strided:
         def stride(off, vs):
-            return off.t.get(vs[0].id, 0) * vs[0].static()[1] if vs else 0
+            return off.t.get(vs[0].id, 0) * stat(vs[0])[1] if vs else 0
         g.sA = (stride(aA.offset, g.m_vars), stride(aA.offset, g.k_vars))
         g.sB = (stride(aB.offset, g.k_vars), stride(aB.offset, g.n_vars))
         g.sC = (stride(aS.offset, g.m_vars), stride(aS.offset, g.n_vars))
         g.offA, g.offB, g.offC = int(a_m[0] + a_k[0]), int(b_k[0] + b_n[0]), int(c_m[0] + c_n[0])
     return g
+
 
 
 class MapMatch:
@@ -191,14 +252,14 @@ def match_map(region, links, remainder, accesses, band):
         return regs.get(v)
 
     def new_reg(v):
-        if len(regs) >= 8:
+        if len(regs) >= 32:
             raise ValueError
         regs[v] = len(regs)
         return regs[v]
 
     def operand(a):
         buf = region.buffers[a.slot]
-        if buf.dtype != "f32" or a.offset is None or len(m.buffers) >= 8:
+        if buf.dtype != "f32" or a.offset is None or len(m.buffers) >= 16:
             raise ValueError
         base = a.offset.c
         for vid, c in a.offset.t.items():
@@ -223,7 +284,7 @@ def match_map(region, links, remainder, accesses, band):
                 m.prog.append(M_ST | (r << 8) | (k << 16))
                 n_mem += 1
             elif n.op == CONST and isinstance(n.value, float):
-                if len(m.consts) >= 16:
+                if len(m.consts) >= 32:
                     return None
                 m.consts.append(n.value)
                 m.prog.append(M_CF | (new_reg(n.dst) << 8) | ((len(m.consts) - 1) << 16))
@@ -246,7 +307,7 @@ def match_map(region, links, remainder, accesses, band):
         op = m.prog[pc] & 0xFF
         ops_seq.append(op)
         pc += 2 if op == M_BF else 1
-    if M_ST not in ops_seq or len(m.prog) > 64:
+    if M_ST not in ops_seq or len(m.prog) > 256:
         return None
     inner = len(m.trips) - 1
     m.vector = m.trips[inner] % 4 == 0 and all(
