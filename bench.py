@@ -444,6 +444,115 @@ def run_ours(args, rank, world, local):
     print(json.dumps(line), flush=True)
 
 
+SWEEP_T = [1, 2, 4, 8, 16, 32, 64, 128]
+SWEEP_U = [1, 2, 4, 8]
+
+
+def run_sweep(args, rank, world, local, impl):
+    """The paper's tile-size / unroll design-space sweep (BASELINE configs[4]).
+
+    512 configurations = tiles T x T (T in 1..128) x unroll U (1, 2, 4, 8) on
+    two targets — the matmul nest (parallel form, 1024^3) and the paper's
+    conv (1,1,1280,1280)*(1,3,3) — each enumerated exhaustively after the
+    identity trial (strategy "grid").  Trials are sharded idx % world; one
+    all_gather_object of the trial records at the end.  Timed: the trial
+    phase (max over ranks, wall clock: every trial includes host-side pass
+    pipelines, plan building and the reference's correctness guard).
+    """
+    import torch
+
+    from paper_2307_16080_b200 import sweep
+    from staircase.tuner import ParamSpace
+
+    space = ParamSpace(tile_sizes=(SWEEP_T, SWEEP_T), unroll_factors=SWEEP_U)
+    targets = [(bk.mm_par1024, 2.0 * 1024 ** 3), (bk.conv_paper, 2.0 * 1280 * 1280 * 9)]
+    if impl == "reference":
+        if rank != 0:
+            return
+        for _ in range(args.warmup):
+            reference_sweep_rate(budget=4)
+        rates = [reference_sweep_rate()[0] for _ in range(max(1, min(args.steps, 3)))]
+        value = statistics.median(rates)
+        note = reference_sweep_rate.__doc__.strip()
+        print(json.dumps({
+            "impl": "reference", "metric": "configs/s (tile/unroll design-space sweep)",
+            "value": value, "unit": "configs/s", "n_gpus": world, "steps": len(rates),
+            "warmup": args.warmup, "ms_per_step": 1e3 / value, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "reference tuner trials at desk scale (full-size sweep "
+                                   "trials are infeasible on the CPU executor)"},
+            "cpu_baseline": {"value": value, "unit": "configs/s", "cores": 1,
+                             "kind": "reference", "sample": note},
+            "e2e": {"value": value, "unit": "configs/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}), flush=True)
+        return
+    b2_prec = args.precision or "exact"
+    import paper_2307_16080_b200 as b2
+
+    b2.configure(precision=b2_prec)
+    total_trials, trial_s, setup_s, flops = 0, 0.0, 0.0, 0.0
+    logs = []
+    for fn, f in targets:
+        timing = {}
+        barrier(world)
+        best, log = sweep.search(fn.module, None, space, budget=1 + len(SWEEP_T) ** 2 *
+                                 len(SWEEP_U), seed=0, strategy="grid", timing=timing)
+        torch.cuda.synchronize()
+        trial_s += max_over_ranks(timing["trials_s"], world)
+        setup_s += max_over_ranks(timing["setup_s"], world)
+        total_trials += len(log)
+        flops += f * len(log)
+        logs.append((fn.__name__, best, log))
+    if rank != 0:
+        return
+    # the reference tuner's per-trial rate on the same sweep machinery at desk
+    # scale (conv_small, reference _evalcy engine): full-size trials would take
+    # minutes to hours each on the CPU executor
+    cpu_rate, cpu_note = reference_sweep_rate()
+    line = {
+        "metric": "configs/s (tile/unroll design-space sweep)", "value": total_trials / trial_s,
+        "unit": "configs/s", "n_gpus": world, "steps": 1, "warmup": 0,
+        "ms_per_step": 1e3 * trial_s, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": b2_prec if b2_prec != "exact" else "f32",
+        "data": "synthetic (tuner make_inputs, seed 0)",
+        "config": {"workload": "512-config sweep: tiles T x T (T=1..128) x unroll (1,2,4,8) on "
+                               "matmul 1024^3 (parallel form) and conv (1,1,1280,1280)*(1,3,3)",
+                   "strategy": "grid (identity first)", "trials": total_trials,
+                   "parallelism": f"trial shard idx % {world}",
+                   "setup_s_max_rank": setup_s,
+                   "best": {n: {"idx": b.idx, "params": b.params, "cost": b.cost}
+                            for n, b, _ in logs}},
+        "gflops_evaluated_per_s": flops / trial_s / 1e9,
+        "e2e": {"value": total_trials / (trial_s + setup_s), "unit": "configs/s",
+                "h2d_bytes_per_step": None, "d2h_bytes_per_step": None},
+        "cpu_baseline": {"value": cpu_rate, "unit": "configs/s", "cores": 1,
+                         "kind": "reference", "sample": cpu_note},
+        "gpu_launches": None,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def reference_sweep_rate(budget=8):
+    """Trials/s of the reference tuner (tuner.search, _evalcy) on conv_small."""
+    import importlib
+
+    from staircase.interp import _evalcy, machine
+    from staircase.tuner import ParamSpace
+
+    ref = importlib.import_module("staircase.tuner.search")
+    space = ParamSpace(tile_sizes=([1, 2, 4, 8, 16], [1, 2, 4, 8, 16]), unroll_factors=(1, 2, 4))
+    saved = machine._engine
+    machine._engine = _evalcy
+    try:
+        t0 = time.perf_counter()
+        ref.search(bk.conv_desk_small.module, None, space, budget=budget, seed=0)
+        dt = time.perf_counter() - t0
+    finally:
+        machine._engine = saved
+    return budget / dt, (f"reference tuner.search, budget {budget}, conv 1x1x18x18*(2,1,3,3) "
+                         f"desk kernel, _evalcy ({dt:.2f} s)")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -451,11 +560,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="mm", choices=["mm", "conv", "ls", "linear32",
-                                                         "ewise"])
+                                                         "ewise", "sweep"])
     ap.add_argument("--precision", default=None, choices=["bf16", "tf32", "exact"])
     args = ap.parse_args()
     rank, world, local = dist_setup()
-    if args.impl == "reference":
+    if args.workload == "sweep":
+        run_sweep(args, rank, world, local, args.impl)
+    elif args.impl == "reference":
         run_reference(args, rank, world)
     else:
         run_ours(args, rank, world, local)

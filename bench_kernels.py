@@ -13,7 +13,7 @@ they live in a module.
               bias nests (two Linear lowerings chained, fill into the output)
   saxpy4k     elementwise y = y + x * 2 over 4096 x 4096 f32
 """
-from staircase import F32, MemRef, constant, parallel, staged
+from staircase import F32, F64, MemRef, constant, parallel, staged
 
 # -- matmul -------------------------------------------------------------------
 
@@ -140,6 +140,39 @@ def linear_stack(x: MemRef[({rows}, 1024), F32], w1t: MemRef[(1024, 4096), F32],
 def saxpy4k(x: MemRef[(4096, 4096), F32], y: MemRef[(4096, 4096), F32]):
     for i, j in parallel((0, 0), (4096, 4096)):
         y[i, j] = y[i, j] + x[i, j] * constant(2.0, F32)
+
+
+# -- design-space sweep targets (tiled / unrolled by the tuner's pipeline) ----------
+
+
+@staged
+def mm_par1024(A: MemRef[(1024, 1024), F32], B: MemRef[(1024, 1024), F32],
+               C: MemRef[(1024, 1024), F32]):
+    for i, k in parallel((0, 0), (1024, 1024)):
+        for j in range(1024):
+            C[i, k] += A[i, j] * B[j, k]
+
+
+@staged
+def conv_paper(inp: MemRef[(1, 1, 1282, 1282), F32], ker: MemRef[(1, 1, 3, 3), F32],
+               out: MemRef[(1, 1, 1280, 1280), F32]):
+    # the paper's tuning target: (1,1,1280,1280) * (1,3,3)
+    for n, co, ho, wo in parallel((0, 0, 0, 0), (1, 1, 1280, 1280)):
+        for ci in range(0, 1):
+            for ki in range(0, 3):
+                for kj in range(0, 3):
+                    out[n, co, ho, wo] += inp[n, ci, ho + ki, wo + kj] * ker[co, ci, ki, kj]
+
+
+@staged
+def conv_desk_small(input: MemRef[(1, 1, 18, 18), F64], kernel: MemRef[(2, 1, 3, 3), F64],
+                    output: MemRef[(1, 2, 16, 16), F64]):
+    # desk-scale tuning target (reference tests/kernels.py:67-88 shapes)
+    for n, co, ho, wo in parallel((0, 0, 0, 0), (1, 2, 16, 16)):
+        for ci in range(0, 1):
+            for ki in range(0, 3):
+                for kj in range(0, 3):
+                    output[n, co, ho, wo] += input[n, ci, ho + ki, wo + kj] * kernel[co, ci, ki, kj]
 
 
 @staged

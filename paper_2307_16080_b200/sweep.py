@@ -1,0 +1,217 @@
+"""The tile-size / unroll design-space sweep, sharded across GPUs.
+
+Reference: ``staircase.tuner.search`` (reference pkg/src/staircase/tuner/
+search.py:237-279) evaluates ``budget`` trials in sequence, trial 0 being the
+identity point; each trial instantiates the pipeline template
+(``default_pipeline``, search.py:38-53), runs it, interprets the result on
+fixed seeded inputs, checks it against the baseline (rel 1e-6 / abs 1e-9,
+search.py:109-138) and scores it with the tally cost model (or wall time).
+
+``search`` here keeps those semantics by reusing the reference's own
+``_Session`` for every trial (baseline, pass pipeline, guard, scoring) and
+only changes *where* trials run: with ``torch.distributed`` initialised,
+trial ``idx`` runs on rank ``idx % world``; every rank then exchanges its
+trial records with one ``all_gather_object`` (NCCL or gloo) and all ranks
+return the same ``(best, log)``.  For the ``random`` strategy the trial
+parameters depend only on the seed (search.py:220-224), so every rank
+regenerates the full sequence and the merged log equals the sequential log
+(``objective="model"``: costs come from the exact tally).  ``grid`` (an
+extension: trial 0 identity, then the Cartesian product in order) shards the
+same way.  ``one_plus_one_es`` depends on earlier costs (search.py:226-234,
+272-275) and runs as identical replicas on every rank.
+
+Trials run on the B200 engine (``install()`` is applied for the duration),
+which is what the reference ``run()`` inside ``_Session`` dispatches to.
+"""
+from __future__ import annotations
+
+import itertools
+import math
+import random
+
+import numpy as np
+
+from .host import ensure_staircase
+
+
+def _dist():
+    try:
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized():
+            return dist
+    except ImportError:
+        pass
+    return None
+
+
+def _fast_buffers_close(got, want):
+    """Vectorised twin of the reference guard's element test
+    (math.isclose(g, w, rel_tol=1e-6, abs_tol=1e-9) over every element,
+    tuner/search.py:128-138): same predicate, numpy instead of a Python loop."""
+    from staircase.interp import Buffer
+
+    if not isinstance(got, Buffer) or got.shape != want.shape:
+        return False
+    if want.dtype not in ("f32", "f64"):
+        return list(got.data) == list(want.data)
+    dt = np.float32 if want.dtype == "f32" else np.float64
+    g = np.frombuffer(got.data, dtype=dt).astype(np.float64)
+    w = np.frombuffer(want.data, dtype=dt).astype(np.float64)
+    with np.errstate(invalid="ignore", over="ignore"):
+        diff = np.abs(g - w)
+        tol = np.maximum(1e-6 * np.maximum(np.abs(g), np.abs(w)), 1e-9)
+        close = (g == w) | (diff <= tol)
+    return bool(np.all(close))
+
+
+def _session_class():
+    ensure_staircase()
+    import importlib
+
+    # the module (staircase.tuner re-exports the function under the same name)
+    ref = importlib.import_module("staircase.tuner.search")
+
+    class Session(ref._Session):
+        """The reference trial session with a vectorised equivalence guard."""
+
+    def _state_matches(got_results, got_args, want_results, want_args):
+        from staircase.interp import Buffer
+
+        if len(got_results) != len(want_results):
+            return False
+        for g, w in zip(got_results, want_results):
+            if isinstance(w, Buffer):
+                if not _fast_buffers_close(g, w):
+                    return False
+            elif not ref._values_close(g, w):
+                return False
+        for g, w in zip(got_args, want_args):
+            if isinstance(w, Buffer) and not _fast_buffers_close(g, w):
+                return False
+        return True
+
+    return Session, ref, _state_matches
+
+
+def _params(space, budget, seed, strategy):
+    """Trial parameters for idx 1..budget-1 (random / grid only)."""
+    out = {}
+    if strategy == "random":
+        from staircase.tuner.search import _sample_random
+
+        rng = random.Random(seed)
+        for idx in range(1, budget):
+            out[idx] = _sample_random(space, rng)
+    else:   # grid
+        pts = itertools.product(*space.tile_sizes, space.unroll_factors)
+        for idx, pt in zip(range(1, budget), pts):
+            out[idx] = (list(pt[:-1]), pt[-1])
+    return out
+
+
+def search(kernel, pipeline_template=None, space=None, budget: int = 20, seed: int = 0,
+           strategy: str = "random", *, func=None, objective="model", mode="sequential",
+           workers=1, engine=None, rank=None, world=None, timing=None):
+    """``tuner.search`` with trials sharded over torch.distributed ranks.
+
+    Returns ``(best, log)`` exactly like the reference; ``log`` is sorted by
+    trial index and identical on every rank.  ``timing`` (a dict), if given,
+    receives this rank's ``setup_s`` (inputs + baseline run), ``trials_s``
+    (its share of the trials), ``gather_s`` and ``trials`` (count).
+    """
+    import time
+
+    t_start = time.perf_counter()
+    ensure_staircase()
+    from staircase.errors import EmptySpace
+    from staircase.interp import machine
+    from staircase.tuner.space import Trial
+
+    if space is None:
+        raise EmptySpace("search needs a ParamSpace")
+    if not isinstance(budget, int) or isinstance(budget, bool) or budget < 1:
+        raise ValueError(f"budget must be a positive integer, got {budget!r}")
+    strategy = {"es": "one_plus_one_es", "1+1-es": "one_plus_one_es"}.get(strategy, strategy)
+    if strategy not in ("random", "one_plus_one_es", "grid"):
+        raise ValueError(f"unknown strategy {strategy!r}")
+    if strategy == "grid":
+        budget = min(budget, 1 + math.prod(len(d) for d in space.tile_sizes) *
+                     len(space.unroll_factors))
+    dist = _dist()
+    if rank is None:
+        rank = dist.get_rank() if dist else 0
+    if world is None:
+        world = dist.get_world_size() if dist else 1
+
+    if engine is None:
+        from . import engine as b200_engine
+
+        engine = b200_engine
+    Session, ref, fast_match = _session_class()
+    saved_engine, saved_match = machine._engine, ref._state_matches
+    machine._engine = engine          # _Session.run() passes no engine= (search.py:170,190)
+    ref._state_matches = fast_match   # same predicate, vectorised
+    try:
+        module = ref._resolve_module(kernel)
+        session = Session(module, func=func, seed=seed, objective=objective,
+                          pipeline_template=pipeline_template, mode=mode, workers=workers)
+        if strategy == "one_plus_one_es":
+            # cost-dependent mutations: sequential by definition; every rank
+            # runs the same replica (no exchange needed)
+            best, log = _es(session, space, budget, seed)
+            return best, log
+        identity = space.identity()
+        params = _params(space, budget, seed, strategy)
+        mine = []
+        t_trials = time.perf_counter()
+        for idx in range(budget):
+            if idx % world != rank:
+                continue
+            if idx == 0:
+                t = session.trial(0, identity["tiles"], identity["unroll"])
+            else:
+                tiles, unroll = params[idx]
+                t = session.trial(idx, tiles, unroll)
+            mine.append((t.idx, t.params, t.cost, t.status, t.seed, t.stats))
+        t_gather = time.perf_counter()
+        if dist is not None and world > 1:
+            gathered = [None] * world
+            dist.all_gather_object(gathered, mine)
+        else:
+            gathered = [mine]
+        if timing is not None:
+            timing.update(setup_s=t_trials - t_start, trials_s=t_gather - t_trials,
+                          gather_s=time.perf_counter() - t_gather, trials=len(mine))
+        records = sorted((r for part in gathered for r in part), key=lambda r: r[0])
+        log = [Trial(i, p, c, s, sd, stats=st) for i, p, c, s, sd, st in records]
+        evaluated = [t for t in log if t.status == "evaluated"]
+        best = min(evaluated, key=lambda t: (t.cost, t.idx))
+        return best, log
+    finally:
+        machine._engine = saved_engine
+        ref._state_matches = saved_match
+
+
+def _es(session, space, budget, seed):
+    """(1+1)-ES exactly as search.py:261-279."""
+    from staircase.tuner.search import _mutate
+
+    identity = space.identity()
+    log = [session.trial(0, identity["tiles"], identity["unroll"])]
+    rng = random.Random(seed)
+    parent = dict(log[0].params)
+    parent_cost = log[0].cost
+    for idx in range(1, budget):
+        tiles, unroll = _mutate(space, parent, rng)
+        trial = session.trial(idx, tiles, unroll)
+        log.append(trial)
+        if trial.status == "evaluated" and trial.cost < parent_cost:
+            parent = dict(trial.params)
+            parent_cost = trial.cost
+    evaluated = [t for t in log if t.status == "evaluated"]
+    best = min(evaluated, key=lambda t: (t.cost, t.idx))
+    return best, log
+
+
+__all__ = ["search"]

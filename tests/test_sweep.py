@@ -1,0 +1,112 @@
+"""Sharded design-space sweep: logs equal the reference tuner's (CPU, gloo).
+
+The reference ``staircase.tuner.search`` (tuner/search.py:237-279) is the
+ground truth: for the same kernel, space, seed, budget and strategy the
+sharded sweep must return an identical log (Trial equality: idx, params,
+cost, status, seed) and the same best trial, for world sizes 1 and 2
+(torch.distributed gloo on 127.0.0.1).  On CPU the trials run on the C
+oracle engine; tests/test_gpu_sweep.py repeats this on the B200 engine.
+"""
+import os
+import socket
+import tempfile
+
+import pytest
+
+import conftest  # noqa: F401  (spawned workers re-import this module: shim first)
+import corpus
+import oracle
+
+SPACE_ARGS = dict(tile_sizes=([1, 2, 4, 8, 16], [1, 2, 4, 8, 16]), unroll_factors=(1, 2, 4))
+
+
+def _space():
+    from staircase.tuner import ParamSpace
+
+    return ParamSpace(**SPACE_ARGS)
+
+
+def _ref(kernel, budget, seed, strategy):
+    from staircase.interp import machine
+    from staircase.tuner import search
+
+    saved = machine._engine
+    machine._engine = oracle
+    try:
+        return search(kernel, None, _space(), budget=budget, seed=seed, strategy=strategy)
+    finally:
+        machine._engine = saved
+
+
+@pytest.mark.parametrize("strategy", ["random", "es"])
+def test_world1_equals_reference(strategy):
+    from paper_2307_16080_b200 import sweep
+
+    oracle.build()
+    kernel = corpus.conv_small.module
+    best_r, log_r = _ref(kernel, 10, 7, strategy)
+    best, log = sweep.search(kernel, None, _space(), budget=10, seed=7, strategy=strategy,
+                             engine=oracle, rank=0, world=1)
+    assert log == log_r
+    assert best == best_r
+
+
+def test_grid_strategy_enumerates_the_space_in_order():
+    from paper_2307_16080_b200 import sweep
+
+    oracle.build()
+    best, log = sweep.search(corpus.conv_small.module, None, _space(), budget=6, seed=0,
+                             strategy="grid", engine=oracle, rank=0, world=1)
+    assert [t.params["tiles"] for t in log] == [[1, 1], [1, 1], [1, 1], [1, 1], [1, 2], [1, 2]]
+    assert [t.params["unroll"] for t in log] == [1, 1, 2, 4, 1, 2]
+    assert best.cost <= log[0].cost
+
+
+def _worker(rank, world, port, out_dir, budget, seed):
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path[:0] = [here, os.path.dirname(here)]
+    import conftest  # noqa: F401  (path + staircase shim)
+    import torch.distributed as dist
+
+    import corpus as c
+    import oracle as o
+    from paper_2307_16080_b200 import sweep
+    from staircase.tuner import ParamSpace
+    from staircase.tuner.log import persist
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        best, log = sweep.search(c.conv_small.module, None, ParamSpace(**SPACE_ARGS),
+                                 budget=budget, seed=seed, strategy="random", engine=o)
+        persist(log, os.path.join(out_dir, f"log{rank}.jsonl"))
+        with open(os.path.join(out_dir, f"best{rank}.txt"), "w") as fh:
+            fh.write(f"{best.idx} {best.cost}")
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def test_world2_gloo_log_equals_reference():
+    import torch.multiprocessing as mp
+    from staircase.tuner.log import load
+
+    oracle.build()
+    budget, seed = 12, 3
+    best_r, log_r = _ref(corpus.conv_small.module, budget, seed, "random")
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(2, _free_port(), d, budget, seed), nprocs=2, join=True)
+        for rank in range(2):
+            log = load(os.path.join(d, f"log{rank}.jsonl"))
+            assert log == log_r
+            idx, cost = open(os.path.join(d, f"best{rank}.txt")).read().split()
+            assert int(idx) == best_r.idx and float(cost) == best_r.cost
