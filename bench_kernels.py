@@ -165,6 +165,25 @@ def conv_paper(inp: MemRef[(1, 1, 1282, 1282), F32], ker: MemRef[(1, 1, 3, 3), F
 
 
 @staged
+def mm_slice1024(A: MemRef[(1, 1024), F32], B: MemRef[(1024, 1024), F32],
+                 C: MemRef[(1, 1024), F32]):
+    # one output row of mm_par1024: same loop structure and reduction length
+    for i, k in parallel((0, 0), (1, 1024)):
+        for j in range(1024):
+            C[i, k] += A[i, j] * B[j, k]
+
+
+@staged
+def conv_paper_slice(inp: MemRef[(1, 1, 10, 1282), F32], ker: MemRef[(1, 1, 3, 3), F32],
+                     out: MemRef[(1, 1, 8, 1280), F32]):
+    for n, co, ho, wo in parallel((0, 0, 0, 0), (1, 1, 8, 1280)):
+        for ci in range(0, 1):
+            for ki in range(0, 3):
+                for kj in range(0, 3):
+                    out[n, co, ho, wo] += inp[n, ci, ho + ki, wo + kj] * ker[co, ci, ki, kj]
+
+
+@staged
 def conv_desk_small(input: MemRef[(1, 1, 18, 18), F64], kernel: MemRef[(2, 1, 3, 3), F64],
                     output: MemRef[(1, 2, 16, 16), F64]):
     # desk-scale tuning target (reference tests/kernels.py:67-88 shapes)
