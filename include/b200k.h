@@ -153,6 +153,26 @@ int b200_gemm_tc(int32_t kind, const void *A, const void *Bt, float *C, int64_t 
                  int32_t max_ctas, int32_t variant, void *stream);
 
 /*
+ * Convolution on the tensor cores (conv_2d_nchw_fchw, valid, stride 1;
+ * reference tests/kernels.py:50-64), engine precision
+ * bf16.  b200_pack_conv_input: NCHW f32 (element strides sstr[4], HOST array)
+ * -> NHWC bf16 with channels zero-padded to cp (multiple of 64).
+ * b200_pack_conv_weight: FCHW f32 -> [F][KH][KW][cp] bf16.
+ * b200_conv2d_tc: out[n,f,h,w] = (init ? init_value : out[..]) + sum over
+ * (ki, kj, c) of in*w, fp32 accumulation in TMEM (tcgen05.mma, TMA operand
+ * boxes, weights resident in shared memory).  out_strides: HOST array of the
+ * NCHW element strides (w stride must be 1).  F in {32, 64, 128}.
+ */
+int b200_pack_conv_input(const float *src, const int64_t *sstr, void *dst, int64_t nb,
+                         int64_t c, int64_t h, int64_t w, int64_t cp, void *stream);
+int b200_pack_conv_weight(const float *src, const int64_t *sstr, void *dst, int64_t f,
+                          int64_t c, int64_t kh, int64_t kw, int64_t cp, void *stream);
+int b200_conv2d_tc(const void *in_nhwc, const void *wt, float *out, const int64_t *out_strides,
+                   int64_t nb, int64_t cp, int64_t hp, int64_t wp, int64_t f, int64_t ho,
+                   int64_t wo, int64_t kh, int64_t kw, int32_t init, float init_value,
+                   void *stream);
+
+/*
  * Runtime specialisation (NVRTC, sm_100a): compile generated CUDA C `src`
  * and return the kernel `kernel` as an opaque handle in *fn.  The engine
  * generates straight-line kernels for region shapes whose generic execution

@@ -56,6 +56,10 @@ SIGNATURES = {
     "b200_map_f32": [_P, _I32, _P, _I32, _P, _P, _I32, _P, _I32, _I32, _I32, _P],
     "b200_gemm_tc": [_I32, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I32, _F32, _P,
                      _I64, _I32, _I32, _P],
+    "b200_pack_conv_input": [_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _P],
+    "b200_pack_conv_weight": [_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _P],
+    "b200_conv2d_tc": [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64,
+                       _I32, _F32, _P],
     "b200_jit_compile": [ctypes.c_char_p, ctypes.c_char_p, _P],
     "b200_jit_launch": [_P, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
                         ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
@@ -192,6 +196,15 @@ def tc_supported(precision, K):
         (K * (2 if precision == "bf16" else 4)) % 16 == 0
 
 
+def conv_tc_supported(cv):
+    """The tcgen05 conv kernel: F in {32, 64, 128}, weights resident in smem."""
+    cp = -(-cv.c // 64) * 64
+    if cv.f not in (32, 64, 128):
+        return False
+    smem = 1024 + cv.kh * cv.kw * (cp // 64) * cv.f * 128 + 5 * 16384 + 2 * cv.f * 512 + 256
+    return smem <= 232448 and cv.out.strides[3] == 1
+
+
 def _direct_call(lib):
     def call(name, *args):
         check(getattr(lib, name)(*args), name)
@@ -288,6 +301,12 @@ class DeviceBackend:
         tA, tB, tC = s.tensor(g.A), s.tensor(g.B), s.tensor(g.C)
         esz = 4 if g.dtype == "f32" else 8
         bias_ptr = s.tensor(bias).data_ptr() + esz * bias_base if bias is not None else None
+        if precision == "bf16" and bias is None:
+            from .templates import conv_view
+
+            cv = conv_view(None, g)
+            if cv is not None and conv_tc_supported(cv):
+                return self.conv_tc(cv, init, init_value)
         if g.strided and g.dtype == "f32":
             return launch_gemm(s.lib, precision, tA.data_ptr() + 4 * g.offA, g.sA,
                                tB.data_ptr() + 4 * g.offB, g.sB, tC.data_ptr() + 4 * g.offC,
@@ -308,6 +327,28 @@ class DeviceBackend:
                   P(tabs[5].data_ptr()), g.M, g.N, g.K, a_k_fast, b_n_fast, init, init_value,
                   P(bias_ptr) if bias_ptr else None, bias_stride, s.stream_ptr)
         return ["contract_exact"]
+
+    def conv_tc(self, cv, init=0, init_value=0.0):
+        """conv_2d_nchw_fchw on the tensor cores (bf16 operands, fp32 accumulate)."""
+        s = self.stage
+        cp = -(-cv.c // 64) * 64
+        inp, ker, out = s.tensor(cv.inp), s.tensor(cv.ker), s.tensor(cv.out)
+        xin = workspace(2, "bfloat16", cv.nb * cv.hp * cv.wp, cp)
+        xw = workspace(3, "bfloat16", cv.f, cv.kh * cv.kw * cp)
+        P = ctypes.c_void_p
+        I4 = ctypes.c_int64 * 4
+        sin, sw, sout = I4(*cv.inp.strides), I4(*cv.ker.strides), I4(*cv.out.strides)
+        if self.recording is not None:
+            self.recording.keep.append((sin, sw, sout))
+        self.keep(sin, sw, sout)
+        self.call("b200_pack_conv_input", P(inp.data_ptr()), sin, P(xin.data_ptr()), cv.nb,
+                  cv.c, cv.hp, cv.wp, cp, s.stream_ptr)
+        self.call("b200_pack_conv_weight", P(ker.data_ptr()), sw, P(xw.data_ptr()), cv.f, cv.c,
+                  cv.kh, cv.kw, cp, s.stream_ptr)
+        self.call("b200_conv2d_tc", P(xin.data_ptr()), P(xw.data_ptr()), P(out.data_ptr()),
+                  sout, cv.nb, cp, cv.hp, cv.wp, cv.f, cv.ho, cv.wo, cv.kh, cv.kw, init,
+                  init_value, s.stream_ptr)
+        return ["pack_conv_input", "pack_conv_weight", "conv2d_tc_bf16"]
 
     def map(self, m):
         """Run a templates.MapMatch: an NVRTC-specialised kernel when the JIT

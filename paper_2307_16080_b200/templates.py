@@ -36,7 +36,7 @@ class ContractMatch:
     """A recognised contraction: operands, groups and addressing."""
 
     __slots__ = ("A", "B", "C", "dtype", "M", "N", "K", "m_vars", "n_vars", "k_vars",
-                 "tables", "strided", "offA", "offB", "offC", "sA", "sB", "sC")
+                 "tables", "strided", "offA", "offB", "offC", "sA", "sB", "sC", "offsets")
 
     def __repr__(self):
         return (f"ContractMatch({self.dtype}, M={self.M}, N={self.N}, K={self.K}, "
@@ -180,6 +180,7 @@ def match_contraction(region, links, remainder, accesses):
 
     g = ContractMatch()
     g.A, g.B, g.C, g.dtype = A, B, C, dtype
+    g.offsets = (aA.offset, aB.offset, aS.offset)
     g.m_vars, g.n_vars, g.k_vars = groups["m"], groups["n"], groups["k"]
     prod = lambda vs: int(np.prod([stat(v)[2] for v in vs])) if vs else 1  # noqa: E731
     g.M, g.N, g.K = prod(g.m_vars), prod(g.n_vars), prod(g.k_vars)
@@ -215,6 +216,87 @@ def match_contraction(region, links, remainder, accesses):
         g.offA, g.offB, g.offC = int(a_m[0] + a_k[0]), int(b_k[0] + b_n[0]), int(c_m[0] + c_n[0])
     return g
 
+
+
+class ConvView:
+    """A contraction that is exactly conv_2d_nchw_fchw (valid, stride 1)."""
+
+    __slots__ = ("nb", "c", "hp", "wp", "f", "ho", "wo", "kh", "kw", "inp", "ker", "out")
+
+    def __repr__(self):
+        return (f"ConvView(nb={self.nb}, c={self.c}, {self.hp}x{self.wp} -> f={self.f}, "
+                f"{self.ho}x{self.wo}, {self.kh}x{self.kw})")
+
+
+def conv_view(region, g):
+    """Recognise out[n,f,h,w] += in[n,c,h+i,w+j] * w[f,c,i,j] (reference
+    tests/kernels.py:50-64) from a ContractMatch's index maps: every variable
+    must start at 0 with step 1 and carry exactly the conv's coefficients."""
+    if g is None or g.dtype != "f32":
+        return None
+    A, B, C = g.A, g.B, g.C
+    if len(A.shape) != 4 or len(B.shape) != 4 or len(C.shape) != 4:
+        return None
+    sa, sb, sc = A.strides, B.strides, C.strides
+    # the operands' base offsets must be 0 (all loops start at 0)
+    a_m, a_k, b_k, b_n, c_m, c_n = g.tables
+    if a_m[0] + a_k[0] != 0 or b_k[0] + b_n[0] != 0 or c_m[0] + c_n[0] != 0:
+        return None
+    trip = {}
+    for v in g.m_vars + g.n_vars + g.k_vars:
+        lb, st, t = v.static()
+        if lb != 0 or st != 1:
+            return None
+    # classify each variable by its coefficient signature
+    offA, offB, offC = _offsets(region, g)
+    roles = {}
+    for v in g.m_vars:
+        sig = (offC.t.get(v.id, 0), offA.t.get(v.id, 0))
+        if sig == (sc[0], sa[0]):
+            roles["n"] = v
+        elif sig == (sc[2], sa[2]):
+            roles["ho"] = v
+        elif sig == (sc[3], sa[3]):
+            roles["wo"] = v
+        else:
+            return None
+    for v in g.n_vars:
+        if (offC.t.get(v.id, 0), offB.t.get(v.id, 0)) != (sc[1], sb[0]):
+            return None
+        roles["co"] = v
+    for v in g.k_vars:
+        sig = (offA.t.get(v.id, 0), offB.t.get(v.id, 0))
+        if sig == (sa[1], sb[1]):
+            roles["ci"] = v
+        elif sig == (sa[2], sb[2]):
+            roles["ki"] = v
+        elif sig == (sa[3], sb[3]):
+            roles["kj"] = v
+        else:
+            return None
+    if len(roles) != len(g.m_vars) + len(g.n_vars) + len(g.k_vars) or \
+            not {"ho", "wo", "co"} <= set(roles):
+        return None
+
+    def t(name):
+        return roles[name].static()[2] if name in roles else 1
+
+    cv = ConvView()
+    cv.nb, cv.f, cv.ho, cv.wo = t("n"), t("co"), t("ho"), t("wo")
+    cv.c, cv.kh, cv.kw = t("ci"), t("ki"), t("kj")
+    if A.shape[0] != cv.nb or A.shape[1] != cv.c or C.shape != (cv.nb, cv.f, cv.ho, cv.wo) or \
+            B.shape != (cv.f, cv.c, cv.kh, cv.kw):
+        return None
+    cv.hp, cv.wp = A.shape[2], A.shape[3]
+    if cv.hp < cv.ho + cv.kh - 1 or cv.wp < cv.wo + cv.kw - 1:
+        return None
+    cv.inp, cv.ker, cv.out = A, B, C
+    return cv
+
+
+def _offsets(region, g):
+    """The element-offset affine forms of C, A, B recorded for g."""
+    return g.offsets
 
 
 class MapMatch:

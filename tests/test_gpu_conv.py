@@ -1,0 +1,73 @@
+"""Tensor-core convolution (b200_conv2d_tc) through the engine, on a B200.
+
+The conv_2d_nchw_fchw nest (reference tests/kernels.py:50-64) is run with
+``configure(precision="bf16")``; inputs and weights are pre-rounded to bf16
+so every product is exact in fp32 and the deviation from the reference's
+sequential f32 chain is accumulation order only.  Bound per output
+(K = C*KH*KW terms):
+
+    |got - want| <= 2*K*2^-24 * sum|in*w| + 4*2^-24*|want|
+
+with ``want`` = out0 + conv(in, w) computed in float64.
+"""
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    # nb, c, f, ho, wo, kh, kw
+    (2, 64, 64, 56, 56, 3, 3),      # the ResNet-50 layer of BASELINE configs[2], 2 images
+    (1, 16, 32, 20, 13, 3, 3),      # ragged tiles, channels padded to 64
+    (3, 128, 64, 17, 24, 3, 3),     # two channel blocks per tap
+    (1, 64, 128, 16, 16, 1, 1),     # F = 128, 1x1
+]
+
+
+def _conv_kernel(nb, c, f, ho, wo, kh, kw):
+    import bench_kernels as bk
+
+    hp, wp = ho + kh - 1, wo + kw - 1
+    src = f'''
+@staged
+def conv_t(inp: MemRef[({nb}, {c}, {hp}, {wp}), F32], ker: MemRef[({f}, {c}, {kh}, {kw}), F32],
+           out: MemRef[({nb}, {f}, {ho}, {wo}), F32]):
+    for n, co, ho, wo in parallel((0, 0, 0, 0), ({nb}, {f}, {ho}, {wo})):
+        for ci in range(0, {c}):
+            for ki in range(0, {kh}):
+                for kj in range(0, {kw}):
+                    out[n, co, ho, wo] += inp[n, ci, ho + ki, wo + kj] * ker[co, ci, ki, kj]
+'''
+    return bk._capture_from_source(src, "conv_t", {}, f"{nb}_{c}_{f}_{ho}_{wo}_{kh}_{kw}")
+
+
+@pytest.mark.parametrize("case", CASES, ids=[str(c) for c in CASES])
+def test_conv_tc_through_engine(case):
+    import torch
+    import torch.nn.functional as Fn
+
+    import paper_2307_16080_b200 as b2
+    from staircase.interp import Buffer, machine
+
+    nb, c, f, ho, wo, kh, kw = case
+    fn = _conv_kernel(*case)
+    g = torch.Generator().manual_seed(7)
+    hp, wp = ho + kh - 1, wo + kw - 1
+    x = (torch.rand(nb, c, hp, wp, generator=g) * 2 - 1).bfloat16().float()
+    w = (torch.rand(f, c, kh, kw, generator=g) * 2 - 1).bfloat16().float()
+    o = torch.rand(nb, f, ho, wo, generator=g) * 2 - 1
+    args = [Buffer(tuple(t.shape), "f32", t.numpy().tobytes()) for t in (x, w, o)]
+    b2.configure(precision="bf16")
+    try:
+        machine.run(fn.module, "conv_t", args, engine=b2.engine)
+    finally:
+        b2.configure(precision="exact")
+    assert b2.engine.last_plan[-1][0] == "conv2d_tc_bf16", b2.engine.last_plan
+    got = torch.frombuffer(args[2].data, dtype=torch.float32).reshape(nb, f, ho, wo).double()
+    want = o.double() + Fn.conv2d(x.double(), w.double())
+    mag = Fn.conv2d(x.double().abs(), w.double().abs())
+    K = c * kh * kw
+    bound = 2 * K * 2.0 ** -24 * mag + 4 * 2.0 ** -24 * want.abs() + 1e-30
+    bad = ((got - want).abs() > bound).sum().item()
+    assert bad == 0, f"{bad} outputs outside the bound"
+    # inputs are untouched
+    assert torch.equal(torch.frombuffer(args[0].data, dtype=torch.float32).reshape(x.shape), x)
