@@ -202,7 +202,9 @@ def conv_tc_supported(cv):
     if cv.f not in (32, 64, 128):
         return False
     smem = 1024 + cv.kh * cv.kw * (cp // 64) * cv.f * 128 + 5 * 16384 + 2 * cv.f * 512 + 256
-    return smem <= 232448 and cv.out.strides[3] == 1
+    # the NCHW output is a 4-D TMA tensor: global strides must be 16-byte multiples
+    aligned = all((s * 4) % 16 == 0 for s in cv.out.strides[:3])
+    return smem <= 232448 and cv.out.strides[3] == 1 and aligned
 
 
 def _direct_call(lib):
