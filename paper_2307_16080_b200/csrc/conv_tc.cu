@@ -235,22 +235,37 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // NCHW f32 (any strides) -> NHWC bf16 with channels padded to cp (zeros).
-// One CTA per (n, h) row: a [C][W] slab transposed through shared memory.
-__global__ void pack_nhwc_kernel(const float *__restrict__ src, int64_t sN, int64_t sC,
-                                 int64_t sH, int64_t sW, __nv_bfloat16 *__restrict__ dst,
-                                 int64_t C, int64_t H, int64_t W, int64_t cp) {
+// A CTA transposes one (n, h) row slab [cp][W] through shared memory per
+// iteration, grid-striding over rows: each warp reads whole channel rows
+// (coalesced along w), each thread then writes 8 channels of one pixel as a
+// single 16-byte vector.
+constexpr int PACK_MAXW = 256;
+__global__ void __launch_bounds__(256) pack_nhwc_kernel(const float *__restrict__ src, int64_t sN,
+                                                        int64_t sC, int64_t sH, int64_t sW,
+                                                        __nv_bfloat16 *__restrict__ dst, int C,
+                                                        int H, int W, int cp, int64_t rows) {
   extern __shared__ float slab[];   // [cp][W + 1]
-  const int64_t n = blockIdx.x / H, h = blockIdx.x % H;
-  const int64_t ld = W + 1;
-  for (int64_t i = threadIdx.x; i < cp * W; i += blockDim.x) {
-    const int64_t c = i / W, w = i % W;
-    slab[c * ld + w] = c < C ? src[n * sN + c * sC + h * sH + w * sW] : 0.f;
-  }
-  __syncthreads();
-  __nv_bfloat16 *out = dst + ((n * H + h) * W) * cp;
-  for (int64_t i = threadIdx.x; i < W * cp; i += blockDim.x) {
-    const int64_t w = i / cp, c = i % cp;
-    out[i] = __float2bfloat16_rn(slab[c * ld + w]);
+  const int ld = W + 1;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int chunks = cp / 8;
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    const int64_t n = row / H, h = row % H;
+    const float *base = src + n * sN + h * sH;
+    for (int c = warp; c < cp; c += 8) {
+      const float *p = base + (int64_t)c * sC;
+      for (int w = lane; w < W; w += 32) slab[c * ld + w] = c < C ? __ldg(p + w * sW) : 0.f;
+    }
+    __syncthreads();
+    uint4 *out = reinterpret_cast<uint4 *>(dst + row * (int64_t)W * cp);
+    for (int i = threadIdx.x; i < W * chunks; i += 256) {
+      const int w = i / chunks, c0 = (i % chunks) * 8;
+      __nv_bfloat162 v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        v[j] = __floats2bfloat162_rn(slab[(c0 + 2 * j) * ld + w], slab[(c0 + 2 * j + 1) * ld + w]);
+      out[i] = *reinterpret_cast<uint4 *>(v);
+    }
+    __syncthreads();
   }
 }
 
@@ -310,14 +325,19 @@ int launch_conv(const void *in_nhwc, const void *wt, float *out, const int64_t *
 
 extern "C" int b200_pack_conv_input(const float *src, const int64_t *sstr, void *dst, int64_t nb,
                                     int64_t c, int64_t h, int64_t w, int64_t cp, void *stream) {
-  if (nb <= 0 || h <= 0 || w <= 0 || cp < c || cp % 64) return B200_EINVAL;
+  if (nb <= 0 || h <= 0 || w <= 0 || cp < c || cp % 64 || w > PACK_MAXW) return B200_EINVAL;
   const size_t smem = (size_t)cp * (w + 1) * 4;
   if (smem > 227 * 1024) return B200_EUNSUPPORTED;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(pack_nhwc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-  pack_nhwc_kernel<<<(unsigned)(nb * h), 256, smem, static_cast<cudaStream_t>(stream)>>>(
-      src, sstr[0], sstr[1], sstr[2], sstr[3], static_cast<__nv_bfloat16 *>(dst), c, h, w, cp);
+  const int64_t rows = nb * h;
+  const int per_sm = (int)((228 * 1024) / (smem + 1024));
+  int64_t blocks = (int64_t)num_sms() * (per_sm < 1 ? 1 : (per_sm > 8 ? 8 : per_sm));
+  if (blocks > rows) blocks = rows;
+  pack_nhwc_kernel<<<(unsigned)blocks, 256, smem, static_cast<cudaStream_t>(stream)>>>(
+      src, sstr[0], sstr[1], sstr[2], sstr[3], static_cast<__nv_bfloat16 *>(dst), (int)c, (int)h,
+      (int)w, (int)cp, rows);
   return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
 }
 

@@ -18,7 +18,7 @@ CASES = [
     # nb, c, f, ho, wo, kh, kw
     (2, 64, 64, 56, 56, 3, 3),      # the ResNet-50 layer of BASELINE configs[2], 2 images
     (1, 16, 32, 20, 12, 3, 3),      # ragged tiles, channels padded to 64
-    (3, 128, 64, 17, 24, 3, 3),     # two channel blocks per tap
+    (3, 128, 32, 17, 24, 3, 3),     # two channel blocks per tap
     (1, 64, 128, 16, 16, 1, 1),     # F = 128, 1x1
 ]
 
