@@ -286,7 +286,9 @@ def load_traffic(key):
 
 KERNEL_OF = {"b200_gemm_tc": "gemm", "b200_gemm_f32_exact": "gemm",
              "b200_contract_exact": "contract", "b200_map_f32": "map", "b200_vm_run": "vm",
-             "b200_pack_operand": "pack"}
+             "b200_pack_operand": "pack", "b200_conv2d_tc": "conv",
+             "b200_pack_conv_input": "pack"}
+TENSOR_KERNELS = ("b200_gemm_tc", "b200_conv2d_tc")
 
 
 # -- arms ----------------------------------------------------------------------------
@@ -414,7 +416,7 @@ def run_ours(args, rank, world, local):
         achieved = wl.bytes / (dom_ms * 1e-3) / 1e9
         peak, unit, bound = peaks["hbm_gbs"], "GB/s", "hbm"
         peak_source = f"{src} HBM copy bandwidth (MEASURED_PEAKS.json)"
-    elif dom == "b200_gemm_tc":
+    elif dom in TENSOR_KERNELS:
         achieved = wl.flops / (dom_ms * 1e-3) / 1e12
         peak = peaks["bf16_tflops"] * (1.0 if prec == "bf16" else 0.5)
         unit, bound = "TFLOP/s", "tensor"

@@ -5,28 +5,49 @@
 // Replaces run_tape on the conv_2d_nchw_fchw nest (reference
 // tests/kernels.py:50-64; the engine recognises it from
 // the separable contraction's index maps) when the engine precision is bf16.
-// GEMM view: M = output pixels, N = F, K = (ki, kj, ci-block of 64) — the
-// tensor core accumulates in fp32, the only deviation from the reference's
-// (ci, ki, kj)-ordered f32 chain being accumulation order and the bf16
-// operand rounding (tolerance: DESIGN.md, tests/test_gpu_conv.py).
+// The tensor core accumulates in fp32; the only deviations from the
+// reference's (ci, ki, kj)-ordered f32 chain are accumulation order and the
+// bf16 operand rounding (tolerance: DESIGN.md, tests/test_gpu_conv.py).
 //
-// Layout: the input is repacked once per call to NHWC bf16 with channels
-// padded to Cp (a multiple of 64) — b200_pack_conv_input — so the A tile of
-// one tap is a single 4-D TMA box {64 ch, 8 w, 16 h, 1 n}: 128 pixel rows of
-// 128 bytes, 128B-swizzled, i.e. exactly the canonical K-major UMMA layout.
-// Taps are coordinate shifts of that box (the nest's input is pre-padded, out
-// of range rows are TMA zero-fill).  Weights ([F][KH][KW][Cp] bf16) stay
-// resident in shared memory for the CTA's lifetime.
-// Structure per CTA (persistent over 16x8-pixel output tiles):
-//   warp 0  TMA producer (weights once, then one A box per k-block, 5 stages)
-//   warp 1  MMA issuer: UMMA 128 x F x 16, 4 per k-block, fp32 in TMEM
-//   warp 2  TMEM allocator (2 accumulator buffers of F columns)
-//   warps 4-7 epilogue: thread = pixel row; TMEM -> +out tile (TMA-loaded
-//           into smem as [f][h][w] fp32) -> TMA store back to NCHW
+// Halo reuse.  The input is repacked once per call to NHWC bf16, channels
+// padded to a multiple of 64 (b200_pack_conv_input), so one pixel of one
+// 64-channel block is a 128-byte row.  Each output tile's input patch arrives
+// as ONE 128B-swizzled TMA box per channel block, and every filter tap is a
+// K-major SW128 UMMA descriptor over that same patch (start shifted by the
+// tap, SBO = one patch row): A traffic per tile is the patch, not one
+// shifted tile per tap.  The 128B swizzle is a function of absolute shared
+// memory address bits, so shifted starts need no descriptor base offset.
+//
+// Two tilings (template R):
+//  R == 1   tile 16 rows x 8 columns (M = 128 = row * 8 + col), patch rows of
+//           PW = 8 + KW - 1 pixels; one UMMA 128 x F x 16 per (tap, 16
+//           channels).
+//  R == KW  (KW * F <= 256) the KW horizontal taps are merged into N: tile
+//           8 rows x (16 - KW + 1) columns, patch rows of 16 pixels (M = 128 =
+//           row * 16 + col), and one UMMA 128 x (KW * F) x 16 per (ki, 16
+//           channels) against the KW weight slices stacked as B rows
+//           (kj, f).  The epilogue sums the KW partial products of output
+//           (h, w) from TMEM lanes (h, w + kj), columns kj * F + f, with warp
+//           shuffles.  At F = 64 a 128 x 64 x 16 UMMA is paced by a per-
+//           instruction cost (~110 cycles measured, 32 of math); N = 192
+//           amortises it over 3x the work.
+//
+// Weights ([F][KH][KW][Cp] bf16, K-major) stay resident in shared memory for
+// the whole kernel.  The epilogue reads and writes the NCHW f32 output
+// directly from registers (a warp covers 2-4 image rows x 8-16 contiguous
+// pixels per channel): no output staging in shared memory, any strides.
+// Structure per CTA (persistent over tiles):
+//   warp 0  TMA producer (weights once; one patch per (tile, channel block))
+//   warp 1  MMA issuer
+//   warp 2  TMEM allocator (2 accumulator buffers of R * F columns)
+//   warps 4-11 epilogue, two warpgroups splitting the output channels:
+//           thread = TMEM lane = tile pixel
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "../../include/b200k.h"
 #include "tc_common.cuh"
@@ -35,17 +56,35 @@ using namespace b200tc;
 
 namespace {
 
-constexpr int TH = 16, TW = 8;            // output tile: 16 rows x 8 columns = 128 pixels
-constexpr int ASTAGES = 5;
-constexpr int A_STAGE = 128 * 128;        // 128 pixel rows x 64 bf16
-constexpr int kThreads = 256;
+constexpr int kMaxStages = 6;             // patch pipeline depth (runtime, smem permitting)
+constexpr int kThreads = 384;              // 4 control warps + 2 epilogue warpgroups
+constexpr size_t kSmemMax = 232448;
 
 struct ConvGeo {
   int64_t nb, cp, hp, wp, f, ho, wo, kh, kw;
-  int64_t th_tiles, tw_tiles, tiles, kblocks;   // kblocks = kh*kw*(cp/64)
+  int64_t so_n, so_f, so_h, so_w;   // output element strides
+  int64_t th_tiles, tw_tiles, tiles;
+  int th, tw;        // output tile rows / valid columns
+  int ph, prow;      // patch rows / patch row length in pixels
+  int cblocks, stages;
+  int patch_bytes;   // bytes one patch box delivers (transaction count)
+  int pstage;        // smem stride of a patch stage (1024-aligned)
   int init;
   float init_value;
+  unsigned long long *stats;   // dev: per-role wait cycles (B200_CONV_STATS), or null
 };
+
+// dev instrumentation: cycles spent in a wait, per role slot
+#define TIMED(slot, stmt)                          \
+  do {                                             \
+    if (g.stats) {                                 \
+      const long long t0_ = clock64();             \
+      stmt;                                        \
+      st[slot] += clock64() - t0_;                 \
+    } else {                                       \
+      stmt;                                        \
+    }                                              \
+  } while (0)
 
 __device__ __forceinline__ void tma_load_4d(const CUtensorMap *map, uint32_t bar, uint32_t dst,
                                             int32_t c0, int32_t c1, int32_t c2, int32_t c3) {
@@ -55,51 +94,73 @@ __device__ __forceinline__ void tma_load_4d(const CUtensorMap *map, uint32_t bar
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
-__device__ __forceinline__ void tma_store_4d(const CUtensorMap *map, uint32_t src, int32_t c0,
-                                             int32_t c1, int32_t c2, int32_t c3) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
-          reinterpret_cast<uint64_t>(map)),
-      "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-      : "memory");
+
+// K-major SW128 operand whose 8-row groups are `sbo` bytes apart; the start
+// may sit anywhere on a 16-byte boundary inside the swizzle atom.
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t addr, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
 }
 
-template <int F>
+// 16 TMEM columns of this warp's 32 lanes, without the completion wait.
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <int F, int R>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tma_in,
-                   const __grid_constant__ CUtensorMap tma_w,
-                   const __grid_constant__ CUtensorMap tma_out, ConvGeo g) {
-  constexpr int B_KBLOCK = F * 128;          // F rows x 64 bf16
-  constexpr int CBUF = F * 128 * 4;          // out tile [F][16][8] fp32
+                   const __grid_constant__ CUtensorMap tma_w, float *__restrict__ out,
+                   ConvGeo g) {
+  constexpr int N = R * F;                   // UMMA N
+  constexpr int SLICE = F * 128;             // one (tap, channel block) weight slice
+  constexpr uint32_t TCOLS = 2 * N <= 32 ? 32 : (2 * N <= 64 ? 64 : (2 * N <= 128 ? 128 :
+                                                  (2 * N <= 256 ? 256 : 512)));
+  constexpr int ROWLEN = R == 1 ? 8 : 16;    // pixels per tile row in the M ordering
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   unsigned char *gbase = smem_raw + (base - smem_u32(smem_raw));
-  const int kb_total = (int)g.kblocks;
-  const uint32_t sB = base;                                   // kb_total x B_KBLOCK
-  const uint32_t sA = base + kb_total * B_KBLOCK;             // ASTAGES x A_STAGE
-  const uint32_t sC = sA + ASTAGES * A_STAGE;                 // 2 x CBUF
-  unsigned char *gC = gbase + (sC - base);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(gC + 2 * CBUF);
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * ASTAGES + 7);
+  const int taps = (int)(g.kh * g.kw);
+  const int nslices = taps * g.cblocks;
+  const int stages = g.stages;
+  const uint32_t pstage = (uint32_t)g.pstage;
+  const uint32_t sB = base;                                   // nslices x SLICE
+  const uint32_t sP = base + nslices * SLICE;                 // stages x patch
+  uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + nslices * SLICE + stages * pstage);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * kMaxStages + 5);
   const uint32_t bar0 = smem_u32(bars);
   auto full = [&](int s) { return bar0 + 8u * s; };
-  auto empty = [&](int s) { return bar0 + 8u * (ASTAGES + s); };
-  auto tfull = [&](int a) { return bar0 + 8u * (2 * ASTAGES + a); };
-  auto tempty = [&](int a) { return bar0 + 8u * (2 * ASTAGES + 2 + a); };
-  auto cbar = [&](int b) { return bar0 + 8u * (2 * ASTAGES + 4 + b); };
-  const uint32_t wbar = bar0 + 8u * (2 * ASTAGES + 6);
+  auto empty = [&](int s) { return bar0 + 8u * (kMaxStages + s); };
+  auto tfull = [&](int a) { return bar0 + 8u * (2 * kMaxStages + a); };
+  auto tempty = [&](int a) { return bar0 + 8u * (2 * kMaxStages + 2 + a); };
+  const uint32_t wbar = bar0 + 8u * (2 * kMaxStages + 4);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  long long st[4] = {0, 0, 0, 0};
+  const long long t_start = clock64();
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < ASTAGES; ++s) {
+    for (int s = 0; s < stages; ++s) {
       mbar_init(full(s), 1);
       mbar_init(empty(s), 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull(a), 1);
-      mbar_init(tempty(a), 128);
-      mbar_init(cbar(a), 1);
+      mbar_init(tempty(a), 256);
     }
     mbar_init(wbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -107,165 +168,288 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(2 * F < 32 ? 32 : 2 * F));
+                 "r"(TCOLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int64_t per_img = g.th_tiles * g.tw_tiles;
+  // 32-bit tile decomposition (tiles < 2^31, checked on the host): 64-bit
+  // division is a long software sequence on the epilogue's critical path
+  const uint32_t per_img = (uint32_t)(g.th_tiles * g.tw_tiles);
+  const uint32_t twt = (uint32_t)g.tw_tiles;
   auto tile_coords = [&](int64_t t, int32_t &n, int32_t &h0, int32_t &w0) {
-    n = (int32_t)(t / per_img);
-    const int64_t r = t % per_img;
-    h0 = (int32_t)((r / g.tw_tiles) * TH);
-    w0 = (int32_t)((r % g.tw_tiles) * TW);
+    const uint32_t tt = (uint32_t)t;
+    const uint32_t nn = tt / per_img, r = tt - nn * per_img;
+    const uint32_t ty = r / twt;
+    n = (int32_t)nn;
+    h0 = (int32_t)(ty * g.th);
+    w0 = (int32_t)((r - ty * twt) * g.tw);
   };
-  const int cblocks = (int)(g.cp / 64);
 
   if (warp == 0) {
     if (lane == 0) {
-      // resident weights: every (tap, channel-block) K slice of B^T
-      mbar_expect_tx(wbar, (uint32_t)(kb_total * B_KBLOCK));
-      for (int kb = 0; kb < kb_total; ++kb)
-        tma_load_2d(&tma_w, wbar, sB + kb * B_KBLOCK, kb * 64, 0);
+      // resident weights: slice (ki, kj, cb) = rows f of columns
+      // [(ki * KW + kj) * cp + cb * 64, +64); R == 1 orders slices
+      // (tap, cb), R > 1 orders them (ki, cb, kj) so that the KW slices of
+      // one (ki, cb) stack into the N = KW * F rows of a single B operand
+      mbar_expect_tx(wbar, (uint32_t)(nslices * SLICE));
+      for (int tap = 0; tap < taps; ++tap) {
+        const int ki = tap / (int)g.kw, kj = tap % (int)g.kw;
+        for (int cb = 0; cb < g.cblocks; ++cb) {
+          const int slot = R == 1 ? tap * g.cblocks + cb : (ki * g.cblocks + cb) * R + kj;
+          tma_load_2d(&tma_w, wbar, sB + slot * SLICE, (int32_t)(tap * g.cp + cb * 64), 0);
+        }
+      }
       int s = 0;
       uint32_t ph = 0;
       for (int64_t t = blockIdx.x; t < g.tiles; t += gridDim.x) {
         int32_t n, h0, w0;
         tile_coords(t, n, h0, w0);
-        for (int kb = 0; kb < kb_total; ++kb) {
-          const int tap = kb / cblocks, cb = kb % cblocks;
-          const int ki = (int)(tap / g.kw), kj = (int)(tap % g.kw);
-          mbar_wait(empty(s), ph ^ 1);
-          mbar_expect_tx(full(s), A_STAGE);
-          tma_load_4d(&tma_in, full(s), sA + s * A_STAGE, cb * 64, w0 + kj, h0 + ki, n);
-          if (++s == ASTAGES) { s = 0; ph ^= 1; }
+        for (int cb = 0; cb < g.cblocks; ++cb) {
+          TIMED(0, mbar_wait(empty(s), ph ^ 1));
+          mbar_expect_tx(full(s), (uint32_t)g.patch_bytes);
+          tma_load_4d(&tma_in, full(s), sP + s * pstage, cb * 64, w0, h0, n);
+          if (++s == stages) { s = 0; ph ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc(0, 128, F);
+      constexpr uint32_t idesc = make_idesc(0, 128, N);
+      // 8-pixel M groups: one patch row apart (R == 1), or back to back
+      // (R > 1: two groups per 16-pixel patch row)
+      const uint32_t sbo = R == 1 ? (uint32_t)g.prow * 128 : 1024;
       mbar_wait(wbar, 0);
       int s = 0;
       uint32_t ph = 0;
       int acc = 0;
       uint32_t aph = 0;
       for (int64_t t = blockIdx.x; t < g.tiles; t += gridDim.x) {
-        mbar_wait(tempty(acc), aph ^ 1);
+        TIMED(2, mbar_wait(tempty(acc), aph ^ 1));
         tc_fence_after();
-        const uint32_t tmem_d = tmem_base + (uint32_t)(acc * F);
-        for (int kb = 0; kb < kb_total; ++kb) {
-          mbar_wait(full(s), ph);
+        const uint32_t tmem_d = tmem_base + (uint32_t)(acc * N);
+        for (int cb = 0; cb < g.cblocks; ++cb) {
+          TIMED(1, mbar_wait(full(s), ph));
           tc_fence_after();
-          const uint32_t a_addr = sA + s * A_STAGE, b_addr = sB + kb * B_KBLOCK;
+          // descriptors advance in 16-byte units of their start-address
+          // field: +2 per 16-channel k step
+          const uint64_t a0 = desc_sw128(sP + s * pstage, sbo);
+          uint32_t acc_flag = cb != 0;
+          if (R == 1) {
+            // per tap: A shifted by (ki * PW + kj) pixels, B = slice (tap, cb)
+            uint64_t ad = a0;
+            uint64_t bd = desc_sw128(sB + cb * SLICE, 1024);
+            const uint64_t b_tap = (uint64_t)(g.cblocks * SLICE) >> 4;
+            for (int ki = 0; ki < (int)g.kh; ++ki) {
+              for (int kj = 0; kj < (int)g.kw; ++kj) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            umma<0, 1>(tmem_d, smem_desc(a_addr + 32 * k), smem_desc(b_addr + 32 * k), idesc,
-                       (kb | k) != 0);
+                for (int k = 0; k < 4; ++k) {
+                  umma<0, 1>(tmem_d, ad + 2 * k, bd + 2 * k, idesc, acc_flag);
+                  acc_flag = 1;
+                }
+                ad += 8;
+                bd += b_tap;
+              }
+              ad += (uint64_t)(g.prow - g.kw) * 8;
+            }
+          } else {
+            // per ki: A shifted by ki patch rows, B = the KW stacked slices
+            // of (ki, cb)
+            for (int ki = 0; ki < (int)g.kh; ++ki) {
+              const uint64_t ad = a0 + (uint64_t)ki * g.prow * 8;
+              const uint64_t bd =
+                  desc_sw128(sB + (ki * g.cblocks + cb) * R * SLICE, 1024);
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                umma<0, 1>(tmem_d, ad + 2 * k, bd + 2 * k, idesc, acc_flag);
+                acc_flag = 1;
+              }
+            }
+          }
           umma_commit(empty(s));
-          if (++s == ASTAGES) { s = 0; ph ^= 1; }
+          if (++s == stages) { s = 0; ph ^= 1; }
         }
         umma_commit(tfull(acc));
         if (++acc == 2) { acc = 0; aph ^= 1; }
       }
     }
   } else if (warp >= 4) {
-    const int r = threadIdx.x - 128;    // pixel row of the tile = TMEM lane
-    const int q = warp - 4;
-    const bool lead_t = r == 0;
-    // out tile as [f][h][w] fp32 (TMA box order: w fastest, then h, then f)
-    auto issue_load = [&](int64_t t, int b) {
+    // two epilogue warpgroups: warp w reads TMEM lanes 32 * (w % 4) + [0, 32)
+    // (its lane quadrant) and warpgroup e takes the 16-column chunks
+    // e, e + 2, e + 4, ... of the F output channels
+    const int m = (warp % 4) * 32 + lane;   // TMEM lane = tile pixel (row * ROWLEN + col)
+    const int e = (warp - 4) / 4;
+    const int hr = m / ROWLEN, wc = m % ROWLEN;
+    const int sf = (int)g.so_f;   // channel stride in elements (< 2^31 / F, host-checked)
+    constexpr int CH = F / 32 > 0 ? F / 32 : 1;   // 16-column chunks per warpgroup
+    // this thread's output pixel of tile t: base pointer and validity
+    auto pixel = [&](int64_t t, bool &valid) -> float * {
       int32_t n, h0, w0;
       tile_coords(t, n, h0, w0);
-      mbar_expect_tx(cbar(b), CBUF);
-      tma_load_4d(&tma_out, cbar(b), sC + b * CBUF, w0, h0, 0, n);
+      valid = t < g.tiles && wc < g.tw && h0 + hr < g.ho && w0 + wc < g.wo;
+      return out + n * g.so_n + (h0 + hr) * g.so_h + (w0 + wc) * g.so_w;
     };
+    // the previous output values of the NEXT tile are loaded while the
+    // current one is written, so DRAM latency overlaps a whole tile
+    float nxt[CH][16];
+    auto fetch = [&](const float *o, bool valid) {
+      if (valid && !g.init) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          if (16 * e + 32 * c >= F) break;
+          const float *pc = o + (16 * e + 32 * c) * sf;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) nxt[c][j] = pc[j * sf];
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < CH; ++c)
+#pragma unroll
+          for (int j = 0; j < 16; ++j) nxt[c][j] = g.init_value;
+      }
+    };
+    bool valid;
+    float *o = pixel(blockIdx.x, valid);
+    fetch(o, valid);
     int acc = 0;
     uint32_t aph = 0;
-    int64_t it = 0;
-    if (lead_t && !g.init && blockIdx.x < g.tiles) issue_load(blockIdx.x, 0);
-    for (int64_t t = blockIdx.x; t < g.tiles; t += gridDim.x, ++it) {
-      const int b = (int)(it & 1);
-      int32_t n, h0, w0;
-      tile_coords(t, n, h0, w0);
-      // prefetch the next tile's out block into the other buffer once its
-      // previous store has drained
-      if (lead_t) {
-        bulk_wait_read<0>();
-        if (!g.init && t + gridDim.x < g.tiles) issue_load(t + gridDim.x, b ^ 1);
-      }
-      mbar_wait(tfull(acc), aph);
-      tc_fence_after();
-      if (!g.init) mbar_wait(cbar(b), (uint32_t)((it >> 1) & 1));
-      else named_bar_sync(1, 128);   // buffer b is free (its store drained above)
-      float *cb = reinterpret_cast<float *>(gC + b * CBUF);
-      const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * F);
-#pragma unroll 1
-      for (int c0 = 0; c0 < F; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld32(trow + (uint32_t)c0, v);
+    for (int64_t t = blockIdx.x; t < g.tiles; t += gridDim.x) {
+      float cur[CH][16];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          float *p = cb + (c0 + j) * 128 + r;
-          const float o = g.init ? g.init_value : *p;
-          *p = o + __uint_as_float(v[j]);
+      for (int c = 0; c < CH; ++c)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) cur[c][j] = nxt[c][j];
+      const bool cur_valid = valid;
+      float *const co = o;
+      o = pixel(t + gridDim.x, valid);
+      fetch(o, valid);
+      TIMED(3, mbar_wait(tfull(acc), aph));
+      tc_fence_after();
+      const uint32_t trow = tmem_base + ((uint32_t)((warp % 4) * 32) << 16) + (uint32_t)(acc * N);
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const int c0 = 16 * e + 32 * c;
+        if (c0 >= F) break;
+        uint32_t v[R][16];
+#pragma unroll
+        for (int kj = 0; kj < R; ++kj) tmem_ld16_nowait(trow + (uint32_t)(kj * F + c0), v[kj]);
+        tmem_wait_ld();
+        // all 16 results first (independent shuffles interleave), then one
+        // branch around the stores
+        float res[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          float sum = __uint_as_float(v[0][j]);
+#pragma unroll
+          for (int kj = 1; kj < R; ++kj)
+            sum += __shfl_down_sync(0xffffffffu, __uint_as_float(v[kj][j]), kj);
+          res[j] = cur[c][j] + sum;
+        }
+        if (cur_valid) {
+          float *pc = co + c0 * sf;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) pc[j * sf] = res[j];
         }
       }
       tc_fence_before();
       mbar_arrive(tempty(acc));
-      fence_proxy_async();
-      named_bar_sync(1, 128);
-      if (lead_t) {
-        tma_store_4d(&tma_out, sC + b * CBUF, w0, h0, 0, n);
-        bulk_commit();
-      }
       if (++acc == 2) { acc = 0; aph ^= 1; }
     }
-    if (lead_t) bulk_wait_all();
+  }
+  if (g.stats && lane == 0) {
+    const unsigned long long tot = (unsigned long long)(clock64() - t_start);
+    if (warp == 0) {
+      atomicAdd(&g.stats[0], (unsigned long long)st[0]);
+      atomicAdd(&g.stats[8], tot);
+    } else if (warp == 1) {
+      atomicAdd(&g.stats[1], (unsigned long long)st[1]);
+      atomicAdd(&g.stats[2], (unsigned long long)st[2]);
+      atomicAdd(&g.stats[9], tot);
+    } else if (warp == 4) {
+      atomicAdd(&g.stats[3], (unsigned long long)st[3]);
+      atomicAdd(&g.stats[10], tot);
+    }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(2 * F < 32 ? 32 : 2 * F));
+                 "r"(TCOLS));
   }
 }
 
 // NCHW f32 (any strides) -> NHWC bf16 with channels padded to cp (zeros).
 // A CTA transposes one (n, h) row slab [cp][W] through shared memory per
-// iteration, grid-striding over rows: each warp reads whole channel rows
-// (coalesced along w), each thread then writes 8 channels of one pixel as a
-// single 16-byte vector.
+// iteration, grid-striding over rows, software-pipelined: the loads of the
+// next 64-channel pass (8 channel rows per warp x WI = ceil(W / 32) pixels
+// per lane, all in flight at once) are issued before the current row is
+// converted and written, so DRAM latency overlaps the shared-memory work —
+// the kernel is latency-bound otherwise.  Lanes convert 8 channels of
+// consecutive pixels (conflict-free column reads of the slab) into a bf16
+// [w][chunk] stage whose 16-byte chunks are XOR-swizzled by (w & 7), and the
+// stage leaves as contiguous 16-byte stores.
 constexpr int PACK_MAXW = 256;
+template <int WI>
 __global__ void __launch_bounds__(256) pack_nhwc_kernel(const float *__restrict__ src, int64_t sN,
                                                         int64_t sC, int64_t sH, int64_t sW,
                                                         __nv_bfloat16 *__restrict__ dst, int C,
                                                         int H, int W, int cp, int64_t rows) {
-  extern __shared__ float slab[];   // [cp][W + 1]
+  extern __shared__ float slab[];   // [cp][W + 1] f32, then [W][cp / 8] x 16 B bf16
   const int ld = W + 1;
+  uint4 *stage = reinterpret_cast<uint4 *>(slab + ((cp * ld + 3) & ~3));
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int chunks = cp / 8;
-  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
-    const int64_t n = row / H, h = row % H;
-    const float *base = src + n * sN + h * sH;
-    for (int c = warp; c < cp; c += 8) {
-      const float *p = base + (int64_t)c * sC;
-      for (int w = lane; w < W; w += 32) slab[c * ld + w] = c < C ? __ldg(p + w * sW) : 0.f;
+  const int chunks = cp / 8;   // multiple of 8
+  const int items = W * chunks;
+  const int passes = cp / 64;
+  float v[8][WI];
+  auto load = [&](int64_t row, int pass) {
+    const float *base = src + (row / H) * sN + (row % H) * sH;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int c = pass * 64 + warp + 8 * k;
+#pragma unroll
+      for (int i = 0; i < WI; ++i) {
+        const int w = lane + 32 * i;
+        v[k][i] = (c < C && w < W) ? __ldg(base + (int64_t)c * sC + (int64_t)w * sW) : 0.f;
+      }
+    }
+  };
+  int64_t row = blockIdx.x;
+  int pass = 0;
+  if (row < rows) load(row, 0);
+  while (row < rows) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+      for (int i = 0; i < WI; ++i)
+        if (lane + 32 * i < W) slab[(pass * 64 + warp + 8 * k) * ld + lane + 32 * i] = v[k][i];
+    if (++pass < passes) {   // more channel passes of this row (disjoint slab rows)
+      load(row, pass);
+      continue;
     }
     __syncthreads();
-    uint4 *out = reinterpret_cast<uint4 *>(dst + row * (int64_t)W * cp);
-    for (int i = threadIdx.x; i < W * chunks; i += 256) {
-      const int w = i / chunks, c0 = (i % chunks) * 8;
-      __nv_bfloat162 v[4];
+    const int64_t next = row + gridDim.x;
+    if (next < rows) load(next, 0);
+    for (int i = threadIdx.x; i < items; i += 256) {
+      const int chunk = i / W, w = i - chunk * W;
+      const float *col = slab + chunk * 8 * ld + w;
+      __nv_bfloat162 b[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        v[j] = __floats2bfloat162_rn(slab[(c0 + 2 * j) * ld + w], slab[(c0 + 2 * j + 1) * ld + w]);
-      out[i] = *reinterpret_cast<uint4 *>(v);
+        b[j] = __floats2bfloat162_rn(col[(2 * j) * ld], col[(2 * j + 1) * ld]);
+      stage[w * chunks + (chunk ^ (w & 7))] = *reinterpret_cast<uint4 *>(b);
     }
     __syncthreads();
+    uint4 *outp = reinterpret_cast<uint4 *>(dst + row * (int64_t)W * cp);
+    for (int i = threadIdx.x; i < items; i += 256) {
+      const int w = i / chunks, chunk = i - w * chunks;
+      outp[i] = stage[w * chunks + (chunk ^ (w & 7))];
+    }
+    row = next;
+    pass = 0;
   }
 }
 
@@ -292,32 +476,59 @@ bool make_map_4d(CUtensorMap *map, CUtensorMapDataType dt, const void *ptr, cons
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int F>
-int launch_conv(const void *in_nhwc, const void *wt, float *out, const int64_t *ostr,
-                const ConvGeo &g, cudaStream_t s) {
-  CUtensorMap mi, mw, mo;
+// Merge factor: the KW horizontal taps go into N when KW * F fits one UMMA
+// (instantiated for 3x3 at F <= 64 and 5x5 at F = 32).  Mirrored by
+// runtime.conv_tc_supported.
+int conv_merge(int64_t f, int64_t kw) {
+  if (getenv("B200_CONV_NOMERGE")) return 1;   // dev knob: force the 16 x 8 tiling
+  return (kw == 3 && (f == 32 || f == 64)) || (kw == 5 && f == 32) ? (int)kw : 1;
+}
+
+// Shared memory of the kernel (weights, `stages` patch stages, barriers,
+// alignment).  Mirrored by runtime.conv_tc_supported.
+size_t conv_smem(int64_t f, int64_t kh, int64_t kw, int64_t cp, int64_t pstage, int stages) {
+  return 1024 + kh * kw * (cp / 64) * f * 128 + stages * pstage + 256;
+}
+
+template <int F, int R>
+int launch_conv(const void *in_nhwc, const void *wt, float *out, ConvGeo &g, cudaStream_t s) {
+  CUtensorMap mi, mw;
   cuuint64_t di[4] = {(cuuint64_t)g.cp, (cuuint64_t)g.wp, (cuuint64_t)g.hp, (cuuint64_t)g.nb};
   cuuint64_t si[3] = {(cuuint64_t)(g.cp * 2), (cuuint64_t)(g.wp * g.cp * 2),
                       (cuuint64_t)(g.hp * g.wp * g.cp * 2)};
-  cuuint32_t bi[4] = {64, TW, TH, 1};
+  // the whole patch of one 64-channel block per box, rows of 128 B, swizzled
+  cuuint32_t bi[4] = {64, (cuuint32_t)g.prow, (cuuint32_t)g.ph, 1};
   if (!make_map_4d(&mi, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, in_nhwc, di, si, bi,
                    CU_TENSOR_MAP_SWIZZLE_128B))
     return B200_ELAUNCH;
   if (!make_map(&mw, 0, wt, F, g.kh * g.kw * g.cp, F)) return B200_ELAUNCH;
-  // out: NCHW f32 with element strides ostr = {n, f, h, w} (w must be 1)
-  cuuint64_t dout[4] = {(cuuint64_t)g.wo, (cuuint64_t)g.ho, (cuuint64_t)F, (cuuint64_t)g.nb};
-  cuuint64_t sout[3] = {(cuuint64_t)(ostr[2] * 4), (cuuint64_t)(ostr[1] * 4),
-                        (cuuint64_t)(ostr[0] * 4)};
-  cuuint32_t bout[4] = {TW, TH, F, 1};
-  if (!make_map_4d(&mo, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, out, dout, sout, bout,
-                   CU_TENSOR_MAP_SWIZZLE_NONE))
-    return B200_ELAUNCH;
-  const size_t smem = 1024 + g.kblocks * F * 128 + ASTAGES * A_STAGE + 2 * F * 128 * 4 + 256;
-  if (smem > 232448) return B200_EUNSUPPORTED;
+  if (conv_smem(F, g.kh, g.kw, g.cp, g.pstage, 2) > kSmemMax) return B200_EUNSUPPORTED;
+  g.stages = kMaxStages;
+  while (conv_smem(F, g.kh, g.kw, g.cp, g.pstage, g.stages) > kSmemMax) --g.stages;
+  const size_t smem = conv_smem(F, g.kh, g.kw, g.cp, g.pstage, g.stages);
   int ctas = num_sms();
   if (g.tiles < ctas) ctas = (int)g.tiles;
-  cudaFuncSetAttribute(conv_tc_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  conv_tc_kernel<F><<<ctas, kThreads, smem, s>>>(mi, mw, mo, g);
+  cudaFuncSetAttribute(conv_tc_kernel<F, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  const bool stats = getenv("B200_CONV_STATS") != nullptr;   // dev: print role wait cycles
+  if (stats) {
+    cudaMalloc(&g.stats, 16 * sizeof(unsigned long long));
+    cudaMemsetAsync(g.stats, 0, 16 * sizeof(unsigned long long), s);
+  }
+  conv_tc_kernel<F, R><<<ctas, kThreads, smem, s>>>(mi, mw, out, g);
+  if (stats) {
+    unsigned long long h[16];
+    cudaMemcpyAsync(h, g.stats, sizeof(h), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    cudaFree(g.stats);
+    const double c = ctas;
+    fprintf(stderr,
+            "conv stats (kcycles/CTA): producer total %.1f wait-empty %.1f | mma total %.1f "
+            "wait-full %.1f wait-tempty %.1f | epilogue total %.1f wait-tfull %.1f | "
+            "R %d stages %d tiles %lld\n",
+            h[8] / c / 1e3, h[0] / c / 1e3, h[9] / c / 1e3, h[1] / c / 1e3, h[2] / c / 1e3,
+            h[10] / c / 1e3, h[3] / c / 1e3, R, g.stages, (long long)g.tiles);
+  }
   return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
 }
 
@@ -326,18 +537,30 @@ int launch_conv(const void *in_nhwc, const void *wt, float *out, const int64_t *
 extern "C" int b200_pack_conv_input(const float *src, const int64_t *sstr, void *dst, int64_t nb,
                                     int64_t c, int64_t h, int64_t w, int64_t cp, void *stream) {
   if (nb <= 0 || h <= 0 || w <= 0 || cp < c || cp % 64 || w > PACK_MAXW) return B200_EINVAL;
-  const size_t smem = (size_t)cp * (w + 1) * 4;
+  const size_t smem = (((size_t)cp * (w + 1) + 3) & ~(size_t)3) * 4 + (size_t)w * cp * 2;
   if (smem > 227 * 1024) return B200_EUNSUPPORTED;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(pack_nhwc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
   const int64_t rows = nb * h;
-  const int per_sm = (int)((228 * 1024) / (smem + 1024));
-  int64_t blocks = (int64_t)num_sms() * (per_sm < 1 ? 1 : (per_sm > 8 ? 8 : per_sm));
-  if (blocks > rows) blocks = rows;
-  pack_nhwc_kernel<<<(unsigned)blocks, 256, smem, static_cast<cudaStream_t>(stream)>>>(
-      src, sstr[0], sstr[1], sstr[2], sstr[3], static_cast<__nv_bfloat16 *>(dst), (int)c, (int)h,
-      (int)w, (int)cp, rows);
+  auto launch = [&](auto kernel) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, smem);
+    int64_t blocks = (int64_t)num_sms() * (per_sm < 1 ? 1 : per_sm);
+    if (blocks > rows) blocks = rows;
+    kernel<<<(unsigned)blocks, 256, smem, static_cast<cudaStream_t>(stream)>>>(
+        src, sstr[0], sstr[1], sstr[2], sstr[3], static_cast<__nv_bfloat16 *>(dst), (int)c,
+        (int)h, (int)w, (int)cp, rows);
+  };
+  switch ((w + 31) / 32) {
+    case 1: launch(pack_nhwc_kernel<1>); break;
+    case 2: launch(pack_nhwc_kernel<2>); break;
+    case 3: launch(pack_nhwc_kernel<3>); break;
+    case 4: launch(pack_nhwc_kernel<4>); break;
+    case 5: launch(pack_nhwc_kernel<5>); break;
+    case 6: launch(pack_nhwc_kernel<6>); break;
+    case 7: launch(pack_nhwc_kernel<7>); break;
+    default: launch(pack_nhwc_kernel<8>); break;
+  }
   return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
 }
 
@@ -358,18 +581,39 @@ extern "C" int b200_conv2d_tc(const void *in_nhwc, const void *wt, float *out,
                               const int64_t *out_strides, int64_t nb, int64_t cp, int64_t hp,
                               int64_t wp, int64_t f, int64_t ho, int64_t wo, int64_t kh,
                               int64_t kw, int32_t init, float init_value, void *stream) {
-  if (out_strides[3] != 1 || cp % 64 || ho + kh - 1 > hp || wo + kw - 1 > wp)
+  if (cp % 64 || ho <= 0 || wo <= 0 || kh <= 0 || kw <= 0 || ho + kh - 1 > hp ||
+      wo + kw - 1 > wp)
     return B200_EINVAL;
-  ConvGeo g{nb, cp, hp, wp, f, ho, wo, kh, kw, 0, 0, 0, 0, init, init_value};
-  g.th_tiles = (ho + TH - 1) / TH;
-  g.tw_tiles = (wo + TW - 1) / TW;
+  ConvGeo g{};
+  g.nb = nb; g.cp = cp; g.hp = hp; g.wp = wp; g.f = f; g.ho = ho; g.wo = wo;
+  g.kh = kh; g.kw = kw; g.init = init; g.init_value = init_value;
+  g.so_n = out_strides[0]; g.so_f = out_strides[1];
+  g.so_h = out_strides[2]; g.so_w = out_strides[3];
+  const int R = conv_merge(f, kw);
+  if (R == 1) {
+    g.th = 16; g.tw = 8; g.prow = (int)(8 + kw - 1);
+  } else {
+    g.th = 8; g.tw = (int)(16 - kw + 1); g.prow = 16;
+  }
+  g.ph = (int)(g.th + kh - 1);
+  g.th_tiles = (ho + g.th - 1) / g.th;
+  g.tw_tiles = (wo + g.tw - 1) / g.tw;
   g.tiles = nb * g.th_tiles * g.tw_tiles;
-  g.kblocks = kh * kw * (cp / 64);
+  g.cblocks = (int)(cp / 64);
+  g.patch_bytes = g.ph * g.prow * 128;
+  g.pstage = (g.patch_bytes + 1023) & ~1023;
+  // 32-bit tile indices and per-pixel channel offsets in the kernel
+  if (g.ph > 256 || g.prow > 256 || g.tiles + 2 * 148 >= (int64_t(1) << 31) ||
+      out_strides[1] < 0 || out_strides[1] * f >= (int64_t(1) << 31))
+    return B200_EUNSUPPORTED;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  switch (f) {
-    case 32: return launch_conv<32>(in_nhwc, wt, out, out_strides, g, s);
-    case 64: return launch_conv<64>(in_nhwc, wt, out, out_strides, g, s);
-    case 128: return launch_conv<128>(in_nhwc, wt, out, out_strides, g, s);
+  switch (f * 16 + R) {
+    case 32 * 16 + 1: return launch_conv<32, 1>(in_nhwc, wt, out, g, s);
+    case 64 * 16 + 1: return launch_conv<64, 1>(in_nhwc, wt, out, g, s);
+    case 128 * 16 + 1: return launch_conv<128, 1>(in_nhwc, wt, out, g, s);
+    case 32 * 16 + 3: return launch_conv<32, 3>(in_nhwc, wt, out, g, s);
+    case 64 * 16 + 3: return launch_conv<64, 3>(in_nhwc, wt, out, g, s);
+    case 32 * 16 + 5: return launch_conv<32, 5>(in_nhwc, wt, out, g, s);
     default: return B200_EUNSUPPORTED;
   }
 }

@@ -197,14 +197,19 @@ def tc_supported(precision, K):
 
 
 def conv_tc_supported(cv):
-    """The tcgen05 conv kernel: F in {32, 64, 128}, weights resident in smem."""
+    """The tcgen05 conv kernel (csrc/conv_tc.cu): F in {32, 64, 128}, weights
+    resident in shared memory next to >= 2 halo-patch stages; any output strides."""
     cp = -(-cv.c // 64) * 64
-    if cv.f not in (32, 64, 128):
+    if cv.f not in (32, 64, 128) or cv.wo + cv.kw - 1 > 256:   # pack kernel: W <= 256
         return False
-    smem = 1024 + cv.kh * cv.kw * (cp // 64) * cv.f * 128 + 5 * 16384 + 2 * cv.f * 512 + 256
-    # the NCHW output is a 4-D TMA tensor: global strides must be 16-byte multiples
-    aligned = all((s * 4) % 16 == 0 for s in cv.out.strides[:3])
-    return smem <= 232448 and cv.out.strides[3] == 1 and aligned
+    merged = (cv.kw == 3 and cv.f in (32, 64)) or (cv.kw == 5 and cv.f == 32)   # conv_merge
+    if merged:   # tile 8 x (16 - kw + 1), patch rows of 16 pixels
+        ph, prow = 8 + cv.kh - 1, 16
+    else:        # tile 16 x 8, patch rows of 8 + kw - 1 pixels
+        ph, prow = 16 + cv.kh - 1, 8 + cv.kw - 1
+    patch = -(-(ph * prow * 128) // 1024) * 1024
+    smem = 1024 + cv.kh * cv.kw * (cp // 64) * cv.f * 128 + 2 * patch + 256
+    return smem <= 232448 and ph <= 256 and prow <= 256
 
 
 def _direct_call(lib):

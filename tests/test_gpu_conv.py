@@ -20,6 +20,9 @@ CASES = [
     (1, 16, 32, 20, 12, 3, 3),      # ragged tiles, channels padded to 64
     (3, 128, 32, 17, 24, 3, 3),     # two channel blocks per tap
     (1, 64, 128, 16, 16, 1, 1),     # F = 128, 1x1
+    (1, 16, 32, 20, 13, 3, 3),      # Wo = 13: output rows not 16-byte multiples
+    (2, 64, 128, 18, 20, 3, 3),     # F = 128 3x3: unmerged 16 x 8 tiling
+    (1, 32, 32, 12, 21, 5, 5),      # 5x5 merged into N = 160
 ]
 
 
@@ -40,18 +43,18 @@ def conv_t(inp: MemRef[({nb}, {c}, {hp}, {wp}), F32], ker: MemRef[({f}, {c}, {kh
     return bk._capture_from_source(src, "conv_t", {}, f"{nb}_{c}_{f}_{ho}_{wo}_{kh}_{kw}")
 
 
-def test_unaligned_output_rows_take_the_exact_path():
-    """Wo = 13 f32 rows are not 16-byte multiples (no TMA): exact kernel, bit-exact."""
+def test_unsupported_filter_count_takes_the_exact_path():
+    """F = 48 has no tensor-core instantiation: exact kernel, bit-exact."""
     import torch
 
     import oracle
     import paper_2307_16080_b200 as b2
     from staircase.interp import Buffer, machine
 
-    fn = _conv_kernel(1, 16, 32, 20, 13, 3, 3)
+    fn = _conv_kernel(1, 16, 48, 20, 13, 3, 3)
     g = torch.Generator().manual_seed(3)
-    ts = [torch.rand(s, generator=g) * 2 - 1 for s in ((1, 16, 22, 15), (32, 16, 3, 3),
-                                                        (1, 32, 20, 13))]
+    ts = [torch.rand(s, generator=g) * 2 - 1 for s in ((1, 16, 22, 15), (48, 16, 3, 3),
+                                                        (1, 48, 20, 13))]
     a1 = [Buffer(tuple(t.shape), "f32", t.numpy().tobytes()) for t in ts]
     a2 = [Buffer(tuple(t.shape), "f32", t.numpy().tobytes()) for t in ts]
     b2.configure(precision="bf16")
