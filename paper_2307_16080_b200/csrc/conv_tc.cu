@@ -57,8 +57,22 @@ using namespace b200tc;
 namespace {
 
 constexpr int kMaxStages = 6;             // patch pipeline depth (runtime, smem permitting)
+constexpr int kMaxOut = 3;                // staged output blocks (runtime)
 constexpr int kThreads = 384;              // 4 control warps + 2 epilogue warpgroups
 constexpr size_t kSmemMax = 232448;
+
+// Tile geometry of tiling R.  ROWLEN: pixels per patch row = per M row group
+// (M = 128 = TH * ROWLEN); TW: output columns per tile — R > 1 loses the
+// last KW - 1 columns of each row to the merged taps' halo, rounded down so
+// that a tile's row is a whole number of 16-byte units (TMA store boxes).
+template <int F, int R>
+struct Tiling {
+  static constexpr int ROWLEN = R == 1 ? 8 : 32;
+  static constexpr int TH = 128 / ROWLEN;
+  static constexpr int TW = R == 1 ? 8 : 28;
+  static constexpr int TPIX = TH * TW;                // staged output pixels per channel
+  static constexpr int OUTBUF = F * TPIX * 4;         // staged output block [F][TH][TW] fp32
+};
 
 struct ConvGeo {
   int64_t nb, cp, hp, wp, f, ho, wo, kh, kw;
@@ -67,6 +81,9 @@ struct ConvGeo {
   int th, tw;        // output tile rows / valid columns
   int ph, prow;      // patch rows / patch row length in pixels
   int cblocks, stages;
+  int nout;          // staged output blocks: previous output TMA-loaded, updated in
+                     // shared memory, TMA-stored (0: unaligned output, the epilogue
+                     // reads and writes global memory directly)
   int patch_bytes;   // bytes one patch box delivers (transaction count)
   int pstage;        // smem stride of a patch stage (1024-aligned)
   int init;
@@ -92,6 +109,14 @@ __device__ __forceinline__ void tma_load_4d(const CUtensorMap *map, uint32_t bar
       "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap *map, uint32_t src, int32_t c0,
+                                             int32_t c1, int32_t c2, int32_t c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
 
@@ -124,13 +149,17 @@ __device__ __forceinline__ void tmem_wait_ld() {
 template <int F, int R>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tma_in,
-                   const __grid_constant__ CUtensorMap tma_w, float *__restrict__ out,
+                   const __grid_constant__ CUtensorMap tma_w,
+                   const __grid_constant__ CUtensorMap tma_out, float *__restrict__ out,
                    ConvGeo g) {
   constexpr int N = R * F;                   // UMMA N
   constexpr int SLICE = F * 128;             // one (tap, channel block) weight slice
   constexpr uint32_t TCOLS = 2 * N <= 32 ? 32 : (2 * N <= 64 ? 64 : (2 * N <= 128 ? 128 :
                                                   (2 * N <= 256 ? 256 : 512)));
-  constexpr int ROWLEN = R == 1 ? 8 : 16;    // pixels per tile row in the M ordering
+  using T = Tiling<F, R>;
+  constexpr int ROWLEN = T::ROWLEN;          // pixels per tile row in the M ordering
+  constexpr int TPIX = T::TPIX;
+  constexpr int OUTBUF = T::OUTBUF;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   unsigned char *gbase = smem_raw + (base - smem_u32(smem_raw));
@@ -140,18 +169,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t pstage = (uint32_t)g.pstage;
   const uint32_t sB = base;                                   // nslices x SLICE
   const uint32_t sP = base + nslices * SLICE;                 // stages x patch
-  uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + nslices * SLICE + stages * pstage);
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * kMaxStages + 5);
+  const uint32_t sO = sP + stages * pstage;                   // nout x OUTBUF
+  float *gO = reinterpret_cast<float *>(gbase + (sO - base));
+  uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + (sO - base) + g.nout * OUTBUF);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * kMaxStages + 5 + 2 * kMaxOut);
   const uint32_t bar0 = smem_u32(bars);
   auto full = [&](int s) { return bar0 + 8u * s; };
   auto empty = [&](int s) { return bar0 + 8u * (kMaxStages + s); };
   auto tfull = [&](int a) { return bar0 + 8u * (2 * kMaxStages + a); };
   auto tempty = [&](int a) { return bar0 + 8u * (2 * kMaxStages + 2 + a); };
   const uint32_t wbar = bar0 + 8u * (2 * kMaxStages + 4);
+  auto ofull = [&](int b) { return bar0 + 8u * (2 * kMaxStages + 5 + b); };
+  auto oempty = [&](int b) { return bar0 + 8u * (2 * kMaxStages + 5 + kMaxOut + b); };
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  long long st[4] = {0, 0, 0, 0};
+  long long st[5] = {0, 0, 0, 0, 0};
   const long long t_start = clock64();
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < stages; ++s) {
@@ -161,6 +194,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull(a), 1);
       mbar_init(tempty(a), 256);
+    }
+    for (int b = 0; b < g.nout; ++b) {
+      mbar_init(ofull(b), 1);
+      mbar_init(oempty(b), 1);   // the storing thread, once the block's store has read it
     }
     mbar_init(wbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -275,6 +312,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++acc == 2) { acc = 0; aph ^= 1; }
       }
     }
+  } else if (warp == 3) {
+    if (lane == 0 && g.nout > 0) {
+      // output-tile loader: the previous output block [F][TH][TW] of each
+      // tile, TMA-loaded into a ring of nout buffers (for init, the buffer
+      // is only handed over once its last store has drained)
+      int b = 0;
+      uint32_t ph = 0;
+      for (int64_t t = blockIdx.x; t < g.tiles; t += gridDim.x) {
+        int32_t n, h0, w0;
+        tile_coords(t, n, h0, w0);
+        mbar_wait(oempty(b), ph ^ 1);
+        if (g.init) {
+          mbar_arrive(ofull(b));
+        } else {
+          mbar_expect_tx(ofull(b), (uint32_t)OUTBUF);
+          tma_load_4d(&tma_out, ofull(b), sO + b * OUTBUF, w0, h0, 0, n);
+        }
+        if (++b == g.nout) { b = 0; ph ^= 1; }
+      }
+    }
   } else if (warp >= 4) {
     // two epilogue warpgroups: warp w reads TMEM lanes 32 * (w % 4) + [0, 32)
     // (its lane quadrant) and warpgroup e takes the 16-column chunks
@@ -282,51 +339,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int m = (warp % 4) * 32 + lane;   // TMEM lane = tile pixel (row * ROWLEN + col)
     const int e = (warp - 4) / 4;
     const int hr = m / ROWLEN, wc = m % ROWLEN;
+    const bool lane_ok = wc < g.tw;         // R > 1: the last KW - 1 (+ pad) columns are halo
     const int sf = (int)g.so_f;   // channel stride in elements (< 2^31 / F, host-checked)
     constexpr int CH = F / 32 > 0 ? F / 32 : 1;   // 16-column chunks per warpgroup
-    // this thread's output pixel of tile t: base pointer and validity
-    auto pixel = [&](int64_t t, bool &valid) -> float * {
-      int32_t n, h0, w0;
-      tile_coords(t, n, h0, w0);
-      valid = t < g.tiles && wc < g.tw && h0 + hr < g.ho && w0 + wc < g.wo;
-      return out + n * g.so_n + (h0 + hr) * g.so_h + (w0 + wc) * g.so_w;
-    };
-    // the previous output values of the NEXT tile are loaded while the
-    // current one is written, so DRAM latency overlaps a whole tile
-    float nxt[CH][16];
-    auto fetch = [&](const float *o, bool valid) {
-      if (valid && !g.init) {
-#pragma unroll
-        for (int c = 0; c < CH; ++c) {
-          if (16 * e + 32 * c >= F) break;
-          const float *pc = o + (16 * e + 32 * c) * sf;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) nxt[c][j] = pc[j * sf];
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < CH; ++c)
-#pragma unroll
-          for (int j = 0; j < 16; ++j) nxt[c][j] = g.init_value;
-      }
-    };
-    bool valid;
-    float *o = pixel(blockIdx.x, valid);
-    fetch(o, valid);
     int acc = 0;
     uint32_t aph = 0;
+    int ob = 0;
+    uint32_t oph = 0;
     for (int64_t t = blockIdx.x; t < g.tiles; t += gridDim.x) {
-      float cur[CH][16];
-#pragma unroll
-      for (int c = 0; c < CH; ++c)
-#pragma unroll
-        for (int j = 0; j < 16; ++j) cur[c][j] = nxt[c][j];
-      const bool cur_valid = valid;
-      float *const co = o;
-      o = pixel(t + gridDim.x, valid);
-      fetch(o, valid);
+      int32_t n, h0, w0;
+      tile_coords(t, n, h0, w0);
+      const bool valid = lane_ok && h0 + hr < g.ho && w0 + wc < g.wo;
+      float *const o = out + n * g.so_n + (h0 + hr) * g.so_h + (w0 + wc) * g.so_w;
       TIMED(3, mbar_wait(tfull(acc), aph));
       tc_fence_after();
+      // staged: this pixel's [c][row][col] slot of the TMA-loaded block,
+      // updated in place and stored back by TMA
+      float *st_px = gO + ob * (OUTBUF / 4) + hr * T::TW + wc;
+      if (g.nout > 0) TIMED(4, mbar_wait(ofull(ob), oph));
       const uint32_t trow = tmem_base + ((uint32_t)((warp % 4) * 32) << 16) + (uint32_t)(acc * N);
 #pragma unroll
       for (int c = 0; c < CH; ++c) {
@@ -335,28 +365,59 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t v[R][16];
 #pragma unroll
         for (int kj = 0; kj < R; ++kj) tmem_ld16_nowait(trow + (uint32_t)(kj * F + c0), v[kj]);
+        float prev[16];
+        if (g.nout > 0 && !g.init) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) prev[j] = lane_ok ? st_px[(c0 + j) * TPIX] : 0.f;
+        } else if (!g.init && valid) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) prev[j] = o[(c0 + j) * sf];
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) prev[j] = g.init_value;
+        }
         tmem_wait_ld();
         // all 16 results first (independent shuffles interleave), then one
         // branch around the stores
-        float res[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           float sum = __uint_as_float(v[0][j]);
 #pragma unroll
           for (int kj = 1; kj < R; ++kj)
             sum += __shfl_down_sync(0xffffffffu, __uint_as_float(v[kj][j]), kj);
-          res[j] = cur[c][j] + sum;
+          prev[j] += sum;
         }
-        if (cur_valid) {
-          float *pc = co + c0 * sf;
+        if (g.nout > 0) {
+          if (lane_ok) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) pc[j * sf] = res[j];
+            for (int j = 0; j < 16; ++j) st_px[(c0 + j) * TPIX] = prev[j];
+          }
+        } else if (valid) {
+          float *pc = o + c0 * sf;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) pc[j * sf] = prev[j];
         }
       }
       tc_fence_before();
       mbar_arrive(tempty(acc));
       if (++acc == 2) { acc = 0; aph ^= 1; }
+      if (g.nout > 0) {
+        // the block goes back by one TMA store (out-of-range rows/columns
+        // clipped); buffer ob - 1 is released once its own store has read it
+        fence_proxy_async();
+        named_bar_sync(1, 256);
+        if (threadIdx.x == 128) {
+          tma_store_4d(&tma_out, sO + ob * OUTBUF, w0, h0, 0, n);
+          bulk_commit();
+          if (t != blockIdx.x) {
+            bulk_wait_read<1>();
+            mbar_arrive(oempty(ob == 0 ? g.nout - 1 : ob - 1));
+          }
+        }
+        if (++ob == g.nout) { ob = 0; oph ^= 1; }
+      }
     }
+    if (g.nout > 0 && threadIdx.x == 128) bulk_wait_all();
   }
   if (g.stats && lane == 0) {
     const unsigned long long tot = (unsigned long long)(clock64() - t_start);
@@ -369,6 +430,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       atomicAdd(&g.stats[9], tot);
     } else if (warp == 4) {
       atomicAdd(&g.stats[3], (unsigned long long)st[3]);
+      atomicAdd(&g.stats[4], (unsigned long long)st[4]);
       atomicAdd(&g.stats[10], tot);
     }
   }
@@ -484,15 +546,21 @@ int conv_merge(int64_t f, int64_t kw) {
   return (kw == 3 && (f == 32 || f == 64)) || (kw == 5 && f == 32) ? (int)kw : 1;
 }
 
-// Shared memory of the kernel (weights, `stages` patch stages, barriers,
-// alignment).  Mirrored by runtime.conv_tc_supported.
-size_t conv_smem(int64_t f, int64_t kh, int64_t kw, int64_t cp, int64_t pstage, int stages) {
-  return 1024 + kh * kw * (cp / 64) * f * 128 + stages * pstage + 256;
+// Shared memory of the kernel (weights, `stages` patch stages, `nout` staged
+// output blocks of `outbuf` bytes, barriers, alignment).  Mirrored by
+// runtime.conv_tc_supported (2 stages, no staged output blocks).
+size_t conv_smem(int64_t f, int64_t kh, int64_t kw, int64_t cp, int64_t pstage, int stages,
+                 int nout, int64_t outbuf) {
+  return 1024 + kh * kw * (cp / 64) * f * 128 + stages * pstage + nout * outbuf + 256;
 }
 
 template <int F, int R>
 int launch_conv(const void *in_nhwc, const void *wt, float *out, ConvGeo &g, cudaStream_t s) {
-  CUtensorMap mi, mw;
+  using T = Tiling<F, R>;
+  auto smem_of = [&](int stages, int nout) {
+    return conv_smem(F, g.kh, g.kw, g.cp, g.pstage, stages, nout, T::OUTBUF);
+  };
+  CUtensorMap mi, mw, mo;
   cuuint64_t di[4] = {(cuuint64_t)g.cp, (cuuint64_t)g.wp, (cuuint64_t)g.hp, (cuuint64_t)g.nb};
   cuuint64_t si[3] = {(cuuint64_t)(g.cp * 2), (cuuint64_t)(g.wp * g.cp * 2),
                       (cuuint64_t)(g.hp * g.wp * g.cp * 2)};
@@ -502,10 +570,32 @@ int launch_conv(const void *in_nhwc, const void *wt, float *out, ConvGeo &g, cud
                    CU_TENSOR_MAP_SWIZZLE_128B))
     return B200_ELAUNCH;
   if (!make_map(&mw, 0, wt, F, g.kh * g.kw * g.cp, F)) return B200_ELAUNCH;
-  if (conv_smem(F, g.kh, g.kw, g.cp, g.pstage, 2) > kSmemMax) return B200_EUNSUPPORTED;
+  if (smem_of(2, 0) > kSmemMax) return B200_EUNSUPPORTED;
+  // output blocks staged through shared memory (TMA load, in-place update,
+  // TMA store) when the NCHW output is a legal tensor map: 16-byte aligned
+  // base and strides, unit w stride.  Box origins are multiples of TW
+  // columns = 32 bytes.
+  g.nout = 0;
+  const bool tma_ok = g.so_w == 1 && (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
+                      (g.so_h * 4) % 16 == 0 && (g.so_f * 4) % 16 == 0 &&
+                      (g.so_n * 4) % 16 == 0;
+  if (tma_ok) {
+    cuuint64_t dout[4] = {(cuuint64_t)g.wo, (cuuint64_t)g.ho, (cuuint64_t)F, (cuuint64_t)g.nb};
+    cuuint64_t sout[3] = {(cuuint64_t)(g.so_h * 4), (cuuint64_t)(g.so_f * 4),
+                          (cuuint64_t)(g.so_n * 4)};
+    cuuint32_t bout[4] = {(cuuint32_t)T::TW, (cuuint32_t)T::TH, F, 1};
+    if (make_map_4d(&mo, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, out, dout, sout, bout,
+                    CU_TENSOR_MAP_SWIZZLE_NONE)) {
+      const char *env = getenv("B200_CONV_NOUT");   // dev knob
+      g.nout = env ? atoi(env) : kMaxOut;
+      if (g.nout > kMaxOut) g.nout = kMaxOut;
+      while (g.nout > 0 && smem_of(2, g.nout) > kSmemMax) --g.nout;
+    }
+  }
+  if (g.nout == 0) mo = mi;   // unused placeholder
   g.stages = kMaxStages;
-  while (conv_smem(F, g.kh, g.kw, g.cp, g.pstage, g.stages) > kSmemMax) --g.stages;
-  const size_t smem = conv_smem(F, g.kh, g.kw, g.cp, g.pstage, g.stages);
+  while (smem_of(g.stages, g.nout) > kSmemMax) --g.stages;
+  const size_t smem = smem_of(g.stages, g.nout);
   int ctas = num_sms();
   if (g.tiles < ctas) ctas = (int)g.tiles;
   cudaFuncSetAttribute(conv_tc_kernel<F, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -515,7 +605,7 @@ int launch_conv(const void *in_nhwc, const void *wt, float *out, ConvGeo &g, cud
     cudaMalloc(&g.stats, 16 * sizeof(unsigned long long));
     cudaMemsetAsync(g.stats, 0, 16 * sizeof(unsigned long long), s);
   }
-  conv_tc_kernel<F, R><<<ctas, kThreads, smem, s>>>(mi, mw, out, g);
+  conv_tc_kernel<F, R><<<ctas, kThreads, smem, s>>>(mi, mw, mo, out, g);
   if (stats) {
     unsigned long long h[16];
     cudaMemcpyAsync(h, g.stats, sizeof(h), cudaMemcpyDeviceToHost, s);
@@ -524,10 +614,12 @@ int launch_conv(const void *in_nhwc, const void *wt, float *out, ConvGeo &g, cud
     const double c = ctas;
     fprintf(stderr,
             "conv stats (kcycles/CTA): producer total %.1f wait-empty %.1f | mma total %.1f "
-            "wait-full %.1f wait-tempty %.1f | epilogue total %.1f wait-tfull %.1f | "
-            "R %d stages %d tiles %lld\n",
+            "wait-full %.1f wait-tempty %.1f | epilogue total %.1f wait-tfull %.1f "
+            "wait-out %.1f | "
+            "R %d stages %d staged output blocks %d tiles %lld\n",
             h[8] / c / 1e3, h[0] / c / 1e3, h[9] / c / 1e3, h[1] / c / 1e3, h[2] / c / 1e3,
-            h[10] / c / 1e3, h[3] / c / 1e3, R, g.stages, (long long)g.tiles);
+            h[10] / c / 1e3, h[3] / c / 1e3, h[4] / c / 1e3, R, g.stages, g.nout,
+            (long long)g.tiles);
   }
   return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
 }
@@ -590,10 +682,10 @@ extern "C" int b200_conv2d_tc(const void *in_nhwc, const void *wt, float *out,
   g.so_n = out_strides[0]; g.so_f = out_strides[1];
   g.so_h = out_strides[2]; g.so_w = out_strides[3];
   const int R = conv_merge(f, kw);
-  if (R == 1) {
+  if (R == 1) {   // Tiling<F, 1>
     g.th = 16; g.tw = 8; g.prow = (int)(8 + kw - 1);
-  } else {
-    g.th = 8; g.tw = (int)(16 - kw + 1); g.prow = 16;
+  } else {        // Tiling<F, KW>: 4 rows of 32 patch pixels, 28 output columns
+    g.th = 4; g.tw = 28; g.prow = 32;
   }
   g.ph = (int)(g.th + kh - 1);
   g.th_tiles = (ho + g.th - 1) / g.th;

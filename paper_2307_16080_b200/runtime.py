@@ -203,8 +203,8 @@ def conv_tc_supported(cv):
     if cv.f not in (32, 64, 128) or cv.wo + cv.kw - 1 > 256:   # pack kernel: W <= 256
         return False
     merged = (cv.kw == 3 and cv.f in (32, 64)) or (cv.kw == 5 and cv.f == 32)   # conv_merge
-    if merged:   # tile 8 x (16 - kw + 1), patch rows of 16 pixels
-        ph, prow = 8 + cv.kh - 1, 16
+    if merged:   # tile 4 x 28, patch rows of 32 pixels
+        ph, prow = 4 + cv.kh - 1, 32
     else:        # tile 16 x 8, patch rows of 8 + kw - 1 pixels
         ph, prow = 16 + cv.kh - 1, 8 + cv.kw - 1
     patch = -(-(ph * prow * 128) // 1024) * 1024
