@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import weakref
 
 import numpy as np
 
@@ -104,6 +105,42 @@ _TORCH_DT = {"f32": "float32", "f64": "float64", "i32": "int32", "i64": "int64"}
 DT_CODE = {"f32": 0, "f64": 1, "i32": 2, "i64": 3}
 
 
+_PINNED = {}              # id(array) -> (address, nbytes) of page-locked Buffer storage
+PIN_MIN_BYTES = 1 << 20
+
+
+def _unpin(key, addr):
+    _PINNED.pop(key, None)
+    try:
+        torch_mod().cuda.cudart().cudaHostUnregister(addr)
+    except Exception:   # interpreter shutdown / context already gone
+        pass
+
+
+def pin_host(arr, host):
+    """Page-lock a Buffer's storage (``array.array``) in place, once.
+
+    The reference mutates memref Buffers in place, so their storage is the
+    staging source and destination of every run; registering it with the
+    driver (cudaHostRegister) turns each copy into a direct DMA instead of a
+    bounce through a pageable staging buffer.  The registration lives as long
+    as the array (weakref finalizer).  B200_PIN=0 disables it.
+    """
+    nbytes = host.numel() * host.element_size()
+    if nbytes < PIN_MIN_BYTES or os.environ.get("B200_PIN", "1") == "0":
+        return
+    key, addr = id(arr), host.data_ptr()
+    if _PINNED.get(key) == (addr, nbytes):
+        return
+    if key in _PINNED:   # storage moved (resized array): drop the stale range
+        _unpin(key, _PINNED[key][0])
+    torch = torch_mod()
+    if int(torch.cuda.cudart().cudaHostRegister(addr, nbytes, 0)) != 0:
+        return
+    _PINNED[key] = (addr, nbytes)
+    weakref.finalize(arr, _unpin, key, addr)
+
+
 class Staging:
     """Device copies of the host Buffers touched by a run (or a Session).
 
@@ -129,6 +166,7 @@ class Staging:
             torch = self.torch
             dt = getattr(torch, _TORCH_DT[buf.dtype])
             host = torch.frombuffer(buf.data, dtype=dt)
+            pin_host(buf.data, host)
             t = host.to("cuda", non_blocking=False)
             ent = (buf, t)
             self.dev[id(buf)] = ent
