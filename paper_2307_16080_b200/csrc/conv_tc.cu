@@ -18,13 +18,13 @@
 // shifted tile per tap.  The 128B swizzle is a function of absolute shared
 // memory address bits, so shifted starts need no descriptor base offset.
 //
-// Two tilings (template R):
+// Two tilings (template R, struct Tiling):
 //  R == 1   tile 16 rows x 8 columns (M = 128 = row * 8 + col), patch rows of
 //           PW = 8 + KW - 1 pixels; one UMMA 128 x F x 16 per (tap, 16
 //           channels).
 //  R == KW  (KW * F <= 256) the KW horizontal taps are merged into N: tile
-//           8 rows x (16 - KW + 1) columns, patch rows of 16 pixels (M = 128 =
-//           row * 16 + col), and one UMMA 128 x (KW * F) x 16 per (ki, 16
+//           4 rows x 28 columns over patch rows of 32 pixels (M = 128 =
+//           row * 32 + col), one UMMA 128 x (KW * F) x 16 per (ki, 16
 //           channels) against the KW weight slices stacked as B rows
 //           (kj, f).  The epilogue sums the KW partial products of output
 //           (h, w) from TMEM lanes (h, w + kj), columns kj * F + f, with warp
@@ -33,13 +33,16 @@
 //           amortises it over 3x the work.
 //
 // Weights ([F][KH][KW][Cp] bf16, K-major) stay resident in shared memory for
-// the whole kernel.  The epilogue reads and writes the NCHW f32 output
-// directly from registers (a warp covers 2-4 image rows x 8-16 contiguous
-// pixels per channel): no output staging in shared memory, any strides.
+// the whole kernel.  Output blocks [F][TH][TW] fp32 are staged through
+// shared memory: TMA-loaded ahead by a loader warp (out += conv reads the
+// previous output), updated in place by the epilogue, TMA-stored (rows and
+// columns past the image clipped).  Outputs that are not a legal tensor map
+// (unaligned strides) take a direct register path instead.
 // Structure per CTA (persistent over tiles):
 //   warp 0  TMA producer (weights once; one patch per (tile, channel block))
 //   warp 1  MMA issuer
 //   warp 2  TMEM allocator (2 accumulator buffers of R * F columns)
+//   warp 3  output-block loader (ring of up to 3 blocks)
 //   warps 4-11 epilogue, two warpgroups splitting the output channels:
 //           thread = TMEM lane = tile pixel
 #include <cuda.h>
@@ -444,86 +447,89 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // NCHW f32 (any strides) -> NHWC bf16 with channels padded to cp (zeros).
-// A CTA transposes one (n, h) row slab [cp][W] through shared memory per
-// iteration, grid-striding over rows, software-pipelined: the loads of the
-// next 64-channel pass (8 channel rows per warp x WI = ceil(W / 32) pixels
-// per lane, all in flight at once) are issued before the current row is
-// converted and written, so DRAM latency overlaps the shared-memory work —
-// the kernel is latency-bound otherwise.  Lanes convert 8 channels of
-// consecutive pixels (conflict-free column reads of the slab) into a bf16
-// [w][chunk] stage whose 16-byte chunks are XOR-swizzled by (w & 7), and the
-// stage leaves as contiguous 16-byte stores.
+// Register transpose, no shared memory.  The input is a set of `lines` of
+// `len` pixels (an image's whole H * W plane when its rows are contiguous,
+// else one row) and a work unit is (line, block of 32 * WI pixels, 64-channel
+// pass).  Warp k of a CTA owns the unit's 8-channel chunk k: its lanes read
+// the 8 channel runs (8 * WI coalesced loads in flight per thread) and each
+// lane writes one pixel's 8 channels as a 16-byte bf16 vector.  The 8 warps
+// of the CTA fill each pixel's 128-byte line within the same few hundred
+// cycles, so L2 merges the 16-byte pieces before DRAM.  Units are
+// grid-strided and the next unit's loads are issued before the current
+// unit's converts and stores (the kernel is latency-bound otherwise).
 constexpr int PACK_MAXW = 256;
+constexpr int PACK_WI = 4;
 template <int WI>
 __global__ void __launch_bounds__(256) pack_nhwc_kernel(const float *__restrict__ src, int64_t sN,
-                                                        int64_t sC, int64_t sH, int64_t sW,
+                                                        int64_t sC, int64_t sH, int64_t sP,
                                                         __nv_bfloat16 *__restrict__ dst, int C,
-                                                        int H, int W, int cp, int64_t rows) {
-  extern __shared__ float slab[];   // [cp][W + 1] f32, then [W][cp / 8] x 16 B bf16
-  const int ld = W + 1;
-  uint4 *stage = reinterpret_cast<uint4 *>(slab + ((cp * ld + 3) & ~3));
+                                                        int lines_per_img, int len, int cp,
+                                                        int64_t lines) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int chunks = cp / 8;   // multiple of 8
-  const int items = W * chunks;
   const int passes = cp / 64;
-  float v[8][WI];
-  auto load = [&](int64_t row, int pass) {
-    const float *base = src + (row / H) * sN + (row % H) * sH;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int c = pass * 64 + warp + 8 * k;
-#pragma unroll
-      for (int i = 0; i < WI; ++i) {
-        const int w = lane + 32 * i;
-        v[k][i] = (c < C && w < W) ? __ldg(base + (int64_t)c * sC + (int64_t)w * sW) : 0.f;
-      }
-    }
+  const int blocks = (len + 32 * WI - 1) / (32 * WI);
+  const int64_t units = lines * blocks * passes;
+  float v[2][8][WI];
+  auto coords = [&](int64_t u, int64_t &line, int &p0, int &c0) {
+    const int64_t lb = u / passes;
+    c0 = (int)(u - lb * passes) * 64 + warp * 8;
+    line = lb / blocks;
+    p0 = (int)(lb - line * blocks) * 32 * WI;
   };
-  int64_t row = blockIdx.x;
-  int pass = 0;
-  if (row < rows) load(row, 0);
-  while (row < rows) {
+  auto load = [&](float (&r)[8][WI], int64_t u) {
+    int64_t line;
+    int p0, c0;
+    coords(u, line, p0, c0);
+    const float *base = src + (line / lines_per_img) * sN + (line % lines_per_img) * sH;
 #pragma unroll
     for (int k = 0; k < 8; ++k)
 #pragma unroll
-      for (int i = 0; i < WI; ++i)
-        if (lane + 32 * i < W) slab[(pass * 64 + warp + 8 * k) * ld + lane + 32 * i] = v[k][i];
-    if (++pass < passes) {   // more channel passes of this row (disjoint slab rows)
-      load(row, pass);
-      continue;
-    }
-    __syncthreads();
-    const int64_t next = row + gridDim.x;
-    if (next < rows) load(next, 0);
-    for (int i = threadIdx.x; i < items; i += 256) {
-      const int chunk = i / W, w = i - chunk * W;
-      const float *col = slab + chunk * 8 * ld + w;
-      __nv_bfloat162 b[4];
+      for (int i = 0; i < WI; ++i) {
+        const int p = p0 + lane + 32 * i;
+        r[k][i] = (c0 + k < C && p < len)
+                      ? __ldg(base + (int64_t)(c0 + k) * sC + (int64_t)p * sP) : 0.f;
+      }
+  };
+  auto store = [&](const float (&r)[8][WI], int64_t u) {
+    int64_t line;
+    int p0, c0;
+    coords(u, line, p0, c0);
+    __nv_bfloat16 *base = dst + line * (int64_t)len * cp + c0;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        b[j] = __floats2bfloat162_rn(col[(2 * j) * ld], col[(2 * j + 1) * ld]);
-      stage[w * chunks + (chunk ^ (w & 7))] = *reinterpret_cast<uint4 *>(b);
+    for (int i = 0; i < WI; ++i) {
+      const int p = p0 + lane + 32 * i;
+      if (p < len) {
+        __nv_bfloat162 b[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = __floats2bfloat162_rn(r[2 * j][i], r[2 * j + 1][i]);
+        *reinterpret_cast<uint4 *>(base + (int64_t)p * cp) = *reinterpret_cast<uint4 *>(b);
+      }
     }
-    __syncthreads();
-    uint4 *outp = reinterpret_cast<uint4 *>(dst + row * (int64_t)W * cp);
-    for (int i = threadIdx.x; i < items; i += 256) {
-      const int w = i / chunks, chunk = i - w * chunks;
-      outp[i] = stage[w * chunks + (chunk ^ (w & 7))];
-    }
-    row = next;
-    pass = 0;
+  };
+  int64_t u = blockIdx.x;
+  if (u < units) load(v[0], u);
+  for (; u < units; u += 2 * (int64_t)gridDim.x) {
+    const int64_t u1 = u + gridDim.x;
+    if (u1 < units) load(v[1], u1);
+    store(v[0], u);
+    if (u1 >= units) break;
+    if (u1 + gridDim.x < units) load(v[0], u1 + gridDim.x);
+    store(v[1], u1);
   }
 }
 
 // FCHW f32 weights -> [F][KH][KW][cp] bf16 (K order: tap, channel).
+// One thread per destination element; 32-bit index math (the tensor is at
+// most F * KH * KW * cp < 2^31 elements, host-checked).
 __global__ void pack_wt_kernel(const float *__restrict__ src, int64_t sF, int64_t sC,
                                int64_t sKH, int64_t sKW, __nv_bfloat16 *__restrict__ dst,
-                               int64_t F, int64_t C, int64_t KH, int64_t KW, int64_t cp) {
-  const int64_t total = F * KH * KW * cp;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = i % cp, tap = (i / cp) % (KH * KW), f = i / (cp * KH * KW);
-    const int64_t ki = tap / KW, kj = tap % KW;
+                               int F, int C, int KH, int KW, int cp) {
+  const int total = F * KH * KW * cp;
+  const int taps = KH * KW;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int c = i % cp, ft = i / cp;
+    const int tap = ft % taps, f = ft / taps;
+    const int ki = tap / KW, kj = tap - ki * KW;
     dst[i] = __float2bfloat16_rn(c < C ? src[f * sF + c * sC + ki * sKH + kj * sKW] : 0.f);
   }
 }
@@ -629,30 +635,19 @@ int launch_conv(const void *in_nhwc, const void *wt, float *out, ConvGeo &g, cud
 extern "C" int b200_pack_conv_input(const float *src, const int64_t *sstr, void *dst, int64_t nb,
                                     int64_t c, int64_t h, int64_t w, int64_t cp, void *stream) {
   if (nb <= 0 || h <= 0 || w <= 0 || cp < c || cp % 64 || w > PACK_MAXW) return B200_EINVAL;
-  const size_t smem = (((size_t)cp * (w + 1) + 3) & ~(size_t)3) * 4 + (size_t)w * cp * 2;
-  if (smem > 227 * 1024) return B200_EUNSUPPORTED;
-  const int64_t rows = nb * h;
-  auto launch = [&](auto kernel) {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, smem);
-    int64_t blocks = (int64_t)num_sms() * (per_sm < 1 ? 1 : per_sm);
-    if (blocks > rows) blocks = rows;
-    kernel<<<(unsigned)blocks, 256, smem, static_cast<cudaStream_t>(stream)>>>(
-        src, sstr[0], sstr[1], sstr[2], sstr[3], static_cast<__nv_bfloat16 *>(dst), (int)c,
-        (int)h, (int)w, (int)cp, rows);
-  };
-  switch ((w + 31) / 32) {
-    case 1: launch(pack_nhwc_kernel<1>); break;
-    case 2: launch(pack_nhwc_kernel<2>); break;
-    case 3: launch(pack_nhwc_kernel<3>); break;
-    case 4: launch(pack_nhwc_kernel<4>); break;
-    case 5: launch(pack_nhwc_kernel<5>); break;
-    case 6: launch(pack_nhwc_kernel<6>); break;
-    case 7: launch(pack_nhwc_kernel<7>); break;
-    default: launch(pack_nhwc_kernel<8>); break;
-  }
+  // rows contiguous (h stride = W * w stride): one line per image plane
+  const bool plane = sstr[2] == w * sstr[3];
+  const int lines_per_img = plane ? 1 : (int)h;
+  const int len = plane ? (int)(h * w) : (int)w;
+  const int64_t lines = nb * lines_per_img;
+  const int64_t units = lines * ((len + 32 * PACK_WI - 1) / (32 * PACK_WI)) * (cp / 64);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pack_nhwc_kernel<PACK_WI>, 256, 0);
+  int64_t blocks = (int64_t)num_sms() * (per_sm < 1 ? 1 : per_sm);
+  if (blocks > units) blocks = units;
+  pack_nhwc_kernel<PACK_WI><<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      src, sstr[0], sstr[1], sstr[2], sstr[3], static_cast<__nv_bfloat16 *>(dst), (int)c,
+      lines_per_img, len, (int)cp, lines);
   return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
 }
 
@@ -661,11 +656,12 @@ extern "C" int b200_pack_conv_weight(const float *src, const int64_t *sstr, void
                                      void *stream) {
   const int64_t total = f * kh * kw * cp;
   if (total <= 0 || cp % 64) return B200_EINVAL;
+  if (total >= (int64_t(1) << 31)) return B200_EUNSUPPORTED;
   int64_t blocks = (total + 255) / 256;
   if (blocks > 4096) blocks = 4096;
   pack_wt_kernel<<<(unsigned)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      src, sstr[0], sstr[1], sstr[2], sstr[3], static_cast<__nv_bfloat16 *>(dst), f, c, kh, kw,
-      cp);
+      src, sstr[0], sstr[1], sstr[2], sstr[3], static_cast<__nv_bfloat16 *>(dst), (int)f,
+      (int)c, (int)kh, (int)kw, (int)cp);
   return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
 }
 

@@ -20,7 +20,7 @@ import weakref
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libb200k.so")
+LIB_PATH = os.environ.get("B200_LIB") or os.path.join(_PKG, "libb200k.so")   # dev: A/B builds
 
 _lib = None
 
