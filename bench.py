@@ -9,7 +9,7 @@ size, C[i,k] += A[i,j] * B[j,k] on f32 Buffers, bf16 tensor-core precision.
 Other workloads (configs[0], [2], [3]): ``linear32`` (Linear(32,32) lowering),
 ``conv`` (conv_2d_nchw_fchw N=256 C=F=64 56x56 3x3, batch-sharded),
 ``ls`` (Linear stack 65536x1024->4096->1024, batch-sharded), ``ewise``
-(y = y + 2x over 4096x4096 f32).
+(y = y + 2x over 8192x8192 f32).
 
 A step is one pass of the hot path over one batch: one run of the nest.
 Data: U(-1,1) f32 from torch.Generator().manual_seed(arg index).
@@ -98,11 +98,11 @@ class Workload:
             self.slice = (bk.linear32, self.flops, "the full Linear(32,32) lowering")
             self.default_precision = "exact"
         elif name == "ewise":
-            self.fn = bk.saxpy4k
-            self.flops = 2.0 * 4096 * 4096
-            self.bytes = 3 * 4096 * 4096 * 4
+            self.fn = bk.saxpy8k
+            self.flops = 2.0 * 8192 * 8192
+            self.bytes = 3 * 8192 * 8192 * 4
             self.scaling = "weak"
-            self.desc = "elementwise y = y + 2x over 4096x4096 f32"
+            self.desc = "elementwise y = y + 2x over 8192x8192 f32 (512 MB working set)"
             self.slice = (bk.saxpy_slice, 2.0 * 16 * 4096, "16x4096 rows of the same nest")
             self.default_precision = "exact"
         else:

@@ -11,7 +11,7 @@ they live in a module.
   linear32    torch.nn.Linear(32,32) lowering
   ls_*        batched Linear stack 65536 x 1024 -> 4096 -> 1024 with fill and
               bias nests (two Linear lowerings chained, fill into the output)
-  saxpy4k     elementwise y = y + x * 2 over 4096 x 4096 f32
+  saxpy8k     elementwise y = y + x * 2 over 8192 x 8192 f32 (512 MB working set > L2)
 """
 from staircase import F32, F64, MemRef, constant, parallel, staged
 
@@ -137,8 +137,8 @@ def linear_stack(x: MemRef[({rows}, 1024), F32], w1t: MemRef[(1024, 4096), F32],
 
 
 @staged
-def saxpy4k(x: MemRef[(4096, 4096), F32], y: MemRef[(4096, 4096), F32]):
-    for i, j in parallel((0, 0), (4096, 4096)):
+def saxpy8k(x: MemRef[(8192, 8192), F32], y: MemRef[(8192, 8192), F32]):
+    for i, j in parallel((0, 0), (8192, 8192)):
         y[i, j] = y[i, j] + x[i, j] * constant(2.0, F32)
 
 
