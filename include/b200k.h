@@ -153,6 +153,19 @@ int b200_gemm_tc(int32_t kind, const void *A, const void *Bt, float *C, int64_t 
                  int32_t max_ctas, int32_t variant, void *stream);
 
 /*
+ * b200_gemm_tc that also writes the final C (after init / bias) rounded to
+ * bf16 into c16 (row-major, leading dimension ld16 >= N): the K-major packed
+ * A operand of a following contraction that reads C — e.g. the second
+ * Linear of a chained Linear stack, whose activations the reference keeps in
+ * an f32 Buffer (the f32 C is still written in full).  Saves the separate
+ * b200_pack_operand pass over C.
+ */
+int b200_gemm_tc_shadow(int32_t kind, const void *A, const void *Bt, float *C, int64_t sCm,
+                        int64_t sCn, int64_t M, int64_t N, int64_t K, int32_t init,
+                        float init_value, const float *bias, int64_t bias_stride,
+                        void *c16, int64_t ld16, void *stream);
+
+/*
  * Convolution on the tensor cores (conv_2d_nchw_fchw, valid, stride 1;
  * reference tests/kernels.py:50-64), engine precision
  * bf16.  b200_pack_conv_input: NCHW f32 (element strides sstr[4], HOST array)

@@ -322,15 +322,17 @@ extern "C" int b200_pack_operand(int32_t kind, const float *src, int64_t s_row, 
   return pack<float>(src, s_row, s_col, static_cast<float *>(dst), rows, cols, s);
 }
 
-extern "C" int b200_gemm_tc(int32_t kind, const void *A, const void *Bt, float *C, int64_t sCm,
-                            int64_t sCn, int64_t M, int64_t N, int64_t K, int32_t init,
-                            float init_value, const float *bias, int64_t bias_stride,
-                            int32_t max_ctas, int32_t variant, void *stream) {
+namespace {
+
+int gemm_tc(int32_t kind, const void *A, const void *Bt, float *C, int64_t sCm, int64_t sCn,
+            int64_t M, int64_t N, int64_t K, int32_t init, float init_value, const float *bias,
+            int64_t bias_stride, int32_t max_ctas, int32_t variant, __nv_bfloat16 *c16,
+            int64_t ld16, void *stream) {
   if (M <= 0 || N <= 0) return B200_OK;
   if (K <= 0 || (kind != 0 && kind != 1)) return B200_EINVAL;
   const int elem = kind == 0 ? 2 : 4;
   if ((K * elem) % 16 != 0) return B200_EUNSUPPORTED;  // TMA row stride alignment
-  Epi ep{C, sCm, sCn, bias, bias_stride, init, init_value};
+  Epi ep{C, sCm, sCn, bias, bias_stride, init, init_value, c16, ld16};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int sms = num_sms();
   if (variant == 0) {
@@ -356,4 +358,24 @@ extern "C" int b200_gemm_tc(int32_t kind, const void *A, const void *Bt, float *
     gemm_tc_kernel<1><<<ctas, kThreads, SMEM_BYTES, s>>>(ma, mb, ep, M, N, K);
   }
   return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
+}
+
+}  // namespace
+
+extern "C" int b200_gemm_tc(int32_t kind, const void *A, const void *Bt, float *C, int64_t sCm,
+                            int64_t sCn, int64_t M, int64_t N, int64_t K, int32_t init,
+                            float init_value, const float *bias, int64_t bias_stride,
+                            int32_t max_ctas, int32_t variant, void *stream) {
+  return gemm_tc(kind, A, Bt, C, sCm, sCn, M, N, K, init, init_value, bias, bias_stride,
+                 max_ctas, variant, nullptr, 0, stream);
+}
+
+extern "C" int b200_gemm_tc_shadow(int32_t kind, const void *A, const void *Bt, float *C,
+                                   int64_t sCm, int64_t sCn, int64_t M, int64_t N, int64_t K,
+                                   int32_t init, float init_value, const float *bias,
+                                   int64_t bias_stride, void *c16, int64_t ld16,
+                                   void *stream) {
+  if (!c16 || ld16 < N) return B200_EINVAL;
+  return gemm_tc(kind, A, Bt, C, sCm, sCn, M, N, K, init, init_value, bias, bias_stride, 0, 0,
+                 static_cast<__nv_bfloat16 *>(c16), ld16, stream);
 }

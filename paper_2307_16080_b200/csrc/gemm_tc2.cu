@@ -237,7 +237,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
             if (lead_t) bulk_wait_read<NCBUF - 1>();
             named_bar_sync(1, 128);
           }
-          epilogue_chunk_smem(gC + b * CBUF, et, nb, N, ep, r);
+          epilogue_chunk_smem(gC + b * CBUF, et, nb, N, ep, r, m_base + et, M);
           fence_proxy_async();
           named_bar_sync(1, 128);
           if (lead_t) {

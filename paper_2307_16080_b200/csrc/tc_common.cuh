@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -204,7 +205,32 @@ struct Epi {
   int64_t bias_stride;
   int init;
   float init_value;
+  // optional bf16 shadow of the final C (row-major, leading dimension ld16):
+  // the next contraction's packed A operand, written by the same epilogue
+  __nv_bfloat16 *c16 = nullptr;
+  int64_t ld16 = 0;
 };
+
+// 32 consecutive final values of row m, columns [nb, nb + 32), into the bf16
+// shadow (4 x 16-byte stores when the whole run is in range).
+__device__ __forceinline__ void shadow_store32(const Epi &ep, int64_t m, int64_t nb, int64_t M,
+                                               int64_t N, const float (&v)[32]) {
+  if (m >= M) return;
+  __nv_bfloat16 *dst = ep.c16 + m * ep.ld16 + nb;
+  if (nb + 32 <= N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      __nv_bfloat162 b[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = __floats2bfloat162_rn(v[8 * q + 2 * j], v[8 * q + 2 * j + 1]);
+      reinterpret_cast<uint4 *>(dst)[q] = *reinterpret_cast<uint4 *>(b);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)   // fully unrolled: v stays in registers
+      if (nb + j < N) dst[j] = __float2bfloat16_rn(v[j]);
+  }
+}
 
 // One thread owns output row m; writes columns [nb, nb+32) from r[].
 __device__ __forceinline__ void epilogue_row32(const Epi &ep, int64_t m, int64_t nb, int64_t M,
@@ -213,6 +239,7 @@ __device__ __forceinline__ void epilogue_row32(const Epi &ep, int64_t m, int64_t
   float *crow = ep.C + m * ep.sCm;
   const bool vec = ep.sCn == 1 && nb + 32 <= N &&
                    ((reinterpret_cast<uintptr_t>(crow + nb) & 15) == 0);
+  float v[32];
   if (vec) {
     float4 *p = reinterpret_cast<float4 *>(crow + nb);
 #pragma unroll
@@ -231,18 +258,24 @@ __device__ __forceinline__ void epilogue_row32(const Epi &ep, int64_t m, int64_t
         o.w += b[3 * ep.bias_stride];
       }
       p[j] = o;
+      v[4 * j] = o.x, v[4 * j + 1] = o.y, v[4 * j + 2] = o.z, v[4 * j + 3] = o.w;
     }
   } else {
-    for (int j = 0; j < 32; ++j) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {   // fully unrolled: v stays in registers
       const int64_t n = nb + j;
-      if (n >= N) break;
-      float *dst = crow + n * ep.sCn;
-      float o = ep.init ? ep.init_value : *dst;
-      o += __uint_as_float(r[j]);
-      if (ep.bias) o += ep.bias[n * ep.bias_stride];
-      *dst = o;
+      v[j] = 0.f;
+      if (n < N) {
+        float *dst = crow + n * ep.sCn;
+        float o = ep.init ? ep.init_value : *dst;
+        o += __uint_as_float(r[j]);
+        if (ep.bias) o += ep.bias[n * ep.bias_stride];
+        *dst = o;
+        v[j] = o;
+      }
     }
   }
+  if (ep.c16) shadow_store32(ep, m, nb, M, N, v);
 }
 
 typedef CUresult (*EncodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
@@ -297,10 +330,32 @@ inline bool make_map_c(CUtensorMap *map, const float *C, int64_t rows, int64_t c
 // Epilogue over one 32-column chunk staged in shared memory by TMA with the
 // 128B swizzle: row r's 16-byte unit j lives at unit j ^ (r & 7).  The
 // thread owning row r adds its accumulator (and bias) in place.
+// m / M: the global row of r and the row count (for the bf16 shadow only).
 __device__ __forceinline__ void epilogue_chunk_smem(unsigned char *chunk, int r, int64_t nb,
                                                     int64_t N, const Epi &ep,
-                                                    const uint32_t (&acc)[32]) {
+                                                    const uint32_t (&acc)[32], int64_t m = 0,
+                                                    int64_t M = 0) {
   float4 *row = reinterpret_cast<float4 *>(chunk + r * 128);
+  // the chunk's 32 bias values, loaded up front (the same addresses for the
+  // whole warp: one broadcast transaction each): 8 x 16-byte loads when the
+  // bias is unit-stride and aligned, element loads otherwise
+  float4 bv[8];
+  if (ep.bias) {
+    const float *b = ep.bias + nb * ep.bias_stride;
+    if (ep.bias_stride == 1 && nb + 32 <= N && (reinterpret_cast<uintptr_t>(b) & 15) == 0) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) bv[j] = __ldg(reinterpret_cast<const float4 *>(b) + j);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int64_t n = nb + 4 * j;
+        bv[j].x = n + 0 < N ? __ldg(b + (4 * j + 0) * ep.bias_stride) : 0.f;
+        bv[j].y = n + 1 < N ? __ldg(b + (4 * j + 1) * ep.bias_stride) : 0.f;
+        bv[j].z = n + 2 < N ? __ldg(b + (4 * j + 2) * ep.bias_stride) : 0.f;
+        bv[j].w = n + 3 < N ? __ldg(b + (4 * j + 3) * ep.bias_stride) : 0.f;
+      }
+    }
+  }
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     float4 *p = row + (j ^ (r & 7));
@@ -311,14 +366,20 @@ __device__ __forceinline__ void epilogue_chunk_smem(unsigned char *chunk, int r,
     o.z += __uint_as_float(acc[4 * j + 2]);
     o.w += __uint_as_float(acc[4 * j + 3]);
     if (ep.bias) {
-      const int64_t n = nb + 4 * j;
-      const float *b = ep.bias + n * ep.bias_stride;
-      o.x += n + 0 < N ? __ldg(b) : 0.f;
-      o.y += n + 1 < N ? __ldg(b + ep.bias_stride) : 0.f;
-      o.z += n + 2 < N ? __ldg(b + 2 * ep.bias_stride) : 0.f;
-      o.w += n + 3 < N ? __ldg(b + 3 * ep.bias_stride) : 0.f;
+      o.x += bv[j].x;
+      o.y += bv[j].y;
+      o.z += bv[j].z;
+      o.w += bv[j].w;
     }
     *p = o;
+    bv[j] = o;   // reused as the final values for the shadow
+  }
+  if (ep.c16) {
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      v[4 * j] = bv[j].x, v[4 * j + 1] = bv[j].y, v[4 * j + 2] = bv[j].z, v[4 * j + 3] = bv[j].w;
+    shadow_store32(ep, m, nb, M, N, v);
   }
 }
 

@@ -51,21 +51,26 @@ ENGINE_NAME = "b200"
 PRECISION = os.environ.get("B200_PRECISION", "exact")
 # Cross-region fusion of queued plans (B200_FUSE=0 disables, for A/B tests).
 FUSE = os.environ.get("B200_FUSE", "1") != "0"
+# bf16 shadows of contraction outputs read as the next contraction's A
+# (fusion.plan_shadows; B200_SHADOW=0 disables, for A/B tests).
+SHADOW = os.environ.get("B200_SHADOW", "1") != "0"
 
 # kernel choice of the last run (tests and bench inspect these)
 last_plan = []
 
 
-def configure(precision=None, fuse=None):
+def configure(precision=None, fuse=None, shadow=None):
     """Select the contraction precision / fusion for subsequent runs."""
-    global PRECISION, FUSE
+    global PRECISION, FUSE, SHADOW
     if precision is not None:
         if precision not in ("exact", "tf32", "bf16"):
             raise ValueError(f"unknown precision {precision!r}")
         PRECISION = precision
     if fuse is not None:
         FUSE = bool(fuse)
-    return {"precision": PRECISION, "fuse": FUSE}
+    if shadow is not None:
+        SHADOW = bool(shadow)
+    return {"precision": PRECISION, "fuse": FUSE, "shadow": SHADOW}
 
 
 class ExecContext:
@@ -265,16 +270,23 @@ class _Run:
         if not self.pending:
             return
         items = fusion.fuse(self.pending) if FUSE else self.pending
+        if SHADOW:
+            fusion.plan_shadows(items)
         self.pending = []
         for it in items:
             if isinstance(it, fusion.ContractItem):
                 kernels = self.be.contract(it.g, PRECISION, init=it.init,
                                            init_value=it.init_value, bias=it.bias,
                                            bias_base=it.bias_base,
-                                           bias_stride=it.bias_stride)
+                                           bias_stride=it.bias_stride,
+                                           shadow_out=it.shadow_out, shadow_in=it.shadow_in)
                 g = it.g
+                fused = list(it.fused)
+                if it.shadow_in or it.shadow_out:
+                    used_in, made_out = getattr(self.be, "last_shadow", (False, False))
+                    fused += ["A<-shadow"] * used_in + ["C->shadow"] * made_out
                 self.plan.append((kernels[-1], g.M, g.N, g.K) +
-                                 ((tuple(it.fused),) if it.fused else ()))
+                                 ((tuple(fused),) if fused else ()))
             else:
                 m = it.m
                 self.be.map(m)

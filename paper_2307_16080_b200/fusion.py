@@ -33,7 +33,8 @@ class MapItem:
 
 
 class ContractItem:
-    __slots__ = ("g", "init", "init_value", "bias", "bias_base", "bias_stride", "fused")
+    __slots__ = ("g", "init", "init_value", "bias", "bias_base", "bias_stride", "fused",
+                 "shadow_out", "shadow_in")
 
     def __init__(self, g):
         self.g = g
@@ -43,6 +44,8 @@ class ContractItem:
         self.bias_base = 0
         self.bias_stride = 0
         self.fused = []
+        self.shadow_out = False   # also write C as the next contraction's packed A
+        self.shadow_in = False    # A is the previous contraction's shadow of its C
 
 
 def _size(buf):
@@ -153,4 +156,43 @@ def fuse(items):
     return out
 
 
-__all__ = ["MapItem", "ContractItem", "fuse"]
+def _dense_rows(buf, off, s, rows, cols):
+    """The operand is the whole buffer, row-major (rows x cols)."""
+    return off == 0 and tuple(s) == (cols, 1) and rows * cols == _size(buf)
+
+
+def plan_shadows(items):
+    """Mark producer/consumer pairs for the bf16 shadow of a contraction's C.
+
+    Chained Linear layers read one contraction's output C as the next one's
+    A operand.  On the tensor-core path that A is packed to bf16 K-major
+    first (a full extra pass over C); instead the producer's epilogue can
+    write the bf16 copy while it writes C (b200_gemm_tc_shadow).  A pair
+    qualifies when both are strided GEMMs, C is the whole buffer row-major
+    and is read as the whole of A row-major with the same M (K = producer
+    N), and no item in between touches that buffer — so the shadow is
+    exactly the pack of the consumer's A.  Whether the tensor-core path runs
+    at all is the backend's decision; an unused mark costs nothing.
+    """
+    for i, p in enumerate(items):
+        if not isinstance(p, ContractItem) or not p.g.strided:
+            continue
+        pg = p.g
+        if not _dense_rows(pg.C, pg.offC, pg.sC, pg.M, pg.N):
+            continue
+        for c in items[i + 1:]:
+            if isinstance(c, ContractItem):
+                cg = c.g
+                if cg.A is pg.C and cg.strided and cg.C is not pg.C and cg.B is not pg.C and \
+                        cg.M == pg.M and cg.K == pg.N and \
+                        _dense_rows(cg.A, cg.offA, cg.sA, cg.M, cg.K):
+                    p.shadow_out = c.shadow_in = True
+                    break
+                if cg.C is pg.C:      # overwritten before a qualifying reader
+                    break
+            elif any(b is pg.C for b in c.m.buffers):   # maps: conservatively
+                break
+    return items
+
+
+__all__ = ["MapItem", "ContractItem", "fuse", "plan_shadows"]

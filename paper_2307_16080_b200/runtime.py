@@ -57,6 +57,8 @@ SIGNATURES = {
     "b200_map_f32": [_P, _I32, _P, _I32, _P, _P, _I32, _P, _I32, _I32, _I32, _P],
     "b200_gemm_tc": [_I32, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I32, _F32, _P,
                      _I64, _I32, _I32, _P],
+    "b200_gemm_tc_shadow": [_I32, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I32, _F32, _P,
+                            _I64, _P, _I64, _P],
     "b200_pack_conv_input": [_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _P],
     "b200_pack_conv_weight": [_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _P],
     "b200_conv2d_tc": [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64,
@@ -258,12 +260,14 @@ def _direct_call(lib):
 
 def launch_gemm(lib, precision, a_ptr, sA, b_ptr, sB, c_ptr, sC, M, N, K, stream,
                 init=0, init_value=0.0, bias_ptr=None, bias_stride=0, max_ctas=0,
-                variant=0, call=None):
+                variant=0, call=None, a_packed=None, c16=None):
     """Enqueue C (+)= A.B with the kernel chosen by ``precision``.
 
     Returns the list of kernel names launched (for the launch count).
     exact -> b200_gemm_f32_exact (bit-identical to the reference);
     bf16/tf32 -> b200_pack_operand x2 + b200_gemm_tc (tcgen05).
+    a_packed: A already packed (a bf16 shadow, M x K) — its pack is skipped;
+    c16: also write C rounded to bf16 (M x N) with b200_gemm_tc_shadow.
     """
     call = call or _direct_call(lib)
     P = ctypes.c_void_p
@@ -274,14 +278,25 @@ def launch_gemm(lib, precision, a_ptr, sA, b_ptr, sB, c_ptr, sC, M, N, K, stream
         return ["gemm_f32_exact"]
     kind = 0 if precision == "bf16" else 1
     dt = "bfloat16" if kind == 0 else "float32"
-    Ap = workspace(0, dt, M, K)
+    names = []
+    if a_packed is not None:
+        Ap = a_packed
+    else:
+        Ap = workspace(0, dt, M, K)
+        call("b200_pack_operand", kind, P(a_ptr), sA[0], sA[1], P(Ap.data_ptr()), M, K, stream)
+        names.append("pack_operand")
     Bp = workspace(1, dt, N, K)
-    call("b200_pack_operand", kind, P(a_ptr), sA[0], sA[1], P(Ap.data_ptr()), M, K, stream)
     call("b200_pack_operand", kind, P(b_ptr), sB[1], sB[0], P(Bp.data_ptr()), N, K, stream)
-    call("b200_gemm_tc", kind, P(Ap.data_ptr()), P(Bp.data_ptr()), P(c_ptr), sC[0], sC[1],
-         M, N, K, init, init_value, P(bias_ptr) if bias_ptr else None, bias_stride,
-         max_ctas, variant, stream)
-    return ["pack_operand", "pack_operand", f"gemm_tc_{precision}"]
+    names.append("pack_operand")
+    if c16 is not None:
+        call("b200_gemm_tc_shadow", kind, P(Ap.data_ptr()), P(Bp.data_ptr()), P(c_ptr), sC[0],
+             sC[1], M, N, K, init, init_value, P(bias_ptr) if bias_ptr else None, bias_stride,
+             P(c16.data_ptr()), N, stream)
+    else:
+        call("b200_gemm_tc", kind, P(Ap.data_ptr()), P(Bp.data_ptr()), P(c_ptr), sC[0], sC[1],
+             M, N, K, init, init_value, P(bias_ptr) if bias_ptr else None, bias_stride,
+             max_ctas, variant, stream)
+    return names + [f"gemm_tc_{precision}"]
 
 
 class Recording:
@@ -314,6 +329,13 @@ class DeviceBackend:
         self.stage = staging or Staging()
         self._keep = None
         self.recording = None    # Recording while recording
+        # bf16 shadow of the last tensor-core contraction's C: ((C address, M,
+        # N), tensor); valid only for the immediately following contraction
+        # (fusion.plan_shadows proves nothing writes C in between).  Two
+        # workspace slots alternate so a consumer can also be a producer.
+        self._shadow = None
+        self._shadow_slot = 0
+        self.last_shadow = (False, False)   # (A from a shadow, C shadow written)
 
     def call(self, name, *args):
         check(getattr(self.stage.lib, name)(*args), name)
@@ -340,8 +362,13 @@ class DeviceBackend:
         self.stage.flush()
 
     def contract(self, g, precision="exact", init=0, init_value=0.0, bias=None, bias_base=0,
-                 bias_stride=0):
-        """Run a templates.ContractMatch (+ fused init / bias); returns kernel names."""
+                 bias_stride=0, shadow_out=False, shadow_in=False):
+        """Run a templates.ContractMatch (+ fused init / bias); returns kernel names.
+
+        shadow_out / shadow_in (fusion.plan_shadows): on the bf16 tensor-core
+        path, also write C as a bf16 K-major operand / take A from the
+        previous contraction's shadow instead of packing it.
+        """
         s = self.stage
         tA, tB, tC = s.tensor(g.A), s.tensor(g.B), s.tensor(g.C)
         esz = 4 if g.dtype == "f32" else 8
@@ -353,11 +380,25 @@ class DeviceBackend:
             if cv is not None and conv_tc_supported(cv):
                 return self.conv_tc(cv, init, init_value)
         if g.strided and g.dtype == "f32":
-            return launch_gemm(s.lib, precision, tA.data_ptr() + 4 * g.offA, g.sA,
-                               tB.data_ptr() + 4 * g.offB, g.sB, tC.data_ptr() + 4 * g.offC,
-                               g.sC, g.M, g.N, g.K, s.stream_ptr, init=init,
-                               init_value=init_value, bias_ptr=bias_ptr,
-                               bias_stride=bias_stride, call=self.call)
+            a_packed = c16 = None
+            if precision == "bf16" and tc_supported(precision, g.K):
+                sh = self._shadow
+                if shadow_in and sh is not None and sh[0] == (tA.data_ptr(), g.M, g.K):
+                    a_packed = sh[1]
+                if shadow_out and tc_supported(precision, g.N):
+                    c16 = workspace(4 + (self._shadow_slot ^ 1), "bfloat16", g.M, g.N)
+            names = launch_gemm(s.lib, precision, tA.data_ptr() + 4 * g.offA, g.sA,
+                                tB.data_ptr() + 4 * g.offB, g.sB, tC.data_ptr() + 4 * g.offC,
+                                g.sC, g.M, g.N, g.K, s.stream_ptr, init=init,
+                                init_value=init_value, bias_ptr=bias_ptr,
+                                bias_stride=bias_stride, call=self.call, a_packed=a_packed,
+                                c16=c16)
+            self._shadow = None
+            if c16 is not None:
+                self._shadow_slot ^= 1
+                self._shadow = ((tC.data_ptr(), g.M, g.N), c16)
+            self.last_shadow = (a_packed is not None, c16 is not None)
+            return names
         torch = s.torch
         tabs = [torch.from_numpy(t).to("cuda") for t in g.tables]
         a_m, a_k, b_k, b_n, c_m, c_n = g.tables

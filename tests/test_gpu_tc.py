@@ -142,3 +142,32 @@ def test_gemm_tc2_split_tail(kind, shape, clusters):
     assert (err > bound).sum().item() == 0
     err2, _, *_ = _run(kind, M, N, K, variant=2, max_ctas=2 * clusters, seed=3)
     assert (err2 == err).all().item()
+
+
+@pytest.mark.parametrize("rows", [256, 300])
+def test_linear_stack_shadow_bit_identical(rows):
+    """Chained Linear lowerings at bf16: the second contraction's A operand
+    comes from the first one's epilogue (b200_gemm_tc_shadow) instead of a
+    separate pack of H.  Both round the same f32 H to bf16 (RN), so every
+    output must be bit-identical to the unshadowed run, H included; the
+    second contraction must launch without an A pack."""
+    import bench_kernels as bk
+    import paper_2307_16080_b200 as b2
+    from staircase.interp import machine
+
+    import harness
+
+    fn = bk.make_linear_stack(rows)
+    outs = {}
+    for shadow in (False, True):
+        args = harness.make_args(fn, seed=3)
+        b2.configure(precision="bf16", shadow=shadow)
+        try:
+            machine.run(fn.module, "linear_stack", args, engine=b2.engine)
+        finally:
+            b2.configure(precision="exact", shadow=True)
+        outs[shadow] = [a.data.tobytes() for a in args]
+        plan = list(b2.engine.last_plan)
+    assert outs[True] == outs[False]
+    assert [p[0] for p in plan] == ["gemm_tc_bf16", "gemm_tc_bf16"]
+    assert "C->shadow" in plan[0][-1] and "A<-shadow" in plan[1][-1]

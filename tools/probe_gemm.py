@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--mnk", type=int, nargs=3, default=[4096, 4096, 4096])
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--cublas", action="store_true", help="also time torch.mm (cuBLAS) bf16")
+    ap.add_argument("--bias", action="store_true", help="fused bias epilogue")
     a = ap.parse_args()
     import torch
 
@@ -31,6 +32,7 @@ def main():
     s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
     P = ctypes.c_void_p
     C = torch.zeros(M, N, device="cuda")
+    bias = torch.randn(N, device="cuda")
     if a.cublas:
         for dt in (torch.bfloat16,):
             X = torch.randn(M, K, device="cuda").to(dt)
@@ -57,8 +59,9 @@ def main():
             for init in a.init:
                 def go():
                     rc = lib.b200_gemm_tc(kind, P(A.data_ptr()), P(Bt.data_ptr()),
-                                          P(C.data_ptr()), N, 1, M, N, K, init, 0.0, None,
-                                          0, 0, variant, s)
+                                          P(C.data_ptr()), N, 1, M, N, K, init, 0.0,
+                                          P(bias.data_ptr()) if a.bias else None,
+                                          1 if a.bias else 0, 0, variant, s)
                     assert rc == 0
                 for _ in range(3):
                     go()
