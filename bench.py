@@ -436,10 +436,14 @@ def run_ours(args, rank, world, local):
             peak_source = (f"{src} HBM copy bandwidth (MEASURED_PEAKS.json); algorithmic bytes "
                            f"= NHWC bf16 input + 2 x f32 output")
     else:
+        # the bit-exact kernels issue a separate, individually rounded
+        # multiply and add per MAC (no FMA: the reference rounds each op), so
+        # their ceiling is one FP32 op per lane per cycle, half the FMA peak
         achieved = wl.flops / (dom_ms * 1e-3) / 1e12
-        peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-        unit, bound = "TFLOP/s", "fp32-simt"
-        peak_source = "derived: 148 SM x 128 FP32 lanes x 2 x sm_max_mhz"
+        peak = 148 * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        unit, bound = "TFLOP/s", "fp32-simt (no FMA)"
+        peak_source = ("derived: 148 SM x 128 FP32 lanes x sm_max_mhz x 1 flop (mul and add "
+                       "issued separately; the FMA peak is 2x)")
     if world == 1:
         cpu_rate, cpu_t = reference_rate(wl)
         cpu_sample = (f"{wl.slice[2]} via staircase _evalcy ({cpu_t:.2f} s); "

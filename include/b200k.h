@@ -186,6 +186,23 @@ int b200_conv2d_tc(const void *in_nhwc, const void *wt, float *out, const int64_
                    void *stream);
 
 /*
+ * Bit-exact direct convolution (conv_2d_nchw_fchw, valid, stride 1;
+ * reference tests/kernels.py:50-64) at the exact precision: out[n,f,h,w] =
+ * (init ? init_value : out[..]) + the ci -> ki -> kj chain of individually
+ * rounded products and sums (interp/_evalpy.py:115-127), f32 (dtype 0) or
+ * f64 (dtype 1).  in / w / out strides are HOST arrays of 4 element strides
+ * (NCHW, FCHW, NCHW).  w_work: DEVICE scratch of f*c*kh*kw elements (the
+ * weights transposed to [C][KH*KW][F]).  Same results as
+ * b200_contract_exact on the conv nest, with operands staged in shared
+ * memory instead of gathered through offset tables.
+ */
+int b200_conv2d_exact(int32_t dtype, const void *in, const int64_t *in_strides, const void *w,
+                      const int64_t *w_strides, void *w_work, void *out,
+                      const int64_t *out_strides, int64_t nb, int64_t c, int64_t hp, int64_t wp,
+                      int64_t f, int64_t ho, int64_t wo, int64_t kh, int64_t kw, int32_t init,
+                      double init_value, void *stream);
+
+/*
  * Runtime specialisation (NVRTC, sm_100a): compile generated CUDA C `src`
  * and return the kernel `kernel` as an opaque handle in *fn.  The engine
  * generates straight-line kernels for region shapes whose generic execution

@@ -63,6 +63,8 @@ SIGNATURES = {
     "b200_pack_conv_weight": [_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _P],
     "b200_conv2d_tc": [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64,
                        _I32, _F32, _P],
+    "b200_conv2d_exact": [_I32, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64,
+                          _I64, _I64, _I64, _I32, ctypes.c_double, _P],
     "b200_jit_compile": [ctypes.c_char_p, ctypes.c_char_p, _P],
     "b200_jit_launch": [_P, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
                         ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
@@ -252,6 +254,20 @@ def conv_tc_supported(cv):
     return smem <= 232448 and ph <= 256 and prow <= 256
 
 
+def conv_exact_supported(cv, esz):
+    """The bit-exact direct conv kernel (csrc/conv_exact.cu): reduction in the
+    nest order ci -> ki -> kj (its rounding order) and the double-buffered
+    staging (8 channels of a 4 x (32 + kw - 1) patch + 8 x kh x kw x 64
+    weights) within shared memory."""
+    order = [r for r in ("ci", "ki", "kj") if r in cv.k_order]
+    if list(cv.k_order) != order:
+        return False
+    pw = 32 + cv.kw - 1
+    pitch = pw + (8 - pw) % 32
+    smem = 2 * 8 * ((4 + cv.kh - 1) * pitch + cv.kh * cv.kw * 64) * esz
+    return smem <= 227 * 1024
+
+
 def _direct_call(lib):
     def call(name, *args):
         check(getattr(lib, name)(*args), name)
@@ -373,12 +389,15 @@ class DeviceBackend:
         tA, tB, tC = s.tensor(g.A), s.tensor(g.B), s.tensor(g.C)
         esz = 4 if g.dtype == "f32" else 8
         bias_ptr = s.tensor(bias).data_ptr() + esz * bias_base if bias is not None else None
-        if precision == "bf16" and bias is None:
+        if bias is None:
             from .templates import conv_view
 
-            cv = conv_view(None, g)
-            if cv is not None and conv_tc_supported(cv):
-                return self.conv_tc(cv, init, init_value)
+            cv = conv_view(None, g, dtypes=("f32", "f64"))
+            if cv is not None:
+                if precision == "bf16" and g.dtype == "f32" and conv_tc_supported(cv):
+                    return self.conv_tc(cv, init, init_value)
+                if conv_exact_supported(cv, esz):
+                    return self.conv_exact(cv, g.dtype, init, init_value)
         if g.strided and g.dtype == "f32":
             a_packed = c16 = None
             if precision == "bf16" and tc_supported(precision, g.K):
@@ -413,6 +432,23 @@ class DeviceBackend:
                   P(tabs[5].data_ptr()), g.M, g.N, g.K, a_k_fast, b_n_fast, init, init_value,
                   P(bias_ptr) if bias_ptr else None, bias_stride, s.stream_ptr)
         return ["contract_exact"]
+
+    def conv_exact(self, cv, dtype, init=0, init_value=0.0):
+        """conv_2d_nchw_fchw, bit-exact, operands staged in shared memory."""
+        s = self.stage
+        inp, ker, out = s.tensor(cv.inp), s.tensor(cv.ker), s.tensor(cv.out)
+        wt = workspace(5, _TORCH_DT[dtype], cv.c * cv.kh * cv.kw, cv.f)
+        P = ctypes.c_void_p
+        I4 = ctypes.c_int64 * 4
+        sin, sw, sout = I4(*cv.inp.strides), I4(*cv.ker.strides), I4(*cv.out.strides)
+        if self.recording is not None:
+            self.recording.keep.append((sin, sw, sout))
+        self.keep(sin, sw, sout)
+        self.call("b200_conv2d_exact", DT_CODE[dtype], P(inp.data_ptr()), sin,
+                  P(ker.data_ptr()), sw, P(wt.data_ptr()), P(out.data_ptr()), sout, cv.nb, cv.c,
+                  cv.hp, cv.wp, cv.f, cv.ho, cv.wo, cv.kh, cv.kw, init, float(init_value),
+                  s.stream_ptr)
+        return ["conv2d_exact"]
 
     def conv_tc(self, cv, init=0, init_value=0.0):
         """conv_2d_nchw_fchw on the tensor cores (bf16 operands, fp32 accumulate)."""

@@ -221,18 +221,20 @@ def match_contraction(region, links, remainder, accesses):
 class ConvView:
     """A contraction that is exactly conv_2d_nchw_fchw (valid, stride 1)."""
 
-    __slots__ = ("nb", "c", "hp", "wp", "f", "ho", "wo", "kh", "kw", "inp", "ker", "out")
+    __slots__ = ("nb", "c", "hp", "wp", "f", "ho", "wo", "kh", "kw", "inp", "ker", "out",
+                 "k_order")   # k_order: the reduction variables' roles in nest order
 
     def __repr__(self):
         return (f"ConvView(nb={self.nb}, c={self.c}, {self.hp}x{self.wp} -> f={self.f}, "
                 f"{self.ho}x{self.wo}, {self.kh}x{self.kw})")
 
 
-def conv_view(region, g):
+def conv_view(region, g, dtypes=("f32",)):
     """Recognise out[n,f,h,w] += in[n,c,h+i,w+j] * w[f,c,i,j] (reference
     tests/kernels.py:50-64) from a ContractMatch's index maps: every variable
-    must start at 0 with step 1 and carry exactly the conv's coefficients."""
-    if g is None or g.dtype != "f32":
+    must start at 0 with step 1 and carry exactly the conv's coefficients.
+    ``k_order`` lists the reduction roles in nest (= rounding) order."""
+    if g is None or g.dtype not in dtypes:
         return None
     A, B, C = g.A, g.B, g.C
     if len(A.shape) != 4 or len(B.shape) != 4 or len(C.shape) != 4:
@@ -291,6 +293,8 @@ def conv_view(region, g):
     if cv.hp < cv.ho + cv.kh - 1 or cv.wp < cv.wo + cv.kw - 1:
         return None
     cv.inp, cv.ker, cv.out = A, B, C
+    by_id = {v.id: name for name, v in roles.items()}
+    cv.k_order = tuple(by_id[v.id] for v in g.k_vars)
     return cv
 
 

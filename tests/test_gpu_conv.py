@@ -62,7 +62,7 @@ def test_unsupported_filter_count_takes_the_exact_path():
         machine.run(fn.module, "conv_t", a1, engine=b2.engine)
     finally:
         b2.configure(precision="exact")
-    assert b2.engine.last_plan[-1][0] == "contract_exact"
+    assert b2.engine.last_plan[-1][0] == "conv2d_exact"
     oracle.build()
     machine.run(fn.module, "conv_t", a2, engine=oracle)
     assert a1[2].data.tobytes() == a2[2].data.tobytes()
