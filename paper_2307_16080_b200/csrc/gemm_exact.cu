@@ -72,8 +72,17 @@ struct Args {
   Addr ad;
 };
 
+// f32 8x8 micro-tiles are held to 128 registers so two CTAs share an SM:
+// with one CTA (8 warps) the FP pipe starved on shared-memory latency (ncu:
+// 12.5 % occupancy, 52 % issue-slot use).
+template <typename T, int TM, int TN>
+struct MinBlocks {
+  static constexpr int value = (sizeof(T) == 4 && TM * TN >= 64) ? 2 : 1;
+};
+
 template <typename T, typename Addr, int BM, int BN, int TM, int TN>
-__global__ void __launch_bounds__(kThreads) contract_exact_kernel(Args<T, Addr> g) {
+__global__ void __launch_bounds__(kThreads, MinBlocks<T, TM, TN>::value)
+    contract_exact_kernel(Args<T, Addr> g) {
   constexpr int PAD = 16 / sizeof(T);
   constexpr int LA = BM * BK / kThreads;  // A elements staged per thread
   constexpr int LB = BN * BK / kThreads;
