@@ -517,12 +517,31 @@ class DeviceBackend:
         P = ctypes.c_void_p
         # the uploads must outlive the (asynchronous) kernel
         self.keep(table, words, iregs, ivals, dtally, err)
-        self.call("b200_vm_run",
-                  P(words.data_ptr()), len(prog.words), P(iregs.data_ptr()),
-                  P(ivals.data_ptr()), len(prog.init_regs), prog.n_regs,
-                  P(table.data_ptr()), len(r.buffers), nd, breg, blb, bst, btr,
-                  1 if prog.count else 0, P(dtally.data_ptr()), P(err.data_ptr()),
-                  s.stream_ptr)
+        from . import native
+
+        if native.available():
+            # the same program specialised to native code (native.py): same
+            # semantics, tally and faults, no per-instruction dispatch
+            env_regs = [v for v in r.env if r.kind[v] != "buf"]
+            src, name, _ = native.vm_source(prog, r.buffers, env_regs)
+            from . import jit
+
+            fn = jit.compile_kernel(src, name)
+            ptrs = s.upload_i64([s.tensor(b).data_ptr() for b in r.buffers])
+            ln = native.NativeLaunch(fn, native.grid_of(prog), ptrs.data_ptr(), ivals.data_ptr(),
+                                     dtally.data_ptr(), err.data_ptr())
+            self.keep(ptrs, ln)
+            if self.recording is not None:
+                self.recording.keep.append((ptrs, ln, ivals, dtally, err))
+            self.call("b200_jit_launch", P(ln.fn), ln.grid, 1, 1, native.THREADS, 1, 1, 0,
+                      ln.argv, s.stream_ptr)
+        else:
+            self.call("b200_vm_run",
+                      P(words.data_ptr()), len(prog.words), P(iregs.data_ptr()),
+                      P(ivals.data_ptr()), len(prog.init_regs), prog.n_regs,
+                      P(table.data_ptr()), len(r.buffers), nd, breg, blb, bst, btr,
+                      1 if prog.count else 0, P(dtally.data_ptr()), P(err.data_ptr()),
+                      s.stream_ptr)
         fault = None
         if checked:
             e = B200VmError.from_buffer_copy(bytes(err.cpu().numpy()))

@@ -1,0 +1,38 @@
+"""Native VM programs (native.py) against the device interpreter (csrc/vm.cu).
+
+Every corpus case is run twice on the B200 through staircase's run() with
+the B200 engine: once with VM regions specialised to native code, once on
+the interpreter.  Buffers, the full tally and error type / message must be
+identical (both must also equal the reference goldens, checked separately
+by tests/test_gpu_parity.py).
+"""
+import pytest
+
+import harness
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(fn, pipe, mode, seed, native_on):
+    import paper_2307_16080_b200 as b2
+    from paper_2307_16080_b200 import native
+
+    saved = native.ENABLED
+    native.ENABLED = native_on
+    try:
+        try:
+            results, args, tally, _ = harness.run_engine(b2.engine, fn, pipe, mode, seed)
+            bufs = [a.data.tobytes() if hasattr(a, "data") else a for a in args]
+            return (bufs, repr(results), tally, None)
+        except Exception as exc:   # faults must match too
+            return (None, None, None, (type(exc).__name__, str(exc)))
+    finally:
+        native.ENABLED = saved
+
+
+@pytest.mark.parametrize("case", harness.CASES, ids=[f"{c[0].__name__}-{c[1]}-{c[3]}"
+                                                     for c in harness.CASES])
+def test_native_equals_interpreter(case):
+    fn, _, pipe, mode = case
+    for seed in (0, 1):
+        assert _run(fn, pipe, mode, seed, True) == _run(fn, pipe, mode, seed, False)
