@@ -395,7 +395,10 @@ def run_ours(args, rank, world, local):
 
     # e2e through the plugin: host Buffers, H2D + D2H inside the timed region
     host = host_inputs(fn, seed_base=100 * rank)
-    machine.run(fn.module, name, host, engine=b2.engine)   # warm
+    # warm: plans / JIT kernels, and the host buffers get page-locked on
+    # their second staging (runtime.pin_host: reused buffers are pinned)
+    for _ in range(2):
+        machine.run(fn.module, name, host, engine=b2.engine)
     torch.cuda.synchronize()
     barrier(world)
     e2e_steps = max(1, min(args.steps, 3))

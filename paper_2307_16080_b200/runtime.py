@@ -110,6 +110,7 @@ DT_CODE = {"f32": 0, "f64": 1, "i32": 2, "i64": 3}
 
 
 _PINNED = {}              # id(array) -> (address, nbytes) of page-locked Buffer storage
+_STAGED_ONCE = {}         # id(array) -> address: staged before, not (yet) pinned
 PIN_MIN_BYTES = 1 << 20
 
 
@@ -128,13 +129,21 @@ def pin_host(arr, host):
     staging source and destination of every run; registering it with the
     driver (cudaHostRegister) turns each copy into a direct DMA instead of a
     bounce through a pageable staging buffer.  The registration lives as long
-    as the array (weakref finalizer).  B200_PIN=0 disables it.
+    as the array (weakref finalizer).  Registration costs milliseconds, so
+    an array is pinned the second time it is staged (it is being reused
+    across runs); one-shot buffers — e.g. a tuner trial's fresh inputs —
+    are copied unpinned.  B200_PIN=0 disables it.
     """
     nbytes = host.numel() * host.element_size()
     if nbytes < PIN_MIN_BYTES or os.environ.get("B200_PIN", "1") == "0":
         return
     key, addr = id(arr), host.data_ptr()
     if _PINNED.get(key) == (addr, nbytes):
+        return
+    if _STAGED_ONCE.get(key) != addr:
+        if key not in _STAGED_ONCE:
+            weakref.finalize(arr, _STAGED_ONCE.pop, key, None)
+        _STAGED_ONCE[key] = addr
         return
     if key in _PINNED:   # storage moved (resized array): drop the stale range
         _unpin(key, _PINNED[key][0])
