@@ -356,7 +356,24 @@ def run_tape(program, code, regs, tally, ctx, backend=None):
         raise
     run.be.flush()
     last_plan = run.plan
+    global last_staging
+    # the run's device copies (== the host Buffers after the flush): kept
+    # until the next run so a caller can post-process on the device (the
+    # sweep's equivalence guard, sweep.py)
+    last_staging = getattr(run.be, "stage", None)
     return rets
+
+
+last_staging = None
+
+
+def device_copy(buf):
+    """The last run's device tensor of ``buf`` (same contents), or None."""
+    st = last_staging
+    if st is None or not hasattr(st, "dev"):
+        return None
+    ent = st.dev.get(id(buf))
+    return ent[1] if ent is not None and ent[0] is buf else None
 
 
 class Session:

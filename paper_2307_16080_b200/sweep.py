@@ -45,23 +45,66 @@ def _dist():
     return None
 
 
+_WANT_DEV = {}   # id(want Buffer) -> (Buffer, float64 device tensor): baseline copies
+
+
+def _close_tensors(g, w):
+    """math.isclose(g, w, rel_tol=1e-6, abs_tol=1e-9) elementwise, all():
+    equal values (infinities included) are close; otherwise both must be
+    finite and |g - w| <= max(1e-6 * max(|g|, |w|), 1e-9); NaN is never
+    close (math.isclose semantics)."""
+    xp_abs = abs
+    diff = xp_abs(g - w)
+    tol = (1e-6 * _maximum(xp_abs(g), xp_abs(w))).clip(min=1e-9)
+    return (g == w) | (_isfinite(g) & _isfinite(w) & (diff <= tol))
+
+
+def _maximum(a, b):
+    import torch
+
+    return torch.maximum(a, b) if isinstance(a, torch.Tensor) else np.maximum(a, b)
+
+
+def _isfinite(a):
+    import torch
+
+    return torch.isfinite(a) if isinstance(a, torch.Tensor) else np.isfinite(a)
+
+
 def _fast_buffers_close(got, want):
     """Vectorised twin of the reference guard's element test
     (math.isclose(g, w, rel_tol=1e-6, abs_tol=1e-9) over every element,
-    tuner/search.py:128-138): same predicate, numpy instead of a Python loop."""
+    tuner/search.py:128-138): the same predicate, evaluated on the GPU on
+    the trial run's own device copy of ``got`` (engine.device_copy) against
+    a cached device copy of the baseline, else with numpy."""
     from staircase.interp import Buffer
 
     if not isinstance(got, Buffer) or got.shape != want.shape:
         return False
+    from . import engine
+
+    tg = engine.device_copy(got)
+    if tg is not None:
+        import torch
+
+        ent = _WANT_DEV.get(id(want))
+        if ent is None or ent[0] is not want:
+            dt = getattr(torch, {"f32": "float32", "f64": "float64", "i32": "int32",
+                                 "i64": "int64"}[want.dtype])
+            tw = torch.frombuffer(want.data, dtype=dt).to("cuda")
+            ent = (want, tw.double() if want.dtype in ("f32", "f64") else tw)
+            _WANT_DEV[id(want)] = ent
+        tw = ent[1]
+        if want.dtype not in ("f32", "f64"):
+            return bool(torch.equal(tg, tw))
+        return bool(_close_tensors(tg.double(), tw).all().item())
     if want.dtype not in ("f32", "f64"):
         return list(got.data) == list(want.data)
     dt = np.float32 if want.dtype == "f32" else np.float64
     g = np.frombuffer(got.data, dtype=dt).astype(np.float64)
     w = np.frombuffer(want.data, dtype=dt).astype(np.float64)
     with np.errstate(invalid="ignore", over="ignore"):
-        diff = np.abs(g - w)
-        tol = np.maximum(1e-6 * np.maximum(np.abs(g), np.abs(w)), 1e-9)
-        close = (g == w) | (diff <= tol)
+        close = _close_tensors(g, w)
     return bool(np.all(close))
 
 
@@ -123,6 +166,7 @@ def search(kernel, pipeline_template=None, space=None, budget: int = 20, seed: i
     import time
 
     t_start = time.perf_counter()
+    _WANT_DEV.clear()   # baseline device copies belong to one search
     ensure_staircase()
     from staircase.errors import EmptySpace
     from staircase.interp import machine

@@ -110,3 +110,27 @@ def test_world2_gloo_log_equals_reference():
             assert log == log_r
             idx, cost = open(os.path.join(d, f"best{rank}.txt")).read().split()
             assert int(idx) == best_r.idx and float(cost) == best_r.cost
+
+
+def test_guard_predicate_is_math_isclose():
+    """The vectorised guard (numpy and torch forms) agrees with the reference's
+    math.isclose(g, w, rel_tol=1e-6, abs_tol=1e-9) on edge values."""
+    import math
+
+    import numpy as np
+    import torch
+
+    from paper_2307_16080_b200.sweep import _close_tensors
+
+    inf, nan = float("inf"), float("nan")
+    vals = [0.0, -0.0, 1e-10, -1e-10, 5e-10, 1.0, 1.0 + 1e-7, 1.0 + 3e-6, -1.0, 3.4e38,
+            1e-300, inf, -inf, nan]
+    g = [a for a in vals for _ in vals]
+    w = [b for _ in vals for b in vals]
+    want = [math.isclose(a, b, rel_tol=1e-6, abs_tol=1e-9) for a, b in zip(g, w)]
+    with np.errstate(invalid="ignore", over="ignore"):
+        got_np = _close_tensors(np.array(g), np.array(w)).tolist()
+    got_t = _close_tensors(torch.tensor(g, dtype=torch.float64),
+                           torch.tensor(w, dtype=torch.float64)).tolist()
+    assert got_np == want
+    assert got_t == want
