@@ -36,11 +36,21 @@ class ContractMatch:
     """A recognised contraction: operands, groups and addressing."""
 
     __slots__ = ("A", "B", "C", "dtype", "M", "N", "K", "m_vars", "n_vars", "k_vars",
-                 "tables", "strided", "offA", "offB", "offC", "sA", "sB", "sC", "offsets")
+                 "_tables", "_make_tables", "origins", "strided", "offA", "offB", "offC",
+                 "sA", "sB", "sC", "offsets")
 
     def __repr__(self):
         return (f"ContractMatch({self.dtype}, M={self.M}, N={self.N}, K={self.K}, "
                 f"strided={self.strided})")
+
+    @property
+    def tables(self):
+        """(a_m, a_k, b_k, b_n, c_m, c_n) int64 element-offset tables, built on
+        first use: only the table-addressed kernel needs them, and for large
+        conv / tiled nests they cost milliseconds of host time per plan."""
+        if self._tables is None:
+            self._tables = self._make_tables()
+        return self._tables
 
 
 def _straight_line(nodes):
@@ -194,13 +204,23 @@ def match_contraction(region, links, remainder, accesses):
 
     used = {v.id for v in vars_ if stat(v)[2] > 1}
     cA, cB, cC = const(aA.offset, used), const(aB.offset, used), const(aS.offset, used)
-    a_m = _table(region, g.m_vars, aA.offset, stat) + cA
-    a_k = _table(region, g.k_vars, aA.offset, stat)
-    b_k = _table(region, g.k_vars, aB.offset, stat) + cB
-    b_n = _table(region, g.n_vars, aB.offset, stat)
-    c_m = _table(region, g.m_vars, aS.offset, stat) + cC
-    c_n = _table(region, g.n_vars, aS.offset, stat)
-    g.tables = (a_m, a_k, b_k, b_n, c_m, c_n)
+
+    def make_tables():
+        return (_table(region, g.m_vars, aA.offset, stat) + cA,
+                _table(region, g.k_vars, aA.offset, stat),
+                _table(region, g.k_vars, aB.offset, stat) + cB,
+                _table(region, g.n_vars, aB.offset, stat),
+                _table(region, g.m_vars, aS.offset, stat) + cC,
+                _table(region, g.n_vars, aS.offset, stat))
+
+    g._tables, g._make_tables = None, make_tables
+
+    def first(off, vs):   # the tables' first entries: every variable at its lb
+        return sum(off.t.get(v.id, 0) * stat(v)[0] for v in vs)
+
+    g.origins = (cA + first(aA.offset, g.m_vars) + first(aA.offset, g.k_vars),
+                 cB + first(aB.offset, g.k_vars) + first(aB.offset, g.n_vars),
+                 cC + first(aS.offset, g.m_vars) + first(aS.offset, g.n_vars))
     # outputs must be distinct (writes of different (m, n) never collide)
     terms = [(abs(aS.offset.t.get(v.id, 0) * stat(v)[1]), stat(v)[2])
              for v in g.m_vars + g.n_vars]
@@ -213,7 +233,7 @@ def match_contraction(region, links, remainder, accesses):
         g.sA = (stride(aA.offset, g.m_vars), stride(aA.offset, g.k_vars))
         g.sB = (stride(aB.offset, g.k_vars), stride(aB.offset, g.n_vars))
         g.sC = (stride(aS.offset, g.m_vars), stride(aS.offset, g.n_vars))
-        g.offA, g.offB, g.offC = int(a_m[0] + a_k[0]), int(b_k[0] + b_n[0]), int(c_m[0] + c_n[0])
+        g.offA, g.offB, g.offC = (int(o) for o in g.origins)
     return g
 
 
@@ -241,8 +261,7 @@ def conv_view(region, g, dtypes=("f32",)):
         return None
     sa, sb, sc = A.strides, B.strides, C.strides
     # the operands' base offsets must be 0 (all loops start at 0)
-    a_m, a_k, b_k, b_n, c_m, c_n = g.tables
-    if a_m[0] + a_k[0] != 0 or b_k[0] + b_n[0] != 0 or c_m[0] + c_n[0] != 0:
+    if tuple(g.origins) != (0, 0, 0):
         return None
     trip = {}
     for v in g.m_vars + g.n_vars + g.k_vars:
