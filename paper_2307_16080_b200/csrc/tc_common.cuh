@@ -239,7 +239,25 @@ __device__ __forceinline__ void epilogue_row32(const Epi &ep, int64_t m, int64_t
   float *crow = ep.C + m * ep.sCm;
   const bool vec = ep.sCn == 1 && nb + 32 <= N &&
                    ((reinterpret_cast<uintptr_t>(crow + nb) & 15) == 0);
-  float v[32];
+  if (ep.c16) {
+    // with the bf16 shadow: final values gathered, then both outputs written
+    // (kept apart from the plain path below, whose code it would bloat)
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int64_t n = nb + j;
+      float o = 0.f;
+      if (n < N) {
+        o = ep.init ? ep.init_value : crow[n * ep.sCn];
+        o += __uint_as_float(r[j]);
+        if (ep.bias) o += ep.bias[n * ep.bias_stride];
+        crow[n * ep.sCn] = o;
+      }
+      v[j] = o;
+    }
+    shadow_store32(ep, m, nb, M, N, v);
+    return;
+  }
   if (vec) {
     float4 *p = reinterpret_cast<float4 *>(crow + nb);
 #pragma unroll
@@ -258,24 +276,18 @@ __device__ __forceinline__ void epilogue_row32(const Epi &ep, int64_t m, int64_t
         o.w += b[3 * ep.bias_stride];
       }
       p[j] = o;
-      v[4 * j] = o.x, v[4 * j + 1] = o.y, v[4 * j + 2] = o.z, v[4 * j + 3] = o.w;
     }
   } else {
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {   // fully unrolled: v stays in registers
+    for (int j = 0; j < 32; ++j) {
       const int64_t n = nb + j;
-      v[j] = 0.f;
-      if (n < N) {
-        float *dst = crow + n * ep.sCn;
-        float o = ep.init ? ep.init_value : *dst;
-        o += __uint_as_float(r[j]);
-        if (ep.bias) o += ep.bias[n * ep.bias_stride];
-        *dst = o;
-        v[j] = o;
-      }
+      if (n >= N) break;
+      float *dst = crow + n * ep.sCn;
+      float o = ep.init ? ep.init_value : *dst;
+      o += __uint_as_float(r[j]);
+      if (ep.bias) o += ep.bias[n * ep.bias_stride];
+      *dst = o;
     }
   }
-  if (ep.c16) shadow_store32(ep, m, nb, M, N, v);
 }
 
 typedef CUresult (*EncodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
