@@ -37,18 +37,6 @@ def nvrtc_compile(src):
     return rc, log.value.decode()
 
 
-class _Capture(SimEngine):
-    """Run the engine on the simulator and collect every MapMatch planned."""
-
-    def __init__(self):
-        super().__init__()
-        self.maps = []
-
-    def run_tape(self, program, code, regs, tally, ctx):
-        out = super().run_tape(program, code, regs, tally, ctx)
-        return out
-
-
 @pytest.mark.skipif(NVRTC is None, reason="libnvrtc not present")
 @pytest.mark.parametrize("fn", [corpus.linear32, corpus.saxpy_f32, corpus.ewise_ops,
                                 corpus.ewise_gpu])
