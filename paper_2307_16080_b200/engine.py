@@ -226,6 +226,8 @@ class _Run:
         except Unsupported as exc:
             self.flush_pending()
             raise E.ModeUnsupported(f"b200 engine: {exc}") from None
+        if _region_hook is not None:   # races.check_races: static race proof
+            _region_hook(r, accesses)
         links, remainder = analysis.chain_of(r)
         safe = analysis.statically_in_bounds(r, accesses) and not analysis.invalid_steps(r)
         band = analysis.choose_band(r, links, accesses) if safe else []
@@ -365,6 +367,7 @@ def run_tape(program, code, regs, tally, ctx, backend=None):
 
 
 last_staging = None
+_region_hook = None   # callable(region, accesses) or None (races.check_races)
 
 
 def device_copy(buf):
