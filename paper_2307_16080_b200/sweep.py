@@ -18,7 +18,9 @@ regenerates the full sequence and the merged log equals the sequential log
 (``objective="model"``: costs come from the exact tally).  ``grid`` (an
 extension: trial 0 identity, then the Cartesian product in order) shards the
 same way.  ``one_plus_one_es`` depends on earlier costs (search.py:226-234,
-272-275) and runs as identical replicas on every rank.
+272-275) and runs as identical replicas on every rank; ``population_es``
+(an extension) evaluates λ mutations of the parent per
+generation, sharded over the ranks, and equals (1+1)-ES at λ = 1.
 
 Trials run on the B200 engine (``install()`` is applied for the duration),
 which is what the reference ``run()`` inside ``_Session`` dispatches to.
@@ -155,11 +157,13 @@ def _params(space, budget, seed, strategy):
 
 def search(kernel, pipeline_template=None, space=None, budget: int = 20, seed: int = 0,
            strategy: str = "random", *, func=None, objective="model", mode="sequential",
-           workers=1, engine=None, rank=None, world=None, timing=None):
+           workers=1, engine=None, rank=None, world=None, timing=None, lam=8):
     """``tuner.search`` with trials sharded over torch.distributed ranks.
 
     Returns ``(best, log)`` exactly like the reference; ``log`` is sorted by
-    trial index and identical on every rank.  ``timing`` (a dict), if given,
+    trial index and identical on every rank.  ``strategy="population_es"``
+    (alias ``"1+lambda-es"``) is the (1+λ)-ES extension, ``lam`` children per
+    generation (see ``_pop_es``).  ``timing`` (a dict), if given,
     receives this rank's ``setup_s`` (inputs + baseline run), ``trials_s``
     (its share of the trials), ``gather_s`` and ``trials`` (count).
     """
@@ -176,9 +180,12 @@ def search(kernel, pipeline_template=None, space=None, budget: int = 20, seed: i
         raise EmptySpace("search needs a ParamSpace")
     if not isinstance(budget, int) or isinstance(budget, bool) or budget < 1:
         raise ValueError(f"budget must be a positive integer, got {budget!r}")
-    strategy = {"es": "one_plus_one_es", "1+1-es": "one_plus_one_es"}.get(strategy, strategy)
-    if strategy not in ("random", "one_plus_one_es", "grid"):
+    strategy = {"es": "one_plus_one_es", "1+1-es": "one_plus_one_es",
+                "1+lambda-es": "population_es", "pop-es": "population_es"}.get(strategy, strategy)
+    if strategy not in ("random", "one_plus_one_es", "grid", "population_es"):
         raise ValueError(f"unknown strategy {strategy!r}")
+    if not isinstance(lam, int) or isinstance(lam, bool) or lam < 1:
+        raise ValueError(f"lam must be a positive integer, got {lam!r}")
     if strategy == "grid":
         budget = min(budget, 1 + math.prod(len(d) for d in space.tile_sizes) *
                      len(space.unroll_factors))
@@ -205,6 +212,14 @@ def search(kernel, pipeline_template=None, space=None, budget: int = 20, seed: i
             # runs the same replica (no exchange needed)
             best, log = _es(session, space, budget, seed)
             return best, log
+        if strategy == "population_es":
+            t_trials = time.perf_counter()
+            best, log = _pop_es(session, space, budget, seed, lam, rank, world, dist)
+            if timing is not None:
+                timing.update(setup_s=t_trials - t_start,
+                              trials_s=time.perf_counter() - t_trials, gather_s=0.0,
+                              trials=sum(1 for t in log if t.idx % world == rank))
+            return best, log
         identity = space.identity()
         params = _params(space, budget, seed, strategy)
         mine = []
@@ -217,17 +232,12 @@ def search(kernel, pipeline_template=None, space=None, budget: int = 20, seed: i
             else:
                 tiles, unroll = params[idx]
                 t = session.trial(idx, tiles, unroll)
-            mine.append((t.idx, t.params, t.cost, t.status, t.seed, t.stats))
+            mine.append(_record(t))
         t_gather = time.perf_counter()
-        if dist is not None and world > 1:
-            gathered = [None] * world
-            dist.all_gather_object(gathered, mine)
-        else:
-            gathered = [mine]
+        records = sorted(_gather(dist, world, mine), key=lambda r: r[0])
         if timing is not None:
             timing.update(setup_s=t_trials - t_start, trials_s=t_gather - t_trials,
                           gather_s=time.perf_counter() - t_gather, trials=len(mine))
-        records = sorted((r for part in gathered for r in part), key=lambda r: r[0])
         log = [Trial(i, p, c, s, sd, stats=st) for i, p, c, s, sd, st in records]
         evaluated = [t for t in log if t.status == "evaluated"]
         best = min(evaluated, key=lambda t: (t.cost, t.idx))
@@ -235,6 +245,58 @@ def search(kernel, pipeline_template=None, space=None, budget: int = 20, seed: i
     finally:
         machine._engine = saved_engine
         ref._state_matches = saved_match
+
+
+def _gather(dist, world, mine):
+    if dist is not None and world > 1:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, mine)
+        return [r for part in gathered for r in part]
+    return list(mine)
+
+
+def _pop_es(session, space, budget, seed, lam, rank, world, dist):
+    """(1+λ)-ES (an extension of search.py:226-234,261-279).
+
+    Each generation draws λ children of the current parent with the
+    reference's ``_mutate`` from one ``random.Random(seed)`` stream, trial
+    indices ``1 + g·λ + j``; children are evaluated on ranks ``idx % world``
+    and exchanged with one all_gather per generation; the parent moves to
+    the best evaluated child (lowest (cost, idx)) on strict improvement.
+    Every rank holds the same parent, so the log does not depend on the
+    world size, and λ = 1 is exactly the reference's (1+1)-ES.
+    """
+    from staircase.tuner.search import _mutate
+    from staircase.tuner.space import Trial
+
+    identity = space.identity()
+    records = _gather(dist, world, [_record(session.trial(0, identity["tiles"],
+                                                          identity["unroll"]))]
+                      if rank == 0 else [])
+    log = [Trial(i, p, c, s, sd, stats=st) for i, p, c, s, sd, st in records]
+    rng = random.Random(seed)
+    parent, parent_cost = dict(log[0].params), log[0].cost
+    idx = 1
+    while idx < budget:
+        kids = [(idx + j, _mutate(space, parent, rng)) for j in range(min(lam, budget - idx))]
+        mine = [_record(session.trial(i, tiles, unroll))
+                for i, (tiles, unroll) in kids if i % world == rank]
+        gen = sorted(_gather(dist, world, mine), key=lambda r: r[0])
+        gen = [Trial(i, p, c, s, sd, stats=st) for i, p, c, s, sd, st in gen]
+        log.extend(gen)
+        evaluated = [t for t in gen if t.status == "evaluated"]
+        if evaluated:
+            top = min(evaluated, key=lambda t: (t.cost, t.idx))
+            if top.cost < parent_cost:
+                parent, parent_cost = dict(top.params), top.cost
+        idx += len(kids)
+    evaluated = [t for t in log if t.status == "evaluated"]
+    best = min(evaluated, key=lambda t: (t.cost, t.idx))
+    return best, log
+
+
+def _record(t):
+    return (t.idx, t.params, t.cost, t.status, t.seed, t.stats)
 
 
 def _es(session, space, budget, seed):

@@ -25,3 +25,14 @@ def test_sweep_on_b200_equals_reference(fn, strategy):
                              rank=0, world=1)
     assert log == log_r
     assert best == best_r
+
+
+def test_population_es_on_b200_equals_its_definition():
+    from paper_2307_16080_b200 import sweep
+    from test_sweep import _pop_es_spec
+
+    oracle.build()
+    best, log = sweep.search(corpus.conv_small.module, None, _space(), budget=17, seed=6,
+                             strategy="population_es", lam=8, rank=0, world=1)
+    assert log == _pop_es_spec(corpus.conv_small.module, 17, 6, 8)
+    assert best.cost <= log[0].cost

@@ -62,7 +62,7 @@ def test_grid_strategy_enumerates_the_space_in_order():
     assert best.cost <= log[0].cost
 
 
-def _worker(rank, world, port, out_dir, budget, seed):
+def _worker(rank, world, port, out_dir, budget, seed, strategy="random", lam=8):
     import sys
 
     here = os.path.dirname(os.path.abspath(__file__))
@@ -80,7 +80,7 @@ def _worker(rank, world, port, out_dir, budget, seed):
                             world_size=world)
     try:
         best, log = sweep.search(c.conv_small.module, None, ParamSpace(**SPACE_ARGS),
-                                 budget=budget, seed=seed, strategy="random", engine=o)
+                                 budget=budget, seed=seed, strategy=strategy, engine=o, lam=lam)
         persist(log, os.path.join(out_dir, f"log{rank}.jsonl"))
         with open(os.path.join(out_dir, f"best{rank}.txt"), "w") as fh:
             fh.write(f"{best.idx} {best.cost}")
@@ -134,3 +134,84 @@ def test_guard_predicate_is_math_isclose():
                            torch.tensor(w, dtype=torch.float64)).tolist()
     assert got_np == want
     assert got_t == want
+
+
+def _pop_es_spec(kernel, budget, seed, lam):
+    """(1+λ)-ES written directly on the reference's _Session (sequential)."""
+    import random
+    import sys
+
+    from staircase.interp import machine
+
+    ref = sys.modules["staircase.tuner.search"]
+
+    saved = machine._engine
+    machine._engine = oracle
+    try:
+        session = ref._Session(kernel, func=None, seed=seed, objective="model",
+                               pipeline_template=None)
+        space = _space()
+        ident = space.identity()
+        log = [session.trial(0, ident["tiles"], ident["unroll"])]
+        rng = random.Random(seed)
+        parent, pcost = dict(log[0].params), log[0].cost
+        while len(log) < budget:
+            n = min(lam, budget - len(log))
+            pts = [ref._mutate(space, parent, rng) for _ in range(n)]
+            gen = [session.trial(len(log) + j, t, u) for j, (t, u) in enumerate(pts)]
+            log += gen
+            ok = [t for t in gen if t.status == "evaluated"]
+            if ok:
+                top = min(ok, key=lambda t: (t.cost, t.idx))
+                if top.cost < pcost:
+                    parent, pcost = dict(top.params), top.cost
+        return log
+    finally:
+        machine._engine = saved
+
+
+def test_population_es_lambda1_is_the_reference_one_plus_one_es():
+    from paper_2307_16080_b200 import sweep
+
+    oracle.build()
+    kernel = corpus.conv_small.module
+    best_r, log_r = _ref(kernel, 10, 5, "es")
+    best, log = sweep.search(kernel, None, _space(), budget=10, seed=5,
+                             strategy="population_es", lam=1, engine=oracle, rank=0, world=1)
+    assert log == log_r
+    assert best == best_r
+
+
+def test_population_es_follows_its_definition():
+    from paper_2307_16080_b200 import sweep
+
+    oracle.build()
+    kernel = corpus.conv_small.module
+    best, log = sweep.search(kernel, None, _space(), budget=11, seed=2,
+                             strategy="1+lambda-es", lam=4, engine=oracle, rank=0, world=1)
+    assert [t.idx for t in log] == list(range(11))
+    assert log == _pop_es_spec(kernel, 11, 2, 4)
+    assert best.cost <= log[0].cost
+    with pytest.raises(ValueError):
+        sweep.search(kernel, None, _space(), budget=3, strategy="population_es", lam=0,
+                     engine=oracle, rank=0, world=1)
+
+
+def test_population_es_world2_gloo_equals_world1():
+    import torch.multiprocessing as mp
+    from staircase.tuner.log import load
+
+    from paper_2307_16080_b200 import sweep
+
+    oracle.build()
+    budget, seed = 13, 4
+    best1, log1 = sweep.search(corpus.conv_small.module, None, _space(), budget=budget,
+                               seed=seed, strategy="population_es", lam=4, engine=oracle,
+                               rank=0, world=1)
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(2, _free_port(), d, budget, seed, "population_es", 4),
+                 nprocs=2, join=True)
+        for rank in range(2):
+            assert load(os.path.join(d, f"log{rank}.jsonl")) == log1
+            idx, cost = open(os.path.join(d, f"best{rank}.txt")).read().split()
+            assert int(idx) == best1.idx and float(cost) == best1.cost
