@@ -21,7 +21,10 @@
 // 128-row x 32-column chunks by TMA (128B swizzle, 4 buffers): the loads of
 // upcoming chunks — including the next tile's — are issued ahead, each thread
 // adds its TMEM row in place, and a TMA bulk store writes the chunk back.
-// (Strided C falls back to per-row 128-bit stores.)
+// The tile's bias is staged in shared memory once per tile (its loads are
+// issued before the accumulator wait); a bf16 shadow of C, when requested,
+// is staged per chunk in shared memory (64B swizzle) and TMA-stored with the
+// chunk.  (Strided C falls back to per-row 128-bit stores.)
 //
 // Replaces run_tape on a recognised matmul / Linear contraction nest
 // (reference tests/kernels.py:24-38) at bf16/tf32 precision.
@@ -37,13 +40,28 @@ namespace b200tc {
 
 namespace {
 
-constexpr int PSTAGES = 5;
 constexpr int PA = 128 * 128;   // A half: 128 rows x 128 B
 constexpr int PB = 128 * 128;   // B half: 128 rows x 128 B
 constexpr int CBUF = 128 * 128; // C chunk: 128 rows x 32 fp32
 constexpr int NCBUF = 4;
+constexpr int SBUF = 128 * 64;  // bf16 shadow chunk: 128 rows x 32 bf16
+constexpr int BIASB = 256 * 4;  // the tile's bias values
 constexpr int PTHREADS = 256;
-constexpr size_t PSMEM = 1024 + PSTAGES * (PA + PB) + NCBUF * CBUF + 256;
+// Shared memory layout: operand stages | C chunks | [shadow chunks] | bias |
+// barriers.  The shadow variant trades one operand stage for two staged
+// shadow chunks (the shadow's TMA stores are coalesced; per-thread row
+// stores of 64 B were not).
+template <bool SH>
+struct Lay {
+  static constexpr int STAGES = SH ? 4 : 5;
+  static constexpr int NSBUF = SH ? 2 : 0;
+  static constexpr size_t C_OFF = (size_t)STAGES * (PA + PB);
+  static constexpr size_t S_OFF = C_OFF + NCBUF * CBUF;
+  static constexpr size_t BIAS_OFF = S_OFF + NSBUF * SBUF;
+  static constexpr size_t BAR_OFF = BIAS_OFF + BIASB;
+  static constexpr size_t SMEM = 1024 + BAR_OFF + 256;
+};
+static_assert(Lay<false>::SMEM <= 232448 && Lay<true>::SMEM <= 232448, "smem");
 
 struct Sched {
   int64_t tiles, nt, kb_total, ncl;
@@ -82,21 +100,27 @@ __device__ __forceinline__ bool get_item(const Sched &s, int64_t cid, int64_t i,
   return true;
 }
 
-template <int KIND>
+template <int KIND, bool SH>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tma_a,
                     const __grid_constant__ CUtensorMap tma_b,
                     const __grid_constant__ CUtensorMap tma_bs,
-                    const __grid_constant__ CUtensorMap tma_c, int use_tma_c, Epi ep, int64_t M,
+                    const __grid_constant__ CUtensorMap tma_c,
+                    const __grid_constant__ CUtensorMap tma_s, int use_tma_c, Epi ep, int64_t M,
                     int64_t N, Sched sch) {
+  using L = Lay<SH>;
+  constexpr int PSTAGES = L::STAGES;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   unsigned char *gbase = smem_raw + (base - smem_u32(smem_raw));
   const uint32_t sA = base;
   const uint32_t sB = base + PSTAGES * PA;
-  const uint32_t sC = base + PSTAGES * (PA + PB);
-  unsigned char *gC = gbase + PSTAGES * (PA + PB);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + PSTAGES * (PA + PB) + NCBUF * CBUF);
+  const uint32_t sC = base + (uint32_t)L::C_OFF;
+  unsigned char *gC = gbase + L::C_OFF;
+  const uint32_t sS = base + (uint32_t)L::S_OFF;
+  unsigned char *gS = gbase + L::S_OFF;
+  float *sBias = reinterpret_cast<float *>(gbase + L::BIAS_OFF);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + L::BAR_OFF);
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * PSTAGES + 4 + NCBUF);
   const uint32_t bar0 = smem_u32(bars);
   auto full = [&](int s) { return bar0 + 8u * s; };
@@ -219,8 +243,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
     Item it;
     for (int64_t i = 0; get_item(sch, cid, i, it); ++i) {
       const int64_t m_base = it.m0 + rank * 128;
+      // the tile's bias: loads issued before the accumulator wait (their
+      // latency hides behind it), staged in shared memory once per tile
+      float b0 = 0.f, b1 = 0.f;
+      if (ep.bias) {
+        const int64_t n0 = it.n0 + et, n1 = n0 + 128;
+        if (n0 < N && et < it.ncols) b0 = __ldg(ep.bias + n0 * ep.bias_stride);
+        if (n1 < N && et + 128 < it.ncols) b1 = __ldg(ep.bias + n1 * ep.bias_stride);
+      }
       mbar_wait_cluster(tfull(acc), aph);
       tc_fence_after();
+      if (ep.bias) {
+        // every reader of the previous tile's values passed that tile's
+        // last chunk barrier
+        sBias[et] = b0;
+        sBias[et + 128] = b1;
+        named_bar_sync(1, 128);
+      }
       const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 256);
       const int nchunks = it.ncols / 32;
 #pragma unroll 1
@@ -233,15 +272,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
           if (load_c) {
             mbar_wait(cbar(b), (uint32_t)((g / NCBUF) & 1));
           } else {
-            // no C load: make sure the store of chunk g-4 has left this buffer
-            if (lead_t) bulk_wait_read<NCBUF - 1>();
+            // no C load: make sure the store of chunk g-4 (shadow: g-2) has
+            // left this buffer
+            if (lead_t) bulk_wait_read<SH ? 1 : NCBUF - 1>();
             named_bar_sync(1, 128);
           }
-          epilogue_chunk_smem(gC + b * CBUF, et, nb, N, ep, r, m_base + et, M);
+          const int sb = (int)(g & 1);
+          epilogue_chunk_smem(gC + b * CBUF, et, nb, N, ep, r, m_base + et, M,
+                              ep.bias ? sBias + c * 32 : nullptr,
+                              SH ? gS + sb * SBUF : nullptr);
           fence_proxy_async();
           named_bar_sync(1, 128);
           if (lead_t) {
             tma_store_2d(&tma_c, sC + b * CBUF, (int32_t)nb, (int32_t)m_base);
+            if (SH) tma_store_2d(&tma_s, sS + sb * SBUF, (int32_t)nb, (int32_t)m_base);
             bulk_commit();
             if (load_c) {
               bulk_wait_read<1>();  // store of chunk g-1 has read buffer (g+3) % 4
@@ -270,6 +314,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
 
 }  // namespace
 
+template <int KIND, bool SH>
+int launch(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mbs,
+           const CUtensorMap &mc, const CUtensorMap &ms, int use_tma_c, const Epi &ep, int64_t M,
+           int64_t N, const Sched &sch, int clusters, cudaStream_t s) {
+  constexpr size_t smem = Lay<SH>::SMEM;
+  cudaFuncSetAttribute(gemm_tc2_kernel<KIND, SH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  gemm_tc2_kernel<KIND, SH><<<2 * clusters, PTHREADS, smem, s>>>(ma, mb, mbs, mc, ms, use_tma_c,
+                                                                 ep, M, N, sch);
+  return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
+}
+
 int launch_gemm_tc2(int kind, const void *A, const void *Bt, const Epi &ep, int64_t M, int64_t N,
                     int64_t K, int max_clusters, cudaStream_t s) {
   Sched sch;
@@ -297,18 +353,16 @@ int launch_gemm_tc2(int kind, const void *A, const void *Bt, const Epi &ep, int6
                   (reinterpret_cast<uintptr_t>(ep.C) & 15) == 0 && ep.sCm >= N;
   if (use_tma_c && !make_map_c(&mc, ep.C, M, N, ep.sCm, 128)) use_tma_c = 0;
   if (!use_tma_c) mc = ma;  // unused placeholder
-  if (kind == 0) {
-    cudaFuncSetAttribute(gemm_tc2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)PSMEM);
-    gemm_tc2_kernel<0><<<2 * clusters, PTHREADS, PSMEM, s>>>(ma, mb, mbs, mc, use_tma_c, ep, M, N,
-                                                            sch);
-  } else {
-    cudaFuncSetAttribute(gemm_tc2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)PSMEM);
-    gemm_tc2_kernel<1><<<2 * clusters, PTHREADS, PSMEM, s>>>(ma, mb, mbs, mc, use_tma_c, ep, M, N,
-                                                            sch);
-  }
-  return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
+  // staged shadow: TMA-storable bf16 rows (16-byte aligned base and pitch)
+  CUtensorMap ms = ma;
+  const bool sh = use_tma_c && ep.c16 && (ep.ld16 * 2) % 16 == 0 && ep.ld16 >= N &&
+                  (reinterpret_cast<uintptr_t>(ep.c16) & 15) == 0 &&
+                  make_map_s16(&ms, ep.c16, M, N, ep.ld16, 128);
+  if (kind == 0)
+    return sh ? launch<0, true>(ma, mb, mbs, mc, ms, use_tma_c, ep, M, N, sch, clusters, s)
+              : launch<0, false>(ma, mb, mbs, mc, ms, use_tma_c, ep, M, N, sch, clusters, s);
+  return sh ? launch<1, true>(ma, mb, mbs, mc, ms, use_tma_c, ep, M, N, sch, clusters, s)
+            : launch<1, false>(ma, mb, mbs, mc, ms, use_tma_c, ep, M, N, sch, clusters, s);
 }
 
 }  // namespace b200tc

@@ -339,20 +339,47 @@ inline bool make_map_c(CUtensorMap *map, const float *C, int64_t rows, int64_t c
   return r == CUDA_SUCCESS;
 }
 
+// 2-D bf16 tensor map over the shadow (row-major, leading dimension ld16) with
+// boxes of 32 columns (64 B, 64B swizzle) x box_rows rows: the staged shadow
+// chunk of the epilogue, written back by one TMA store.
+inline bool make_map_s16(CUtensorMap *map, void *c16, int64_t rows, int64_t cols, int64_t ld16,
+                         uint32_t box_rows) {
+  EncodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld16 * 2)};
+  cuuint32_t box[2] = {32, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, c16, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // Epilogue over one 32-column chunk staged in shared memory by TMA with the
 // 128B swizzle: row r's 16-byte unit j lives at unit j ^ (r & 7).  The
 // thread owning row r adds its accumulator (and bias) in place.
 // m / M: the global row of r and the row count (for the bf16 shadow only).
+// sbias (optional): the chunk's 32 bias values already staged in shared
+// memory (zero past N).  s16 (optional): the chunk's bf16 shadow buffer in
+// shared memory (32 columns = 64 B per row, 64B swizzle: row r's 16-byte
+// unit q lives at unit q ^ ((r >> 1) & 3)), stored by TMA afterwards;
+// without it the shadow goes straight to global memory.
 __device__ __forceinline__ void epilogue_chunk_smem(unsigned char *chunk, int r, int64_t nb,
                                                     int64_t N, const Epi &ep,
                                                     const uint32_t (&acc)[32], int64_t m = 0,
-                                                    int64_t M = 0) {
+                                                    int64_t M = 0,
+                                                    const float *sbias = nullptr,
+                                                    unsigned char *s16 = nullptr) {
   float4 *row = reinterpret_cast<float4 *>(chunk + r * 128);
   // the chunk's 32 bias values, loaded up front (the same addresses for the
   // whole warp: one broadcast transaction each): 8 x 16-byte loads when the
   // bias is unit-stride and aligned, element loads otherwise
   float4 bv[8];
-  if (ep.bias) {
+  if (sbias) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) bv[j] = reinterpret_cast<const float4 *>(sbias)[j];
+  } else if (ep.bias) {
     const float *b = ep.bias + nb * ep.bias_stride;
     if (ep.bias_stride == 1 && nb + 32 <= N && (reinterpret_cast<uintptr_t>(b) & 15) == 0) {
 #pragma unroll
@@ -386,7 +413,18 @@ __device__ __forceinline__ void epilogue_chunk_smem(unsigned char *chunk, int r,
     *p = o;
     bv[j] = o;   // reused as the final values for the shadow
   }
-  if (ep.c16) {
+  if (s16) {
+    uint4 *srow = reinterpret_cast<uint4 *>(s16 + r * 64);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      __nv_bfloat162 b[4];
+      b[0] = __floats2bfloat162_rn(bv[2 * q].x, bv[2 * q].y);
+      b[1] = __floats2bfloat162_rn(bv[2 * q].z, bv[2 * q].w);
+      b[2] = __floats2bfloat162_rn(bv[2 * q + 1].x, bv[2 * q + 1].y);
+      b[3] = __floats2bfloat162_rn(bv[2 * q + 1].z, bv[2 * q + 1].w);
+      srow[q ^ ((r >> 1) & 3)] = *reinterpret_cast<uint4 *>(b);
+    }
+  } else if (ep.c16) {
     float v[32];
 #pragma unroll
     for (int j = 0; j < 8; ++j)

@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--cublas", action="store_true", help="also time torch.mm (cuBLAS) bf16")
     ap.add_argument("--bias", action="store_true", help="fused bias epilogue")
+    ap.add_argument("--shadow", action="store_true", help="also write the bf16 shadow of C")
     a = ap.parse_args()
     import torch
 
@@ -57,7 +58,16 @@ def main():
         Bt = torch.randn(N, K, device="cuda").to(elt)
         for variant in a.variant:
             for init in a.init:
+                S16 = torch.empty(M, N, device="cuda", dtype=torch.bfloat16) if a.shadow else None
+
                 def go():
+                    if a.shadow:
+                        rc = lib.b200_gemm_tc_shadow(
+                            kind, P(A.data_ptr()), P(Bt.data_ptr()), P(C.data_ptr()), N, 1, M, N,
+                            K, init, 0.0, P(bias.data_ptr()) if a.bias else None,
+                            1 if a.bias else 0, P(S16.data_ptr()), N, s)
+                        assert rc == 0
+                        return
                     rc = lib.b200_gemm_tc(kind, P(A.data_ptr()), P(Bt.data_ptr()),
                                           P(C.data_ptr()), N, 1, M, N, K, init, 0.0,
                                           P(bias.data_ptr()) if a.bias else None,
@@ -74,7 +84,8 @@ def main():
                 e1.record()
                 torch.cuda.synchronize()
                 ms = e0.elapsed_time(e1) / a.iters
-                print(f"kind={kind} variant={variant} init={init} M={M} N={N} K={K} "
+                print(f"kind={kind} variant={variant} init={init} bias={int(a.bias)} "
+                      f"shadow={int(a.shadow)} M={M} N={N} K={K} "
                       f"ms={ms:.4f} TFLOP/s={2*M*N*K/ms/1e9:.1f}", flush=True)
 
 
