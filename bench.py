@@ -409,12 +409,11 @@ def run_ours(args, rank, world, local):
     torch.cuda.synchronize()
     e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
     e2e_ms = max_over_ranks(e2e_ms, world)
-    h2d = sum(len(b.data) * b.data.itemsize for b in host)
-    d2h = sum(len(b.data) * b.data.itemsize for b in host[-1:])
-    if wl.name == "ls":
-        d2h = sum(len(b.data) * b.data.itemsize for b in (host[3], host[6]))
-    elif wl.name == "linear32":
-        d2h = sum(len(b.data) * b.data.itemsize for b in (host[3], host[4]))
+    # the bytes the last run actually moved (runtime.Staging counters): every
+    # input read by the device once, every written buffer back once; buffers
+    # a fused fill overwrites entirely are not uploaded
+    st = b2.engine.last_staging
+    h2d, d2h = st.h2d_bytes, st.d2h_bytes
 
     if rank != 0:
         return

@@ -54,6 +54,9 @@ FUSE = os.environ.get("B200_FUSE", "1") != "0"
 # bf16 shadows of contraction outputs read as the next contraction's A
 # (fusion.plan_shadows; B200_SHADOW=0 disables, for A/B tests).
 SHADOW = os.environ.get("B200_SHADOW", "1") != "0"
+# Row-panel pipelining of the host copies of large contractions / convs
+# (runtime.Staging.stream_rows; B200_STREAM_IO=0 disables, for A/B tests).
+STREAM_IO = os.environ.get("B200_STREAM_IO", "1") != "0"
 
 # kernel choice of the last run (tests and bench inspect these)
 last_plan = []
@@ -110,7 +113,7 @@ class _Run:
     def __init__(self, program, ctx, backend=None):
         self.program = program
         self.ctx = ctx
-        self.be = backend if backend is not None else DeviceBackend()
+        self.be = backend if backend is not None else DeviceBackend(stream_io=STREAM_IO)
         self.plan = []
         self.pending = []     # queued MapItem / ContractItem, program order
 
@@ -249,7 +252,7 @@ class _Run:
                 return
 
         # generic tier: the device tape VM (runs in order after queued plans)
-        self.flush_pending()
+        self.flush_pending({id(r.buffers[slot]) for slot in written})
         count = st is None
         try:
             prog = vmcode.encode(r, links, remainder, band, count, checked=not safe)
@@ -268,20 +271,34 @@ class _Run:
         self.plan.append(("vm", len(band), "checked" if not safe else "unchecked",
                           "count" if count else "static"))
 
-    def flush_pending(self):
+    def flush_pending(self, trigger_writes=()):
+        """Execute the queued plans.  ``trigger_writes``: ids of the buffers
+        the region that forced the flush will write (already marked dirty)."""
         if not self.pending:
             return
         items = fusion.fuse(self.pending) if FUSE else self.pending
         if SHADOW:
             fusion.plan_shadows(items)
         self.pending = []
-        for it in items:
+        # last_writer[i]: no later queued plan (nor the triggering region)
+        # writes item i's output, so a write-back streamed by item i is final
+        later = set(trigger_writes)
+        last_writer = [False] * len(items)
+        for i in range(len(items) - 1, -1, -1):
+            it = items[i]
+            if isinstance(it, fusion.ContractItem):
+                last_writer[i] = id(it.g.C) not in later
+                later.add(id(it.g.C))
+            else:
+                later.update(id(b) for b in it.m.buffers)
+        for it, last in zip(items, last_writer):
             if isinstance(it, fusion.ContractItem):
                 kernels = self.be.contract(it.g, PRECISION, init=it.init,
                                            init_value=it.init_value, bias=it.bias,
                                            bias_base=it.bias_base,
                                            bias_stride=it.bias_stride,
-                                           shadow_out=it.shadow_out, shadow_in=it.shadow_in)
+                                           shadow_out=it.shadow_out, shadow_in=it.shadow_in,
+                                           last_writer=last)
                 g = it.g
                 fused = list(it.fused)
                 if it.shadow_in or it.shadow_out:

@@ -14,6 +14,7 @@ re-planning; bench.py uses this for device-resident timing.
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import weakref
 
@@ -171,19 +172,35 @@ class Staging:
         self.dev = {}        # id(Buffer) -> (Buffer, tensor)
         self.dirty = set()
         self.stream = self.torch.cuda.current_stream()
+        self.h2d_bytes = 0   # host <-> device traffic of this staging (bench e2e)
+        self.d2h_bytes = 0
+        self.panels = 0      # row panels run with pipelined copies (stream_rows)
+        self._wb_event = None   # last streamed write-back (see stream_rows)
 
     @property
     def stream_ptr(self):
         return ctypes.c_void_p(self.torch.cuda.current_stream().cuda_stream)
 
-    def tensor(self, buf):
+    def host(self, buf):
+        return self.torch.frombuffer(buf.data, dtype=getattr(self.torch, _TORCH_DT[buf.dtype]))
+
+    def staged(self, buf):
+        ent = self.dev.get(id(buf))
+        return ent is not None and ent[0] is buf
+
+    def tensor(self, buf, overwrite=False):
+        """The device copy of ``buf`` (uploaded on first use).  ``overwrite``:
+        the caller's kernel writes every element before reading any, so a
+        first use allocates without copying the host contents."""
         ent = self.dev.get(id(buf))
         if ent is None or ent[0] is not buf:
-            torch = self.torch
-            dt = getattr(torch, _TORCH_DT[buf.dtype])
-            host = torch.frombuffer(buf.data, dtype=dt)
-            pin_host(buf.data, host)
-            t = host.to("cuda", non_blocking=False)
+            host = self.host(buf)
+            if overwrite:
+                t = self.torch.empty_like(host, device="cuda")
+            else:
+                pin_host(buf.data, host)
+                t = host.to("cuda", non_blocking=False)
+                self.h2d_bytes += host.numel() * host.element_size()
             ent = (buf, t)
             self.dev[id(buf)] = ent
         return ent[1]
@@ -197,11 +214,66 @@ class Staging:
             if key not in self.dev:
                 continue   # marked but never staged: the device never touched it
             buf, t = self.dev[key]
-            dt = getattr(torch, _TORCH_DT[buf.dtype])
-            host = torch.frombuffer(buf.data, dtype=dt)
+            host = self.host(buf)
             host.copy_(t)
+            self.d2h_bytes += host.numel() * host.element_size()
         self.dirty.clear()
         torch.cuda.current_stream().synchronize()
+        if self._wb_event is not None:
+            self._wb_event.synchronize()
+            self._wb_event = None
+
+    def stream_rows(self, panels, ins, out, launch, written_back=True):
+        """Run ``launch(r0, r1)`` over row panels with the host copies overlapped.
+
+        The row-major buffers in ``ins`` (uploaded, panel by panel, on a copy
+        stream) and ``out`` (``(buf, upload)``: the output, uploaded first
+        unless the kernel overwrites it, and written back panel by panel on a
+        second copy stream) are split along their leading dimension; panel
+        p's kernels wait only for panel p's uploads, and panel p's write-back
+        overlaps the uploads and kernels of the panels after it (PCIe is full
+        duplex: both directions run at once).  Every buffer ends staged
+        (registered in ``dev``); the current stream then waits for the
+        write-backs, so later kernels cannot overwrite rows still being
+        copied out.  ``panels``: [(r0, r1)] covering the leading dimension.
+        """
+        torch = self.torch
+        cur = torch.cuda.current_stream()
+        up, down = _copy_streams(torch)
+        up.wait_stream(cur)     # device storage may be recycled from earlier kernels
+        obuf, oup = out
+        rows = obuf.shape[0]
+        views = []
+        for buf in ins + [obuf]:
+            host = self.host(buf)
+            pin_host(buf.data, host)
+            t = torch.empty_like(host, device="cuda")
+            self.dev[id(buf)] = (buf, t)
+            views.append((host.view(buf.shape[0], -1), t.view(buf.shape[0], -1)))
+        hin, (ho, to) = views[:-1], views[-1]
+        esz = to.element_size()
+        for r0, r1 in panels:
+            with torch.cuda.stream(up):
+                for (h, t) in hin + ([(ho, to)] if oup else []):
+                    t[r0:r1].copy_(h[r0:r1], non_blocking=True)
+                    self.h2d_bytes += (r1 - r0) * t.shape[1] * esz
+            ev = torch.cuda.Event()
+            ev.record(up)
+            cur.wait_event(ev)
+            launch(r0, r1)
+            self.panels += 1
+            if written_back:
+                done = torch.cuda.Event()
+                done.record(cur)
+                down.wait_event(done)
+                with torch.cuda.stream(down):
+                    ho[r0:r1].copy_(to[r0:r1], non_blocking=True)
+                self.d2h_bytes += (r1 - r0) * to.shape[1] * esz
+        assert panels[-1][1] == rows
+        if written_back:
+            self._wb_event = torch.cuda.Event()
+            self._wb_event.record(down)
+            cur.wait_event(self._wb_event)
 
     def buffer_table(self, buffers):
         """A device array of b200_buffer for the given host Buffers."""
@@ -227,6 +299,17 @@ class Staging:
 
     def upload_i64(self, values):
         return self.upload_bytes(np.asarray(values, dtype=np.int64).tobytes())
+
+
+_COPY_STREAMS = {}
+
+
+def _copy_streams(torch):
+    """(upload, write-back) side streams of the current device."""
+    dev = torch.cuda.current_device()
+    if dev not in _COPY_STREAMS:
+        _COPY_STREAMS[dev] = (torch.cuda.Stream(), torch.cuda.Stream())
+    return _COPY_STREAMS[dev]
 
 
 PRECISIONS = ("exact", "tf32", "bf16")
@@ -288,7 +371,7 @@ def _direct_call(lib):
 
 def launch_gemm(lib, precision, a_ptr, sA, b_ptr, sB, c_ptr, sC, M, N, K, stream,
                 init=0, init_value=0.0, bias_ptr=None, bias_stride=0, max_ctas=0,
-                variant=0, call=None, a_packed=None, c16=None):
+                variant=0, call=None, a_packed=None, c16=None, b_packed=None):
     """Enqueue C (+)= A.B with the kernel chosen by ``precision``.
 
     Returns the list of kernel names launched (for the launch count).
@@ -296,6 +379,7 @@ def launch_gemm(lib, precision, a_ptr, sA, b_ptr, sB, c_ptr, sC, M, N, K, stream
     bf16/tf32 -> b200_pack_operand x2 + b200_gemm_tc (tcgen05).
     a_packed: A already packed (a bf16 shadow, M x K) — its pack is skipped;
     c16: also write C rounded to bf16 (M x N) with b200_gemm_tc_shadow.
+    b_packed: B already packed (N x K, see pack_b) — its pack is skipped.
     """
     call = call or _direct_call(lib)
     P = ctypes.c_void_p
@@ -313,9 +397,11 @@ def launch_gemm(lib, precision, a_ptr, sA, b_ptr, sB, c_ptr, sC, M, N, K, stream
         Ap = workspace(0, dt, M, K)
         call("b200_pack_operand", kind, P(a_ptr), sA[0], sA[1], P(Ap.data_ptr()), M, K, stream)
         names.append("pack_operand")
-    Bp = workspace(1, dt, N, K)
-    call("b200_pack_operand", kind, P(b_ptr), sB[1], sB[0], P(Bp.data_ptr()), N, K, stream)
-    names.append("pack_operand")
+    if b_packed is not None:
+        Bp = b_packed
+    else:
+        Bp = pack_b(lib, precision, b_ptr, sB, N, K, stream, call)
+        names.append("pack_operand")
     if c16 is not None:
         call("b200_gemm_tc_shadow", kind, P(Ap.data_ptr()), P(Bp.data_ptr()), P(c_ptr), sC[0],
              sC[1], M, N, K, init, init_value, P(bias_ptr) if bias_ptr else None, bias_stride,
@@ -325,6 +411,46 @@ def launch_gemm(lib, precision, a_ptr, sA, b_ptr, sB, c_ptr, sC, M, N, K, stream
              M, N, K, init, init_value, P(bias_ptr) if bias_ptr else None, bias_stride,
              max_ctas, variant, stream)
     return names + [f"gemm_tc_{precision}"]
+
+
+def pack_b(lib, precision, b_ptr, sB, N, K, stream, call=None):
+    """B (K x N, strides sB) packed K-major for b200_gemm_tc (workspace slot 1)."""
+    call = call or _direct_call(lib)
+    kind = 0 if precision == "bf16" else 1
+    Bp = workspace(1, "bfloat16" if kind == 0 else "float32", N, K)
+    call("b200_pack_operand", kind, ctypes.c_void_p(b_ptr), sB[1], sB[0],
+         ctypes.c_void_p(Bp.data_ptr()), N, K, stream)
+    return Bp
+
+
+# Host-copy pipelining (Staging.stream_rows): only when the streamed bytes
+# are worth several panels; each panel ~32 MB of traffic, 2..8 panels.
+STREAM_MIN_BYTES = 48 << 20
+STREAM_PANEL_BYTES = 32 << 20
+
+
+def _row_major(buf):
+    st, acc = [], 1
+    for d in reversed(buf.shape):
+        st.append(acc)
+        acc *= d
+    return tuple(buf.strides) == tuple(reversed(st))
+
+
+def _rows_of(buf, rows, cols):
+    """buf is exactly a dense row-major rows x cols block (leading dim = rows)."""
+    return (len(buf.shape) >= 1 and buf.shape[0] == rows and _row_major(buf) and
+            math.prod(buf.shape) == rows * cols)
+
+
+def row_panels(rows, row_bytes, align):
+    total = rows * row_bytes
+    if total < STREAM_MIN_BYTES or rows < 2 * align:
+        return None
+    p = max(2, min(8, total // STREAM_PANEL_BYTES))
+    step = -(-rows // p)
+    step = -(-step // align) * align
+    return [(r, min(rows, r + step)) for r in range(0, rows, step)]
 
 
 class Recording:
@@ -353,8 +479,11 @@ class Recording:
 class DeviceBackend:
     """Executes region plans on the B200 through libb200k.so."""
 
-    def __init__(self, staging=None):
+    def __init__(self, staging=None, stream_io=False):
         self.stage = staging or Staging()
+        # pipeline the host copies of large first-use plans (engine runs;
+        # a Session keeps its buffers resident and writes back on sync())
+        self.stream_io = stream_io
         self._keep = None
         self.recording = None    # Recording while recording
         # bf16 shadow of the last tensor-core contraction's C: ((C address, M,
@@ -389,27 +518,50 @@ class DeviceBackend:
     def flush(self):
         self.stage.flush()
 
+    def _streaming(self, out, *others):
+        """Host-copy pipelining applies: an engine run (not recording), the
+        output not yet on the device and not aliasing an operand."""
+        return (self.stream_io and self.recording is None and not self.stage.staged(out) and
+                all(o is not out for o in others))
+
     def contract(self, g, precision="exact", init=0, init_value=0.0, bias=None, bias_base=0,
-                 bias_stride=0, shadow_out=False, shadow_in=False):
+                 bias_stride=0, shadow_out=False, shadow_in=False, last_writer=False):
         """Run a templates.ContractMatch (+ fused init / bias); returns kernel names.
 
         shadow_out / shadow_in (fusion.plan_shadows): on the bf16 tensor-core
         path, also write C as a bf16 K-major operand / take A from the
-        previous contraction's shadow instead of packing it.
+        previous contraction's shadow instead of packing it.  last_writer
+        (engine.flush_pending): nothing queued after this plan writes C, so
+        a write-back streamed here is final and C needs no flush copy.
         """
         s = self.stage
-        tA, tB, tC = s.tensor(g.A), s.tensor(g.B), s.tensor(g.C)
         esz = 4 if g.dtype == "f32" else 8
-        bias_ptr = s.tensor(bias).data_ptr() + esz * bias_base if bias is not None else None
         if bias is None:
             from .templates import conv_view
 
             cv = conv_view(None, g, dtypes=("f32", "f64"))
             if cv is not None:
                 if precision == "bf16" and g.dtype == "f32" and conv_tc_supported(cv):
-                    return self.conv_tc(cv, init, init_value)
+                    return self.conv_tc(cv, init, init_value, last_writer)
                 if conv_exact_supported(cv, esz):
-                    return self.conv_exact(cv, g.dtype, init, init_value)
+                    return self.conv_exact(cv, g.dtype, init, init_value, last_writer)
+        bias_ptr = s.tensor(bias).data_ptr() + esz * bias_base if bias is not None else None
+        dense_c = (g.strided and g.offC == 0 and tuple(g.sC) == (g.N, 1) and
+                   _rows_of(g.C, g.M, g.N))
+        if (g.strided and g.dtype == "f32" and dense_c and
+                self._streaming(g.C, g.A, g.B, bias)):
+            stream_a = (not s.staged(g.A) and g.A is not g.B and g.offA == 0 and
+                        tuple(g.sA) == (g.K, 1) and _rows_of(g.A, g.M, g.K))
+            panels = row_panels(g.M, 4 * (g.N * (1 if init else 2) + (g.K if stream_a else 0)),
+                                256)
+            if panels is not None:
+                return self._gemm_streamed(g, precision, panels, stream_a, init, init_value,
+                                           bias_ptr, bias_stride, shadow_out, shadow_in,
+                                           last_writer)
+        tA, tB = s.tensor(g.A), s.tensor(g.B)
+        # a fused fill over all of a dense C: its old contents are never read
+        tC = s.tensor(g.C, overwrite=bool(init) and dense_c and g.C is not g.A and
+                      g.C is not g.B and g.C is not bias)
         if g.strided and g.dtype == "f32":
             a_packed = c16 = None
             if precision == "bf16" and tc_supported(precision, g.K):
@@ -430,6 +582,53 @@ class DeviceBackend:
                 self._shadow = ((tC.data_ptr(), g.M, g.N), c16)
             self.last_shadow = (a_packed is not None, c16 is not None)
             return names
+        return self._contract_tables(g, tA, tB, tC, init, init_value, bias_ptr, bias_stride)
+
+    def _gemm_streamed(self, g, precision, panels, stream_a, init, init_value, bias_ptr,
+                       bias_stride, shadow_out, shadow_in, last_writer):
+        """C (+)= A.B over row panels of M with the host copies pipelined
+        (Staging.stream_rows): panel p's GEMM overlaps the upload of panel
+        p+1 and the write-back of panel p-1.  B is uploaded (and, on the
+        tensor-core path, packed) once."""
+        s = self.stage
+        tB = s.tensor(g.B)
+        a_packed = c16 = Bp = None
+        tc = tc_supported(precision, g.K)
+        if not stream_a:
+            tA = s.tensor(g.A)
+            sh = self._shadow
+            if (tc and precision == "bf16" and shadow_in and sh is not None and
+                    sh[0] == (tA.data_ptr(), g.M, g.K)):
+                a_packed = sh[1]
+        if tc:
+            Bp = pack_b(s.lib, precision, tB.data_ptr() + 4 * g.offB, g.sB, g.N, g.K,
+                        s.stream_ptr, self.call)
+            if precision == "bf16" and shadow_out and tc_supported(precision, g.N):
+                c16 = workspace(4 + (self._shadow_slot ^ 1), "bfloat16", g.M, g.N)
+        names = []
+
+        def launch(r0, r1):
+            tA, tC = s.dev[id(g.A)][1], s.dev[id(g.C)][1]
+            names[:] = launch_gemm(
+                s.lib, precision, tA.data_ptr() + 4 * (g.offA + r0 * g.sA[0]), g.sA,
+                tB.data_ptr() + 4 * g.offB, g.sB, tC.data_ptr() + 4 * (r0 * g.N), g.sC,
+                r1 - r0, g.N, g.K, s.stream_ptr, init=init, init_value=init_value,
+                bias_ptr=bias_ptr, bias_stride=bias_stride, call=self.call,
+                c16=c16[r0:r1] if c16 is not None else None, b_packed=Bp,
+                a_packed=a_packed[r0:r1] if a_packed is not None else None)
+
+        s.stream_rows(panels, [g.A] if stream_a else [], (g.C, not init), launch)
+        if last_writer:
+            s.dirty.discard(id(g.C))
+        self._shadow = None
+        if c16 is not None:
+            self._shadow_slot ^= 1
+            self._shadow = ((s.dev[id(g.C)][1].data_ptr(), g.M, g.N), c16)
+        self.last_shadow = (a_packed is not None, c16 is not None)
+        return (["pack_operand"] if tc else []) + names
+
+    def _contract_tables(self, g, tA, tB, tC, init, init_value, bias_ptr, bias_stride):
+        s = self.stage
         torch = s.torch
         tabs = [torch.from_numpy(t).to("cuda") for t in g.tables]
         a_m, a_k, b_k, b_n, c_m, c_n = g.tables
@@ -445,10 +644,46 @@ class DeviceBackend:
                   P(bias_ptr) if bias_ptr else None, bias_stride, s.stream_ptr)
         return ["contract_exact"]
 
-    def conv_exact(self, cv, dtype, init=0, init_value=0.0):
+    def _conv_panels(self, cv, esz, init):
+        """Image panels for a streamed conv, or (None, False)."""
+        s = self.stage
+        if not (self._streaming(cv.out, cv.inp, cv.ker) and _row_major(cv.out) and
+                cv.out.shape[0] == cv.nb):
+            return None, False
+        stream_in = (not s.staged(cv.inp) and cv.inp is not cv.ker and _row_major(cv.inp) and
+                     cv.inp.shape[0] == cv.nb)
+        row = esz * (cv.out.strides[0] * (1 if init else 2) +
+                     (cv.inp.strides[0] if stream_in else 0))
+        return row_panels(cv.nb, row, 1), stream_in
+
+    def _conv_run(self, cv, esz, init, last_writer, launch):
+        """launch(inp_ptr, out_ptr, nb) over the whole batch, or over image
+        panels with the host copies pipelined (Staging.stream_rows)."""
+        s = self.stage
+        panels, stream_in = self._conv_panels(cv, esz, init)
+        if panels is None:
+            inp = s.tensor(cv.inp)
+            out = s.tensor(cv.out, overwrite=bool(init) and _row_major(cv.out) and
+                           cv.out is not cv.inp and cv.out is not cv.ker)
+            launch(inp.data_ptr(), out.data_ptr(), cv.nb)
+            return
+        if not stream_in:
+            s.tensor(cv.inp)
+
+        def panel(n0, n1):
+            inp, out = s.dev[id(cv.inp)][1], s.dev[id(cv.out)][1]
+            launch(inp.data_ptr() + esz * n0 * cv.inp.strides[0],
+                   out.data_ptr() + esz * n0 * cv.out.strides[0], n1 - n0)
+
+        s.stream_rows(panels, [cv.inp] if stream_in else [], (cv.out, not init), panel)
+        if last_writer:
+            s.dirty.discard(id(cv.out))
+
+    def conv_exact(self, cv, dtype, init=0, init_value=0.0, last_writer=False):
         """conv_2d_nchw_fchw, bit-exact, operands staged in shared memory."""
         s = self.stage
-        inp, ker, out = s.tensor(cv.inp), s.tensor(cv.ker), s.tensor(cv.out)
+        esz = 4 if dtype == "f32" else 8
+        ker = s.tensor(cv.ker)
         wt = workspace(5, _TORCH_DT[dtype], cv.c * cv.kh * cv.kw, cv.f)
         P = ctypes.c_void_p
         I4 = ctypes.c_int64 * 4
@@ -456,18 +691,20 @@ class DeviceBackend:
         if self.recording is not None:
             self.recording.keep.append((sin, sw, sout))
         self.keep(sin, sw, sout)
-        self.call("b200_conv2d_exact", DT_CODE[dtype], P(inp.data_ptr()), sin,
-                  P(ker.data_ptr()), sw, P(wt.data_ptr()), P(out.data_ptr()), sout, cv.nb, cv.c,
-                  cv.hp, cv.wp, cv.f, cv.ho, cv.wo, cv.kh, cv.kw, init, float(init_value),
-                  s.stream_ptr)
+
+        def launch(inp_ptr, out_ptr, nb):
+            self.call("b200_conv2d_exact", DT_CODE[dtype], P(inp_ptr), sin, P(ker.data_ptr()),
+                      sw, P(wt.data_ptr()), P(out_ptr), sout, nb, cv.c, cv.hp, cv.wp, cv.f,
+                      cv.ho, cv.wo, cv.kh, cv.kw, init, float(init_value), s.stream_ptr)
+
+        self._conv_run(cv, esz, init, last_writer, launch)
         return ["conv2d_exact"]
 
-    def conv_tc(self, cv, init=0, init_value=0.0):
+    def conv_tc(self, cv, init=0, init_value=0.0, last_writer=False):
         """conv_2d_nchw_fchw on the tensor cores (bf16 operands, fp32 accumulate)."""
         s = self.stage
         cp = -(-cv.c // 64) * 64
-        inp, ker, out = s.tensor(cv.inp), s.tensor(cv.ker), s.tensor(cv.out)
-        xin = workspace(2, "bfloat16", cv.nb * cv.hp * cv.wp, cp)
+        ker = s.tensor(cv.ker)
         xw = workspace(3, "bfloat16", cv.f, cv.kh * cv.kw * cp)
         P = ctypes.c_void_p
         I4 = ctypes.c_int64 * 4
@@ -475,14 +712,19 @@ class DeviceBackend:
         if self.recording is not None:
             self.recording.keep.append((sin, sw, sout))
         self.keep(sin, sw, sout)
-        self.call("b200_pack_conv_input", P(inp.data_ptr()), sin, P(xin.data_ptr()), cv.nb,
-                  cv.c, cv.hp, cv.wp, cp, s.stream_ptr)
         self.call("b200_pack_conv_weight", P(ker.data_ptr()), sw, P(xw.data_ptr()), cv.f, cv.c,
                   cv.kh, cv.kw, cp, s.stream_ptr)
-        self.call("b200_conv2d_tc", P(xin.data_ptr()), P(xw.data_ptr()), P(out.data_ptr()),
-                  sout, cv.nb, cp, cv.hp, cv.wp, cv.f, cv.ho, cv.wo, cv.kh, cv.kw, init,
-                  init_value, s.stream_ptr)
-        return ["pack_conv_input", "pack_conv_weight", "conv2d_tc_bf16"]
+
+        def launch(inp_ptr, out_ptr, nb):
+            xin = workspace(2, "bfloat16", nb * cv.hp * cv.wp, cp)
+            self.call("b200_pack_conv_input", P(inp_ptr), sin, P(xin.data_ptr()), nb, cv.c,
+                      cv.hp, cv.wp, cp, s.stream_ptr)
+            self.call("b200_conv2d_tc", P(xin.data_ptr()), P(xw.data_ptr()), P(out_ptr), sout,
+                      nb, cp, cv.hp, cv.wp, cv.f, cv.ho, cv.wo, cv.kh, cv.kw, init, init_value,
+                      s.stream_ptr)
+
+        self._conv_run(cv, 4, init, last_writer, launch)
+        return ["pack_conv_weight", "pack_conv_input", "conv2d_tc_bf16"]
 
     def map(self, m):
         """Run a templates.MapMatch: an NVRTC-specialised kernel when the JIT

@@ -1,0 +1,80 @@
+"""Pipelined host copies (runtime.Staging.stream_rows) leave results unchanged.
+
+Large first-use contractions and convs are split into row / image panels
+whose uploads, kernels and write-backs overlap (engine.STREAM_IO).  With the
+size thresholds lowered, test-size plans run as several panels; every buffer
+and the tally must equal the unstreamed run's bit for bit (and the C
+oracle's on the exact path), including a GEMM whose output a later,
+unfused region modifies (the streamed write-back must not be final there).
+"""
+import pytest
+
+import bench_kernels as bk
+import harness
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+GEMM_THEN_VM = '''
+@staged
+def gemm_then_vm(A: MemRef[(512, 64), F32], B: MemRef[(64, 96), F32],
+                 C: MemRef[(512, 96), F32]):
+    for i in range(512):
+        for k in range(64):
+            for j in range(96):
+                C[i, j] = C[i, j] + A[i, k] * B[k, j]
+    for i in range(96):
+        for j in range(i):
+            C[i, j] = C[j, i] + C[i, j]
+'''
+
+
+def _gemm_then_vm():
+    return bk._capture_from_source(GEMM_THEN_VM, "gemm_then_vm", {}, "stream")
+
+
+def _run(fn, precision, stream, monkeypatch):
+    import paper_2307_16080_b200 as b2
+    from paper_2307_16080_b200 import engine, runtime
+
+    monkeypatch.setattr(engine, "STREAM_IO", stream)
+    monkeypatch.setattr(runtime, "STREAM_MIN_BYTES", 1)
+    monkeypatch.setattr(runtime, "STREAM_PANEL_BYTES", 1 << 12)
+    b2.configure(precision=precision)
+    try:
+        _, bufs, tally, _ = harness.run_engine(b2.engine, fn, None, "sequential", 5)
+    finally:
+        b2.configure(precision="exact")
+    return bufs, tally, list(engine.last_plan), engine.last_staging.panels
+
+
+CASES = [("mm1024", "exact"), ("mm1024", "bf16"), ("ls512", "exact"), ("ls512", "bf16"),
+         ("conv4", "exact"), ("conv4", "bf16"), ("gemm_then_vm", "exact")]
+
+
+def _fn(name):
+    return {"mm1024": lambda: bk.mm_par1024, "ls512": lambda: bk.make_linear_stack(512),
+            "conv4": lambda: bk.make_conv(4), "gemm_then_vm": _gemm_then_vm}[name]()
+
+
+@pytest.mark.parametrize("name,precision", CASES)
+def test_streamed_equals_unstreamed(name, precision, monkeypatch):
+    fn = _fn(name)
+    want, t_want, plan_want, panels0 = _run(fn, precision, False, monkeypatch)
+    got, t_got, plan_got, panels = _run(fn, precision, True, monkeypatch)
+    assert panels0 == 0 and panels >= 2, (panels0, panels)
+    assert plan_got == plan_want
+    assert t_got == t_want
+    for g, w in zip(got, want):
+        assert g.data.tobytes() == w.data.tobytes()
+
+
+def test_streamed_write_back_before_a_later_writer_matches_the_oracle(monkeypatch):
+    fn = _gemm_then_vm()
+    got, t_got, plan, panels = _run(fn, "exact", True, monkeypatch)
+    assert panels >= 2 and plan[0][0] == "gemm_f32_exact" and plan[-1][0] == "vm", plan
+    oracle.build()
+    _, want, t_want, _ = harness.run_engine(oracle, fn, None, "sequential", 5)
+    assert t_got == t_want
+    for g, w in zip(got, want):
+        assert g.data.tobytes() == w.data.tobytes()

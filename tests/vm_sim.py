@@ -66,8 +66,9 @@ class SimBackend:
         self.dirty.clear()
 
     def contract(self, g, precision="exact", init=0, init_value=0.0, bias=None, bias_base=0,
-                 bias_stride=0, shadow_out=False, shadow_in=False):
-        # bf16 shadows only exist on the tensor-core path: nothing to model
+                 bias_stride=0, shadow_out=False, shadow_in=False, last_writer=False):
+        # bf16 shadows only exist on the tensor-core path, and host-copy
+        # pipelining is a staging detail: nothing to model
         assert precision == "exact", "the simulator models the exact path only"
         self.launches.append("contract")
         A, B, C = self.arr(g.A), self.arr(g.B), self.arr(g.C)
