@@ -76,7 +76,9 @@ class Workload:
                          f"-> 56x56, 3x3, f32")
             self.slice = (bk.conv_slice, 2.0 * 2 * 8 * 56 * 64 * 9,
                           "1x2x8x56 outputs of the conv nest (C=64, 3x3)")
-            self.default_precision = "exact"
+            # the tcgen05 implicit-GEMM conv, like mm / ls; --precision exact
+            # runs the bit-exact FP32 kernel
+            self.default_precision = "bf16"
             # algorithmic DRAM bytes of b200_conv2d_tc: the NHWC bf16 input
             # once, the f32 output read and written (out += conv)
             self.tc_bytes = nb * 58 * 58 * 64 * 2 + 2 * nb * 64 * 56 * 56 * 4

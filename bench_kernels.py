@@ -215,7 +215,7 @@ def _capture_from_source(src, name, ns, size):
     d = os.path.join(tempfile.gettempdir(), "b200_bench_kernels")
     os.makedirs(d, exist_ok=True)
     path = os.path.join(d, f"{name}_{size}.py")
-    header = ("from staircase import F32, MemRef, constant, parallel, staged\n")
+    header = ("from staircase import F32, F64, MemRef, constant, parallel, staged\n")
     with open(path, "w") as fh:
         fh.write(header + src)
     spec = importlib.util.spec_from_file_location(f"_b200_{name}_{size}", path)

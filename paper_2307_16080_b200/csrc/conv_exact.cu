@@ -29,6 +29,7 @@
 // generic table-addressed kernel.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/b200k.h"
 
@@ -184,6 +185,329 @@ __global__ void __launch_bounds__(kThreads) conv_exact_kernel(ConvArgs<T> g) {
   }
 }
 
+// Compile-time KH x KW (KW <= 5) variant, the one the 3x3 conv runs.  Same
+// CTA tile, chain order and staging scheme as conv_exact_kernel, but lane l
+// owns rows l / 8 and l / 8 + 4 and the 4 CONSECUTIVE columns 4 (l % 8) ..
+// +3: per (channel, filter row) a thread reads its 2 x (4 + KW - 1) inputs
+// once as 16-byte vectors (a quarter warp reads one 128-byte patch row:
+// conflict-free) and reuses them for all KW taps, so the shared-memory reads
+// per 128 FP32 ops drop from 10 to ~3.  Channel chunks are staged with
+// vector cp.async (input pairs, weight quads) when the layout allows, and
+// float outputs are read / written as 16-byte vectors.
+constexpr int RPITCH = TW + 8;   // patch row pitch: 4 (l % 8) + 8 <= pitch
+
+template <typename T, int KH, int KW>
+__global__ void __launch_bounds__(kThreads) conv_rows_kernel(ConvArgs<T> g, int vec_in,
+                                                             int vec_w, int vec_out) {
+  static_assert(KW <= 5, "input run of 4 + KW - 1 values must fit two 4-vectors");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int PH = TH + KH - 1, PW = TW + KW - 1, TAPS = KH * KW;
+  constexpr int IN_ELEMS = CC * PH * RPITCH;
+  constexpr int W_ELEMS = CC * TAPS * FT;
+  constexpr int RUN = 4 + KW - 1;
+  T *in_s = reinterpret_cast<T *>(smem_raw);          // [2][CC][PH][RPITCH]
+  T *w_s = in_s + 2 * IN_ELEMS;                       // [2][CC][TAPS][FT]
+
+  const int t = threadIdx.x, warp = t / 32, lane = t % 32;
+  const int r = lane / 8, cg = lane % 8;
+  int tile = blockIdx.x;
+  const int tw_i = tile % g.tw_tiles;
+  tile /= g.tw_tiles;
+  const int th_i = tile % g.th_tiles;
+  const int n = tile / g.th_tiles;
+  const int h0 = th_i * TH, w0 = tw_i * TW;
+  const int f0 = blockIdx.y * FT;
+  const int fw = f0 + warp * FX;
+
+  const T *in_n = g.in + (int64_t)n * g.si[0];
+  auto stage = [&](int c0, int b) {
+    T *is = in_s + b * IN_ELEMS;
+    if (vec_in) {   // pairs: unit column stride, even strides, aligned base
+      constexpr int PV = (PW + 1) / 2;
+      for (int e = t; e < CC * PH * PV; e += kThreads) {
+        const int cc = e / (PH * PV), rem = e - cc * (PH * PV);
+        const int y = rem / PV, x = 2 * (rem - y * PV);
+        const int ci = c0 + cc, hy = h0 + y, wx = w0 + x;
+        const int avail = (ci < g.c && hy < g.hp && wx < g.wp) ? min(2, g.wp - wx) : 0;
+        const T *src = avail ? in_n + ci * g.si[1] + hy * g.si[2] + wx : g.in;
+        const uint32_t d =
+            static_cast<uint32_t>(__cvta_generic_to_shared(is + (cc * PH + y) * RPITCH + x));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(d), "l"(src),
+                     "n"(2 * sizeof(T)), "r"(avail * (int)sizeof(T))
+                     : "memory");
+      }
+    } else {
+      for (int e = t; e < CC * PH * PW; e += kThreads) {
+        const int cc = e / (PH * PW), rem = e - cc * (PH * PW);
+        const int y = rem / PW, x = rem - y * PW;
+        const int ci = c0 + cc, hy = h0 + y, wx = w0 + x;
+        const bool ok = ci < g.c && hy < g.hp && wx < g.wp;
+        const T *src = ok ? in_n + ci * g.si[1] + hy * g.si[2] + wx * g.si[3] : g.in;
+        cp_async(is + (cc * PH + y) * RPITCH + x, src, ok);
+      }
+    }
+    T *ws = w_s + b * W_ELEMS;
+    if (vec_w) {    // 16-byte groups of filters (F a multiple of the group)
+      constexpr int WV = 16 / sizeof(T);
+      for (int e = t; e < W_ELEMS / WV; e += kThreads) {
+        const int fi = (e % (FT / WV)) * WV, ct = e / (FT / WV);
+        const int ff = f0 + fi;
+        const bool ok = c0 * TAPS + ct < g.c * TAPS && ff < g.f;
+        const T *src = ok ? g.w + ((int64_t)c0 * TAPS + ct) * g.f + ff : g.w;
+        const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(ws + ct * FT + fi));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src),
+                     "r"(ok ? 16 : 0)
+                     : "memory");
+      }
+    } else {
+      for (int e = t; e < W_ELEMS; e += kThreads) {
+        const int fi = e % FT, ct = e / FT;
+        const int ff = f0 + fi;
+        const bool ok = c0 * TAPS + ct < g.c * TAPS && ff < g.f;
+        const T *src = ok ? g.w + ((int64_t)c0 * TAPS + ct) * g.f + ff : g.w;
+        cp_async(ws + e, src, ok);
+      }
+    }
+    cp_commit();
+  };
+
+  // pixel i: row h0 + r + 4 (i / 4), column w0 + 4 cg + i % 4
+  T acc[PX][FX];
+  const int wo0 = w0 + 4 * cg;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int ho = h0 + r + 4 * q;
+#pragma unroll
+    for (int j = 0; j < FX; ++j) {
+      const int ff = fw + j;
+      T *o = g.out + (int64_t)n * g.so[0] + (int64_t)ff * g.so[1] + (int64_t)ho * g.so[2];
+      if (!g.init && vec_out && ho < g.ho && wo0 + 3 < g.wo && ff < g.f) {
+        const float4 v = *reinterpret_cast<const float4 *>(o + wo0);
+        acc[4 * q][j] = v.x, acc[4 * q + 1][j] = v.y, acc[4 * q + 2][j] = v.z,
+        acc[4 * q + 3][j] = v.w;
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int wo = wo0 + u;
+          acc[4 * q + u][j] = (!g.init && ho < g.ho && wo < g.wo && ff < g.f)
+                                  ? o[(int64_t)wo * g.so[3]] : g.init_value;
+        }
+      }
+    }
+  }
+
+  const int chunks = (g.c + CC - 1) / CC;
+  stage(0, 0);
+  for (int k = 0; k < chunks; ++k) {
+    const int b = k & 1;
+    if (k + 1 < chunks) {
+      stage((k + 1) * CC, b ^ 1);   // buffer b^1 was last read before the barrier below
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+    const T *is = in_s + b * IN_ELEMS + r * RPITCH + 4 * cg;
+    const T *ws = w_s + b * W_ELEMS + warp * FX;
+    const int cn = min(CC, g.c - k * CC);
+    for (int cc = 0; cc < cn; ++cc) {
+#pragma unroll
+      for (int ki = 0; ki < KH; ++ki) {
+        T x[2][8];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const T *row = is + (cc * PH + ki + 4 * q) * RPITCH;
+#pragma unroll
+          for (int u = 0; u < RUN; ++u) x[q][u] = row[u];
+        }
+        const T *wrow = ws + (cc * TAPS + ki * KW) * FT;
+#pragma unroll
+        for (int kj = 0; kj < KW; ++kj) {
+          T wv[FX];
+#pragma unroll
+          for (int j = 0; j < FX; ++j) wv[j] = wrow[kj * FT + j];
+#pragma unroll
+          for (int i = 0; i < PX; ++i)
+#pragma unroll
+            for (int j = 0; j < FX; ++j)
+              acc[i][j] = add_rn(acc[i][j], mul_rn(x[i / 4][i % 4 + kj], wv[j]));
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int ho = h0 + r + 4 * q;
+    if (ho >= g.ho) continue;
+#pragma unroll
+    for (int j = 0; j < FX; ++j) {
+      const int ff = fw + j;
+      if (ff >= g.f) continue;
+      T *o = g.out + (int64_t)n * g.so[0] + (int64_t)ff * g.so[1] + (int64_t)ho * g.so[2];
+      if (vec_out && wo0 + 3 < g.wo) {
+        *reinterpret_cast<float4 *>(o + wo0) =
+            make_float4(acc[4 * q][j], acc[4 * q + 1][j], acc[4 * q + 2][j], acc[4 * q + 3][j]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (wo0 + u < g.wo) o[(int64_t)(wo0 + u) * g.so[3]] = acc[4 * q + u][j];
+      }
+    }
+  }
+}
+
+// Width-matched variant for output widths that are multiples of 8 * PXW
+// (ResNet's 56 = 8 x 7): lane l owns ONE row (l / 8) and PXW consecutive
+// columns PXW (l % 8) .. + PXW - 1, so a CTA tile is 4 rows x 8 PXW columns x
+// 64 filters with no idle columns (the 32-wide tiles of conv_rows_kernel
+// leave 8 of every 64 columns idle at width 56).  Its input run of
+// PXW + KW - 1 values per (channel, filter row) is read with scalar loads: at
+// a row pitch of 8 (mod 32) the 4 rows x 8 runs (stride PXW, odd) of a warp
+// hit 32 distinct banks.
+constexpr int PTH = 4;           // rows per CTA
+
+template <typename T, int KH, int KW, int PXW>
+__global__ void __launch_bounds__(kThreads) conv_runs_kernel(ConvArgs<T> g, int vec_in,
+                                                             int vec_w) {
+  constexpr int TWR = 8 * PXW;
+  constexpr int PH = PTH + KH - 1, PW = TWR + KW - 1, TAPS = KH * KW;
+  constexpr int PITCH = PW + ((8 - PW) % 32 + 32) % 32;
+  constexpr int IN_ELEMS = CC * PH * PITCH;
+  constexpr int W_ELEMS = CC * TAPS * FT;
+  constexpr int RUN = PXW + KW - 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T *in_s = reinterpret_cast<T *>(smem_raw);          // [2][CC][PH][PITCH]
+  T *w_s = in_s + 2 * IN_ELEMS;                       // [2][CC][TAPS][FT]
+
+  const int t = threadIdx.x, warp = t / 32, lane = t % 32;
+  const int r = lane / 8, cg = lane % 8;
+  int tile = blockIdx.x;
+  const int tw_i = tile % g.tw_tiles;
+  tile /= g.tw_tiles;
+  const int th_i = tile % g.th_tiles;
+  const int n = tile / g.th_tiles;
+  const int h0 = th_i * PTH, w0 = tw_i * TWR;
+  const int f0 = blockIdx.y * FT;
+  const int fw = f0 + warp * FX;
+
+  const T *in_n = g.in + (int64_t)n * g.si[0];
+  auto stage = [&](int c0, int b) {
+    T *is = in_s + b * IN_ELEMS;
+    if (vec_in) {
+      constexpr int PV = (PW + 1) / 2;
+      for (int e = t; e < CC * PH * PV; e += kThreads) {
+        const int cc = e / (PH * PV), rem = e - cc * (PH * PV);
+        const int y = rem / PV, x = 2 * (rem - y * PV);
+        const int ci = c0 + cc, hy = h0 + y, wx = w0 + x;
+        const int avail = (ci < g.c && hy < g.hp && wx < g.wp) ? min(2, g.wp - wx) : 0;
+        const T *src = avail ? in_n + ci * g.si[1] + hy * g.si[2] + wx : g.in;
+        const uint32_t d =
+            static_cast<uint32_t>(__cvta_generic_to_shared(is + (cc * PH + y) * PITCH + x));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(d), "l"(src),
+                     "n"(2 * sizeof(T)), "r"(avail * (int)sizeof(T))
+                     : "memory");
+      }
+    } else {
+      for (int e = t; e < CC * PH * PW; e += kThreads) {
+        const int cc = e / (PH * PW), rem = e - cc * (PH * PW);
+        const int y = rem / PW, x = rem - y * PW;
+        const int ci = c0 + cc, hy = h0 + y, wx = w0 + x;
+        const bool ok = ci < g.c && hy < g.hp && wx < g.wp;
+        const T *src = ok ? in_n + ci * g.si[1] + hy * g.si[2] + wx * g.si[3] : g.in;
+        cp_async(is + (cc * PH + y) * PITCH + x, src, ok);
+      }
+    }
+    T *ws = w_s + b * W_ELEMS;
+    if (vec_w) {
+      constexpr int WV = 16 / sizeof(T);
+      for (int e = t; e < W_ELEMS / WV; e += kThreads) {
+        const int fi = (e % (FT / WV)) * WV, ct = e / (FT / WV);
+        const int ff = f0 + fi;
+        const bool ok = c0 * TAPS + ct < g.c * TAPS && ff < g.f;
+        const T *src = ok ? g.w + ((int64_t)c0 * TAPS + ct) * g.f + ff : g.w;
+        const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(ws + ct * FT + fi));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src),
+                     "r"(ok ? 16 : 0)
+                     : "memory");
+      }
+    } else {
+      for (int e = t; e < W_ELEMS; e += kThreads) {
+        const int fi = e % FT, ct = e / FT;
+        const int ff = f0 + fi;
+        const bool ok = c0 * TAPS + ct < g.c * TAPS && ff < g.f;
+        const T *src = ok ? g.w + ((int64_t)c0 * TAPS + ct) * g.f + ff : g.w;
+        cp_async(ws + e, src, ok);
+      }
+    }
+    cp_commit();
+  };
+
+  // pixel u: row h0 + r, column w0 + PXW cg + u
+  T acc[PXW][FX];
+  const int ho = h0 + r, wo0 = w0 + PXW * cg;
+#pragma unroll
+  for (int j = 0; j < FX; ++j) {
+    const int ff = fw + j;
+    const T *o = g.out + (int64_t)n * g.so[0] + (int64_t)ff * g.so[1] + (int64_t)ho * g.so[2];
+#pragma unroll
+    for (int u = 0; u < PXW; ++u) {
+      const int wo = wo0 + u;
+      acc[u][j] = (!g.init && ho < g.ho && wo < g.wo && ff < g.f) ? o[(int64_t)wo * g.so[3]]
+                                                                  : g.init_value;
+    }
+  }
+
+  const int chunks = (g.c + CC - 1) / CC;
+  stage(0, 0);
+  for (int k = 0; k < chunks; ++k) {
+    const int b = k & 1;
+    if (k + 1 < chunks) {
+      stage((k + 1) * CC, b ^ 1);   // buffer b^1 was last read before the barrier below
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+    const T *is = in_s + b * IN_ELEMS + r * PITCH + PXW * cg;
+    const T *ws = w_s + b * W_ELEMS + warp * FX;
+    const int cn = min(CC, g.c - k * CC);
+    for (int cc = 0; cc < cn; ++cc) {
+#pragma unroll
+      for (int ki = 0; ki < KH; ++ki) {
+        T x[RUN];
+        const T *row = is + (cc * PH + ki) * PITCH;
+#pragma unroll
+        for (int u = 0; u < RUN; ++u) x[u] = row[u];
+        const T *wrow = ws + (cc * TAPS + ki * KW) * FT;
+#pragma unroll
+        for (int kj = 0; kj < KW; ++kj) {
+          T wv[FX];
+#pragma unroll
+          for (int j = 0; j < FX; ++j) wv[j] = wrow[kj * FT + j];
+#pragma unroll
+          for (int u = 0; u < PXW; ++u)
+#pragma unroll
+            for (int j = 0; j < FX; ++j) acc[u][j] = add_rn(acc[u][j], mul_rn(x[u + kj], wv[j]));
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+  if (ho >= g.ho) return;
+#pragma unroll
+  for (int j = 0; j < FX; ++j) {
+    const int ff = fw + j;
+    if (ff >= g.f) continue;
+    T *o = g.out + (int64_t)n * g.so[0] + (int64_t)ff * g.so[1] + (int64_t)ho * g.so[2];
+#pragma unroll
+    for (int u = 0; u < PXW; ++u)
+      if (wo0 + u < g.wo) o[(int64_t)(wo0 + u) * g.so[3]] = acc[u][j];
+  }
+}
+
 // FCHW weights (any strides) -> [C][KH * KW][F], f fastest.
 template <typename T>
 __global__ void transpose_w_kernel(const T *__restrict__ w, int64_t s0, int64_t s1, int64_t s2,
@@ -229,8 +553,44 @@ int launch(const void *in, const int64_t *si, const void *w, const int64_t *sw, 
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kernel<<<grid, kThreads, smem, s>>>(g);
   };
-  if (kh == 3 && kw == 3) go(conv_exact_kernel<T, 3, 3>);
-  else go(conv_exact_kernel<T, 0, 0>);
+  const char *variant = getenv("B200_CONV_EXACT");   // dev A/B: "old", "rows", "runs"
+  // 56-wide runs tiles when they pad the width less than 32-wide tiles
+  const bool runs = kh == 3 && kw == 3 &&
+                    (variant ? variant[0] == 'r' && variant[1] == 'u'
+                             : (wo + 55) / 56 * 56 <= (wo + 31) / 32 * 32);
+  if (runs) {
+    auto even = [](int64_t v) { return (v & 1) == 0; };
+    const int vec_in = si[3] == 1 && even(si[0]) && even(si[1]) && even(si[2]) &&
+                       (reinterpret_cast<uintptr_t>(in) % (2 * sizeof(T))) == 0;
+    const int vec_w = (f % (16 / sizeof(T))) == 0 &&
+                      (reinterpret_cast<uintptr_t>(w_work) % 16) == 0;
+    constexpr int PW = 56 + 2, PITCH = PW + ((8 - PW) % 32 + 32) % 32;
+    const size_t rsmem = 2 * (size_t)CC * ((PTH + 2) * PITCH + 9 * FT) * sizeof(T);
+    ConvArgs<T> gr = g;
+    gr.th_tiles = (int)((ho + PTH - 1) / PTH);
+    gr.tw_tiles = (int)((wo + 55) / 56);
+    dim3 rgrid((unsigned)(nb * gr.th_tiles * gr.tw_tiles), (unsigned)((f + FT - 1) / FT));
+    auto kernel = conv_runs_kernel<T, 3, 3, 7>;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem);
+    kernel<<<rgrid, kThreads, rsmem, s>>>(gr, vec_in, vec_w);
+  } else if (kh == 3 && kw == 3 && !(variant && variant[0] == 'o')) {
+    // the consecutive-column variant: its own pitch and vector staging flags
+    auto even = [](int64_t v) { return (v & 1) == 0; };
+    const int vec_in = si[3] == 1 && even(si[0]) && even(si[1]) && even(si[2]) &&
+                       (reinterpret_cast<uintptr_t>(in) % (2 * sizeof(T))) == 0;
+    const int vec_w = (f % (16 / sizeof(T))) == 0 &&
+                      (reinterpret_cast<uintptr_t>(w_work) % 16) == 0;
+    const int vec_out = sizeof(T) == 4 && so[3] == 1 && so[0] % 4 == 0 && so[1] % 4 == 0 &&
+                        so[2] % 4 == 0 && (reinterpret_cast<uintptr_t>(out) % 16) == 0;
+    const size_t rsmem = 2 * (size_t)CC * ((TH + 2) * RPITCH + 9 * FT) * sizeof(T);
+    auto kernel = conv_rows_kernel<T, 3, 3>;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem);
+    kernel<<<grid, kThreads, rsmem, s>>>(g, vec_in, vec_w, vec_out);
+  } else if (kh == 3 && kw == 3) {
+    go(conv_exact_kernel<T, 3, 3>);
+  } else {
+    go(conv_exact_kernel<T, 0, 0>);
+  }
   return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
 }
 

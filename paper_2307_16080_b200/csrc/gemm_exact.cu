@@ -25,6 +25,9 @@
 // offset (the separable half) is looked up once per CTA.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
+
+#include <type_traits>
 
 #include "../../include/b200k.h"
 
@@ -51,6 +54,7 @@ struct Strided {
 struct Tables {
   const int64_t *a_m, *a_k, *b_k, *b_n, *c_m, *c_n;
   bool a_k_fast, b_n_fast;
+  int64_t sAm = 0, sBk = 0;   // unused: only the strided form takes the VEC path
   __device__ __forceinline__ int64_t am(int64_t m) const { return __ldg(a_m + m); }
   __device__ __forceinline__ int64_t ak(int64_t k) const { return __ldg(a_k + k); }
   __device__ __forceinline__ int64_t bk(int64_t k) const { return __ldg(b_k + k); }
@@ -80,7 +84,10 @@ struct MinBlocks {
   static constexpr int value = (sizeof(T) == 4 && TM * TN >= 64) ? 2 : 1;
 };
 
-template <typename T, typename Addr, int BM, int BN, int TM, int TN>
+// VEC (strided f32 only): A k-contiguous and B n-contiguous with 16-byte
+// aligned rows and K, N multiples of 4 — the tiles are staged with 16-byte
+// global loads (A transposed into As by four scalar stores, B stored as is).
+template <typename T, typename Addr, int BM, int BN, int TM, int TN, bool VEC = false>
 __global__ void __launch_bounds__(kThreads, MinBlocks<T, TM, TN>::value)
     contract_exact_kernel(Args<T, Addr> g) {
   constexpr int PAD = 16 / sizeof(T);
@@ -127,7 +134,49 @@ __global__ void __launch_bounds__(kThreads, MinBlocks<T, TM, TN>::value)
   const int64_t bcol_fix = (bfast && n_fix < g.N) ? g.ad.bn(n_fix) : 0;
 
   T ra[LA], rb[LB];
+  // VEC: per-thread operand pointers (rows / columns fixed for the CTA)
+  const float *vp_a[VEC ? LA / 4 : 1];
+  bool vm_a[VEC ? LA / 4 : 1];
+  const float *vp_b = nullptr;
+  bool vm_b = false;
+  if constexpr (VEC) {
+#pragma unroll
+    for (int i = 0; i < LA / 4; ++i) {
+      const int64_t m = m0 + t / 4 + i * (kThreads / 4);
+      vm_a[i] = m < g.M;
+      vp_a[i] = reinterpret_cast<const float *>(g.A) + (vm_a[i] ? m : 0) * g.ad.sAm +
+                4 * (t % 4);
+    }
+    const int64_t n = n0 + 4 * (t % (BN / 4));
+    vm_b = n < g.N;
+    vp_b = reinterpret_cast<const float *>(g.B) + (vm_b ? n : 0);
+  }
   auto load = [&](int64_t k0) {
+    if constexpr (VEC) {
+      // A: LA / 4 vectors per thread (rows t / 4 + 64 i, k quad t % 4),
+      // from per-thread row pointers set up once (vp_a below)
+#pragma unroll
+      for (int i = 0; i < LA / 4; ++i) {
+        const float4 v = (vm_a[i] && k0 + 4 * (t % 4) < g.K)
+                             ? __ldg(reinterpret_cast<const float4 *>(vp_a[i] + k0))
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+        ra[4 * i] = v.x, ra[4 * i + 1] = v.y, ra[4 * i + 2] = v.z, ra[4 * i + 3] = v.w;
+      }
+      // B goes straight to shared memory (cp.async, zero-filled past the
+      // edges): no staging registers, so the 8x8 tile fits 128 registers
+      const int buf = (int)((k0 / BK) & 1);
+#pragma unroll
+      for (int i = 0; i < LB / 4; ++i) {
+        const int kr = t / (BN / 4) + i * (kThreads / (BN / 4)), nq = 4 * (t % (BN / 4));
+        const bool ok = vm_b && k0 + kr < g.K;
+        const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(&Bs[buf][kr][nq]));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d),
+                     "l"(ok ? vp_b + (k0 + kr) * g.ad.sBk : g.B), "r"(ok ? 16 : 0)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      return;
+    }
 #pragma unroll
     for (int i = 0; i < LA; ++i) {
       const int e = t + i * kThreads;
@@ -152,6 +201,16 @@ __global__ void __launch_bounds__(kThreads, MinBlocks<T, TM, TN>::value)
     }
   };
   auto store = [&](int buf) {
+    if constexpr (VEC) {
+#pragma unroll
+      for (int i = 0; i < LA / 4; ++i) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          As[buf][4 * (t % 4) + u][t / 4 + i * (kThreads / 4)] = ra[4 * i + u];
+      }
+      asm volatile("cp.async.wait_group 0;" ::: "memory");   // this thread's B copies
+      return;
+    }
 #pragma unroll
     for (int i = 0; i < LA; ++i) {
       const int e = t + i * kThreads;
@@ -177,8 +236,7 @@ __global__ void __launch_bounds__(kThreads, MinBlocks<T, TM, TN>::value)
     if (kt + 1 < ktiles) load((kt + 1) * BK);
     const int64_t krem = g.K - kt * BK;
     const int kn = krem >= BK ? BK : (int)krem;
-#pragma unroll 4
-    for (int kk = 0; kk < kn; ++kk) {
+    auto step = [&](int kk) {
       T av[TM], bv[TN];
 #pragma unroll
       for (int i = 0; i < HM; ++i) {
@@ -194,6 +252,15 @@ __global__ void __launch_bounds__(kThreads, MinBlocks<T, TM, TN>::value)
       for (int i = 0; i < TM; ++i)
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j] = add_rn(acc[i][j], mul_rn(av[i], bv[j]));
+    };
+    if (kn == BK) {
+      // full k-tile: constant trip count, no remainder test (a full unroll
+      // hoists too many operand loads: spills at 128 registers)
+#pragma unroll 4
+      for (int kk = 0; kk < BK; ++kk) step(kk);
+    } else {
+#pragma unroll 1
+      for (int kk = 0; kk < kn; ++kk) step(kk);
     }
     if (kt + 1 < ktiles) {
       store(cur ^ 1);   // cur^1 was last read before the previous barrier
@@ -216,13 +283,21 @@ __global__ void __launch_bounds__(kThreads, MinBlocks<T, TM, TN>::value)
   }
 }
 
-template <typename T, typename Addr, int BM, int BN, int TM, int TN>
+template <typename T, typename Addr, int BM, int BN, int TM, int TN, bool VEC = false>
 int launch_tile(const Args<T, Addr> &g, void *stream) {
   dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM));
   if (grid.y > 65535u) return B200_EINVAL;
-  contract_exact_kernel<T, Addr, BM, BN, TM, TN>
+  contract_exact_kernel<T, Addr, BM, BN, TM, TN, VEC>
       <<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(g);
   return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
+}
+
+// 16-byte staging applies (see contract_exact_kernel's VEC)
+inline bool vec_ok(const Args<float, Strided> &g) {
+  const auto &a = g.ad;
+  return a.sAk == 1 && a.sBn == 1 && a.sAm % 4 == 0 && a.sBk % 4 == 0 && g.K % 4 == 0 &&
+         g.N % 4 == 0 && (reinterpret_cast<uintptr_t>(g.A) & 15) == 0 &&
+         (reinterpret_cast<uintptr_t>(g.B) & 15) == 0 && !getenv("B200_GEMM_EXACT_NOVEC");
 }
 
 template <typename Addr>
@@ -236,6 +311,8 @@ int launch(const Args<float, Addr> &g, void *stream) {
   if (g.M * g.N <= 64 * 64) return launch_tile<float, Addr, 32, 32, 2, 2>(g, stream);
   if (big_ctas < 148) return launch_tile<float, Addr, 64, 64, 4, 4>(g, stream);
   if (g.N <= 64) return launch_tile<float, Addr, 256, 64, 8, 8>(g, stream);
+  if constexpr (std::is_same<Addr, Strided>::value)
+    if (vec_ok(g)) return launch_tile<float, Addr, 128, 128, 8, 8, true>(g, stream);
   return launch_tile<float, Addr, 128, 128, 8, 8>(g, stream);
 }
 

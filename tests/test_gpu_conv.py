@@ -99,3 +99,53 @@ def test_conv_tc_through_engine(case):
     assert bad == 0, f"{bad} outputs outside the bound"
     # inputs are untouched
     assert torch.equal(torch.frombuffer(args[0].data, dtype=torch.float32).reshape(x.shape), x)
+
+
+EXACT_CASES = [
+    # nb, c, f, ho, wo, dtype
+    (2, 64, 64, 56, 56, "F32"),     # the ResNet layer's shape, 2 images (56-wide runs tiles)
+    (1, 16, 48, 10, 40, "F32"),     # ragged rows (10 = 2 x 4 + 2), F = 48 < 64
+    (1, 12, 30, 9, 37, "F32"),      # F = 30: scalar weight staging; odd width
+    (2, 8, 20, 7, 56, "F64"),       # f64 (the reference's desk kernels)
+    (1, 20, 16, 13, 20, "F32"),     # narrow: 32-wide tiles
+]
+
+
+@pytest.mark.parametrize("variant", ["auto", "old", "rows", "runs"])
+@pytest.mark.parametrize("case", EXACT_CASES, ids=[str(c) for c in EXACT_CASES])
+def test_conv_exact_variants_bit_identical(case, variant, monkeypatch):
+    """Every variant of b200_conv2d_exact (generic, 32-wide rows, 56-wide
+    runs) reproduces the reference's f32 / f64 chain bit for bit."""
+    import torch
+
+    import bench_kernels as bk
+    import oracle
+    import paper_2307_16080_b200 as b2
+    from staircase.interp import Buffer, machine
+
+    nb, c, f, ho, wo, dt = case
+    if variant != "auto":
+        monkeypatch.setenv("B200_CONV_EXACT", variant)
+    hp, wp = ho + 2, wo + 2
+    src = f'''
+@staged
+def conv_e(inp: MemRef[({nb}, {c}, {hp}, {wp}), {dt}], ker: MemRef[({f}, {c}, 3, 3), {dt}],
+           out: MemRef[({nb}, {f}, {ho}, {wo}), {dt}]):
+    for n, co, ho, wo in parallel((0, 0, 0, 0), ({nb}, {f}, {ho}, {wo})):
+        for ci in range(0, {c}):
+            for ki in range(0, 3):
+                for kj in range(0, 3):
+                    out[n, co, ho, wo] += inp[n, ci, ho + ki, wo + kj] * ker[co, ci, ki, kj]
+'''
+    fn = bk._capture_from_source(src, "conv_e", {}, f"{nb}_{c}_{f}_{ho}_{wo}_{dt}")
+    tdt, bdt = (torch.float32, "f32") if dt == "F32" else (torch.float64, "f64")
+    g = torch.Generator().manual_seed(11)
+    ts = [(torch.rand(s, generator=g, dtype=torch.float64) * 2 - 1).to(tdt)
+          for s in ((nb, c, hp, wp), (f, c, 3, 3), (nb, f, ho, wo))]
+    a1 = [Buffer(tuple(t.shape), bdt, t.numpy().tobytes()) for t in ts]
+    a2 = [Buffer(tuple(t.shape), bdt, t.numpy().tobytes()) for t in ts]
+    machine.run(fn.module, "conv_e", a1, engine=b2.engine)
+    assert b2.engine.last_plan[-1][0] == "conv2d_exact", b2.engine.last_plan
+    oracle.build()
+    machine.run(fn.module, "conv_e", a2, engine=oracle)
+    assert a1[2].data.tobytes() == a2[2].data.tobytes()
