@@ -531,6 +531,9 @@ def run_sweep(args, rank, world, local, impl):
     import paper_2307_16080_b200 as b2
 
     b2.configure(precision=b2_prec)
+    from paper_2307_16080_b200 import runtime as b2rt
+
+    t0_totals = dict(b2rt.TOTALS)
     total_trials, trial_s, setup_s, flops = 0, 0.0, 0.0, 0.0
     logs = []
     for fn, f in targets:
@@ -544,6 +547,7 @@ def run_sweep(args, rank, world, local, impl):
         total_trials += len(log)
         flops += f * len(log)
         logs.append((fn.__name__, best, log))
+    moved = {k: b2rt.TOTALS[k] - t0_totals[k] for k in t0_totals}
     if rank != 0:
         return
     # the reference tuner's per-trial rate on the same sweep machinery at desk
@@ -564,11 +568,14 @@ def run_sweep(args, rank, world, local, impl):
                    "best": {n: {"idx": b.idx, "params": b.params, "cost": b.cost}
                             for n, b, _ in logs}},
         "gflops_evaluated_per_s": flops / trial_s / 1e9,
+        # one step = the whole sweep on this rank (every trial's inputs are
+        # host Buffers staged to the device and its results written back)
         "e2e": {"value": total_trials / (trial_s + setup_s), "unit": "configs/s",
-                "h2d_bytes_per_step": None, "d2h_bytes_per_step": None},
+                "h2d_bytes_per_step": moved["h2d_bytes"],
+                "d2h_bytes_per_step": moved["d2h_bytes"]},
         "cpu_baseline": {"value": cpu_rate, "unit": "configs/s", "cores": 1,
                          "kind": "reference", "sample": cpu_note},
-        "gpu_launches": None,
+        "gpu_launches": moved["launches"],
     }
     print(json.dumps(line), flush=True)
 

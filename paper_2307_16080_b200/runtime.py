@@ -200,13 +200,19 @@ class Staging:
             else:
                 pin_host(buf.data, host)
                 t = host.to("cuda", non_blocking=False)
-                self.h2d_bytes += host.numel() * host.element_size()
+                self._count(h2d=host.numel() * host.element_size())
             ent = (buf, t)
             self.dev[id(buf)] = ent
         return ent[1]
 
     def mark_dirty(self, buf):
         self.dirty.add(id(buf))
+
+    def _count(self, h2d=0, d2h=0):
+        self.h2d_bytes += h2d
+        self.d2h_bytes += d2h
+        TOTALS["h2d_bytes"] += h2d
+        TOTALS["d2h_bytes"] += d2h
 
     def flush(self):
         torch = self.torch
@@ -216,7 +222,7 @@ class Staging:
             buf, t = self.dev[key]
             host = self.host(buf)
             host.copy_(t)
-            self.d2h_bytes += host.numel() * host.element_size()
+            self._count(d2h=host.numel() * host.element_size())
         self.dirty.clear()
         torch.cuda.current_stream().synchronize()
         if self._wb_event is not None:
@@ -256,7 +262,7 @@ class Staging:
             with torch.cuda.stream(up):
                 for (h, t) in hin + ([(ho, to)] if oup else []):
                     t[r0:r1].copy_(h[r0:r1], non_blocking=True)
-                    self.h2d_bytes += (r1 - r0) * t.shape[1] * esz
+                    self._count(h2d=(r1 - r0) * t.shape[1] * esz)
             ev = torch.cuda.Event()
             ev.record(up)
             cur.wait_event(ev)
@@ -268,7 +274,7 @@ class Staging:
                 down.wait_event(done)
                 with torch.cuda.stream(down):
                     ho[r0:r1].copy_(to[r0:r1], non_blocking=True)
-                self.d2h_bytes += (r1 - r0) * to.shape[1] * esz
+                self._count(d2h=(r1 - r0) * to.shape[1] * esz)
         assert panels[-1][1] == rows
         if written_back:
             self._wb_event = torch.cuda.Event()
@@ -300,6 +306,11 @@ class Staging:
     def upload_i64(self, values):
         return self.upload_bytes(np.asarray(values, dtype=np.int64).tobytes())
 
+
+# process-wide counters (bench.py's sweep line): entry-point calls made by
+# DeviceBackend (one kernel launch each, or a fixed few for the packing
+# entry points) and host <-> device bytes staged
+TOTALS = {"launches": 0, "h2d_bytes": 0, "d2h_bytes": 0}
 
 _COPY_STREAMS = {}
 
@@ -496,6 +507,7 @@ class DeviceBackend:
 
     def call(self, name, *args):
         check(getattr(self.stage.lib, name)(*args), name)
+        TOTALS["launches"] += 1
         if self.recording is not None:
             self.recording.calls.append((name, args))
 

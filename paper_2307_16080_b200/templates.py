@@ -37,7 +37,7 @@ class ContractMatch:
 
     __slots__ = ("A", "B", "C", "dtype", "M", "N", "K", "m_vars", "n_vars", "k_vars",
                  "_tables", "_make_tables", "origins", "strided", "offA", "offB", "offC",
-                 "sA", "sB", "sC", "offsets")
+                 "sA", "sB", "sC", "offsets", "stat")
 
     def __repr__(self):
         return (f"ContractMatch({self.dtype}, M={self.M}, N={self.N}, K={self.K}, "
@@ -189,6 +189,7 @@ def match_contraction(region, links, remainder, accesses):
         groups[key].sort(key=lambda v: -abs(aS.offset.t.get(v.id, 0) * stat(v)[1]))
 
     g = ContractMatch()
+    g.stat = stat   # (lb, step, trip) per variable, unrolled ones re-rolled
     g.A, g.B, g.C, g.dtype = A, B, C, dtype
     g.offsets = (aA.offset, aB.offset, aS.offset)
     g.m_vars, g.n_vars, g.k_vars = groups["m"], groups["n"], groups["k"]
@@ -251,9 +252,13 @@ class ConvView:
 
 def conv_view(region, g, dtypes=("f32",)):
     """Recognise out[n,f,h,w] += in[n,c,h+i,w+j] * w[f,c,i,j] (reference
-    tests/kernels.py:50-64) from a ContractMatch's index maps: every variable
-    must start at 0 with step 1 and carry exactly the conv's coefficients.
-    ``k_order`` lists the reduction roles in nest (= rounding) order."""
+    tests/kernels.py:50-64) from a ContractMatch's index maps.  Every variable
+    starts at 0 and carries exactly one role's coefficients; an output role
+    may be carried by several variables — the origin and offset loops of a
+    tiled nest (passes/tiling.py: index = origin + offset) — when together
+    they enumerate 0 .. extent-1 exactly once (mixed radix: steps 1, t0,
+    t0 t1, ...).  Reduction roles take one variable each; ``k_order`` lists
+    them in nest (= rounding) order."""
     if g is None or g.dtype not in dtypes:
         return None
     A, B, C = g.A, g.B, g.C
@@ -263,48 +268,50 @@ def conv_view(region, g, dtypes=("f32",)):
     # the operands' base offsets must be 0 (all loops start at 0)
     if tuple(g.origins) != (0, 0, 0):
         return None
-    trip = {}
     for v in g.m_vars + g.n_vars + g.k_vars:
-        lb, st, t = v.static()
-        if lb != 0 or st != 1:
+        lb, st, t = g.stat(v)
+        if lb != 0 or st < 1:
             return None
     # classify each variable by its coefficient signature
     offA, offB, offC = _offsets(region, g)
     roles = {}
     for v in g.m_vars:
         sig = (offC.t.get(v.id, 0), offA.t.get(v.id, 0))
-        if sig == (sc[0], sa[0]):
-            roles["n"] = v
-        elif sig == (sc[2], sa[2]):
-            roles["ho"] = v
-        elif sig == (sc[3], sa[3]):
-            roles["wo"] = v
-        else:
+        role = {(sc[0], sa[0]): "n", (sc[2], sa[2]): "ho", (sc[3], sa[3]): "wo"}.get(sig)
+        if role is None:
             return None
+        roles.setdefault(role, []).append(v)
     for v in g.n_vars:
         if (offC.t.get(v.id, 0), offB.t.get(v.id, 0)) != (sc[1], sb[0]):
             return None
-        roles["co"] = v
+        roles.setdefault("co", []).append(v)
     for v in g.k_vars:
         sig = (offA.t.get(v.id, 0), offB.t.get(v.id, 0))
-        if sig == (sa[1], sb[1]):
-            roles["ci"] = v
-        elif sig == (sa[2], sb[2]):
-            roles["ki"] = v
-        elif sig == (sa[3], sb[3]):
-            roles["kj"] = v
-        else:
+        role = {(sa[1], sb[1]): "ci", (sa[2], sb[2]): "ki", (sa[3], sb[3]): "kj"}.get(sig)
+        if role is None or role in roles:
             return None
-    if len(roles) != len(g.m_vars) + len(g.n_vars) + len(g.k_vars) or \
-            not {"ho", "wo", "co"} <= set(roles):
-        return None
+        if g.stat(v)[1] != 1:
+            return None
+        roles[role] = [v]
+    # a role without a variable has extent 1 (trip-1 loops are folded into
+    # the constants); the shape checks below confirm every extent
 
-    def t(name):
-        return roles[name].static()[2] if name in roles else 1
+    def extent(name):
+        if name not in roles:
+            return 1
+        step = 1
+        for v in sorted(roles[name], key=lambda v: g.stat(v)[1]):
+            _, st, t = g.stat(v)
+            if st != step:
+                return None   # not an exact mixed-radix cover of 0 .. extent-1
+            step *= t
+        return step
 
     cv = ConvView()
-    cv.nb, cv.f, cv.ho, cv.wo = t("n"), t("co"), t("ho"), t("wo")
-    cv.c, cv.kh, cv.kw = t("ci"), t("ki"), t("kj")
+    cv.nb, cv.f, cv.ho, cv.wo = extent("n"), extent("co"), extent("ho"), extent("wo")
+    cv.c, cv.kh, cv.kw = extent("ci"), extent("ki"), extent("kj")
+    if None in (cv.nb, cv.f, cv.ho, cv.wo):
+        return None
     if A.shape[0] != cv.nb or A.shape[1] != cv.c or C.shape != (cv.nb, cv.f, cv.ho, cv.wo) or \
             B.shape != (cv.f, cv.c, cv.kh, cv.kw):
         return None
@@ -312,7 +319,7 @@ def conv_view(region, g, dtypes=("f32",)):
     if cv.hp < cv.ho + cv.kh - 1 or cv.wp < cv.wo + cv.kw - 1:
         return None
     cv.inp, cv.ker, cv.out = A, B, C
-    by_id = {v.id: name for name, v in roles.items()}
+    by_id = {vs[0].id: name for name, vs in roles.items() if name in ("ci", "ki", "kj")}
     cv.k_order = tuple(by_id[v.id] for v in g.k_vars)
     return cv
 

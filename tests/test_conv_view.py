@@ -1,0 +1,65 @@
+"""templates.conv_view recognises tiled / unrolled conv nests (CPU).
+
+The sweep's configurations tile the conv's parallel loops (passes/tiling.py:
+index = origin + offset) and unroll its innermost reduction loop
+(passes/unroll.py); each such nest is still conv_2d_nchw_fchw, so it must map
+to the same ConvView (and run on the direct conv kernels) — with the
+reduction roles in nest order, the order the kernels round in.  Nests that
+are not a conv must not.
+"""
+import pytest
+
+import harness
+from vm_sim import SimEngine
+
+
+def _capture_matches(fn, pipe, monkeypatch):
+    from paper_2307_16080_b200 import engine, templates
+
+    got = []
+    orig = templates.match_contraction
+
+    def wrap(*a, **k):
+        g = orig(*a, **k)
+        got.append(g)
+        return g
+
+    monkeypatch.setattr(engine.templates, "match_contraction", wrap)
+    harness.run_engine(SimEngine(), fn, pipe, "sequential", 4)
+    return [g for g in got if g is not None]
+
+
+@pytest.mark.parametrize("sizes,unroll", [([1, 2, 8, 7], 3), ([1, 1, 2, 2], 3), ([2, 4], 1),
+                                          ([1, 1, 4, 4], 2), ([1, 1, 1, 1], 1)])
+def test_tiled_conv_is_a_conv(sizes, unroll, monkeypatch):
+    from staircase.tuner.search import default_pipeline
+
+    import test_gpu_conv as tg
+    from paper_2307_16080_b200 import templates
+
+    fn = tg._conv_kernel(2, 16, 8, 16, 28, 3, 3)
+    (g,) = _capture_matches(fn, default_pipeline(sizes, unroll), monkeypatch)
+    cv = templates.conv_view(None, g, ("f32",))
+    assert cv is not None
+    assert (cv.nb, cv.c, cv.f, cv.ho, cv.wo, cv.kh, cv.kw) == (2, 16, 8, 16, 28, 3, 3)
+    assert cv.k_order == ("ci", "ki", "kj")
+
+
+def test_matmul_is_not_a_conv(monkeypatch):
+    import corpus
+    from paper_2307_16080_b200 import templates
+
+    for g in _capture_matches(corpus.matmul_par, None, monkeypatch):
+        assert templates.conv_view(None, g, ("f32",)) is None
+
+
+def test_single_channel_conv_is_a_conv(monkeypatch):
+    """The paper's conv (1,1,1282,1282)*(1,1,3,3): N = C = F = 1, so those
+    loops have trip 1 and carry no variable."""
+    import bench_kernels as bk
+    from paper_2307_16080_b200 import templates
+
+    (g,) = _capture_matches(bk.conv_paper, None, monkeypatch)
+    cv = templates.conv_view(None, g, ("f32",))
+    assert cv is not None
+    assert (cv.nb, cv.c, cv.f, cv.ho, cv.wo, cv.kh, cv.kw) == (1, 1, 1, 1280, 1280, 3, 3)

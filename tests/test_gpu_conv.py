@@ -149,3 +149,25 @@ def conv_e(inp: MemRef[({nb}, {c}, {hp}, {wp}), {dt}], ker: MemRef[({f}, {c}, 3,
     oracle.build()
     machine.run(fn.module, "conv_e", a2, engine=oracle)
     assert a1[2].data.tobytes() == a2[2].data.tobytes()
+
+
+@pytest.mark.parametrize("sizes,unroll", [("1, 1, 4, 8", 1), ("1, 2, 8, 7", 3), ("2, 4", 1),
+                                          ("1, 1, 2, 2", 3)])
+def test_tiled_conv_takes_the_direct_kernel_bit_exact(sizes, unroll):
+    """Tiled (and unrolled) conv nests — the sweep's configurations — are
+    recognised as convolutions (origin + offset loops per output role) and
+    run on the direct exact kernel, bit-identical to the reference."""
+    import harness
+    import oracle
+    import paper_2307_16080_b200 as b2
+    from staircase.tuner.search import default_pipeline
+
+    fn = _conv_kernel(2, 16, 8, 16, 28, 3, 3)
+    pipe = default_pipeline([int(x) for x in sizes.split(",")], unroll)
+    _, got, t_got, _ = harness.run_engine(b2.engine, fn, pipe, "sequential", 4)
+    assert b2.engine.last_plan[-1][0] == "conv2d_exact", b2.engine.last_plan
+    oracle.build()
+    _, want, t_want, _ = harness.run_engine(oracle, fn, pipe, "sequential", 4)
+    assert t_got == t_want
+    for g, w in zip(got, want):
+        assert g.data.tobytes() == w.data.tobytes()
