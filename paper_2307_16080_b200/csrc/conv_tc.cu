@@ -518,6 +518,86 @@ __global__ void __launch_bounds__(256) pack_nhwc_kernel(const float *__restrict_
   }
 }
 
+// Same units and register transpose as pack_nhwc_kernel, but the CTA's
+// [32 WI pixels][64 channels] bf16 tile is assembled in shared memory (128B
+// swizzle: pixel p's 16-byte chunk k at k ^ (p & 7), so a quarter warp's
+// 16-byte stores hit 8 distinct bank groups) and written by ONE TMA store of
+// whole 128-byte pixel rows (pixels past the line clipped by the tensor
+// map), instead of 16-byte pieces from eight warps that L2 has to merge.
+// Two tiles alternate; a tile is rewritten only after its store has read it.
+template <int WI>
+__global__ void __launch_bounds__(256) pack_nhwc_tma_kernel(
+    const float *__restrict__ src, int64_t sN, int64_t sC, int64_t sH, int64_t sP,
+    const __grid_constant__ CUtensorMap tmap, int C, int lines_per_img, int len, int cp,
+    int64_t lines) {
+  constexpr int TILE = 32 * WI * 128;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  unsigned char *gbase = smem_raw + (base - smem_u32(smem_raw));
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int passes = cp / 64;
+  const int blocks = (len + 32 * WI - 1) / (32 * WI);
+  const int64_t units = lines * blocks * passes;
+  float v[2][8][WI];
+  auto coords = [&](int64_t u, int64_t &line, int &p0, int &c0) {
+    const int64_t lb = u / passes;
+    c0 = (int)(u - lb * passes) * 64;
+    line = lb / blocks;
+    p0 = (int)(lb - line * blocks) * 32 * WI;
+  };
+  auto load = [&](float (&r)[8][WI], int64_t u) {
+    int64_t line;
+    int p0, c0;
+    coords(u, line, p0, c0);
+    c0 += warp * 8;
+    const float *bp = src + (line / lines_per_img) * sN + (line % lines_per_img) * sH;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+      for (int i = 0; i < WI; ++i) {
+        const int p = p0 + lane + 32 * i;
+        r[k][i] = (c0 + k < C && p < len)
+                      ? __ldg(bp + (int64_t)(c0 + k) * sC + (int64_t)p * sP) : 0.f;
+      }
+  };
+  int b = 0;
+  auto put = [&](const float (&r)[8][WI], int64_t u) {
+    if (threadIdx.x == 0) bulk_wait_read<1>();   // the store of this tile's last use has read it
+    __syncthreads();
+    unsigned char *tile = gbase + b * TILE;
+#pragma unroll
+    for (int i = 0; i < WI; ++i) {
+      const int p = lane + 32 * i;
+      __nv_bfloat162 h[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) h[j] = __floats2bfloat162_rn(r[2 * j][i], r[2 * j + 1][i]);
+      *reinterpret_cast<uint4 *>(tile + p * 128 + ((warp ^ (p & 7)) << 4)) =
+          *reinterpret_cast<uint4 *>(h);
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int64_t line;
+      int p0, c0;
+      coords(u, line, p0, c0);
+      tma_store_4d(&tmap, base + b * TILE, c0, p0, (int32_t)line, 0);
+      bulk_commit();
+    }
+    b ^= 1;
+  };
+  int64_t u = blockIdx.x;
+  if (u < units) load(v[0], u);
+  for (; u < units; u += 2 * (int64_t)gridDim.x) {
+    const int64_t u1 = u + gridDim.x;
+    if (u1 < units) load(v[1], u1);
+    put(v[0], u);
+    if (u1 >= units) break;
+    if (u1 + gridDim.x < units) load(v[0], u1 + gridDim.x);
+    put(v[1], u1);
+  }
+  if (threadIdx.x == 0) bulk_wait_all();
+}
+
 // FCHW f32 weights -> [F][KH][KW][cp] bf16 (K order: tap, channel).
 // One thread per destination element; 32-bit index math (the tensor is at
 // most F * KH * KW * cp < 2^31 elements, host-checked).
@@ -641,6 +721,28 @@ extern "C" int b200_pack_conv_input(const float *src, const int64_t *sstr, void 
   const int len = plane ? (int)(h * w) : (int)w;
   const int64_t lines = nb * lines_per_img;
   const int64_t units = lines * ((len + 32 * PACK_WI - 1) / (32 * PACK_WI)) * (cp / 64);
+  // the TMA-stored variant: dst rows of cp bf16 (a 16-byte multiple) as a
+  // [lines][len][cp] tensor, 1024-byte-aligned shared tiles
+  CUtensorMap tmap;
+  const cuuint64_t dims[4] = {(cuuint64_t)cp, (cuuint64_t)len, (cuuint64_t)lines, 1};
+  const cuuint64_t strides[3] = {(cuuint64_t)(cp * 2), (cuuint64_t)(len * cp * 2),
+                                 (cuuint64_t)(lines * len * cp * 2)};
+  const cuuint32_t box[4] = {64, 32 * PACK_WI, 1, 1};
+  if (!getenv("B200_PACK_OLD") && (reinterpret_cast<uintptr_t>(dst) & 15) == 0 &&
+      make_map_4d(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, dst, dims, strides, box,
+                  CU_TENSOR_MAP_SWIZZLE_128B)) {
+    const int smem = 1024 + 2 * 32 * PACK_WI * 128;
+    auto kernel = pack_nhwc_tma_kernel<PACK_WI>;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, smem);
+    int64_t blocks = (int64_t)num_sms() * (per_sm < 1 ? 1 : per_sm);
+    if (blocks > units) blocks = units;
+    kernel<<<(unsigned)blocks, 256, smem, static_cast<cudaStream_t>(stream)>>>(
+        src, sstr[0], sstr[1], sstr[2], sstr[3], tmap, (int)c, lines_per_img, len, (int)cp,
+        lines);
+    return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
+  }
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pack_nhwc_kernel<PACK_WI>, 256, 0);
   int64_t blocks = (int64_t)num_sms() * (per_sm < 1 ? 1 : per_sm);
