@@ -290,6 +290,8 @@ class _Run:
                 last_writer[i] = id(it.g.C) not in later
                 later.add(id(it.g.C))
             else:
+                # conservatively every operand of a map counts as written
+                last_writer[i] = not any(id(b) in later for b in it.m.buffers)
                 later.update(id(b) for b in it.m.buffers)
         for it, last in zip(items, last_writer):
             if isinstance(it, fusion.ContractItem):
@@ -308,7 +310,7 @@ class _Run:
                                  ((tuple(fused),) if fused else ()))
             else:
                 m = it.m
-                self.be.map(m)
+                self.be.map(m, last_writer=last)
                 self.plan.append(("map_" + m.kind, tuple(m.trips),
                                   "vec4" if m.vector else "scalar"))
 

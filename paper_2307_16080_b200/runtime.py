@@ -229,7 +229,7 @@ class Staging:
             self._wb_event.synchronize()
             self._wb_event = None
 
-    def stream_rows(self, panels, ins, out, launch, written_back=True):
+    def stream_rows(self, panels, ins, out, launch, written_back=True, rows=None):
         """Run ``launch(r0, r1)`` over row panels with the host copies overlapped.
 
         The row-major buffers in ``ins`` (uploaded, panel by panel, on a copy
@@ -241,21 +241,24 @@ class Staging:
         duplex: both directions run at once).  Every buffer ends staged
         (registered in ``dev``); the current stream then waits for the
         write-backs, so later kernels cannot overwrite rows still being
-        copied out.  ``panels``: [(r0, r1)] covering the leading dimension.
+        copied out.  ``panels``: [(r0, r1)] covering the leading dimension
+        (or ``rows`` equal slices of every buffer's flat storage).
         """
         torch = self.torch
         cur = torch.cuda.current_stream()
         up, down = _copy_streams(torch)
         up.wait_stream(cur)     # device storage may be recycled from earlier kernels
         obuf, oup = out
-        rows = obuf.shape[0]
+        lead = rows
+        rows = rows or obuf.shape[0]
         views = []
         for buf in ins + [obuf]:
             host = self.host(buf)
             pin_host(buf.data, host)
             t = torch.empty_like(host, device="cuda")
             self.dev[id(buf)] = (buf, t)
-            views.append((host.view(buf.shape[0], -1), t.view(buf.shape[0], -1)))
+            r = lead or buf.shape[0]
+            views.append((host.view(r, -1), t.view(r, -1)))
         hin, (ho, to) = views[:-1], views[-1]
         esz = to.element_size()
         for r0, r1 in panels:
@@ -738,12 +741,72 @@ class DeviceBackend:
         self._conv_run(cv, 4, init, last_writer, launch)
         return ["pack_conv_weight", "pack_conv_input", "conv2d_tc_bf16"]
 
-    def map(self, m):
+    def _map_stream_plan(self, m):
+        """Row panels for a pointwise plan over whole dense buffers (one
+        output), or None: (panels, rows, streamed inputs, output, output read)."""
+        if not (self.stream_io and self.recording is None) or len(m.trips) != 1:
+            return None
+        s = self.stage
+        T = m.trips[0]
+        loads, stores = set(), set()
+        pc = 0
+        while pc < len(m.prog):
+            w = m.prog[pc]
+            op, k = w & 0xFF, (w >> 16) & 0xFF
+            (loads if op == 0 else stores if op == 3 else set()).add(k)
+            pc += 2 if op == 2 else 1
+        outs = {id(m.buffers[k]): m.buffers[k] for k in stores}
+        if len(outs) != 1:
+            return None
+        (out,) = outs.values()
+        if s.staged(out):
+            return None
+        for b, base, c in zip(m.buffers, m.bases, m.coefs):
+            if base != 0 or list(c) != [1] or math.prod(b.shape) != T or not _row_major(b):
+                return None
+        rows = 1024
+        if T % rows or (T // rows) % 4:
+            return None
+        ins = list({id(m.buffers[k]): m.buffers[k] for k in loads
+                    if m.buffers[k] is not out and not s.staged(m.buffers[k])}.values())
+        out_read = any(m.buffers[k] is out for k in loads)
+        per_row = 4 * (T // rows) * (len(ins) + (2 if out_read else 1))
+        panels = row_panels(rows, per_row, 1)
+        return None if panels is None else (panels, rows, ins, out, out_read)
+
+    def map(self, m, last_writer=False):
         """Run a templates.MapMatch: an NVRTC-specialised kernel when the JIT
-        is available (straight-line native code), else b200_map_f32."""
+        is available (straight-line native code), else b200_map_f32.  Large
+        first-use maps over whole buffers run as row panels with their host
+        copies pipelined (Staging.stream_rows)."""
         s = self.stage
         from . import jit
 
+        plan = self._map_stream_plan(m) if jit.available() else None
+        if plan is not None:
+            from .templates import MapMatch
+
+            panels, rows, ins, out, out_read = plan
+            for b in m.buffers:
+                if b is not out and all(b is not x for x in ins):
+                    s.tensor(b)
+            per = m.trips[0] // rows
+
+            def launch(r0, r1):
+                mp = MapMatch()
+                for k in MapMatch.__slots__:
+                    setattr(mp, k, getattr(m, k))
+                mp.trips = [(r1 - r0) * per]
+                ptrs = [s.dev[id(b)][1].data_ptr() + 4 * r0 * per for b in m.buffers]
+                ln = jit.map_launch(mp, ptrs)
+                self.keep(ln)
+                self.call("b200_jit_launch", ctypes.c_void_p(ln.fn), ln.grid, 1, 1, 256, 1, 1,
+                          0, ln.argv, s.stream_ptr)
+
+            s.stream_rows(panels, ins, (out, out_read), launch, rows=rows)
+            if last_writer:
+                s.dirty.discard(id(out))
+            return ["map_jit"]
         if jit.available():
             ptrs = [s.tensor(b).data_ptr() + 4 * base for b, base in zip(m.buffers, m.bases)]
             ln = jit.map_launch(m, ptrs)

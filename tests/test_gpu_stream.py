@@ -49,12 +49,34 @@ def _run(fn, precision, stream, monkeypatch):
 
 
 CASES = [("mm1024", "exact"), ("mm1024", "bf16"), ("ls512", "exact"), ("ls512", "bf16"),
-         ("conv4", "exact"), ("conv4", "bf16"), ("gemm_then_vm", "exact")]
+         ("conv4", "exact"), ("conv4", "bf16"), ("gemm_then_vm", "exact"), ("saxpy", "exact"),
+         ("fill_then_scale", "exact")]
+
+FILL_THEN_SCALE = '''
+@staged
+def fill_then_scale(x: MemRef[(256, 512), F32], y: MemRef[(256, 512), F32]):
+    for i, j in parallel((0, 0), (256, 512)):
+        y[i, j] = constant(1.5, F32)
+    for i, j in parallel((0, 0), (256, 512)):
+        y[i, j] = y[i, j] * x[i, j]
+'''
+
+SAXPY = '''
+@staged
+def saxpy_s(x: MemRef[(512, 1024), F32], y: MemRef[(512, 1024), F32]):
+    for i, j in parallel((0, 0), (512, 1024)):
+        y[i, j] = y[i, j] + x[i, j] * constant(2.0, F32)
+'''
+
 
 
 def _fn(name):
     return {"mm1024": lambda: bk.mm_par1024, "ls512": lambda: bk.make_linear_stack(512),
-            "conv4": lambda: bk.make_conv(4), "gemm_then_vm": _gemm_then_vm}[name]()
+            "conv4": lambda: bk.make_conv(4), "gemm_then_vm": _gemm_then_vm,
+            "saxpy": lambda: bk._capture_from_source(SAXPY, "saxpy_s", {}, "stream"),
+            "fill_then_scale": lambda: bk._capture_from_source(FILL_THEN_SCALE,
+                                                               "fill_then_scale", {},
+                                                               "stream")}[name]()
 
 
 @pytest.mark.parametrize("name,precision", CASES)

@@ -47,9 +47,9 @@ def test_map_kernels_compile(fn, monkeypatch):
     seen = []
     orig = vm_sim.SimBackend.map
 
-    def spy(self, m):
+    def spy(self, m, **kw):
         seen.append(m)
-        return orig(self, m)
+        return orig(self, m, **kw)
 
     monkeypatch.setattr(vm_sim.SimBackend, "map", spy)
     mode = "gpu_emulated" if fn is corpus.ewise_gpu else "sequential"

@@ -86,7 +86,7 @@ class SimBackend:
         C[coff] = acc
         return ["contract_exact"]
 
-    def map(self, m):
+    def map(self, m, last_writer=False):
         """b200_map_f32 semantics: every box point runs the program in order."""
         self.launches.append(("map", m.kind, m.vector))
         arrs = [self.arr(b) for b in m.buffers]
