@@ -20,6 +20,7 @@
 #ifndef B200K_H
 #define B200K_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -211,6 +212,15 @@ int b200_conv2d_exact(int32_t dtype, const void *in, const int64_t *in_strides, 
  */
 int b200_jit_compile(const char *src, const char *kernel, void **fn);
 const char *b200_jit_log(void);
+
+/*
+ * The same compilation split in two for the on-disk kernel cache (jit.py):
+ * b200_jit_cubin compiles to an sm_100a cubin image (no device needed;
+ * *size = image bytes, B200_EINVAL if cap is too small), b200_jit_load turns
+ * an image into the kernel's CUfunction.
+ */
+int b200_jit_cubin(const char *src, void *out, size_t cap, size_t *size);
+int b200_jit_load(const void *image, const char *kernel, void **fn);
 
 /* Launch a b200_jit_compile kernel; args = array of pointers to argument values. */
 int b200_jit_launch(void *fn, uint32_t gx, uint32_t gy, uint32_t gz, uint32_t bx, uint32_t by,

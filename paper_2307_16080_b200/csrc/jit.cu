@@ -105,12 +105,9 @@ bool init_driver() {
   return g_drv.ok;
 }
 
-}  // namespace
-
-// Compile `src` and return the CUfunction for `kernel` in *fn (opaque).
-extern "C" int b200_jit_compile(const char *src, const char *kernel, void **fn) {
-  std::lock_guard<std::mutex> lock(g_mu);
-  if (!init_nvrtc() || !init_driver()) return B200_EUNSUPPORTED;
+// NVRTC: `src` -> sm_100a cubin (caller holds g_mu).
+int compile_cubin(const char *src, std::vector<char> &cubin) {
+  if (!init_nvrtc()) return B200_EUNSUPPORTED;
   nvrtcProgram_ prog;
   if (g_nv.create(&prog, src, "b200_jit.cu", 0, nullptr, nullptr) != 0) return B200_EINVAL;
   const char *opts[] = {"-arch=sm_100a", "--fmad=false", "-std=c++17", "-default-device",
@@ -126,11 +123,17 @@ extern "C" int b200_jit_compile(const char *src, const char *kernel, void **fn) 
   }
   size_t cn = 0;
   g_nv.cubin_size(prog, &cn);
-  std::vector<char> cubin(cn);
+  cubin.resize(cn);
   g_nv.cubin(prog, cubin.data());
   g_nv.destroy(&prog);
+  return B200_OK;
+}
+
+// cubin image -> CUfunction (caller holds g_mu).
+int load_cubin(const void *image, const char *kernel, void **fn) {
+  if (!init_driver()) return B200_EUNSUPPORTED;
   CUmodule mod;
-  if (g_drv.load(&mod, cubin.data()) != CUDA_SUCCESS) {
+  if (g_drv.load(&mod, image) != CUDA_SUCCESS) {
     g_log = "cuModuleLoadData failed";
     return B200_ELAUNCH;
   }
@@ -142,6 +145,39 @@ extern "C" int b200_jit_compile(const char *src, const char *kernel, void **fn) 
   *fn = reinterpret_cast<void *>(f);
   return B200_OK;
 }
+
+}  // namespace
+
+// Compile `src` and return the CUfunction for `kernel` in *fn (opaque).
+extern "C" int b200_jit_compile(const char *src, const char *kernel, void **fn) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  if (!init_nvrtc() || !init_driver()) return B200_EUNSUPPORTED;
+  std::vector<char> cubin;
+  const int rc = compile_cubin(src, cubin);
+  return rc != B200_OK ? rc : load_cubin(cubin.data(), kernel, fn);
+}
+
+// Compile `src` to an sm_100a cubin without loading it (no GPU needed): the
+// image is copied into out (capacity cap bytes); *size receives its length
+// (B200_EINVAL with *size set when cap is too small).
+extern "C" int b200_jit_cubin(const char *src, void *out, size_t cap, size_t *size) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  std::vector<char> cubin;
+  const int rc = compile_cubin(src, cubin);
+  if (rc != B200_OK) return rc;
+  *size = cubin.size();
+  if (cubin.size() > cap) return B200_EINVAL;
+  memcpy(out, cubin.data(), cubin.size());
+  return B200_OK;
+}
+
+// Load a cubin produced by b200_jit_cubin (e.g. from the on-disk kernel
+// cache) and return the CUfunction for `kernel`.
+extern "C" int b200_jit_load(const void *image, const char *kernel, void **fn) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  return load_cubin(image, kernel, fn);
+}
+
 
 // The compiler log of the last b200_jit_compile (for diagnostics).
 extern "C" const char *b200_jit_log(void) { return g_log.c_str(); }

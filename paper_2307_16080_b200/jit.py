@@ -6,7 +6,14 @@ nest body a register, each f32 op an explicit ``__f*_rn`` intrinsic (so the
 result is the reference's per-op rounding, reference interp/_evalpy.py:
 115-127), loads/stores 128-bit when the innermost walk is contiguous.
 Kernels are cached per generated source, so repeated runs and tuner trials
-with the same nest shape compile once.
+with the same nest shape compile once — in memory, and as cubin images on
+disk (``B200_JIT_CACHE``, default ``~/.cache/paper_2307_16080_b200/jit``;
+``B200_JIT_DISK=0`` disables it) so a new process (a CLI ``run``, a tuner
+rank) loads instead of recompiling.  The key is the SHA-1 of the generated
+CUDA C plus the compile options: the source is a function of the ``.sir``
+program's nest, its shapes and constants (".sir as the
+kernel-cache key"), and keying on it also separates programs that print
+alike but specialise differently.
 """
 from __future__ import annotations
 
@@ -20,6 +27,11 @@ from .runtime import check, load_library
 
 _CACHE = {}
 ENABLED = os.environ.get("B200_JIT", "1") != "0"
+DISK = os.environ.get("B200_JIT_DISK", "1") != "0"
+CACHE_DIR = os.environ.get("B200_JIT_CACHE") or os.path.join(
+    os.path.expanduser("~"), ".cache", "paper_2307_16080_b200", "jit")
+# must change whenever csrc/jit.cu's NVRTC options change
+OPTIONS_TAG = "sm_100a --fmad=false -std=c++17 -default-device -lineinfo"
 
 
 def available():
@@ -29,17 +41,67 @@ def available():
     return hasattr(lib, "b200_jit_compile")
 
 
+def cache_key(src):
+    return hashlib.sha1((OPTIONS_TAG + "\n" + src).encode()).hexdigest()
+
+
+def cubin(src, name="kernel"):
+    """NVRTC-compile ``src`` to an sm_100a cubin image (bytes); no GPU needed."""
+    lib = load_library()
+    cap = 1 << 20
+    while True:
+        buf = ctypes.create_string_buffer(cap)
+        size = ctypes.c_size_t(0)
+        rc = lib.b200_jit_cubin(src.encode(), buf, cap, ctypes.byref(size))
+        if rc == 0:
+            return buf.raw[:size.value]
+        if size.value > cap:
+            cap = size.value
+            continue
+        log = lib.b200_jit_log().decode(errors="replace")
+        raise RuntimeError(f"NVRTC compile of {name} failed ({rc}):\n{log}\n{src}")
+
+
+def _disk_get(key):
+    try:
+        with open(os.path.join(CACHE_DIR, key + ".cubin"), "rb") as fh:
+            data = fh.read()
+        return data if data[:4] == b"\x7fELF" else None
+    except OSError:
+        return None
+
+
+def _disk_put(key, image):
+    try:
+        os.makedirs(CACHE_DIR, exist_ok=True)
+        tmp = os.path.join(CACHE_DIR, f".{key}.{os.getpid()}.tmp")
+        with open(tmp, "wb") as fh:
+            fh.write(image)
+        os.replace(tmp, os.path.join(CACHE_DIR, key + ".cubin"))   # atomic for readers
+    except OSError:
+        pass   # a read-only home: the in-memory cache still applies
+
+
 def compile_kernel(src, name):
-    """Compile (cached) and return the opaque CUfunction handle."""
-    key = hashlib.sha1(src.encode()).hexdigest()
+    """Compile (cached in memory and on disk) and return the opaque CUfunction."""
+    key = cache_key(src)
     fn = _CACHE.get(key)
     if fn is None:
         lib = load_library()
+        image = _disk_get(key) if DISK else None
+        fresh = image is None
+        if fresh:
+            image = cubin(src, name)
         out = ctypes.c_void_p()
-        rc = lib.b200_jit_compile(src.encode(), name.encode(), ctypes.byref(out))
+        rc = lib.b200_jit_load(image, name.encode(), ctypes.byref(out))
+        if rc != 0 and not fresh:   # a stale or damaged cache entry: rebuild it
+            image, fresh = cubin(src, name), True
+            rc = lib.b200_jit_load(image, name.encode(), ctypes.byref(out))
         if rc != 0:
             log = lib.b200_jit_log().decode(errors="replace")
-            raise RuntimeError(f"NVRTC compile of {name} failed ({rc}):\n{log}\n{src}")
+            raise RuntimeError(f"loading the JIT kernel {name} failed ({rc}): {log}")
+        if fresh and DISK:
+            _disk_put(key, image)
         fn = out.value
         _CACHE[key] = fn
     return fn
@@ -131,4 +193,5 @@ def map_launch(m, ptrs):
     return Launch(fn, blocks, ptrs)
 
 
-__all__ = ["available", "compile_kernel", "map_source", "map_launch", "Launch"]
+__all__ = ["available", "cache_key", "compile_kernel", "cubin", "map_source", "map_launch",
+           "Launch"]

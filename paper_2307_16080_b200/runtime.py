@@ -67,6 +67,8 @@ SIGNATURES = {
     "b200_conv2d_exact": [_I32, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64,
                           _I64, _I64, _I64, _I32, ctypes.c_double, _P],
     "b200_jit_compile": [ctypes.c_char_p, ctypes.c_char_p, _P],
+    "b200_jit_cubin": [ctypes.c_char_p, _P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)],
+    "b200_jit_load": [ctypes.c_char_p, ctypes.c_char_p, _P],
     "b200_jit_launch": [_P, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
                         ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
                         _P, _P],

@@ -36,3 +36,24 @@ def test_native_equals_interpreter(case):
     fn, _, pipe, mode = case
     for seed in (0, 1):
         assert _run(fn, pipe, mode, seed, True) == _run(fn, pipe, mode, seed, False)
+
+
+def test_kernels_load_from_the_disk_cache(tmp_path, monkeypatch):
+    """A new process (simulated: empty in-memory cache) loads the NVRTC
+    kernels of a run from the on-disk cache without compiling, and the run's
+    buffers and tally are unchanged."""
+    import corpus
+    import harness
+    import paper_2307_16080_b200 as b2
+    from paper_2307_16080_b200 import jit
+
+    monkeypatch.setattr(jit, "CACHE_DIR", str(tmp_path))
+    monkeypatch.setattr(jit, "_CACHE", {})
+    _, want, t_want, _ = harness.run_engine(b2.engine, corpus.ewise_ops, None, "sequential", 2)
+    assert list(tmp_path.glob("*.cubin")), "nothing was cached"
+    monkeypatch.setattr(jit, "_CACHE", {})
+    monkeypatch.setattr(jit, "cubin", lambda *a, **k: pytest.fail("recompiled"))
+    _, got, t_got, _ = harness.run_engine(b2.engine, corpus.ewise_ops, None, "sequential", 2)
+    assert t_got == t_want
+    for g, w in zip(got, want):
+        assert g.data.tobytes() == w.data.tobytes()

@@ -59,3 +59,26 @@ def test_map_kernels_compile(fn, monkeypatch):
         src, name, total = jit.map_source(m)
         rc, log = nvrtc_compile(src)
         assert rc == 0, log + "\n" + src
+
+
+@pytest.mark.skipif(NVRTC is None, reason="libnvrtc not present")
+def test_disk_kernel_cache_round_trip(tmp_path, monkeypatch):
+    """b200_jit_cubin compiles without a device; the on-disk cache stores the
+    image under the source+options key and hands it back; damaged entries
+    are ignored."""
+    from paper_2307_16080_b200 import jit
+
+    monkeypatch.setattr(jit, "CACHE_DIR", str(tmp_path))
+    src = ('extern "C" __global__ void k(float* p) '
+           '{ p[threadIdx.x] = __fmul_rn(p[threadIdx.x], 2.0f); }\n')
+    image = jit.cubin(src, "k")
+    assert image[:4] == b"\x7fELF"
+    key = jit.cache_key(src)
+    assert jit._disk_get(key) is None
+    jit._disk_put(key, image)
+    assert jit._disk_get(key) == image
+    assert key != jit.cache_key(src + " ")
+    monkeypatch.setattr(jit, "OPTIONS_TAG", jit.OPTIONS_TAG + " -G")
+    assert jit.cache_key(src) != key            # options are part of the key
+    (tmp_path / "bad.cubin").write_bytes(b"not an elf")
+    assert jit._disk_get("bad") is None
