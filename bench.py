@@ -296,7 +296,7 @@ KERNEL_OF = {"b200_gemm_tc": "gemm", "b200_gemm_f32_exact": "gemm",
              "b200_jit_launch": "map"}
 TENSOR_KERNELS = ("b200_gemm_tc", "b200_conv2d_tc")
 # entry points that run the same kernel (timed together as one family)
-ALIASES = {"b200_gemm_tc_shadow": "b200_gemm_tc"}
+ALIASES = {"b200_gemm_tc_shadow": "b200_gemm_tc", "b200_gemm_tc_kn": "b200_gemm_tc"}
 
 
 # -- arms ----------------------------------------------------------------------------

@@ -161,6 +161,18 @@ int b200_gemm_tc(int32_t kind, const void *A, const void *Bt, float *C, int64_t 
  * an f32 Buffer (the f32 C is still written in full).  Saves the separate
  * b200_pack_operand pass over C.
  */
+/*
+ * b200_gemm_tc with B given as a K x N row-major bf16 tensor — the matmul
+ * nest's own B layout, converted to bf16 but not transposed — read MN-major
+ * by the tensor cores (no transposing pack).  kind must be 0 (bf16); c16 /
+ * ld16 as in b200_gemm_tc_shadow, c16 may be NULL.  N must be a multiple of
+ * 64 (B200_EUNSUPPORTED otherwise).
+ */
+int b200_gemm_tc_kn(int32_t kind, const void *A, const void *B, float *C, int64_t sCm,
+                    int64_t sCn, int64_t M, int64_t N, int64_t K, int32_t init,
+                    float init_value, const float *bias, int64_t bias_stride, void *c16,
+                    int64_t ld16, void *stream);
+
 int b200_gemm_tc_shadow(int32_t kind, const void *A, const void *Bt, float *C, int64_t sCm,
                         int64_t sCn, int64_t M, int64_t N, int64_t K, int32_t init,
                         float init_value, const float *bias, int64_t bias_stride,

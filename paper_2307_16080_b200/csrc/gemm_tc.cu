@@ -327,7 +327,7 @@ namespace {
 int gemm_tc(int32_t kind, const void *A, const void *Bt, float *C, int64_t sCm, int64_t sCn,
             int64_t M, int64_t N, int64_t K, int32_t init, float init_value, const float *bias,
             int64_t bias_stride, int32_t max_ctas, int32_t variant, __nv_bfloat16 *c16,
-            int64_t ld16, void *stream) {
+            int64_t ld16, void *stream, const void *Bkn = nullptr) {
   if (M <= 0 || N <= 0) return B200_OK;
   if (K <= 0 || (kind != 0 && kind != 1)) return B200_EINVAL;
   const int elem = kind == 0 ? 2 : 4;
@@ -340,6 +340,7 @@ int gemm_tc(int32_t kind, const void *A, const void *Bt, float *C, int64_t sCm, 
     const int64_t pair_tiles = ((M + 255) / 256) * ((N + 255) / 256);
     variant = pair_tiles >= sms / 2 ? 2 : 1;
   }
+  if (Bkn) return launch_gemm_tc2(kind, A, nullptr, ep, M, N, K, max_ctas / 2, s, Bkn);
   if (variant == 2) return launch_gemm_tc2(kind, A, Bt, ep, M, N, K, max_ctas / 2, s);
   CUtensorMap ma, mb;
   if (!make_map(&ma, kind, A, M, K, BM) || !make_map(&mb, kind, Bt, N, K, BN))
@@ -378,4 +379,17 @@ extern "C" int b200_gemm_tc_shadow(int32_t kind, const void *A, const void *Bt, 
   if (!c16 || ld16 < N) return B200_EINVAL;
   return gemm_tc(kind, A, Bt, C, sCm, sCn, M, N, K, init, init_value, bias, bias_stride, 0, 0,
                  static_cast<__nv_bfloat16 *>(c16), ld16, stream);
+}
+
+// C (+)= A . B with B given as a K x N row-major bf16 tensor (the matmul
+// nest's own B layout, converted but not transposed), read MN-major by the
+// CTA-pair kernel; c16 / ld16 as in b200_gemm_tc_shadow (c16 may be null).
+extern "C" int b200_gemm_tc_kn(int32_t kind, const void *A, const void *B, float *C,
+                               int64_t sCm, int64_t sCn, int64_t M, int64_t N, int64_t K,
+                               int32_t init, float init_value, const float *bias,
+                               int64_t bias_stride, void *c16, int64_t ld16, void *stream) {
+  if (kind != 0) return B200_EUNSUPPORTED;
+  if (c16 && ld16 < N) return B200_EINVAL;
+  return gemm_tc(kind, A, nullptr, C, sCm, sCn, M, N, K, init, init_value, bias, bias_stride, 0,
+                 2, static_cast<__nv_bfloat16 *>(c16), ld16, stream, B);
 }

@@ -100,7 +100,7 @@ __device__ __forceinline__ bool get_item(const Sched &s, int64_t cid, int64_t i,
   return true;
 }
 
-template <int KIND, bool SH>
+template <int KIND, bool SH, bool BMN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tma_a,
                     const __grid_constant__ CUtensorMap tma_b,
@@ -173,7 +173,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
         // each CTA stages half of the item's columns of B^T
         const int brows = it.ncols / 2;
         const CUtensorMap *mb = brows == 128 ? &tma_b : &tma_bs;
-        const uint32_t bytes = 2u * (PA + brows * 128);
+        // MN-major B: 64 (N) x 64 (K) boxes, at least one (a narrow tail
+        // item reads a full box and uses its first brows columns)
+        const int nbox = brows >= 64 ? brows / 64 : 1;
+        const uint32_t bytes = BMN ? 2u * (PA + nbox * 8192) : 2u * (PA + brows * 128);
         const int32_t m0 = (int32_t)(it.m0 + rank * 128);
         const int32_t n0 = (int32_t)(it.n0 + rank * brows);
         for (int64_t kb = 0; kb < kb_total; ++kb) {
@@ -181,7 +184,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
           if (leader) mbar_expect_tx(full(s), bytes);
           const uint32_t lf = map_to_rank(full(s), 0);
           tma_load_2d_pair(&tma_a, lf, sA + s * PA, (int32_t)(kb * BK), m0);
-          tma_load_2d_pair(mb, lf, sB + s * PB, (int32_t)(kb * BK), n0);
+          if (BMN) {
+            // one box: nbox 64-wide N chunks x 64 K rows (chunks 8 KB apart)
+            tma_load_3d_pair(nbox == 2 ? &tma_b : &tma_bs, lf, sB + s * PB, n0 % 64,
+                             (int32_t)(kb * BK), n0 / 64);
+          } else {
+            tma_load_2d_pair(mb, lf, sB + s * PB, (int32_t)(kb * BK), n0);
+          }
           if (++s == PSTAGES) { s = 0; ph ^= 1; }
         }
       }
@@ -194,7 +203,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
       uint32_t aph = 0;
       Item it;
       for (int64_t i = 0; get_item(sch, cid, i, it); ++i) {
-        const uint32_t idesc = make_idesc(KIND, 256, it.ncols);
+        const uint32_t idesc = make_idesc(KIND, 256, it.ncols) | (BMN ? 1u << 16 : 0u);
         mbar_wait_cluster(tempty(acc), aph ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + (uint32_t)(acc * 256);
@@ -204,8 +213,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
           const uint32_t a_addr = sA + s * PA, b_addr = sB + s * PB;
 #pragma unroll
           for (int k = 0; k < BK / UK; ++k)
-            umma<KIND, 2>(tmem_d, smem_desc(a_addr + 32 * k), smem_desc(b_addr + 32 * k), idesc,
-                          (kb | k) != 0);
+            umma<KIND, 2>(tmem_d, smem_desc(a_addr + 32 * k),
+                          BMN ? smem_desc_mn(b_addr + 2048 * k, 8192) : smem_desc(b_addr + 32 * k),
+                          idesc, (kb | k) != 0);
           umma_commit_pair(empty(s), 0x3);
           if (++s == PSTAGES) { s = 0; ph ^= 1; }
         }
@@ -314,20 +324,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
 
 }  // namespace
 
-template <int KIND, bool SH>
+template <int KIND, bool SH, bool BMN = false>
 int launch(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mbs,
            const CUtensorMap &mc, const CUtensorMap &ms, int use_tma_c, const Epi &ep, int64_t M,
            int64_t N, const Sched &sch, int clusters, cudaStream_t s) {
   constexpr size_t smem = Lay<SH>::SMEM;
-  cudaFuncSetAttribute(gemm_tc2_kernel<KIND, SH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)smem);
-  gemm_tc2_kernel<KIND, SH><<<2 * clusters, PTHREADS, smem, s>>>(ma, mb, mbs, mc, ms, use_tma_c,
-                                                                 ep, M, N, sch);
+  auto kernel = gemm_tc2_kernel<KIND, SH, BMN>;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kernel<<<2 * clusters, PTHREADS, smem, s>>>(ma, mb, mbs, mc, ms, use_tma_c, ep, M, N, sch);
   return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
 }
 
+// K x N row-major bf16 B viewed as [N / 64][K][64] (a 64-wide N chunk's
+// rows are its 128-byte swizzled K rows): boxes of `chunks` x 64 K x 64 N.
+// N must be a multiple of 64 for the view (host-checked); the K tail is
+// zero-filled.
+bool make_map_kn(CUtensorMap *map, const void *B, int64_t K, int64_t N, uint32_t chunks) {
+  EncodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {64, (cuuint64_t)K, (cuuint64_t)(N / 64)};
+  cuuint64_t strides[2] = {(cuuint64_t)(N * 2), 128};
+  cuuint32_t box[3] = {64, 64, chunks};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(B), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int launch_gemm_tc2(int kind, const void *A, const void *Bt, const Epi &ep, int64_t M, int64_t N,
-                    int64_t K, int max_clusters, cudaStream_t s) {
+                    int64_t K, int max_clusters, cudaStream_t s, const void *Bkn) {
+  if (Bkn && (kind != 0 || N % 64 != 0)) return B200_EUNSUPPORTED;
   Sched sch;
   sch.nt = (N + 255) / 256;
   sch.tiles = ((M + 255) / 256) * sch.nt;
@@ -345,9 +371,14 @@ int launch_gemm_tc2(int kind, const void *A, const void *Bt, const Epi &ep, int6
     sch.split = S >= 8 ? 8 : (S >= 4 ? 4 : (S >= 2 ? 2 : 1));
   }
   CUtensorMap ma, mb, mbs, mc;
-  if (!make_map(&ma, kind, A, M, K, 128) || !make_map(&mb, kind, Bt, N, K, 128) ||
-      !make_map(&mbs, kind, Bt, N, K, (uint32_t)(128 / sch.split)))
+  if (!make_map(&ma, kind, A, M, K, 128)) return B200_ELAUNCH;
+  if (Bkn) {
+    if (!make_map_kn(&mb, Bkn, K, N, 2) || !make_map_kn(&mbs, Bkn, K, N, 1))
+      return B200_ELAUNCH;
+  } else if (!make_map(&mb, kind, Bt, N, K, 128) ||
+             !make_map(&mbs, kind, Bt, N, K, (uint32_t)(128 / sch.split))) {
     return B200_ELAUNCH;
+  }
   // staged epilogue needs unit column stride and 16-byte aligned rows
   int use_tma_c = ep.sCn == 1 && (ep.sCm * 4) % 16 == 0 &&
                   (reinterpret_cast<uintptr_t>(ep.C) & 15) == 0 && ep.sCm >= N;
@@ -358,6 +389,10 @@ int launch_gemm_tc2(int kind, const void *A, const void *Bt, const Epi &ep, int6
   const bool sh = use_tma_c && ep.c16 && (ep.ld16 * 2) % 16 == 0 && ep.ld16 >= N &&
                   (reinterpret_cast<uintptr_t>(ep.c16) & 15) == 0 &&
                   make_map_s16(&ms, ep.c16, M, N, ep.ld16, 128);
+  if (Bkn)
+    return sh ? launch<0, true, true>(ma, mb, mbs, mc, ms, use_tma_c, ep, M, N, sch, clusters, s)
+              : launch<0, false, true>(ma, mb, mbs, mc, ms, use_tma_c, ep, M, N, sch, clusters,
+                                       s);
   if (kind == 0)
     return sh ? launch<0, true>(ma, mb, mbs, mc, ms, use_tma_c, ep, M, N, sch, clusters, s)
               : launch<0, false>(ma, mb, mbs, mc, ms, use_tma_c, ep, M, N, sch, clusters, s);

@@ -88,6 +88,16 @@ __device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap *map, uint32_
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d_pair(const CUtensorMap *map, uint32_t bar,
+                                                 uint32_t dst, int32_t c0, int32_t c1,
+                                                 int32_t c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 // TMA store (bulk group) from local smem to global, OOB elements clipped.
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, uint32_t src, int32_t c0,
                                              int32_t c1) {
@@ -137,8 +147,21 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
   return d;
 }
 
+// MN-major, 128B-swizzled B operand (rows = K, 64 contiguous N per 128-byte
+// row): the canonical ((8 x 16 B, n), (8 rows, k)) layout with the 64-wide N
+// chunks `lbo` bytes apart and 8-row K groups 1024 bytes apart.
+__device__ __forceinline__ uint64_t smem_desc_mn(uint32_t addr, uint32_t lbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);  // start address
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;   // LBO: next 64-wide N chunk
+  d |= (uint64_t)(1024 >> 4) << 32;        // SBO: next 8 K rows
+  d |= (uint64_t)1 << 46;                  // descriptor version (sm100)
+  d |= (uint64_t)2 << 61;                  // SWIZZLE_128B
+  return d;
+}
+
 // Instruction descriptor: fp32 accumulate, bf16 (kind 0) / tf32 (kind 1)
-// operands, both K-major, shape M x N.
+// operands, both K-major, shape M x N (bit 16 = B MN-major, set by callers).
 __host__ __device__ constexpr uint32_t make_idesc(int kind, int M, int N) {
   return (1u << 4) | ((kind == 0 ? 1u : 2u) << 7) | ((kind == 0 ? 1u : 2u) << 10) |
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
@@ -443,8 +466,9 @@ inline int num_sms() {
   return n;
 }
 
-// 2-CTA launcher (gemm_tc2.cu)
+// 2-CTA launcher (gemm_tc2.cu).  Bkn (bf16 only): B as a K x N row-major
+// tensor read MN-major, instead of the K-major N x K pack Bt.
 int launch_gemm_tc2(int kind, const void *A, const void *Bt, const Epi &ep, int64_t M, int64_t N,
-                    int64_t K, int max_clusters, cudaStream_t s);
+                    int64_t K, int max_clusters, cudaStream_t s, const void *Bkn = nullptr);
 
 }  // namespace b200tc

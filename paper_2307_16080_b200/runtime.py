@@ -60,6 +60,8 @@ SIGNATURES = {
                      _I64, _I32, _I32, _P],
     "b200_gemm_tc_shadow": [_I32, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I32, _F32, _P,
                             _I64, _P, _I64, _P],
+    "b200_gemm_tc_kn": [_I32, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I32, _F32, _P,
+                        _I64, _P, _I64, _P],
     "b200_pack_conv_input": [_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _P],
     "b200_pack_conv_weight": [_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _P],
     "b200_conv2d_tc": [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64,
@@ -395,7 +397,7 @@ def launch_gemm(lib, precision, a_ptr, sA, b_ptr, sB, c_ptr, sC, M, N, K, stream
     bf16/tf32 -> b200_pack_operand x2 + b200_gemm_tc (tcgen05).
     a_packed: A already packed (a bf16 shadow, M x K) — its pack is skipped;
     c16: also write C rounded to bf16 (M x N) with b200_gemm_tc_shadow.
-    b_packed: B already packed (N x K, see pack_b) — its pack is skipped.
+    b_packed: B already packed ((tensor, kn) from pack_b) — its pack is skipped.
     """
     call = call or _direct_call(lib)
     P = ctypes.c_void_p
@@ -414,11 +416,16 @@ def launch_gemm(lib, precision, a_ptr, sA, b_ptr, sB, c_ptr, sC, M, N, K, stream
         call("b200_pack_operand", kind, P(a_ptr), sA[0], sA[1], P(Ap.data_ptr()), M, K, stream)
         names.append("pack_operand")
     if b_packed is not None:
-        Bp = b_packed
+        Bp, kn = b_packed if isinstance(b_packed, tuple) else (b_packed, False)
     else:
-        Bp = pack_b(lib, precision, b_ptr, sB, N, K, stream, call)
+        Bp, kn = pack_b(lib, precision, b_ptr, sB, N, K, stream, call)
         names.append("pack_operand")
-    if c16 is not None:
+    if kn:
+        call("b200_gemm_tc_kn", kind, P(Ap.data_ptr()), P(Bp.data_ptr()), P(c_ptr), sC[0], sC[1],
+             M, N, K, init, init_value, P(bias_ptr) if bias_ptr else None, bias_stride,
+             P(c16.data_ptr()) if c16 is not None else None, N if c16 is not None else 0,
+             stream)
+    elif c16 is not None:
         call("b200_gemm_tc_shadow", kind, P(Ap.data_ptr()), P(Bp.data_ptr()), P(c_ptr), sC[0],
              sC[1], M, N, K, init, init_value, P(bias_ptr) if bias_ptr else None, bias_stride,
              P(c16.data_ptr()), N, stream)
@@ -429,14 +436,27 @@ def launch_gemm(lib, precision, a_ptr, sA, b_ptr, sB, c_ptr, sC, M, N, K, stream
     return names + [f"gemm_tc_{precision}"]
 
 
+GEMM_KN = os.environ.get("B200_GEMM_KN", "1") != "0"
+
+
 def pack_b(lib, precision, b_ptr, sB, N, K, stream, call=None):
-    """B (K x N, strides sB) packed K-major for b200_gemm_tc (workspace slot 1)."""
+    """Pack B (K x N, strides sB) for the tensor cores (workspace slot 1).
+
+    Returns (tensor, kn).  bf16 with N-contiguous rows, N a multiple of 64:
+    converted in place order (K x N, a plain row conversion) and read MN-major by
+    b200_gemm_tc_kn (kn True); otherwise transposed to the K-major N x K
+    operand of b200_gemm_tc."""
     call = call or _direct_call(lib)
     kind = 0 if precision == "bf16" else 1
+    if GEMM_KN and kind == 0 and sB[1] == 1 and N % 64 == 0:
+        Bp = workspace(1, "bfloat16", K, N)
+        call("b200_pack_operand", kind, ctypes.c_void_p(b_ptr), sB[0], sB[1],
+             ctypes.c_void_p(Bp.data_ptr()), K, N, stream)
+        return Bp, True
     Bp = workspace(1, "bfloat16" if kind == 0 else "float32", N, K)
     call("b200_pack_operand", kind, ctypes.c_void_p(b_ptr), sB[1], sB[0],
          ctypes.c_void_p(Bp.data_ptr()), N, K, stream)
-    return Bp
+    return Bp, False
 
 
 # Host-copy pipelining (Staging.stream_rows): only when the streamed bytes

@@ -171,3 +171,70 @@ def test_linear_stack_shadow_bit_identical(rows):
     assert outs[True] == outs[False]
     assert [p[0] for p in plan] == ["gemm_tc_bf16", "gemm_tc_bf16"]
     assert "C->shadow" in plan[0][-1] and "A<-shadow" in plan[1][-1]
+
+
+@pytest.mark.parametrize("shape", [(128, 256, 64), (300, 512, 200), (1024, 1024, 1024),
+                                   (4096, 4096, 512), (1000, 1024, 1000), (256, 192, 136)])
+@pytest.mark.parametrize("mode", ["acc", "init_bias", "shadow"])
+def test_gemm_tc_kn_equals_kmajor(shape, mode):
+    """b200_gemm_tc_kn (B read MN-major from its K x N layout) computes the
+    same products in the same order as the K-major CTA-pair kernel over the
+    transposed pack: C (and the bf16 shadow) bitwise equal; tail items with
+    narrow N included (split waves)."""
+    import torch
+
+    from paper_2307_16080_b200 import runtime
+
+    lib = runtime.load_library()
+    M, N, K = shape
+    g = torch.Generator(device="cuda").manual_seed(5)
+    A = (torch.rand(M, K, device="cuda", generator=g) * 2 - 1).bfloat16()
+    Bkn = (torch.rand(K, N, device="cuda", generator=g) * 2 - 1).bfloat16()
+    Bt = Bkn.t().contiguous()
+    C0 = torch.rand(M, N, device="cuda", generator=g) * 2 - 1
+    bias = torch.rand(N, device="cuda", generator=g)
+    init, bptr = (1, bias) if mode == "init_bias" else (0, None)
+    P = ctypes.c_void_p
+    s = P(torch.cuda.current_stream().cuda_stream)
+    outs = []
+    for kn in (False, True):
+        C = C0.clone()
+        c16 = torch.zeros(M, N, dtype=torch.bfloat16, device="cuda") if mode == "shadow" else None
+        bp = P(bptr.data_ptr()) if bptr is not None else None
+        if kn:
+            rc = lib.b200_gemm_tc_kn(0, P(A.data_ptr()), P(Bkn.data_ptr()), P(C.data_ptr()), N,
+                                     1, M, N, K, init, 0.25, bp, 1,
+                                     P(c16.data_ptr()) if c16 is not None else None,
+                                     N if c16 is not None else 0, s)
+        elif c16 is not None:
+            rc = lib.b200_gemm_tc_shadow(0, P(A.data_ptr()), P(Bt.data_ptr()), P(C.data_ptr()),
+                                         N, 1, M, N, K, init, 0.25, bp, 1, P(c16.data_ptr()), N,
+                                         s)
+        else:
+            rc = lib.b200_gemm_tc(0, P(A.data_ptr()), P(Bt.data_ptr()), P(C.data_ptr()), N, 1,
+                                  M, N, K, init, 0.25, bp, 1, 0, 2, s)
+        assert rc == 0
+        torch.cuda.synchronize()
+        outs.append((C, c16))
+    assert torch.equal(outs[0][0], outs[1][0])
+    if mode == "shadow":
+        assert torch.equal(outs[0][1], outs[1][1])
+        assert torch.equal(outs[1][1], outs[1][0].bfloat16())
+
+
+def test_gemm_tc_kn_rejects_ragged_n():
+    """The MN-major view needs N % 64 == 0; other widths are refused (the
+    engine then packs B transposed for b200_gemm_tc)."""
+    import torch
+
+    from paper_2307_16080_b200 import runtime
+
+    lib = runtime.load_library()
+    P = ctypes.c_void_p
+    A = torch.zeros(128, 64, dtype=torch.bfloat16, device="cuda")
+    B = torch.zeros(64, 72, dtype=torch.bfloat16, device="cuda")
+    C = torch.zeros(128, 72, device="cuda")
+    s = P(torch.cuda.current_stream().cuda_stream)
+    rc = lib.b200_gemm_tc_kn(0, P(A.data_ptr()), P(B.data_ptr()), P(C.data_ptr()), 72, 1, 128,
+                             72, 64, 0, 0.0, None, 0, None, 0, s)
+    assert rc != 0
