@@ -388,7 +388,7 @@ extern "C" int b200_gemm_tc_kn(int32_t kind, const void *A, const void *B, float
                                int64_t sCm, int64_t sCn, int64_t M, int64_t N, int64_t K,
                                int32_t init, float init_value, const float *bias,
                                int64_t bias_stride, void *c16, int64_t ld16, void *stream) {
-  if (kind != 0) return B200_EUNSUPPORTED;
+  if (kind != 0) return B200_EUNSUPPORTED;   // MN-major is bf16-only (see gemm_tc2.cu)
   if (c16 && ld16 < N) return B200_EINVAL;
   return gemm_tc(kind, A, nullptr, C, sCm, sCn, M, N, K, init, init_value, bias, bias_stride, 0,
                  2, static_cast<__nv_bfloat16 *>(c16), ld16, stream, B);

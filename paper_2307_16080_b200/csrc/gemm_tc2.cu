@@ -136,6 +136,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
   constexpr int ELEM = KIND == 0 ? 2 : 4;
   constexpr int BK = 128 / ELEM;
   constexpr int UK = 32 / ELEM;
+  constexpr int CH = 128 / ELEM;        // MN-major B: N elements per 128-byte row
+  constexpr uint32_t CHB = BK * 128;    // bytes of one N chunk (BK rows)
   const int64_t kb_total = sch.kb_total;
 
   if (warp == 0 && lane == 0) {
@@ -173,10 +175,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
         // each CTA stages half of the item's columns of B^T
         const int brows = it.ncols / 2;
         const CUtensorMap *mb = brows == 128 ? &tma_b : &tma_bs;
-        // MN-major B: 64 (N) x 64 (K) boxes, at least one (a narrow tail
-        // item reads a full box and uses its first brows columns)
-        const int nbox = brows >= 64 ? brows / 64 : 1;
-        const uint32_t bytes = BMN ? 2u * (PA + nbox * 8192) : 2u * (PA + brows * 128);
+        // MN-major B: chunks of CH (N) x BK (K) (128-byte rows), at least
+        // one (a narrow tail item reads a whole chunk and uses its first
+        // brows columns)
+        const int nbox = brows >= CH ? brows / CH : 1;
+        const uint32_t bytes = BMN ? 2u * (PA + nbox * CHB) : 2u * (PA + brows * 128);
         const int32_t m0 = (int32_t)(it.m0 + rank * 128);
         const int32_t n0 = (int32_t)(it.n0 + rank * brows);
         for (int64_t kb = 0; kb < kb_total; ++kb) {
@@ -185,9 +188,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
           const uint32_t lf = map_to_rank(full(s), 0);
           tma_load_2d_pair(&tma_a, lf, sA + s * PA, (int32_t)(kb * BK), m0);
           if (BMN) {
-            // one box: nbox 64-wide N chunks x 64 K rows (chunks 8 KB apart)
-            tma_load_3d_pair(nbox == 2 ? &tma_b : &tma_bs, lf, sB + s * PB, n0 % 64,
-                             (int32_t)(kb * BK), n0 / 64);
+            // one box: nbox N chunks x BK K rows (chunks CHB bytes apart)
+            tma_load_3d_pair(brows == 128 ? &tma_b : &tma_bs, lf, sB + s * PB, n0 % CH,
+                             (int32_t)(kb * BK), n0 / CH);
           } else {
             tma_load_2d_pair(mb, lf, sB + s * PB, (int32_t)(kb * BK), n0);
           }
@@ -214,7 +217,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
 #pragma unroll
           for (int k = 0; k < BK / UK; ++k)
             umma<KIND, 2>(tmem_d, smem_desc(a_addr + 32 * k),
-                          BMN ? smem_desc_mn(b_addr + 2048 * k, 8192) : smem_desc(b_addr + 32 * k),
+                          BMN ? smem_desc_mn(b_addr + 128 * UK * k, CHB)
+                              : smem_desc(b_addr + 32 * k),
                           idesc, (kb | k) != 0);
           umma_commit_pair(empty(s), 0x3);
           if (++s == PSTAGES) { s = 0; ph ^= 1; }
@@ -339,20 +343,26 @@ int launch(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mbs,
 // rows are its 128-byte swizzled K rows): boxes of `chunks` x 64 K x 64 N.
 // N must be a multiple of 64 for the view (host-checked); the K tail is
 // zero-filled.
-bool make_map_kn(CUtensorMap *map, const void *B, int64_t K, int64_t N, uint32_t chunks) {
+bool make_map_kn(CUtensorMap *map, int kind, const void *B, int64_t K, int64_t N,
+                 uint32_t chunks) {
   EncodeTiled enc = get_encode();
   if (!enc) return false;
-  cuuint64_t dims[3] = {64, (cuuint64_t)K, (cuuint64_t)(N / 64)};
-  cuuint64_t strides[2] = {(cuuint64_t)(N * 2), 128};
-  cuuint32_t box[3] = {64, 64, chunks};
+  const int elem = kind == 0 ? 2 : 4;
+  const cuuint32_t ch = 128 / elem;     // N per chunk row; K rows per box = BK = ch too
+  cuuint64_t dims[3] = {ch, (cuuint64_t)K, (cuuint64_t)(N / ch)};
+  cuuint64_t strides[2] = {(cuuint64_t)(N * elem), 128};
+  cuuint32_t box[3] = {ch, ch, chunks};
   cuuint32_t estr[3] = {1, 1, 1};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(B), dims, strides, box,
+  return enc(map, kind == 0 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+             3, const_cast<void *>(B), dims, strides, box,
              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 int launch_gemm_tc2(int kind, const void *A, const void *Bt, const Epi &ep, int64_t M, int64_t N,
                     int64_t K, int max_clusters, cudaStream_t s, const void *Bkn) {
+  // MN-major operands are a 16-bit-type feature: tf32 B read MN-major came
+  // out wrong on the B200 (tools/probe_gemm_kn.py --kind 1), so kind 0 only
   if (Bkn && (kind != 0 || N % 64 != 0)) return B200_EUNSUPPORTED;
   Sched sch;
   sch.nt = (N + 255) / 256;
@@ -373,7 +383,10 @@ int launch_gemm_tc2(int kind, const void *A, const void *Bt, const Epi &ep, int6
   CUtensorMap ma, mb, mbs, mc;
   if (!make_map(&ma, kind, A, M, K, 128)) return B200_ELAUNCH;
   if (Bkn) {
-    if (!make_map_kn(&mb, Bkn, K, N, 2) || !make_map_kn(&mbs, Bkn, K, N, 1))
+    // whole halves: 128 N = 128 / CH chunks; tail items: their brows in chunks
+    const int64_t ch = kind == 0 ? 64 : 32, tail = 128 / sch.split;
+    if (!make_map_kn(&mb, kind, Bkn, K, N, (uint32_t)(128 / ch)) ||
+        !make_map_kn(&mbs, kind, Bkn, K, N, (uint32_t)(tail >= ch ? tail / ch : 1)))
       return B200_ELAUNCH;
   } else if (!make_map(&mb, kind, Bt, N, K, 128) ||
              !make_map(&mbs, kind, Bt, N, K, (uint32_t)(128 / sch.split))) {

@@ -15,6 +15,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--mnk", type=int, nargs=3, default=[4096, 4096, 4096])
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--kind", type=int, default=0, help="0 bf16, 1 tf32")
     a = ap.parse_args()
     import torch
 
@@ -24,8 +25,15 @@ def main():
     M, N, K = a.mnk
     P = ctypes.c_void_p
     s = P(torch.cuda.current_stream().cuda_stream)
-    A = torch.randn(M, K, device="cuda").bfloat16()
-    Bkn = torch.randn(K, N, device="cuda").bfloat16()
+    kind = a.kind
+    if kind == 0:
+        A = torch.randn(M, K, device="cuda").bfloat16()
+        Bkn = torch.randn(K, N, device="cuda").bfloat16()
+    else:   # tf32-representable f32 (low 13 mantissa bits clear)
+        def tf32(t):
+            return (t.view(torch.int32) & ~0x1FFF).view(torch.float32)
+        A = tf32(torch.randn(M, K, device="cuda"))
+        Bkn = tf32(torch.randn(K, N, device="cuda"))
     Bt = Bkn.t().contiguous()
     C0 = torch.randn(M, N, device="cuda")
     res = {}
@@ -34,10 +42,10 @@ def main():
 
         def go():
             if name == "kmajor":
-                rc = lib.b200_gemm_tc(0, P(A.data_ptr()), P(Bt.data_ptr()), P(C.data_ptr()), N, 1,
+                rc = lib.b200_gemm_tc(kind, P(A.data_ptr()), P(Bt.data_ptr()), P(C.data_ptr()), N, 1,
                                       M, N, K, 0, 0.0, None, 0, 0, 2, s)
             else:
-                rc = lib.b200_gemm_tc_kn(0, P(A.data_ptr()), P(Bkn.data_ptr()), P(C.data_ptr()),
+                rc = lib.b200_gemm_tc_kn(kind, P(A.data_ptr()), P(Bkn.data_ptr()), P(C.data_ptr()),
                                          N, 1, M, N, K, 0, 0.0, None, 0, None, 0, s)
             assert rc == 0, rc
 
