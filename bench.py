@@ -478,6 +478,9 @@ def run_ours(args, rank, world, local):
                 "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "cpu_baseline": {"value": cpu_rate, "unit": "GFLOP/s", "cores": 1,
                          "kind": "reference", "sample": cpu_sample},
+        # device time per step of every entry point the step launches
+        # (graph-replayed repeats of each recorded call, CUDA events)
+        "step_kernels_ms": {k: round(v, 4) for k, v in sorted(fam.items())},
         "clocks": clk, "gpu_launches": rec.launches * args.steps,
         "checksums": sums,
     }

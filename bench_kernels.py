@@ -212,12 +212,20 @@ def _capture_from_source(src, name, ns, size):
     key = (name, size)
     if key in _GEN:
         return _GEN[key]
+    import hashlib
+
     d = os.path.join(tempfile.gettempdir(), "b200_bench_kernels")
     os.makedirs(d, exist_ok=True)
-    path = os.path.join(d, f"{name}_{size}.py")
     header = ("from staircase import F32, F64, MemRef, constant, parallel, staged\n")
-    with open(path, "w") as fh:
-        fh.write(header + src)
+    text = header + src
+    # content-addressed, written atomically: several ranks (or test workers)
+    # capture the same kernel concurrently and must never read a partial file
+    path = os.path.join(d, f"{name}_{size}_{hashlib.sha1(text.encode()).hexdigest()[:12]}.py")
+    if not os.path.exists(path):
+        tmp = f"{path}.{os.getpid()}.tmp"
+        with open(tmp, "w") as fh:
+            fh.write(text)
+        os.replace(tmp, path)
     spec = importlib.util.spec_from_file_location(f"_b200_{name}_{size}", path)
     mod = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(mod)
