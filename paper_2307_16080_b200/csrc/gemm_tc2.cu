@@ -65,6 +65,7 @@ static_assert(Lay<false>::SMEM <= 232448 && Lay<true>::SMEM <= 232448, "smem");
 
 struct Sched {
   int64_t tiles, nt, kb_total, ncl;
+  int64_t group_m;   // M-blocks walked together by the grouped raster
   int64_t waves;   // full waves of whole tiles
   int64_t rem;     // tiles in the partial wave
   int64_t split;   // N sub-tiles per tail tile (1, 2, 4 or 8)
@@ -89,7 +90,7 @@ __device__ __forceinline__ bool get_item(const Sched &s, int64_t cid, int64_t i,
   }
   // grouped raster: GROUP_M consecutive M-blocks walk N together, so one wave
   // of tiles touches ~GROUP_M A panels and ~waves/GROUP_M B panels (L2 reuse)
-  constexpr int64_t GROUP_M = 8;
+  const int64_t GROUP_M = s.group_m;
   const int64_t mt = s.tiles / s.nt;
   const int64_t group = t / (GROUP_M * s.nt);
   const int64_t first_m = group * GROUP_M;
@@ -375,6 +376,9 @@ int launch_gemm_tc2(int kind, const void *A, const void *Bt, const Epi &ep, int6
   sch.waves = sch.tiles / clusters;
   sch.rem = sch.tiles - sch.waves * clusters;
   sch.split = 1;
+  const char *genv = getenv("B200_TC2_GROUP");   // dev A/B knob
+  sch.group_m = genv ? atoi(genv) : 8;
+  if (sch.group_m < 1) sch.group_m = 1;
   const char *env = getenv("B200_TC2_SPLIT");
   if (sch.rem > 0 && !(env && env[0] == '0')) {
     const int64_t S = clusters / sch.rem;

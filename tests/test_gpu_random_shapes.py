@@ -1,0 +1,113 @@
+"""Seeded random shapes through the whole engine on the B200, against the C
+oracle: matmul nests (plain and row-major-transposed B) and convolutions of
+random sizes — odd extents, one-element dimensions, non-square filters —
+must be bit-identical (buffers and the 25-slot tally) at exact precision,
+and within the stated bf16 bound at bf16 precision.
+"""
+import random
+
+import numpy as np
+import pytest
+
+import bench_kernels as bk
+import harness
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+MM = '''
+@staged
+def mm_r(A: MemRef[({M}, {K}), F32], B: MemRef[({K}, {N}), F32], C: MemRef[({M}, {N}), F32]):
+    for i, j in parallel((0, 0), ({M}, {N})):
+        for k in range(0, {K}):
+            C[i, j] += A[i, k] * B[k, j]
+'''
+
+CONV = '''
+@staged
+def conv_r(inp: MemRef[({nb}, {c}, {hp}, {wp}), F32], ker: MemRef[({f}, {c}, {kh}, {kw}), F32],
+           out: MemRef[({nb}, {f}, {ho}, {wo}), F32]):
+    for n, co, ho, wo in parallel((0, 0, 0, 0), ({nb}, {f}, {ho}, {wo})):
+        for ci in range(0, {c}):
+            for ki in range(0, {kh}):
+                for kj in range(0, {kw}):
+                    out[n, co, ho, wo] += inp[n, ci, ho + ki, wo + kj] * ker[co, ci, ki, kj]
+'''
+
+
+def _mm_shape(seed):
+    r = random.Random(seed)
+    return dict(M=r.choice([1, 3, 17, 64, 96, 130, 257]), N=r.choice([1, 8, 31, 64, 72, 200]),
+                K=r.choice([1, 5, 16, 33, 64, 100, 136]))
+
+
+def _conv_shape(seed):
+    r = random.Random(1000 + seed)
+    kh, kw = r.choice([(1, 1), (3, 3), (5, 5), (1, 3), (3, 1), (2, 4)])
+    ho, wo = r.randint(1, 20), r.randint(1, 40)
+    return dict(nb=r.randint(1, 3), c=r.choice([1, 3, 8, 16, 20]), f=r.choice([1, 4, 8, 32, 48]),
+                ho=ho, wo=wo, hp=ho + kh - 1, wp=wo + kw - 1, kh=kh, kw=kw)
+
+
+def _both(fn, seed):
+    import paper_2307_16080_b200 as b2
+
+    _, got, t_got, _ = harness.run_engine(b2.engine, fn, None, "sequential", seed)
+    plan = list(b2.engine.last_plan)
+    oracle.build()
+    _, want, t_want, _ = harness.run_engine(oracle, fn, None, "sequential", seed)
+    return got, t_got, want, t_want, plan
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_random_matmul_exact(seed):
+    shp = _mm_shape(seed)
+    fn = bk._capture_from_source(MM.format(**shp), "mm_r", {}, "_".join(map(str, shp.values())))
+    got, t_got, want, t_want, plan = _both(fn, seed)
+    assert t_got == t_want, plan
+    for g, w in zip(got, want):
+        assert g.data.tobytes() == w.data.tobytes(), (shp, plan)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_random_conv_exact(seed):
+    shp = _conv_shape(seed)
+    fn = bk._capture_from_source(CONV.format(**shp), "conv_r", {},
+                                 "_".join(map(str, shp.values())))
+    got, t_got, want, t_want, plan = _both(fn, seed)
+    assert t_got == t_want, plan
+    for g, w in zip(got, want):
+        assert g.data.tobytes() == w.data.tobytes(), (shp, plan)
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_matmul_bf16_within_bound(seed):
+    """bf16 precision on bf16-representable inputs: every output within
+    2 K 2^-24 sum|a b| + 4 2^-24 |want| of the float64 result."""
+    import paper_2307_16080_b200 as b2
+    from staircase.interp import Buffer, machine
+
+    shp = _mm_shape(100 + seed)
+    M, N, K = shp["M"], shp["N"], shp["K"]
+    fn = bk._capture_from_source(MM.format(**shp), "mm_r", {}, "_".join(map(str, shp.values())))
+    rng = np.random.default_rng(seed)
+
+    def bf16(x):
+        import torch
+
+        return torch.from_numpy(x).bfloat16().float().numpy()
+
+    A = bf16(rng.uniform(-1, 1, (M, K)).astype(np.float32))
+    B = bf16(rng.uniform(-1, 1, (K, N)).astype(np.float32))
+    C = rng.uniform(-1, 1, (M, N)).astype(np.float32)
+    args = [Buffer(x.shape, "f32", x.tobytes()) for x in (A, B, C)]
+    b2.configure(precision="bf16")
+    try:
+        machine.run(fn.module, "mm_r", args, engine=b2.engine)
+    finally:
+        b2.configure(precision="exact")
+    got = np.frombuffer(args[2].data, dtype=np.float32).reshape(M, N).astype(np.float64)
+    want = C.astype(np.float64) + A.astype(np.float64) @ B.astype(np.float64)
+    mag = np.abs(A.astype(np.float64)) @ np.abs(B.astype(np.float64))
+    bound = 2 * K * 2.0 ** -24 * mag + 4 * 2.0 ** -24 * np.abs(want) + 1e-30
+    assert (np.abs(got - want) <= bound).all(), (shp, b2.engine.last_plan)
