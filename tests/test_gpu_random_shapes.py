@@ -111,3 +111,32 @@ def test_random_matmul_bf16_within_bound(seed):
     mag = np.abs(A.astype(np.float64)) @ np.abs(B.astype(np.float64))
     bound = 2 * K * 2.0 ** -24 * mag + 4 * 2.0 ** -24 * np.abs(want) + 1e-30
     assert (np.abs(got - want) <= bound).all(), (shp, b2.engine.last_plan)
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_random_tile_unroll_pipelines_exact(seed):
+    """The sweep's knobs on random nests: random tile sizes (tiling applies
+    only where they divide the trip counts) and unroll factors on random
+    matmul / conv shapes; engine == oracle, bit for bit, tally included."""
+    import paper_2307_16080_b200 as b2
+    from staircase.tuner.search import default_pipeline
+
+    r = random.Random(5000 + seed)
+    if seed % 2 == 0:
+        shp = _mm_shape(200 + seed)
+        fn = bk._capture_from_source(MM.format(**shp), "mm_r", {},
+                                     "_".join(map(str, shp.values())))
+        tiles = [r.choice([1, 2, 4, 8, 16]) for _ in range(2)]
+    else:
+        shp = _conv_shape(200 + seed)
+        fn = bk._capture_from_source(CONV.format(**shp), "conv_r", {},
+                                     "_".join(map(str, shp.values())))
+        tiles = [r.choice([1, 2, 4, 8]) for _ in range(4)]
+    pipe = default_pipeline(tiles, r.choice([1, 2, 3, 4]))
+    _, got, t_got, _ = harness.run_engine(b2.engine, fn, pipe, "sequential", seed)
+    plan = list(b2.engine.last_plan)
+    oracle.build()
+    _, want, t_want, _ = harness.run_engine(oracle, fn, pipe, "sequential", seed)
+    assert t_got == t_want, (shp, pipe, plan)
+    for g, w in zip(got, want):
+        assert g.data.tobytes() == w.data.tobytes(), (shp, pipe, plan)
