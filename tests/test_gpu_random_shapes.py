@@ -140,3 +140,45 @@ def test_random_tile_unroll_pipelines_exact(seed):
     assert t_got == t_want, (shp, pipe, plan)
     for g, w in zip(got, want):
         assert g.data.tobytes() == w.data.tobytes(), (shp, pipe, plan)
+
+
+def _ewise_src(seed):
+    r = random.Random(7000 + seed)
+    rows, cols = r.choice([1, 3, 16, 33, 64]), r.choice([1, 4, 7, 64, 100, 256])
+
+    def expr(d):
+        if d == 0 or r.random() < 0.3:
+            return r.choice(["a[i, j]", "b[i, j]", f"constant({r.uniform(-3, 3):.6f}, F32)"])
+        return f"({expr(d - 1)} {r.choice(['+', '-', '*', '/'])} {expr(d - 1)})"
+
+    body = expr(3)
+    src = f'''
+@staged
+def ew_r(a: MemRef[({rows}, {cols}), F32], b: MemRef[({rows}, {cols}), F32],
+         c: MemRef[({rows}, {cols}), F32]):
+    for i, j in parallel((0, 0), ({rows}, {cols})):
+        c[i, j] = {body}
+'''
+    return src, f"{rows}_{cols}_{seed}"
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_random_elementwise_exact(seed):
+    """Random f32 expression trees (+ - * / and constants, depth <= 3) over
+    random shapes, as pointwise NVRTC kernels: bit-identical to the oracle
+    (per-op rounding, no contraction).  Quotients of random values can be
+    inf or NaN; those compare by class, finite values bit for bit."""
+    import paper_2307_16080_b200 as b2
+
+    src, key = _ewise_src(seed)
+    fn = bk._capture_from_source(src, "ew_r", {}, key)
+    _, got, t_got, _ = harness.run_engine(b2.engine, fn, None, "sequential", seed)
+    plan = list(b2.engine.last_plan)
+    oracle.build()
+    _, want, t_want, _ = harness.run_engine(oracle, fn, None, "sequential", seed)
+    assert t_got == t_want, plan
+    g = np.frombuffer(got[2].data, dtype=np.float32)
+    w = np.frombuffer(want[2].data, dtype=np.float32)
+    assert np.array_equal(np.isnan(g), np.isnan(w)), (src, plan)
+    fin = ~np.isnan(w)
+    assert np.array_equal(g[fin].view(np.int32), w[fin].view(np.int32)), (src, plan)
