@@ -182,3 +182,56 @@ def test_random_elementwise_exact(seed):
     assert np.array_equal(np.isnan(g), np.isnan(w)), (src, plan)
     fin = ~np.isnan(w)
     assert np.array_equal(g[fin].view(np.int32), w[fin].view(np.int32)), (src, plan)
+
+
+def _irregular_src(seed):
+    r = random.Random(9000 + seed)
+    n = r.choice([5, 16, 33, 64])
+    thr = f"{r.uniform(-0.5, 0.5):.4f}"
+    k1, k2 = f"{r.uniform(-2, 2):.4f}", f"{r.uniform(-2, 2):.4f}"
+    kind = seed % 3
+    if kind == 0:    # triangular, reads what earlier iterations wrote
+        body = f'''
+    for i in range(1, {n}):
+        for j in range(i):
+            v = a[i, j] + a[j, i] * constant({k1}, F32)
+            if v > constant({thr}, F32):
+                a[i, j] = v
+            else:
+                a[i, j] = a[i - 1, j] - v'''
+    elif kind == 1:  # running sums along rows (loop-carried)
+        body = f'''
+    for i in range(0, {n}):
+        for j in range(1, {n}):
+            a[i, j] = a[i, j - 1] * constant({k1}, F32) + a[i, j]'''
+    else:            # data-dependent branch inside a parallel nest
+        body = f'''
+    for i, j in parallel((0, 0), ({n}, {n})):
+        v = a[i, j]
+        if v > constant({thr}, F32):
+            b[i, j] = v * constant({k1}, F32)
+        else:
+            b[i, j] = v + constant({k2}, F32)'''
+    src = f'''
+@staged
+def irr_r(a: MemRef[({n}, {n}), F32], b: MemRef[({n}, {n}), F32]):{body}
+'''
+    return src, f"{n}_{seed}"
+
+
+@pytest.mark.parametrize("seed", range(15))
+def test_random_irregular_nests_exact(seed):
+    """Nests no template matches (triangular bounds, loop-carried updates,
+    data-dependent branches) run as NVRTC-specialised VM programs: buffers
+    and tally bit-identical to the oracle."""
+    import paper_2307_16080_b200 as b2
+
+    src, key = _irregular_src(seed)
+    fn = bk._capture_from_source(src, "irr_r", {}, key)
+    _, got, t_got, _ = harness.run_engine(b2.engine, fn, None, "sequential", seed)
+    plan = list(b2.engine.last_plan)
+    oracle.build()
+    _, want, t_want, _ = harness.run_engine(oracle, fn, None, "sequential", seed)
+    assert t_got == t_want, (src, plan)
+    for g, w in zip(got, want):
+        assert g.data.tobytes() == w.data.tobytes(), (src, plan)
