@@ -3,7 +3,10 @@
 //
 // Each CTA stages its own half of the operands — 128 rows of A and 128 rows of
 // B^T per 128-byte K slice — so per SM the TMA traffic per MMA is half of the
-// single-CTA 128x256 kernel's.  Only the leader CTA (cluster rank 0) issues
+// single-CTA 128x256 kernel's.  B comes either K-major (the transposed N x K
+// pack) or, for bf16, MN-major straight from its K x N layout (BMN: one 3-D
+// TMA box of two 64-wide N chunks x 64 K rows per stage, descriptor LBO = the
+// 8 KB chunk stride, SBO = 1 KB per 8 K rows, instruction bit 16 set).  Only the leader CTA (cluster rank 0) issues
 // MMAs; both CTAs' TMA loads complete on the leader's full-barrier, MMA
 // commits are multicast to both CTAs' empty / tmem-full barriers, and both
 // CTAs' epilogues release the accumulator buffer on the leader's tmem-empty
