@@ -43,3 +43,16 @@ def test_verify_and_opt_match_reference(tmp_path):
     finally:
         machine._engine = saved
         b2.configure(precision="exact")
+
+
+def test_device_mode_argument_rewrite():
+    """`run --mode b200[:precision]` maps to the reference's
+    sequential mode with the engine's precision set; other modes untouched."""
+    from paper_2307_16080_b200.__main__ import _device_mode
+
+    assert _device_mode(["run", "--mode", "b200", "--func", "f"], "exact") == (
+        ["run", "--mode", "sequential", "--func", "f"], "exact")
+    assert _device_mode(["run", "--mode=b200:bf16"], "exact") == (
+        ["run", "--mode", "sequential"], "bf16")
+    assert _device_mode(["run", "--mode", "worksharing:2"], "tf32") == (
+        ["run", "--mode", "worksharing:2"], "tf32")

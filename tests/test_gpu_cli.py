@@ -78,3 +78,33 @@ def test_cli_run_matches_reference(tmp_path, fn, mode):
     assert s_b == s_r
     for f in sorted(os.listdir(dir_r)):
         assert open(os.path.join(dir_b, f)).read() == open(os.path.join(dir_r, f)).read(), f
+
+
+def test_cli_run_device_mode_matches_reference(tmp_path):
+    """`run --mode b200` writes what the reference's `run --mode sequential`
+    writes (buffers byte-identical, stats equal but wall time)."""
+    import paper_2307_16080_b200.__main__ as ours
+    from staircase import cli
+    from staircase.interp import machine
+
+    fn = corpus.matmul_96
+    sir, args = _write_inputs(str(tmp_path), fn, seed=7)
+    saved = machine._engine
+    results = {}
+    for tag, main, mode in (("ref", cli.main, "sequential"), ("b200", ours.main, "b200")):
+        outdir = os.path.join(str(tmp_path), tag)
+        argv = ["run", "--input", sir, "--func", fn.__name__, "--mode", mode, "--out", outdir,
+                "--args", *args]
+        try:
+            results[tag] = _run(main, argv) + (outdir,)
+        finally:
+            machine._engine = saved
+    (rc_r, out_r, _, dir_r), (rc_b, out_b, _, dir_b) = results["ref"], results["b200"]
+    assert rc_r == rc_b == 0
+    s_r, s_b = json.loads(out_r), json.loads(out_b)
+    for s in (s_r, s_b):
+        s.pop("wall_time")
+        s["outputs"] = [os.path.basename(p) for p in s["outputs"]]
+    assert s_b == s_r
+    for f in sorted(os.listdir(dir_r)):
+        assert open(os.path.join(dir_b, f)).read() == open(os.path.join(dir_r, f)).read(), f
