@@ -74,6 +74,11 @@ struct Args {
   int init;
   T init_value;
   Addr ad;
+  // linear tile order (ntn > 0): block b computes tile tile_base + b / sub of
+  // the grid of (BM x sub BN) tiles, ntn of them per row, columns
+  // (b % sub) BN .. +BN of it; otherwise the 2-D grid (blockIdx.y, .x)
+  int64_t tile_base = 0, ntn = 0;
+  int sub = 1;
 };
 
 // f32 8x8 micro-tiles are held to 128 registers so two CTAs share an SM:
@@ -81,7 +86,7 @@ struct Args {
 // 12.5 % occupancy, 52 % issue-slot use).
 template <typename T, int TM, int TN>
 struct MinBlocks {
-  static constexpr int value = (sizeof(T) == 4 && TM * TN >= 64) ? 2 : 1;
+  static constexpr int value = (sizeof(T) == 4 && TM * TN >= 32) ? 2 : 1;
 };
 
 // VEC (strided f32 only): A k-contiguous and B n-contiguous with 16-byte
@@ -100,8 +105,15 @@ __global__ void __launch_bounds__(kThreads, MinBlocks<T, TM, TN>::value)
   __shared__ __align__(16) T As[2][BK][BM + PAD];
   __shared__ __align__(16) T Bs[2][BK][BN];
 
-  const int64_t m0 = (int64_t)blockIdx.y * BM;
-  const int64_t n0 = (int64_t)blockIdx.x * BN;
+  int64_t m0, n0;
+  if (g.ntn > 0) {
+    const int64_t tl = g.tile_base + blockIdx.x / g.sub;
+    m0 = (tl / g.ntn) * BM;
+    n0 = (tl % g.ntn) * ((int64_t)BN * g.sub) + (int64_t)(blockIdx.x % g.sub) * BN;
+  } else {
+    m0 = (int64_t)blockIdx.y * BM;
+    n0 = (int64_t)blockIdx.x * BN;
+  }
   const int t = threadIdx.x;
   const int tx = t % TX;
   const int ty = t / TX;
@@ -292,6 +304,47 @@ int launch_tile(const Args<T, Addr> &g, void *stream) {
   return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
 }
 
+template <typename T, typename Addr, int BM, int BN, int TM, int TN, bool VEC = false>
+int launch_linear(const Args<T, Addr> &g, int64_t blocks, void *stream) {
+  if (blocks <= 0) return B200_OK;
+  if (blocks >= (int64_t(1) << 31)) return B200_EINVAL;
+  contract_exact_kernel<T, Addr, BM, BN, TM, TN, VEC>
+      <<<(unsigned)blocks, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(g);
+  return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
+}
+
+inline int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+// 128 x 128 tiles.  Optional balanced last round (B200_GEMM_EXACT_TAIL=1):
+// 2 CTAs per SM give S slots; T = q S + r tiles run as q full rounds of whole
+// tiles and, when 2 r <= S, one round of 2 r half-width (128 x 64, 8 x 4 per
+// thread) tiles.  Measured at 4096^3 (1024 tiles, S = 296): no gain (5.12 vs
+// 5.08 ms) — a CTA left alone on an SM in the last round runs faster, so the
+// last round is not a whole round's time — hence off by default.  Every
+// output keeps its full-K chain either way.
+template <typename Addr, bool VEC>
+int launch_128(const Args<float, Addr> &g, void *stream) {
+  const int64_t tn = (g.N + 127) / 128, tiles = ((g.M + 127) / 128) * tn;
+  const int64_t slots = 2 * (int64_t)sm_count();
+  const int64_t rem = tiles % slots;
+  if (tiles <= slots || rem == 0 || 2 * rem > slots || !getenv("B200_GEMM_EXACT_TAIL"))
+    return launch_tile<float, Addr, 128, 128, 8, 8, VEC>(g, stream);
+  Args<float, Addr> g1 = g, g2 = g;
+  g1.ntn = tn, g1.tile_base = 0, g1.sub = 1;
+  g2.ntn = tn, g2.tile_base = tiles - rem, g2.sub = 2;
+  const int rc = launch_linear<float, Addr, 128, 128, 8, 8, VEC>(g1, tiles - rem, stream);
+  if (rc != B200_OK) return rc;
+  return launch_linear<float, Addr, 128, 64, 8, 4, VEC>(g2, 2 * rem, stream);
+}
+
 // 16-byte staging applies (see contract_exact_kernel's VEC)
 inline bool vec_ok(const Args<float, Strided> &g) {
   const auto &a = g.ad;
@@ -312,8 +365,8 @@ int launch(const Args<float, Addr> &g, void *stream) {
   if (big_ctas < 148) return launch_tile<float, Addr, 64, 64, 4, 4>(g, stream);
   if (g.N <= 64) return launch_tile<float, Addr, 256, 64, 8, 8>(g, stream);
   if constexpr (std::is_same<Addr, Strided>::value)
-    if (vec_ok(g)) return launch_tile<float, Addr, 128, 128, 8, 8, true>(g, stream);
-  return launch_tile<float, Addr, 128, 128, 8, 8>(g, stream);
+    if (vec_ok(g)) return launch_128<Addr, true>(g, stream);
+  return launch_128<Addr, false>(g, stream);
 }
 
 template <typename Addr>

@@ -235,3 +235,29 @@ def test_random_irregular_nests_exact(seed):
     assert t_got == t_want, (src, plan)
     for g, w in zip(got, want):
         assert g.data.tobytes() == w.data.tobytes(), (src, plan)
+
+
+@pytest.mark.parametrize("shape", [(4096, 4096, 8), (3900, 4096, 12), (4096, 4000, 5)])
+def test_exact_gemm_balanced_last_round(shape, monkeypatch):
+    """Shapes whose 128 x 128 tile count leaves a short last round run that
+    round as half-width tiles (gemm_exact.cu launch_128): C must still be
+    the reference's per-op-rounded f32 chain, bit for bit (numpy float32
+    emulation of the chain in k order)."""
+    import paper_2307_16080_b200 as b2
+    from staircase.interp import Buffer, machine
+
+    monkeypatch.setenv("B200_GEMM_EXACT_TAIL", "1")   # the split is opt-in
+    M, N, K = shape
+    fn = bk._capture_from_source(MM.format(M=M, N=N, K=K), "mm_r", {}, f"{M}_{N}_{K}")
+    rng = np.random.default_rng(M + N + K)
+    A = rng.uniform(-1, 1, (M, K)).astype(np.float32)
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    C = rng.uniform(-1, 1, (M, N)).astype(np.float32)
+    args = [Buffer(x.shape, "f32", x.tobytes()) for x in (A, B, C)]
+    machine.run(fn.module, "mm_r", args, engine=b2.engine)
+    assert b2.engine.last_plan[-1][0] == "gemm_f32_exact"
+    want = C.copy()
+    for k in range(K):
+        want = (want + (A[:, k, None] * B[None, k, :]).astype(np.float32)).astype(np.float32)
+    got = np.frombuffer(args[2].data, dtype=np.float32).reshape(M, N)
+    assert np.array_equal(got.view(np.int32), want.view(np.int32))
