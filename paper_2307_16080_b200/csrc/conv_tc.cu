@@ -598,6 +598,87 @@ __global__ void __launch_bounds__(256) pack_nhwc_tma_kernel(
   if (threadIdx.x == 0) bulk_wait_all();
 }
 
+// All-bulk variant for whole-plane lines (the usual dense NCHW input): the
+// unit's [64 channels][128 pixels] f32 block arrives by one TMA load (rows of
+// 512 bytes; pixels past the plane and channels past C zero-filled, which is
+// the channel padding), double-buffered; each thread reads its 4 pixels' 8
+// channels from shared memory (consecutive pixels across lanes: no bank
+// conflicts), converts, and assembles the swizzled bf16 tile that one TMA
+// store writes back.  No global loads by threads: the HBM stream is all TMA.
+constexpr int BULK_PX = 128;
+__global__ void __launch_bounds__(256) pack_nhwc_bulk_kernel(
+    const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, int len,
+    int cp, int64_t lines) {
+  constexpr int IN_TILE = 64 * BULK_PX * 4, OUT_TILE = BULK_PX * 128;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  unsigned char *gbase = smem_raw + (base - smem_u32(smem_raw));
+  const uint32_t sIn = base, sOut = base + 2 * IN_TILE;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + 2 * IN_TILE + 2 * OUT_TILE);
+  const uint32_t bar0 = smem_u32(bars);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int passes = cp / 64;
+  const int blocks = (len + BULK_PX - 1) / BULK_PX;
+  const int64_t units = lines * blocks * passes;
+  auto coords = [&](int64_t u, int64_t &line, int &p0, int &c0) {
+    const int64_t lb = u / passes;
+    c0 = (int)(u - lb * passes) * 64;
+    line = lb / blocks;
+    p0 = (int)(lb - line * blocks) * BULK_PX;
+  };
+  auto issue = [&](int64_t u, int st) {
+    int64_t line;
+    int p0, c0;
+    coords(u, line, p0, c0);
+    mbar_expect_tx(bar0 + 8u * st, IN_TILE);
+    tma_load_4d(&tin, bar0 + 8u * st, sIn + st * IN_TILE, p0, c0, (int32_t)line, 0);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(bar0, 1);
+    mbar_init(bar0 + 8, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t u0 = blockIdx.x, step = gridDim.x;
+  if (threadIdx.x == 0) {
+    if (u0 < units) issue(u0, 0);
+    if (u0 + step < units) issue(u0 + step, 1);
+  }
+  int st = 0, ob = 0;
+  uint32_t ph = 0;
+  for (int64_t u = u0; u < units; u += step) {
+    mbar_wait(bar0 + 8u * st, ph);
+    if (threadIdx.x == 0) bulk_wait_read<1>();   // the store of out tile ob's last use has read it
+    __syncthreads();
+    const float *in = reinterpret_cast<const float *>(gbase + st * IN_TILE);   // [64][128]
+    unsigned char *tile = gbase + 2 * IN_TILE + ob * OUT_TILE;
+#pragma unroll
+    for (int i = 0; i < BULK_PX / 32; ++i) {
+      const int p = lane + 32 * i;
+      __nv_bfloat162 h[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        h[j] = __floats2bfloat162_rn(in[(8 * warp + 2 * j) * BULK_PX + p],
+                                     in[(8 * warp + 2 * j + 1) * BULK_PX + p]);
+      *reinterpret_cast<uint4 *>(tile + p * 128 + ((warp ^ (p & 7)) << 4)) =
+          *reinterpret_cast<uint4 *>(h);
+    }
+    fence_proxy_async();
+    __syncthreads();   // input stage st consumed, out tile ob complete
+    if (threadIdx.x == 0) {
+      int64_t line;
+      int p0, c0;
+      coords(u, line, p0, c0);
+      tma_store_4d(&tout, sOut + ob * OUT_TILE, c0, p0, (int32_t)line, 0);
+      bulk_commit();
+      if (u + 2 * step < units) issue(u + 2 * step, st);
+    }
+    ob ^= 1;
+    if (++st == 2) { st = 0; ph ^= 1; }
+  }
+  if (threadIdx.x == 0) bulk_wait_all();
+}
+
 // FCHW f32 weights -> [F][KH][KW][cp] bf16 (K order: tap, channel).
 // One thread per destination element; 32-bit index math (the tensor is at
 // most F * KH * KW * cp < 2^31 elements, host-checked).
@@ -728,9 +809,37 @@ extern "C" int b200_pack_conv_input(const float *src, const int64_t *sstr, void 
   const cuuint64_t strides[3] = {(cuuint64_t)(cp * 2), (cuuint64_t)(len * cp * 2),
                                  (cuuint64_t)(lines * len * cp * 2)};
   const cuuint32_t box[4] = {64, 32 * PACK_WI, 1, 1};
-  if (!getenv("B200_PACK_OLD") && (reinterpret_cast<uintptr_t>(dst) & 15) == 0 &&
-      make_map_4d(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, dst, dims, strides, box,
+  const bool tma_out = !getenv("B200_PACK_OLD") && (reinterpret_cast<uintptr_t>(dst) & 15) == 0 &&
+                       make_map_4d(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, dst, dims, strides,
+                                   box, CU_TENSOR_MAP_SWIZZLE_128B);
+  // all-bulk loads: whole-plane lines with unit pixel stride and 16-byte
+  // channel / image strides, viewed as [nb][C][len] f32
+  CUtensorMap imap;
+  const cuuint64_t idims[4] = {(cuuint64_t)len, (cuuint64_t)c, (cuuint64_t)nb, 1};
+  const cuuint64_t istr[3] = {(cuuint64_t)(sstr[1] * 4), (cuuint64_t)(sstr[0] * 4),
+                              (cuuint64_t)(nb * sstr[0] * 4)};
+  const cuuint32_t ibox[4] = {BULK_PX, 64, 1, 1};
+  const cuuint32_t obox[4] = {64, BULK_PX, 1, 1};
+  CUtensorMap omap;
+  if (tma_out && plane && sstr[3] == 1 && sstr[1] % 4 == 0 && sstr[0] % 4 == 0 &&
+      (reinterpret_cast<uintptr_t>(src) & 15) == 0 && !getenv("B200_PACK_NOBULK") &&
+      make_map_4d(&imap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, src, idims, istr, ibox,
+                  CU_TENSOR_MAP_SWIZZLE_NONE) &&
+      make_map_4d(&omap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, dst, dims, strides, obox,
                   CU_TENSOR_MAP_SWIZZLE_128B)) {
+    const int64_t bunits = lines * ((len + BULK_PX - 1) / BULK_PX) * (cp / 64);
+    const int smem = 1024 + 2 * 64 * BULK_PX * 4 + 2 * BULK_PX * 128 + 64;
+    cudaFuncSetAttribute(pack_nhwc_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         smem);
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pack_nhwc_bulk_kernel, 256, smem);
+    int64_t blocks = (int64_t)num_sms() * (per_sm < 1 ? 1 : per_sm);
+    if (blocks > bunits) blocks = bunits;
+    pack_nhwc_bulk_kernel<<<(unsigned)blocks, 256, smem, static_cast<cudaStream_t>(stream)>>>(
+        imap, omap, len, (int)cp, lines);
+    return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
+  }
+  if (tma_out) {
     const int smem = 1024 + 2 * 32 * PACK_WI * 128;
     auto kernel = pack_nhwc_tma_kernel<PACK_WI>;
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
