@@ -23,6 +23,7 @@ CASES = [
     (1, 16, 32, 20, 13, 3, 3),      # Wo = 13: output rows not 16-byte multiples
     (2, 64, 128, 18, 20, 3, 3),     # F = 128 3x3: unmerged 16 x 8 tiling
     (1, 32, 32, 12, 21, 5, 5),      # 5x5 merged into N = 160
+    (2, 100, 64, 14, 14, 3, 3),     # C = 100: second channel block zero-padded by the TMA pack
 ]
 
 
