@@ -292,7 +292,8 @@ def load_traffic(key):
 KERNEL_OF = {"b200_gemm_tc": "gemm", "b200_gemm_f32_exact": "gemm",
              "b200_contract_exact": "contract", "b200_map_f32": "map", "b200_vm_run": "vm",
              "b200_pack_operand": "pack", "b200_conv2d_tc": "conv",
-             "b200_pack_conv_input": "pack", "b200_conv2d_exact": "conv",
+             "b200_pack_conv_input": "pack", "b200_pack_conv": "pack",
+             "b200_conv2d_exact": "conv",
              "b200_jit_launch": "map"}
 TENSOR_KERNELS = ("b200_gemm_tc", "b200_conv2d_tc")
 # entry points that run the same kernel (timed together as one family)

@@ -193,6 +193,15 @@ int b200_pack_conv_input(const float *src, const int64_t *sstr, void *dst, int64
                          int64_t c, int64_t h, int64_t w, int64_t cp, void *stream);
 int b200_pack_conv_weight(const float *src, const int64_t *sstr, void *dst, int64_t f,
                           int64_t c, int64_t kh, int64_t kw, int64_t cp, void *stream);
+/*
+ * b200_pack_conv_input and b200_pack_conv_weight in one launch when the
+ * input takes the all-bulk pack (dense planes, 16-byte channel / image
+ * strides), else the two packs back to back.  Same arguments as the two.
+ */
+int b200_pack_conv(const float *src, const int64_t *sstr, void *dst, int64_t nb, int64_t c,
+                   int64_t h, int64_t w, int64_t cp, const float *ker, const int64_t *wstr,
+                   void *wdst, int64_t f, int64_t kh, int64_t kw, void *stream);
+
 int b200_conv2d_tc(const void *in_nhwc, const void *wt, float *out, const int64_t *out_strides,
                    int64_t nb, int64_t cp, int64_t hp, int64_t wp, int64_t f, int64_t ho,
                    int64_t wo, int64_t kh, int64_t kw, int32_t init, float init_value,

@@ -606,9 +606,29 @@ __global__ void __launch_bounds__(256) pack_nhwc_tma_kernel(
 // conflicts), converts, and assembles the swizzled bf16 tile that one TMA
 // store writes back.  No global loads by threads: the HBM stream is all TMA.
 constexpr int BULK_PX = 128;
+// FCHW f32 weights -> [F][KH][KW][cp] bf16, optionally packed by the same
+// launch as the input (b200_pack_conv: the weights are a few hundred KB, so
+// their share of each CTA hides behind its first TMA load)
+struct WPack {
+  const float *src;
+  int64_t sF, sC, sKH, sKW;
+  __nv_bfloat16 *dst;   // null: no weights in this launch
+  int F, C, KH, KW, cp;
+};
+__device__ __forceinline__ void pack_weights(const WPack &w, int64_t first, int64_t stride) {
+  const int total = w.F * w.KH * w.KW * w.cp, taps = w.KH * w.KW;
+  for (int64_t i = first; i < total; i += stride) {
+    const int c = (int)(i % w.cp), ft = (int)(i / w.cp);
+    const int tap = ft % taps, f = ft / taps;
+    const int ki = tap / w.KW, kj = tap - ki * w.KW;
+    w.dst[i] = __float2bfloat16_rn(
+        c < w.C ? w.src[f * w.sF + c * w.sC + ki * w.sKH + kj * w.sKW] : 0.f);
+  }
+}
+
 __global__ void __launch_bounds__(256) pack_nhwc_bulk_kernel(
     const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, int len,
-    int cp, int64_t lines) {
+    int cp, int64_t lines, WPack wp) {
   constexpr int IN_TILE = 64 * BULK_PX * 4, OUT_TILE = BULK_PX * 128;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -644,6 +664,9 @@ __global__ void __launch_bounds__(256) pack_nhwc_bulk_kernel(
     if (u0 < units) issue(u0, 0);
     if (u0 + step < units) issue(u0 + step, 1);
   }
+  if (wp.dst)   // while the first loads are in flight
+    pack_weights(wp, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                 (int64_t)gridDim.x * blockDim.x);
   int st = 0, ob = 0;
   uint32_t ph = 0;
   for (int64_t u = u0; u < units; u += step) {
@@ -793,8 +816,12 @@ int launch_conv(const void *in_nhwc, const void *wt, float *out, ConvGeo &g, cud
 
 }  // namespace
 
-extern "C" int b200_pack_conv_input(const float *src, const int64_t *sstr, void *dst, int64_t nb,
-                                    int64_t c, int64_t h, int64_t w, int64_t cp, void *stream) {
+namespace {
+// The input pack; `wp` (dst non-null) is folded into the launch when the
+// all-bulk kernel applies (*wp_done set), else left to the caller.
+int pack_input(const float *src, const int64_t *sstr, void *dst, int64_t nb, int64_t c,
+               int64_t h, int64_t w, int64_t cp, cudaStream_t stream, WPack wp, bool *wp_done) {
+  *wp_done = false;
   if (nb <= 0 || h <= 0 || w <= 0 || cp < c || cp % 64 || w > PACK_MAXW) return B200_EINVAL;
   // rows contiguous (h stride = W * w stride): one line per image plane
   const bool plane = sstr[2] == w * sstr[3];
@@ -835,8 +862,9 @@ extern "C" int b200_pack_conv_input(const float *src, const int64_t *sstr, void 
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pack_nhwc_bulk_kernel, 256, smem);
     int64_t blocks = (int64_t)num_sms() * (per_sm < 1 ? 1 : per_sm);
     if (blocks > bunits) blocks = bunits;
-    pack_nhwc_bulk_kernel<<<(unsigned)blocks, 256, smem, static_cast<cudaStream_t>(stream)>>>(
-        imap, omap, len, (int)cp, lines);
+    pack_nhwc_bulk_kernel<<<(unsigned)blocks, 256, smem, stream>>>(imap, omap, len, (int)cp,
+                                                                  lines, wp);
+    *wp_done = wp.dst != nullptr;
     return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
   }
   if (tma_out) {
@@ -860,6 +888,30 @@ extern "C" int b200_pack_conv_input(const float *src, const int64_t *sstr, void 
       src, sstr[0], sstr[1], sstr[2], sstr[3], static_cast<__nv_bfloat16 *>(dst), (int)c,
       lines_per_img, len, (int)cp, lines);
   return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
+}
+}  // namespace
+
+extern "C" int b200_pack_conv_input(const float *src, const int64_t *sstr, void *dst, int64_t nb,
+                                    int64_t c, int64_t h, int64_t w, int64_t cp, void *stream) {
+  bool unused;
+  return pack_input(src, sstr, dst, nb, c, h, w, cp, static_cast<cudaStream_t>(stream),
+                    WPack{}, &unused);
+}
+
+extern "C" int b200_pack_conv(const float *src, const int64_t *sstr, void *dst, int64_t nb,
+                              int64_t c, int64_t h, int64_t w, int64_t cp, const float *ker,
+                              const int64_t *swt, void *wdst, int64_t f, int64_t kh, int64_t kw,
+                              void *stream) {
+  const int64_t total = f * kh * kw * cp;
+  if (total <= 0 || cp % 64) return B200_EINVAL;
+  if (total >= (int64_t(1) << 31)) return B200_EUNSUPPORTED;
+  WPack wp{ker, swt[0], swt[1], swt[2], swt[3], static_cast<__nv_bfloat16 *>(wdst), (int)f,
+           (int)c, (int)kh, (int)kw, (int)cp};
+  bool done = false;
+  const int rc = pack_input(src, sstr, dst, nb, c, h, w, cp, static_cast<cudaStream_t>(stream),
+                            wp, &done);
+  if (rc != B200_OK || done) return rc;
+  return b200_pack_conv_weight(ker, swt, wdst, f, c, kh, kw, cp, stream);
 }
 
 extern "C" int b200_pack_conv_weight(const float *src, const int64_t *sstr, void *dst, int64_t f,

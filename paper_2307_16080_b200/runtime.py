@@ -63,6 +63,8 @@ SIGNATURES = {
     "b200_gemm_tc_kn": [_I32, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I32, _F32, _P,
                         _I64, _P, _I64, _P],
     "b200_pack_conv_input": [_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _P],
+    "b200_pack_conv": [_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _P, _P, _P, _I64, _I64, _I64,
+                       _P],
     "b200_pack_conv_weight": [_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _P],
     "b200_conv2d_tc": [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64,
                        _I32, _F32, _P],
@@ -749,19 +751,24 @@ class DeviceBackend:
         if self.recording is not None:
             self.recording.keep.append((sin, sw, sout))
         self.keep(sin, sw, sout)
-        self.call("b200_pack_conv_weight", P(ker.data_ptr()), sw, P(xw.data_ptr()), cv.f, cv.c,
-                  cv.kh, cv.kw, cp, s.stream_ptr)
+        first = [True]   # the first input pack also packs the weights (one launch)
 
         def launch(inp_ptr, out_ptr, nb):
             xin = workspace(2, "bfloat16", nb * cv.hp * cv.wp, cp)
-            self.call("b200_pack_conv_input", P(inp_ptr), sin, P(xin.data_ptr()), nb, cv.c,
-                      cv.hp, cv.wp, cp, s.stream_ptr)
+            if first[0]:
+                first[0] = False
+                self.call("b200_pack_conv", P(inp_ptr), sin, P(xin.data_ptr()), nb, cv.c,
+                          cv.hp, cv.wp, cp, P(ker.data_ptr()), sw, P(xw.data_ptr()), cv.f,
+                          cv.kh, cv.kw, s.stream_ptr)
+            else:
+                self.call("b200_pack_conv_input", P(inp_ptr), sin, P(xin.data_ptr()), nb, cv.c,
+                          cv.hp, cv.wp, cp, s.stream_ptr)
             self.call("b200_conv2d_tc", P(xin.data_ptr()), P(xw.data_ptr()), P(out_ptr), sout,
                       nb, cp, cv.hp, cv.wp, cv.f, cv.ho, cv.wo, cv.kh, cv.kw, init, init_value,
                       s.stream_ptr)
 
         self._conv_run(cv, 4, init, last_writer, launch)
-        return ["pack_conv_weight", "pack_conv_input", "conv2d_tc_bf16"]
+        return ["pack_conv", "conv2d_tc_bf16"]
 
     def _map_stream_plan(self, m):
         """Row panels for a pointwise plan over whole dense buffers (one
