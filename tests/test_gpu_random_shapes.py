@@ -261,3 +261,52 @@ def test_exact_gemm_balanced_last_round(shape, monkeypatch):
         want = (want + (A[:, k, None] * B[None, k, :]).astype(np.float32)).astype(np.float32)
     got = np.frombuffer(args[2].data, dtype=np.float32).reshape(M, N)
     assert np.array_equal(got.view(np.int32), want.view(np.int32))
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_conv_bf16_within_bound(seed):
+    """The tensor-core conv (F in {32, 64, 128}; 1x1, 3x3, 5x5; random
+    batch, channels and sizes) on bf16-representable inputs: every output
+    within 2 K 2^-24 sum|x w| + 4 2^-24 |want| of the float64 conv."""
+    import torch
+    import torch.nn.functional as Fn
+
+    import paper_2307_16080_b200 as b2
+    from staircase.interp import Buffer, machine
+
+    r = random.Random(11000 + seed)
+    f, (kh, kw) = r.choice([(32, (3, 3)), (64, (3, 3)), (32, (5, 5)), (64, (1, 1)),
+                            (128, (1, 1)), (128, (3, 3))])
+    nb, c = r.randint(1, 3), r.choice([8, 16, 64, 70, 128])
+    ho, wo = r.randint(1, 24), r.randint(1, 40)
+    hp, wp = ho + kh - 1, wo + kw - 1
+    shp = dict(nb=nb, c=c, f=f, ho=ho, wo=wo, hp=hp, wp=wp, kh=kh, kw=kw)
+    fn = bk._capture_from_source(CONV.format(**shp), "conv_r", {},
+                                 "_".join(map(str, shp.values())))
+    g = torch.Generator().manual_seed(seed)
+    x = (torch.rand(nb, c, hp, wp, generator=g) * 2 - 1).bfloat16().float()
+    w = (torch.rand(f, c, kh, kw, generator=g) * 2 - 1).bfloat16().float()
+    o = torch.rand(nb, f, ho, wo, generator=g) * 2 - 1
+    args = [Buffer(tuple(t.shape), "f32", t.numpy().tobytes()) for t in (x, w, o)]
+    b2.configure(precision="bf16")
+    try:
+        machine.run(fn.module, "conv_r", args, engine=b2.engine)
+    finally:
+        b2.configure(precision="exact")
+    got = torch.frombuffer(args[2].data, dtype=torch.float32).reshape(nb, f, ho, wo).double()
+    want = o.double() + Fn.conv2d(x.double(), w.double())
+    mag = Fn.conv2d(x.double().abs(), w.double().abs())
+    bound = 2 * c * kh * kw * 2.0 ** -24 * mag + 4 * 2.0 ** -24 * want.abs() + 1e-30
+    # the tensor-core kernel keeps the whole filter resident in shared memory
+    # (runtime.conv_tc_supported); e.g. 5x5 over two 64-channel blocks does
+    # not fit and takes the exact kernel
+    from types import SimpleNamespace
+
+    from paper_2307_16080_b200.runtime import conv_tc_supported
+
+    fits = conv_tc_supported(SimpleNamespace(c=c, f=f, kh=kh, kw=kw, wo=wo))
+    kernels = {"conv2d_tc_bf16" if fits else "conv2d_exact"}
+    if kh == kw == 1:
+        kernels.add("gemm_tc_bf16")   # a 1x1 conv with a single row/column is a strided GEMM
+    assert b2.engine.last_plan[-1][0] in kernels, (shp, b2.engine.last_plan)
+    assert ((got - want).abs() <= bound).all(), (shp, b2.engine.last_plan)
