@@ -219,12 +219,17 @@ def irr_r(a: MemRef[({n}, {n}), F32], b: MemRef[({n}, {n}), F32]):{body}
     return src, f"{n}_{seed}"
 
 
+@pytest.mark.parametrize("native", [True, False], ids=["native", "interpreter"])
 @pytest.mark.parametrize("seed", range(15))
-def test_random_irregular_nests_exact(seed):
+def test_random_irregular_nests_exact(seed, native, monkeypatch):
     """Nests no template matches (triangular bounds, loop-carried updates,
-    data-dependent branches) run as NVRTC-specialised VM programs: buffers
-    and tally bit-identical to the oracle."""
+    data-dependent branches) run as NVRTC-specialised VM programs — or, with
+    the native tier off, on the device VM interpreter: buffers and tally
+    bit-identical to the oracle either way."""
     import paper_2307_16080_b200 as b2
+    from paper_2307_16080_b200 import native as nat
+
+    monkeypatch.setattr(nat, "ENABLED", native)
 
     src, key = _irregular_src(seed)
     fn = bk._capture_from_source(src, "irr_r", {}, key)
