@@ -162,14 +162,17 @@ def ew_r(a: MemRef[({rows}, {cols}), F32], b: MemRef[({rows}, {cols}), F32],
     return src, f"{rows}_{cols}_{seed}"
 
 
+@pytest.mark.parametrize("jit_on", [True, False], ids=["nvrtc", "map_f32"])
 @pytest.mark.parametrize("seed", range(20))
-def test_random_elementwise_exact(seed):
+def test_random_elementwise_exact(seed, jit_on, monkeypatch):
     """Random f32 expression trees (+ - * / and constants, depth <= 3) over
     random shapes, as pointwise NVRTC kernels: bit-identical to the oracle
     (per-op rounding, no contraction).  Quotients of random values can be
     inf or NaN; those compare by class, finite values bit for bit."""
     import paper_2307_16080_b200 as b2
+    from paper_2307_16080_b200 import jit
 
+    monkeypatch.setattr(jit, "ENABLED", jit_on)   # off: the b200_map_f32 kernel
     src, key = _ewise_src(seed)
     fn = bk._capture_from_source(src, "ew_r", {}, key)
     _, got, t_got, _ = harness.run_engine(b2.engine, fn, None, "sequential", seed)
