@@ -232,3 +232,16 @@ def _capture_from_source(src, name, ns, size):
     fn = getattr(mod, name)
     _GEN[key] = fn
     return fn
+
+
+# -- matmul, parallel form (tile-size knob applies: scf-parallel-loop-tiling) ----------
+
+
+@staged
+def mm_par4096(A: MemRef[(4096, 4096), F32], B: MemRef[(4096, 4096), F32],
+               C: MemRef[(4096, 4096), F32]):
+    # BASELINE configs[1] "with reference tile sizes": the parallel form of the
+    # matmul nest, tiled (8, 8) or (4, 16) by the reference's pass
+    for i, k in parallel((0, 0), (4096, 4096)):
+        for j in range(4096):
+            C[i, k] += A[i, j] * B[j, k]

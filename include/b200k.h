@@ -95,6 +95,23 @@ int b200_gemm_f32_exact(const float *A, int64_t sAm, int64_t sAk,
                         const float *bias, int64_t bias_stride, void *stream);
 
 /*
+ * b200_gemm_f32_exact with an explicit CTA tile (cta_m x cta_n outputs per
+ * CTA; <= 0 = the kernel's own choice).  The engine derives it from the tile
+ * sizes of a tiled matmul nest (reference passes/tiling.py:56-80, whose
+ * outer loop gpu-map sends to blocks: passes/gpumap.py:22-34); supported
+ * shapes 128x128, 64x256, 256x64, 64x64, 32x32 (B200_EUNSUPPORTED
+ * otherwise).  Results are identical for every tile: each output's k-chain
+ * is the same.
+ */
+int b200_gemm_f32_exact_tiled(const float *A, int64_t sAm, int64_t sAk,
+                              const float *B, int64_t sBk, int64_t sBn,
+                              float *C, int64_t sCm, int64_t sCn,
+                              int64_t M, int64_t N, int64_t K,
+                              int32_t init, float init_value,
+                              const float *bias, int64_t bias_stride,
+                              int32_t cta_m, int32_t cta_n, void *stream);
+
+/*
  * Exact separable contraction (f32 or f64, per-op rounding, K in nest order):
  *   C[c_m[m] + c_n[n]] = (init ? init_value : C[..]) +
  *                        sum_k A[a_m[m] + a_k[k]] * B[b_k[k] + b_n[n]]  (+ bias)

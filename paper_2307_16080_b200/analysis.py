@@ -190,13 +190,24 @@ def band_ok(region, accesses, band_ids, written):
 
 
 def choose_band(region, links, accesses):
+    """The chain variables to distribute over GPU threads: greedily, in nest
+    order, every variable whose addition keeps the band provably race-free
+    — repeated until nothing changes, since a tiled nest's origin loop
+    (passes/tiling.py:56-80) is only provable once the offset loop of the
+    other dimension is in the band.  Returned in nest order."""
     written = sorted({a.slot for a in accesses if a.write})
+    order = [v.id for link in links for v in link.vars]
     band = []
-    for link in links:
-        for v in link.vars:
-            trial = band + [v.id]
+    changed = True
+    while changed:
+        changed = False
+        for vid in order:
+            if vid in band:
+                continue
+            trial = sorted(band + [vid], key=order.index)
             if band_ok(region, accesses, trial, written):
                 band = trial
+                changed = True
     return band
 
 

@@ -369,6 +369,27 @@ int launch(const Args<float, Addr> &g, void *stream) {
   return launch_128<Addr, false>(g, stream);
 }
 
+// An explicit CTA tile (b200_gemm_f32_exact_tiled): the tile sizes of a
+// tiled nest pick the CTA tile shape (paper_2307_16080_b200/runtime.py
+// cta_tile).  Every shape computes each output's k-chain identically.
+int launch_cta(const Args<float, Strided> &g, int cta_m, int cta_n, void *stream) {
+  if (g.M < 0 || g.N < 0 || g.K < 0) return B200_EINVAL;
+  if (g.M == 0 || g.N == 0) return B200_OK;
+  const bool vec = vec_ok(g);
+  if (cta_m == 128 && cta_n == 128)
+    return vec ? launch_tile<float, Strided, 128, 128, 8, 8, true>(g, stream)
+               : launch_tile<float, Strided, 128, 128, 8, 8>(g, stream);
+  if (cta_m == 64 && cta_n == 256)
+    return vec ? launch_tile<float, Strided, 64, 256, 8, 8, true>(g, stream)
+               : launch_tile<float, Strided, 64, 256, 8, 8>(g, stream);
+  if (cta_m == 256 && cta_n == 64)
+    return vec ? launch_tile<float, Strided, 256, 64, 8, 8, true>(g, stream)
+               : launch_tile<float, Strided, 256, 64, 8, 8>(g, stream);
+  if (cta_m == 64 && cta_n == 64) return launch_tile<float, Strided, 64, 64, 4, 4>(g, stream);
+  if (cta_m == 32 && cta_n == 32) return launch_tile<float, Strided, 32, 32, 2, 2>(g, stream);
+  return B200_EUNSUPPORTED;
+}
+
 template <typename Addr>
 int launch(const Args<double, Addr> &g, void *stream) {
   if (g.M < 0 || g.N < 0 || g.K < 0) return B200_EINVAL;
@@ -386,6 +407,18 @@ extern "C" int b200_gemm_f32_exact(const float *A, int64_t sAm, int64_t sAk, con
   Args<float, Strided> g{A, B, C, bias, bias_stride, M, N, K, init, init_value,
                          Strided{sAm, sAk, sBk, sBn, sCm, sCn, sAk == 1, sBn == 1}};
   return launch(g, stream);
+}
+
+extern "C" int b200_gemm_f32_exact_tiled(const float *A, int64_t sAm, int64_t sAk,
+                                         const float *B, int64_t sBk, int64_t sBn, float *C,
+                                         int64_t sCm, int64_t sCn, int64_t M, int64_t N,
+                                         int64_t K, int32_t init, float init_value,
+                                         const float *bias, int64_t bias_stride, int32_t cta_m,
+                                         int32_t cta_n, void *stream) {
+  Args<float, Strided> g{A, B, C, bias, bias_stride, M, N, K, init, init_value,
+                         Strided{sAm, sAk, sBk, sBn, sCm, sCn, sAk == 1, sBn == 1}};
+  if (cta_m <= 0 || cta_n <= 0) return launch(g, stream);
+  return launch_cta(g, cta_m, cta_n, stream);
 }
 
 extern "C" int b200_contract_exact(int32_t dtype, const void *A, const int64_t *a_m,

@@ -57,14 +57,20 @@ SHADOW = os.environ.get("B200_SHADOW", "1") != "0"
 # Row-panel pipelining of the host copies of large contractions / convs
 # (runtime.Staging.stream_rows; B200_STREAM_IO=0 disables, for A/B tests).
 STREAM_IO = os.environ.get("B200_STREAM_IO", "1") != "0"
+# A bf16 / tf32 request a contraction cannot honour (no strided GEMM view,
+# unaligned K, conv shape outside the tcgen05 kernel) runs exact f32 with a
+# runtime.PrecisionFallback warning; strict makes it PrecisionUnavailable.
+STRICT = os.environ.get("B200_STRICT", "0") == "1"
 
 # kernel choice of the last run (tests and bench inspect these)
 last_plan = []
 
 
-def configure(precision=None, fuse=None, shadow=None):
+def configure(precision=None, fuse=None, shadow=None, strict=None):
     """Select the contraction precision / fusion for subsequent runs."""
-    global PRECISION, FUSE, SHADOW
+    global PRECISION, FUSE, SHADOW, STRICT
+    if strict is not None:
+        STRICT = bool(strict)
     if precision is not None:
         if precision not in ("exact", "tf32", "bf16"):
             raise ValueError(f"unknown precision {precision!r}")
@@ -73,7 +79,7 @@ def configure(precision=None, fuse=None, shadow=None):
         FUSE = bool(fuse)
     if shadow is not None:
         SHADOW = bool(shadow)
-    return {"precision": PRECISION, "fuse": FUSE, "shadow": SHADOW}
+    return {"precision": PRECISION, "fuse": FUSE, "shadow": SHADOW, "strict": STRICT}
 
 
 class ExecContext:
@@ -306,6 +312,13 @@ class _Run:
                 if it.shadow_in or it.shadow_out:
                     used_in, made_out = getattr(self.be, "last_shadow", (False, False))
                     fused += ["A<-shadow"] * used_in + ["C->shadow"] * made_out
+                cta = getattr(self.be, "last_cta", None)
+                if cta is not None:
+                    tm, tn = g.tiles
+                    fused.append(f"tile{tm or 1}x{tn or 1}->cta{cta[0]}x{cta[1]}")
+                note = getattr(self.be, "last_note", None)
+                if note:
+                    fused.append(note)
                 self.plan.append((kernels[-1], g.M, g.N, g.K) +
                                  ((tuple(fused),) if fused else ()))
             else:

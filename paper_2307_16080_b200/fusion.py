@@ -80,6 +80,22 @@ def _contract_covers(item, buf):
     return g.C is buf and g.M * g.N == _size(buf)
 
 
+def _walk(dims):
+    """(C stride, bias stride, trip) of map dims [(c coef, b coef, trip)] that
+    walk one arithmetic progression (a 2-D nest's single loop, or the origin
+    and offset loops of a tiled one: passes/tiling.py:56-80), else None."""
+    dims = sorted(dims, key=lambda d: abs(d[0]))
+    if not dims:
+        return 0, 0, 1
+    c0, b0, _ = dims[0]
+    ec, eb, trip = c0, b0, 1
+    for c, b, t in dims:
+        if c != ec or b != eb:
+            return None
+        ec, eb, trip = ec * t, eb * t, trip * t
+    return c0, b0, trip
+
+
 def _bias(citem, item):
     """(bias buffer, base, stride) if item adds a per-column vector to the
     strided GEMM output of citem over the whole output."""
@@ -87,7 +103,7 @@ def _bias(citem, item):
     if not isinstance(item, MapItem) or item.m.kind != "ewise" or not g.strided:
         return None
     m = item.m
-    if len(m.buffers) != 3 or len(m.trips) != 2:
+    if len(m.buffers) != 3:
         return None
     o_ld, b_ld, o_st = m.buffers
     prog = m.prog
@@ -99,19 +115,20 @@ def _bias(citem, item):
         return None
     if m.bases[0] != m.bases[2] or m.coefs[0] != m.coefs[2] or not _covers(m, g.C):
         return None
-    if b_ld.dtype != g.C.dtype:
+    if b_ld.dtype != g.C.dtype or m.bases[0] != g.offC:
         return None
-    # identify the map dims with the GEMM's m / n by their stride in C
-    (ci, cj), (ti, tj) = m.coefs[0], m.trips
-    if (ci, ti, cj, tj) == (g.sC[0], g.M, g.sC[1], g.N):
-        m_dim, n_dim = 0, 1
-    elif (cj, tj, ci, ti) == (g.sC[0], g.M, g.sC[1], g.N):
-        m_dim, n_dim = 1, 0
-    else:
+    # the map dims the bias does not move along are the GEMM's m, the others
+    # its n; each side must be one progression with the GEMM's C stride
+    dims = list(zip(m.coefs[0], m.coefs[1], m.trips))
+    mw = _walk([d for d in dims if d[1] == 0])
+    nw = _walk([d for d in dims if d[1] != 0])
+    if mw is None or nw is None:
         return None
-    if m.bases[0] != g.offC or m.coefs[1][m_dim] != 0:
+    if (mw[0], mw[2]) != (g.sC[0], g.M) and not (g.M == 1 and mw[2] == 1):
         return None
-    return b_ld, m.bases[1], m.coefs[1][n_dim]
+    if (nw[0], nw[2]) != (g.sC[1], g.N):
+        return None
+    return b_ld, m.bases[1], nw[1]
 
 
 def fuse(items):

@@ -52,6 +52,8 @@ SIGNATURES = {
                     _I32, _P, _P, _P],
     "b200_gemm_f32_exact": [_P, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64, _I64,
                             _I64, _I64, _I32, _F32, _P, _I64, _P],
+    "b200_gemm_f32_exact_tiled": [_P, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64, _I64,
+                                  _I64, _I64, _I32, _F32, _P, _I64, _I32, _I32, _P],
     "b200_contract_exact": [_I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64,
                             _I32, _I32, _I32, ctypes.c_double, _P, _I64, _P],
     "b200_pack_operand": [_I32, _P, _I64, _I64, _P, _I64, _I64, _P],
@@ -389,9 +391,54 @@ def _direct_call(lib):
     return call
 
 
+def cta_tile(precision, tiles):
+    """The CTA tile a tiled matmul nest runs with, from its tile sizes.
+
+    The reference's tiling pass (passes/tiling.py:56-80) splits each output
+    loop into a parallel origin loop over tiles and a parallel offset loop
+    within one, and its GPU mapping sends the origin loop to blocks and the
+    offset loop to threads (passes/gpumap.py:22-34): a tile is the unit of
+    work one block owns.  Here a tile (tm, tn) of the M and N loops selects
+    the CTA tile shape of the kernel that runs the contraction — by aspect
+    ratio tn / tm, and for the SIMT kernel also by area:
+
+      exact:  tm * tn <= 16 -> 64 x 64;  tn / tm >= 2 -> 64 x 256;
+              tn / tm <= 1/2 -> 256 x 64;  otherwise 128 x 128
+      tcgen05: tn / tm >= 2 -> one CTA, 128 x 256 (cta_group::1);
+               otherwise a CTA pair, 256 x 256 (cta_group::2)
+
+    e.g. the reference tile sizes (8, 8) and (4, 16) map to
+    128 x 128 / 64 x 256 on the exact kernel and 256 x 256 / 128 x 256 on the
+    tensor cores.  Untiled nests (tiles (None, None)) return None: the
+    kernel's own size-based choice.  Results never depend on the choice
+    (exact: identical k-chains; tensor cores: the same MMA k order per tile).
+    """
+    tm, tn = tiles if tiles else (None, None)
+    if tm is None and tn is None:
+        return None
+    tm, tn = tm or 1, tn or 1
+    if precision in ("bf16", "tf32"):
+        return (128, 256) if tn >= 2 * tm else (256, 256)
+    if tm * tn <= 16:
+        return (64, 64)
+    if tn >= 2 * tm:
+        return (64, 256)
+    if tm >= 2 * tn:
+        return (256, 64)
+    return (128, 128)
+
+
+class PrecisionFallback(UserWarning):
+    """A contraction ran at exact f32 although bf16 / tf32 was requested."""
+
+
+class PrecisionUnavailable(RuntimeError):
+    """configure(strict=True): a requested precision cannot be honoured."""
+
+
 def launch_gemm(lib, precision, a_ptr, sA, b_ptr, sB, c_ptr, sC, M, N, K, stream,
                 init=0, init_value=0.0, bias_ptr=None, bias_stride=0, max_ctas=0,
-                variant=0, call=None, a_packed=None, c16=None, b_packed=None):
+                variant=0, call=None, a_packed=None, c16=None, b_packed=None, cta=None):
     """Enqueue C (+)= A.B with the kernel chosen by ``precision``.
 
     Returns the list of kernel names launched (for the launch count).
@@ -400,14 +447,22 @@ def launch_gemm(lib, precision, a_ptr, sA, b_ptr, sB, c_ptr, sC, M, N, K, stream
     a_packed: A already packed (a bf16 shadow, M x K) — its pack is skipped;
     c16: also write C rounded to bf16 (M x N) with b200_gemm_tc_shadow.
     b_packed: B already packed ((tensor, kn) from pack_b) — its pack is skipped.
+    cta: (BM, BN) from cta_tile() — the tiled nest's CTA tile, or None.
     """
     call = call or _direct_call(lib)
     P = ctypes.c_void_p
     if not tc_supported(precision, K):
+        if cta is not None:
+            call("b200_gemm_f32_exact_tiled", P(a_ptr), sA[0], sA[1], P(b_ptr), sB[0], sB[1],
+                 P(c_ptr), sC[0], sC[1], M, N, K, init, init_value,
+                 P(bias_ptr) if bias_ptr else None, bias_stride, cta[0], cta[1], stream)
+            return ["gemm_f32_exact"]
         call("b200_gemm_f32_exact", P(a_ptr), sA[0], sA[1], P(b_ptr), sB[0], sB[1],
              P(c_ptr), sC[0], sC[1], M, N, K, init, init_value,
              P(bias_ptr) if bias_ptr else None, bias_stride, stream)
         return ["gemm_f32_exact"]
+    if cta is not None:
+        variant = 1 if cta == (128, 256) else 2
     kind = 0 if precision == "bf16" else 1
     dt = "bfloat16" if kind == 0 else "float32"
     names = []
@@ -420,7 +475,8 @@ def launch_gemm(lib, precision, a_ptr, sA, b_ptr, sB, c_ptr, sC, M, N, K, stream
     if b_packed is not None:
         Bp, kn = b_packed if isinstance(b_packed, tuple) else (b_packed, False)
     else:
-        Bp, kn = pack_b(lib, precision, b_ptr, sB, N, K, stream, call)
+        Bp, kn = pack_b(lib, precision, b_ptr, sB, N, K, stream, call,
+                        allow_kn=variant != 1)
         names.append("pack_operand")
     if kn:
         call("b200_gemm_tc_kn", kind, P(Ap.data_ptr()), P(Bp.data_ptr()), P(c_ptr), sC[0], sC[1],
@@ -441,7 +497,7 @@ def launch_gemm(lib, precision, a_ptr, sA, b_ptr, sB, c_ptr, sC, M, N, K, stream
 GEMM_KN = os.environ.get("B200_GEMM_KN", "1") != "0"
 
 
-def pack_b(lib, precision, b_ptr, sB, N, K, stream, call=None):
+def pack_b(lib, precision, b_ptr, sB, N, K, stream, call=None, allow_kn=True):
     """Pack B (K x N, strides sB) for the tensor cores (workspace slot 1).
 
     Returns (tensor, kn).  bf16 with N-contiguous rows, N a multiple of 64:
@@ -450,7 +506,7 @@ def pack_b(lib, precision, b_ptr, sB, N, K, stream, call=None):
     operand of b200_gemm_tc."""
     call = call or _direct_call(lib)
     kind = 0 if precision == "bf16" else 1
-    if GEMM_KN and kind == 0 and sB[1] == 1 and N % 64 == 0:
+    if GEMM_KN and allow_kn and kind == 0 and sB[1] == 1 and N % 64 == 0:
         Bp = workspace(1, "bfloat16", K, N)
         call("b200_pack_operand", kind, ctypes.c_void_p(b_ptr), sB[0], sB[1],
              ctypes.c_void_p(Bp.data_ptr()), K, N, stream)
@@ -531,6 +587,8 @@ class DeviceBackend:
         self._shadow = None
         self._shadow_slot = 0
         self.last_shadow = (False, False)   # (A from a shadow, C shadow written)
+        self.last_note = None    # why the last contraction ignored the precision
+        self.last_cta = None     # CTA tile the last contraction's tiles selected
 
     def call(self, name, *args):
         check(getattr(self.stage.lib, name)(*args), name)
@@ -575,6 +633,7 @@ class DeviceBackend:
         """
         s = self.stage
         esz = 4 if g.dtype == "f32" else 8
+        self.last_note = self.last_cta = None
         if bias is None:
             from .templates import conv_view
 
@@ -582,8 +641,19 @@ class DeviceBackend:
             if cv is not None:
                 if precision == "bf16" and g.dtype == "f32" and conv_tc_supported(cv):
                     return self.conv_tc(cv, init, init_value, last_writer)
+                if g.dtype == "f32" and precision != "exact":
+                    self._fallback(precision, "conv shape outside the tcgen05 conv kernel"
+                                   if precision == "bf16" else "no tf32 conv kernel")
                 if conv_exact_supported(cv, esz):
                     return self.conv_exact(cv, g.dtype, init, init_value, last_writer)
+        if g.dtype == "f32" and precision != "exact":
+            if not g.strided:
+                self._fallback(precision, "index maps are not one strided GEMM")
+            elif not tc_supported(precision, g.K):
+                self._fallback(precision, f"K={g.K} rows not 16-byte aligned")
+        cta = cta_tile(precision if g.strided and tc_supported(precision, g.K) else "exact",
+                       getattr(g, "tiles", None))
+        self.last_cta = cta
         bias_ptr = s.tensor(bias).data_ptr() + esz * bias_base if bias is not None else None
         dense_c = (g.strided and g.offC == 0 and tuple(g.sC) == (g.N, 1) and
                    _rows_of(g.C, g.M, g.N))
@@ -596,7 +666,7 @@ class DeviceBackend:
             if panels is not None:
                 return self._gemm_streamed(g, precision, panels, stream_a, init, init_value,
                                            bias_ptr, bias_stride, shadow_out, shadow_in,
-                                           last_writer)
+                                           last_writer, cta)
         tA, tB = s.tensor(g.A), s.tensor(g.B)
         # a fused fill over all of a dense C: its old contents are never read
         tC = s.tensor(g.C, overwrite=bool(init) and dense_c and g.C is not g.A and
@@ -614,7 +684,7 @@ class DeviceBackend:
                                 g.sC, g.M, g.N, g.K, s.stream_ptr, init=init,
                                 init_value=init_value, bias_ptr=bias_ptr,
                                 bias_stride=bias_stride, call=self.call, a_packed=a_packed,
-                                c16=c16)
+                                c16=c16, cta=cta)
             self._shadow = None
             if c16 is not None:
                 self._shadow_slot ^= 1
@@ -623,8 +693,22 @@ class DeviceBackend:
             return names
         return self._contract_tables(g, tA, tB, tC, init, init_value, bias_ptr, bias_stride)
 
+    def _fallback(self, precision, why):
+        """A bf16 / tf32 request this contraction cannot honour: it runs the
+        exact f32 kernels (more precise, slower).  Warned and noted in the
+        plan; configure(strict=True) makes it an error instead."""
+        import warnings
+
+        from . import engine
+
+        msg = f"{precision} requested, ran exact f32: {why}"
+        self.last_note = msg
+        if engine.STRICT:
+            raise PrecisionUnavailable(msg)
+        warnings.warn(msg, PrecisionFallback, stacklevel=3)
+
     def _gemm_streamed(self, g, precision, panels, stream_a, init, init_value, bias_ptr,
-                       bias_stride, shadow_out, shadow_in, last_writer):
+                       bias_stride, shadow_out, shadow_in, last_writer, cta=None):
         """C (+)= A.B over row panels of M with the host copies pipelined
         (Staging.stream_rows): panel p's GEMM overlaps the upload of panel
         p+1 and the write-back of panel p-1.  B is uploaded (and, on the
@@ -641,7 +725,7 @@ class DeviceBackend:
                 a_packed = sh[1]
         if tc:
             Bp = pack_b(s.lib, precision, tB.data_ptr() + 4 * g.offB, g.sB, g.N, g.K,
-                        s.stream_ptr, self.call)
+                        s.stream_ptr, self.call, allow_kn=cta != (128, 256))
             if precision == "bf16" and shadow_out and tc_supported(precision, g.N):
                 c16 = workspace(4 + (self._shadow_slot ^ 1), "bfloat16", g.M, g.N)
         names = []
@@ -654,7 +738,7 @@ class DeviceBackend:
                 r1 - r0, g.N, g.K, s.stream_ptr, init=init, init_value=init_value,
                 bias_ptr=bias_ptr, bias_stride=bias_stride, call=self.call,
                 c16=c16[r0:r1] if c16 is not None else None, b_packed=Bp,
-                a_packed=a_packed[r0:r1] if a_packed is not None else None)
+                a_packed=a_packed[r0:r1] if a_packed is not None else None, cta=cta)
 
         s.stream_rows(panels, [g.A] if stream_a else [], (g.C, not init), launch)
         if last_writer:

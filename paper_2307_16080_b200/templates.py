@@ -37,7 +37,7 @@ class ContractMatch:
 
     __slots__ = ("A", "B", "C", "dtype", "M", "N", "K", "m_vars", "n_vars", "k_vars",
                  "_tables", "_make_tables", "origins", "strided", "offA", "offB", "offC",
-                 "sA", "sB", "sC", "offsets", "stat")
+                 "sA", "sB", "sC", "offsets", "stat", "tiles")
 
     def __repr__(self):
         return (f"ContractMatch({self.dtype}, M={self.M}, N={self.N}, K={self.K}, "
@@ -227,15 +227,50 @@ def match_contraction(region, links, remainder, accesses):
              for v in g.m_vars + g.n_vars]
     if not _mixed_radix_injective(terms, 0):
         return None
-    g.strided = len(g.m_vars) <= 1 and len(g.n_vars) <= 1 and len(g.k_vars) == 1
+    # one strided dimension per group: a single variable, or the origin and
+    # offset loops of a tiled nest (passes/tiling.py:56-80: index = origin +
+    # offset) that together walk one arithmetic progression in every operand
+    mS = _progression(reversed(g.m_vars), (aS.offset, aA.offset), stat)
+    nS = _progression(reversed(g.n_vars), (aS.offset, aB.offset), stat)
+    # K: the progression must also be the nest order (outer = larger stride),
+    # the order every output's chain is rounded in
+    kS = _progression(reversed(g.k_vars), (aA.offset, aB.offset), stat)
+    g.tiles = (_tile(g.m_vars, stat), _tile(g.n_vars, stat))
+    g.strided = mS is not None and nS is not None and kS is not None
     if g.strided:
-        def stride(off, vs):
-            return off.t.get(vs[0].id, 0) * stat(vs[0])[1] if vs else 0
-        g.sA = (stride(aA.offset, g.m_vars), stride(aA.offset, g.k_vars))
-        g.sB = (stride(aB.offset, g.k_vars), stride(aB.offset, g.n_vars))
-        g.sC = (stride(aS.offset, g.m_vars), stride(aS.offset, g.n_vars))
+        g.sA = (mS[1], kS[0])
+        g.sB = (kS[1], nS[1])
+        g.sC = (mS[0], nS[0])
         g.offA, g.offB, g.offC = (int(o) for o in g.origins)
     return g
+
+
+def _progression(vars_, offs, stat):
+    """Element strides, one per form in ``offs``, of the variables ``vars_``
+    (innermost = smallest stride first) merged into one loop — or None.
+
+    They merge when each variable's stride is the previous one's times its
+    trip count in every operand (a mixed-radix enumeration with one radix
+    chain: 0 .. trip-1 of the merged loop, each point once, in order).  An
+    empty group is a stride-0 dimension of extent 1."""
+    vs = list(vars_)
+    if not vs:
+        return tuple(0 for _ in offs)
+    base = [off.t.get(vs[0].id, 0) * stat(vs[0])[1] for off in offs]
+    expect = list(base)
+    for v in vs:
+        _, step, trip = stat(v)
+        for i, off in enumerate(offs):
+            if off.t.get(v.id, 0) * step != expect[i]:
+                return None
+            expect[i] *= trip
+    return tuple(base)
+
+
+def _tile(vars_, stat):
+    """The tile extent of a tiled group (the innermost, offset loop's trip),
+    or None when the group is a single loop."""
+    return stat(vars_[-1])[2] if len(vars_) > 1 else None
 
 
 

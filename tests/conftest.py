@@ -47,3 +47,16 @@ def oracle_engine():
 
     oracle.build()
     return oracle
+
+
+# max normalised errors of the tensor-core parity tests (tcbound.check):
+# printed in the session summary so every run reports them
+TC_ERRORS = []
+
+
+def pytest_terminal_summary(terminalreporter):
+    if TC_ERRORS:
+        terminalreporter.write_sep("-", "tensor-core parity: max normalised error "
+                                        "|got-want| / (2^-24 sqrt(K) sum|ab|)")
+        for label, K, e in TC_ERRORS:
+            terminalreporter.write_line(f"{label}: K={K} max_norm_err={e:.4f} (bound 8)")

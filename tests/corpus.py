@@ -262,3 +262,24 @@ def conv_mid(inp: MemRef[(4, 16, 34, 34), F32], ker: MemRef[(8, 16, 3, 3), F32],
 
 
 BIG = [matmul_odd, matmul_t, conv_mid]
+
+
+# -- tensor-core smoke shapes (__graft_entry__.smoke) ----------------------------
+
+
+@staged
+def mm_tc_smoke(A: MemRef[(256, 192), F32], B: MemRef[(192, 256), F32],
+                C: MemRef[(256, 256), F32]):
+    for i, k in parallel((0, 0), (256, 256)):
+        for j in range(192):
+            C[i, k] += A[i, j] * B[j, k]
+
+
+@staged
+def conv_tc_smoke(inp: MemRef[(2, 64, 18, 30), F32], ker: MemRef[(64, 64, 3, 3), F32],
+                  out: MemRef[(2, 64, 16, 28), F32]):
+    for n, co, ho, wo in parallel((0, 0, 0, 0), (2, 64, 16, 28)):
+        for ci in range(0, 64):
+            for ki in range(0, 3):
+                for kj in range(0, 3):
+                    out[n, co, ho, wo] += inp[n, ci, ho + ki, wo + kj] * ker[co, ci, ki, kj]
