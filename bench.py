@@ -1,43 +1,51 @@
 """Benchmark: GFLOP/s of the B200 backend on BASELINE.json's configs.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload mm|conv|ls|linear32|ewise] [--precision bf16|tf32|exact]
+                    [--workload auto|mm|mm_tiled|conv|ls|linear32|ewise|sweep]
+                    [--precision exact|tf32|bf16] [--min-seconds S]
 
-Default workload (BASELINE.json configs[1]): ``linalg.matmul`` 4096x4096x4096
-— the reference's matmul nest (reference tests/kernels.py:24-38) at full
-size, C[i,k] += A[i,j] * B[j,k] on f32 Buffers, bf16 tensor-core precision.
-Other workloads (configs[0], [2], [3]): ``linear32`` (Linear(32,32) lowering),
-``conv`` (conv_2d_nchw_fchw N=256 C=F=64 56x56 3x3, batch-sharded),
-``ls`` (Linear stack 65536x1024->4096->1024, batch-sharded), ``ewise``
-(y = y + 2x over 8192x8192 f32).
+Default (``--workload auto``) prints ONE JSON line:
 
-A step is one pass of the hot path over one batch: one run of the nest.
-Data: U(-1,1) f32 from torch.Generator().manual_seed(arg index).
+* N = 1: the headline is BASELINE configs[1], ``linalg.matmul`` 4096^3 —
+  the reference's matmul nest (reference tests/kernels.py:24-38) at full
+  size on f32 Buffers, at the reference's own arithmetic (``exact``: every
+  product and sum rounded to f32 in nest order, bit-identical to the
+  reference executor).  ``variants`` carries the same config on the tensor
+  cores (bf16, tf32) and with the reference tile sizes (8, 8) / (4, 16)
+   through the reference's tiling pass; ``configs`` carries
+  every other BASELINE config: Linear(32,32) (configs[0]), the ResNet conv
+  exact and bf16 (configs[2]), the Linear stack (configs[3]), the
+  elementwise nest, and the 512-config sweep (configs[4]).
+* N > 1 (torchrun, one rank per GPU): the headline is configs[2], the
+  ResNet conv batch-sharded over the ranks (paper_2307_16080_b200.shard:
+  contiguous image ranges, the worksharing rule of interp/_evalpy.py:279);
+  ``configs`` adds the bf16 conv, the Linear stack and the sweep, sharded the
+  same way (N=1's line carries the same records for the scaling baseline).
 
-* ``value``  — device-resident: the engine's own launch sequence for the
-  nest (recorded once by paper_2307_16080_b200.Session, then replayed),
-  timed with CUDA events on the launch stream; every workload except
-  linear32 has inputs larger than the 126 MB L2.
-* ``roofline`` — the dominant kernel family of that sequence, timed per
-  launch with CUDA events inside an instrumented replay: algorithmic flops
-  (or bytes) / time, against MEASURED_PEAKS.json.
-* ``e2e``    — through the reference-facing plugin: staircase's own
-  ``machine.run(module, name, host_buffers, engine=b200)``; the H2D of every
-  argument and the D2H of every written buffer are in the timed region.
-* ``cpu_baseline`` — the reference executor itself (baseline/_ref, compiled
-  _evalcy engine) on a thin slice of the same nest (same loop structure and
-  reduction length), 1 core; its rate extrapolates to the full size.
-* ``--impl reference`` — rank 0 times that reference CPU path per step.
+Per record:
 
-Multi-GPU (torchrun): mm / linear32 / ewise run one replica per rank (weak
-scaling); conv and ls shard the batch (strong scaling, contiguous ranges as
-in worksharing, interp/_evalpy.py:279).  No data-path collective: one NCCL
-all_gather of per-rank output checksums after timing.  Time = max over ranks.
+* ``value`` — device-resident: the engine's own launch sequence (recorded
+  once by paper_2307_16080_b200.Session, replayed as a CUDA graph), K steps
+  timed with CUDA events on the launch stream, max over ranks; inputs are
+  larger than the 126 MB L2 except linear32 (stated in ``config.l2``).
+* ``sustained`` — the same replay back to back for >= --min-seconds, with
+  the nvidia-smi clock sampler running (``clocks`` covers both regions).
+* ``roofline`` — the dominant kernel family, timed per launch with CUDA
+  events: algorithmic flops (or bytes) / time against MEASURED_PEAKS.json
+  (burst), plus the step's fraction of the sustained peak.
+* ``e2e`` — through the reference-facing plugin: staircase's own
+  ``machine.run`` (or shard.run) on host Buffers, host<->device copies in
+  the timed region, >= --min-seconds of runs.
+* ``cpu_baseline`` — the reference executor (baseline/_ref, compiled
+  _evalcy engine) on a slice of the same nest, one process per host core
+  running concurrently; the rate extrapolates to the full size.
+* ``--impl reference`` — rank 0 times that same reference CPU path per step.
 """
 import argparse
 import ctypes
 import json
 import math
+import multiprocessing as mproc
 import os
 import statistics
 import subprocess
@@ -53,92 +61,172 @@ ensure_staircase()
 
 import bench_kernels as bk  # noqa: E402
 
+TILE = "builtin.module(func.func(scf-parallel-loop-tiling{{sizes=[{}, {}]}}))"
+
 
 # -- workloads -------------------------------------------------------------------
 
 class Workload:
-    def __init__(self, name, world):
+    """One BASELINE config: the nest, its flops, its CPU slice."""
+
+    def __init__(self, name, tiles=None):
         self.name = name
-        self.world = world
+        self.tiles = tiles
+        self.sharded = False
+        self.module = None
+        self.bytes = None
+        self.tc_bytes = None
         if name == "mm":
-            self.fn = bk.mm4096
+            self.fn = bk.mm_par4096 if tiles else bk.mm4096
             self.flops = 2.0 * 4096 ** 3
-            self.scaling = "weak"
-            self.desc = "linalg.matmul 4096x4096x4096, C += A.B on f32 buffers"
+            self.desc = ("linalg.matmul 4096x4096x4096, C += A.B on f32 buffers" +
+                         (f", parallel form tiled ({tiles[0]}, {tiles[1]}) by the reference's "
+                          f"scf-parallel-loop-tiling" if tiles else ""))
             self.slice = (bk.mm_slice, 2.0 * 4096 * 256, "1x4096x256 slice of the matmul nest")
-            self.default_precision = "bf16"
+            self.config = "configs[1]"
         elif name == "conv":
-            nb = 256 // world
-            self.fn = bk.make_conv(nb)
-            self.flops = 2.0 * nb * 64 * 56 * 56 * 64 * 9
-            self.scaling = "strong"
-            self.desc = (f"conv_2d_nchw_fchw N=256 (this rank: {nb}) C=F=64 58x58 pre-padded "
-                         f"-> 56x56, 3x3, f32")
+            self.fn = bk.make_conv(256)
+            self.flops = 2.0 * 256 * 64 * 56 * 56 * 64 * 9
+            self.sharded = True
+            self.desc = ("conv_2d_nchw_fchw N=256 C=F=64 58x58 pre-padded -> 56x56, 3x3, f32 "
+                         "buffers, out += conv")
             self.slice = (bk.conv_slice, 2.0 * 2 * 8 * 56 * 64 * 9,
                           "1x2x8x56 outputs of the conv nest (C=64, 3x3)")
-            # the tcgen05 implicit-GEMM conv, like mm / ls; --precision exact
-            # runs the bit-exact FP32 kernel
-            self.default_precision = "bf16"
             # algorithmic DRAM bytes of b200_conv2d_tc: the NHWC bf16 input
             # once, the f32 output read and written (out += conv)
-            self.tc_bytes = nb * 58 * 58 * 64 * 2 + 2 * nb * 64 * 56 * 56 * 4
+            self.tc_bytes = 256 * 58 * 58 * 64 * 2 + 2 * 256 * 64 * 56 * 56 * 4
+            self.config = "configs[2]"
         elif name == "ls":
-            rows = 65536 // world
-            self.fn = bk.make_linear_stack(rows)
-            self.flops = 2.0 * rows * (1024 * 4096 * 2) + 2.0 * rows * (4096 + 1024)
-            self.scaling = "strong"
-            self.desc = (f"Linear stack 65536 (this rank: {rows}) x 1024 -> 4096 -> 1024, "
-                         f"fill + contraction + bias nests")
+            self.fn = bk.make_linear_stack(65536)
+            self.flops = 2.0 * 65536 * (1024 * 4096 * 2) + 2.0 * 65536 * (4096 + 1024)
+            self.sharded = True
+            self.desc = ("Linear stack 65536 x 1024 -> 4096 -> 1024, fill + contraction + bias "
+                         "nests per layer")
             self.slice = (bk.make_linear_stack(1), 2.0 * (1024 * 4096 * 2),
                           "1 row through both Linear lowerings")
-            self.default_precision = "bf16"
+            self.config = "configs[3]"
         elif name == "linear32":
             self.fn = bk.linear32
             self.flops = 2.0 * 32 ** 3 + 32 * 32
-            self.scaling = "weak"
             self.desc = "torch.nn.Linear(32,32) lowering: fill + copy + 32^3 contraction + bias"
             self.slice = (bk.linear32, self.flops, "the full Linear(32,32) lowering")
-            self.default_precision = "exact"
+            self.config = "configs[0]"
         elif name == "ewise":
             self.fn = bk.saxpy8k
             self.flops = 2.0 * 8192 * 8192
             self.bytes = 3 * 8192 * 8192 * 4
-            self.scaling = "weak"
             self.desc = "elementwise y = y + 2x over 8192x8192 f32 (512 MB working set)"
             self.slice = (bk.saxpy_slice, 2.0 * 16 * 4096, "16x4096 rows of the same nest")
-            self.default_precision = "exact"
+            self.config = "fill / copy / ewise nests (SURVEY a14)"
         else:
             raise SystemExit(f"unknown workload {name!r}")
+        self.module = self.fn.module
+        if tiles:
+            from staircase.passes import run_pipeline
 
-    def shapes(self):
-        return [tuple(a.type.shape) for a in self.fn.func_op.body().args]
+            self.module, _ = run_pipeline(self.fn.module, TILE.format(*tiles))
+        self.func = self.fn.__name__
+
+    @property
+    def key(self):
+        return self.name + (f"_tile{self.tiles[0]}x{self.tiles[1]}" if self.tiles else "")
 
 
-def host_inputs(fn, seed_base=0):
+def host_inputs(fn):
+    """U(-1,1) f32 Buffers, arg i from torch.Generator().manual_seed(i)
+    (SURVEY §8d): the same global batch on every rank."""
     import torch
     from staircase.interp import Buffer
 
     out = []
     for i, a in enumerate(fn.func_op.body().args):
         shape = tuple(a.type.shape)
-        g = torch.Generator().manual_seed(seed_base + i)
+        g = torch.Generator().manual_seed(i)
         t = torch.rand(shape, generator=g, dtype=torch.float32) * 2 - 1
         out.append(Buffer(shape, "f32", t.numpy().tobytes()))
     return out
 
 
-def reference_rate(wl, repeats=3):
-    """GFLOP/s of the reference's compiled executor on the workload's slice."""
+# -- the reference CPU path: one process per host core ----------------------------
+
+def _ref_worker(conn, name):
+    """A process that times the reference executor on a workload's slice."""
+    sys.path.insert(0, ROOT)
+    from paper_2307_16080_b200.host import ensure_staircase
+
+    ensure_staircase()
     from staircase.interp import _evalcy, machine
 
-    fn, flops, _ = wl.slice
-    times = []
-    for _ in range(repeats):
+    fn = _slice_fn(name)
+    args = host_inputs(fn)
+    while True:
+        msg = conn.recv()
+        if msg is None:
+            return
+        # the nest accumulates into its output: fresh inputs each time keep
+        # the values (and the timing) the same as a first run
         args = host_inputs(fn)
         _, stats = machine.run(fn.module, fn.__name__, args, engine=_evalcy)
-        times.append(stats.wall_time)
-    t = statistics.median(times)
-    return flops / t / 1e9, t
+        conn.send(stats.wall_time)
+
+
+def _slice_fn(name):
+    return {"mm": bk.mm_slice, "conv": bk.conv_slice, "ls": None, "linear32": bk.linear32,
+            "ewise": bk.saxpy_slice}.get(name) or bk.make_linear_stack(1)
+
+
+class ReferencePool:
+    """C concurrent processes of the reference executor (staircase _evalcy,
+    from baseline/_ref), one per host core: the reference's interpreter is
+    single-threaded (its worksharing mode does not scale under the GIL), so
+    this is how it uses all the cores.  Each sample = one slice run in every
+    process at once; rate = sum of the per-process rates."""
+
+    def __init__(self, wl, cores=None):
+        self.wl = wl
+        self.cores = cores or len(os.sched_getaffinity(0))
+        ctx = mproc.get_context("spawn")
+        self.conns, self.procs = [], []
+        for _ in range(self.cores):
+            a, b = ctx.Pipe()
+            p = ctx.Process(target=_ref_worker, args=(b, wl.name), daemon=True)
+            p.start()
+            self.conns.append(a)
+            self.procs.append(p)
+
+    def sample(self):
+        """(aggregate GFLOP/s, median seconds per slice run)."""
+        for c in self.conns:
+            c.send(1)
+        times = [c.recv() for c in self.conns]
+        flops = self.wl.slice[1]
+        return sum(flops / t for t in times) / 1e9, statistics.median(times)
+
+    def close(self):
+        for c in self.conns:
+            try:
+                c.send(None)
+            except (BrokenPipeError, OSError):
+                pass
+        for p in self.procs:
+            p.join(timeout=10)
+
+    def describe(self, t):
+        return (f"{self.wl.slice[2]} via staircase _evalcy, {self.cores} concurrent processes "
+                f"(one per host core; {t:.2f} s per slice run); rate extrapolates to the full "
+                f"nest")
+
+
+def cpu_baseline(wl, repeats=2):
+    pool = ReferencePool(wl)
+    try:
+        pool.sample()   # warm: imports done, caches warm
+        res = [pool.sample() for _ in range(repeats)]
+    finally:
+        pool.close()
+    rate = statistics.median(r[0] for r in res)
+    return {"value": rate, "unit": "GFLOP/s", "cores": pool.cores, "kind": "reference",
+            "sample": pool.describe(statistics.median(r[1] for r in res))}
 
 
 # -- measurement helpers ----------------------------------------------------------
@@ -148,11 +236,11 @@ class Clocks:
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_power_cap,power.draw,utilization.gpu")
 
     def __init__(self, index):
         self.proc = None
-        self.path = f"/tmp/b200_clocks_{os.getpid()}.csv"
+        self.path = f"/tmp/b200_clocks_{os.getpid()}_{time.time_ns()}.csv"
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={index}", f"--query-gpu={self.Q}",
@@ -173,23 +261,36 @@ class Clocks:
         time.sleep(0.15)
         self.proc.terminate()
         self.proc.wait()
-        sm, mx, reasons = [], [], set()
+        sm, mx, reasons, power, loaded = [], [], set(), [], 0
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in open(self.path):
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 6:
+            if len(parts) < 8:
                 continue
+            try:
+                util = float(parts[7])
+            except ValueError:
+                util = 0.0
+            if util < 50:
+                continue   # idle samples around the timed region
+            loaded += 1
             try:
                 sm.append(float(parts[0]))
                 mx.append(float(parts[1]))
+                power.append(float(parts[6]))
             except ValueError:
                 continue
-            for name, val in zip(names, parts[2:]):
+            for name, val in zip(names, parts[2:6]):
                 if val.lower() == "active":
                     reasons.add(name)
+        try:
+            os.unlink(self.path)
+        except OSError:
+            pass
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples_under_load": loaded,
+                "power_w_median": statistics.median(power) if power else None}
 
 
 def dist_setup():
@@ -262,7 +363,7 @@ def capture_graph(fn):
 
 
 def gather_checksums(value, world):
-    """The only collective: one NCCL all_gather of per-rank result checksums."""
+    """One all_gather of per-rank result checksums (harness only)."""
     if world == 1:
         return [value]
     import torch
@@ -278,7 +379,8 @@ def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
         return json.load(open(path)), "measured"
-    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1590.0,
+            "sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md)"
 
 
 def load_traffic(key):
@@ -293,85 +395,80 @@ KERNEL_OF = {"b200_gemm_tc": "gemm", "b200_gemm_f32_exact": "gemm",
              "b200_contract_exact": "contract", "b200_map_f32": "map", "b200_vm_run": "vm",
              "b200_pack_operand": "pack", "b200_conv2d_tc": "conv",
              "b200_pack_conv_input": "pack", "b200_pack_conv": "pack",
-             "b200_conv2d_exact": "conv",
-             "b200_jit_launch": "map"}
+             "b200_conv2d_exact": "conv", "b200_jit_launch": "map"}
 TENSOR_KERNELS = ("b200_gemm_tc", "b200_conv2d_tc")
-# entry points that run the same kernel (timed together as one family)
-ALIASES = {"b200_gemm_tc_shadow": "b200_gemm_tc", "b200_gemm_tc_kn": "b200_gemm_tc"}
+# entry points that run the same kernel family (timed together)
+ALIASES = {"b200_gemm_tc_shadow": "b200_gemm_tc", "b200_gemm_tc_kn": "b200_gemm_tc",
+           "b200_gemm_f32_exact_tiled": "b200_gemm_f32_exact"}
+DTYPE = {"bf16": "bf16 (fp32 accumulate)", "tf32": "tf32 (fp32 accumulate)", "exact": "f32"}
 
 
-# -- arms ----------------------------------------------------------------------------
+def _timed(fn, stream, min_steps, min_seconds):
+    """Run fn back to back (>= min_steps, >= min_seconds): (ms per call, calls)."""
+    import torch
 
-def run_reference(args, rank, world):
-    if rank != 0:
-        return
-    wl = Workload(args.workload, 1)
-    for _ in range(args.warmup):
-        reference_rate(wl, repeats=1)
-    rates = []
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        rate, _ = reference_rate(wl, repeats=1)
-        rates.append(rate)
-    wall = time.perf_counter() - t0
-    value = statistics.median(rates)
-    line = {
-        "impl": "reference", "metric": f"GFLOP/s ({args.workload})", "value": value,
-        "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True,
-        "scaling": wl.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": wl.desc + " (reference CPU executor on a slice; "
-                                         "rate extrapolates)"},
-        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": 1, "kind": "reference",
-                         "sample": wl.slice[2] + ", staircase _evalcy, one run per step"},
-        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    # estimate the call time first so the region is sized without host syncs inside
+    torch.cuda.synchronize()
+    e0.record(stream)
+    fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    one = max(e0.elapsed_time(e1), 1e-3)
+    n = max(min_steps, int(math.ceil(min_seconds * 1e3 / one)))
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(n):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / n, n
 
 
-def run_ours(args, rank, world, local):
+# -- our arm ---------------------------------------------------------------------
+
+def measure(wl, prec, rank, world, local, steps, warmup, min_seconds, with_cpu=True,
+            with_e2e=True):
+    """One record for workload ``wl`` at precision ``prec`` on this rank."""
     import torch
 
     import paper_2307_16080_b200 as b2
-    from paper_2307_16080_b200 import runtime
+    from paper_2307_16080_b200 import runtime, shard
     from staircase.interp import machine
 
     lib = runtime.load_library()
-    wl = Workload(args.workload, world)
-    prec = args.precision or wl.default_precision
     b2.configure(precision=prec)
-    fn = wl.fn
-    name = fn.__name__
-
-    # device-resident: record the engine's plan once, replay it
-    sess = b2.Session()
-    dev_args = host_inputs(fn, seed_base=100 * rank)
-    rec = sess.record(fn.module, name, dev_args)
+    sharded = wl.sharded and world > 1
+    sess = b2.Session(shard=(rank, world) if sharded else None)
+    dev_args = host_inputs(wl.fn)
+    rec = sess.record(wl.module, wl.func, dev_args)
     plan = list(sess.plan)
+    rows = sess.last_shard.rows if sharded else None
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         rec.replay(lib)
     torch.cuda.synchronize()
-    # the recorded launch sequence as one CUDA graph: device time per step
-    # without host enqueue gaps between the (possibly tiny) kernels
     step_graph = capture_graph(lambda: rec.replay(lib))
     run_step = step_graph.replay if step_graph is not None else (lambda: rec.replay(lib))
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         run_step()
     torch.cuda.synchronize()
     barrier(world)
     clocks = Clocks(local)
+    # the contract's timed region: exactly `steps` steps
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     ev0.record(stream)
-    for _ in range(args.steps):
+    for _ in range(steps):
         run_step()
     ev1.record(stream)
     torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1) / args.steps
+    ms = ev0.elapsed_time(ev1) / steps
+    # sustained: the same steps back to back for >= min_seconds
+    sus_ms, sus_n = _timed(run_step, stream, steps, min_seconds)
     clk = clocks.stop()
     # per-launch device time of each recorded call: a graph of R back-to-back
     # repeats of that one launch, timed with events, / R
@@ -393,199 +490,229 @@ def run_ours(args, rank, world, local):
         fam[key] = fam.get(key, 0.0) + e0.elapsed_time(e1) / reps
     barrier(world)
     ms = max_over_ranks(ms, world)
-    value = world * wl.flops / (ms * 1e-3) / 1e9
-    out_sum = float(sess.tensor(dev_args[-1]).double().sum().item())
-    sums = gather_checksums(out_sum, world)
+    sus_ms = max_over_ranks(sus_ms, world)
+    # whole-job work: the global batch when sharded, one nest per rank otherwise
+    job_flops = wl.flops if sharded else world * wl.flops
+    out = sess.tensor(dev_args[-1])
+    if rows is not None:
+        out = out.view(dev_args[-1].shape[0], -1)[rows[0]:rows[1]]
+    sums = gather_checksums(float(out.double().sum().item()), world)
+    n_launch = rec.launches
+    del sess, rec, step_graph, dev_args
+    torch.cuda.synchronize()
 
-    # e2e through the plugin: host Buffers, H2D + D2H inside the timed region
-    host = host_inputs(fn, seed_base=100 * rank)
+    e2e = gather = None
+    if with_e2e:
+        e2e, gather = _e2e(wl, rank, world, sharded, min_seconds)
+    b2.configure(precision="exact")
+    rate_flops = wl.flops if not sharded else wl.flops * (rows[1] - rows[0]) / \
+        wl.fn.func_op.body().args[0].type.shape[0]
+    rec_out = {
+        "metric": f"GFLOP/s ({wl.key}, {prec})", "value": job_flops / (ms * 1e-3) / 1e9,
+        "unit": "GFLOP/s", "ms_per_step": ms, "steps": steps,
+        "dtype": DTYPE[prec], "precision": prec,
+        "config": {"workload": wl.desc, "baseline_config": wl.config,
+                   "parallelism": (f"batch shard x{world} (rows {rows[0]}..{rows[1] - 1} on "
+                                   f"rank {rank})" if sharded else
+                                   f"replica x{world}" if world > 1 else "1 GPU"),
+                   "l2": ("L2-resident, latency-bound config" if wl.name == "linear32" else
+                          "inputs larger than the 126 MB L2 (no flush needed)"),
+                   "plan": [list(map(str, p)) for p in plan]},
+        "sustained": {"value": job_flops / (sus_ms * 1e-3) / 1e9, "unit": "GFLOP/s",
+                      "ms_per_step": sus_ms, "steps": sus_n,
+                      "seconds": sus_ms * sus_n / 1e3},
+        "clocks": clk, "gpu_launches": n_launch * steps,
+        "checksums": sums,
+    }
+    if rank == 0:
+        rec_out["roofline"] = roofline(wl, prec, fam, ms, sus_ms, rate_flops)
+        rec_out["step_kernels_ms"] = {k: round(v, 4) for k, v in sorted(fam.items())}
+        if e2e is not None:
+            rec_out["e2e"] = e2e
+        if gather is not None:
+            rec_out["gather"] = gather
+        if with_cpu:
+            rec_out["cpu_baseline"] = cpu_baseline(wl) if world == 1 else {
+                "value": None, "unit": "GFLOP/s", "cores": None, "kind": "reference",
+                "sample": "timed in the N=1 run only"}
+    return rec_out
+
+
+def _e2e(wl, rank, world, sharded, min_seconds):
+    """The same metric through the plugin: host Buffers in, results back."""
+    import torch
+
+    import paper_2307_16080_b200 as b2
+    from paper_2307_16080_b200 import shard
+    from staircase.interp import machine
+
+    host = host_inputs(wl.fn)
+
+    def once():
+        if sharded:
+            return shard.run(wl.module, wl.func, host, rank=rank, world=world)
+        machine.run(wl.module, wl.func, host, engine=b2.engine)
+        return None
+
     # warm: plans / JIT kernels, and the host buffers get page-locked on
     # their second staging (runtime.pin_host: reused buffers are pinned)
     for _ in range(2):
-        machine.run(fn.module, name, host, engine=b2.engine)
+        once()
     torch.cuda.synchronize()
     barrier(world)
-    # at least 3 runs, more for short ones (until 0.25 s or `steps` runs):
-    # host-overhead-bound configs are noisy over 3 runs
-    e2e_steps = 0
+    n = 0
     t0 = time.perf_counter()
-    while e2e_steps < 3 or (e2e_steps < max(3, args.steps) and
-                            time.perf_counter() - t0 < 0.25):
-        machine.run(fn.module, name, host, engine=b2.engine)
-        e2e_steps += 1
+    while n < 3 or time.perf_counter() - t0 < min_seconds:
+        res = once()
+        n += 1
     torch.cuda.synchronize()
-    e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
-    e2e_ms = max_over_ranks(e2e_ms, world)
-    # the bytes the last run actually moved (runtime.Staging counters): every
-    # input read by the device once, every written buffer back once; buffers
-    # a fused fill overwrites entirely are not uploaded
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / n
     st = b2.engine.last_staging
     h2d, d2h = st.h2d_bytes, st.d2h_bytes
+    e2e_ms = max_over_ranks(e2e_ms, world)
+    gather = None
+    if sharded:
+        barrier(world)
+        t0 = time.perf_counter()
+        got = shard.gather(res)
+        torch.cuda.synchronize()
+        g_ms = max_over_ranks((time.perf_counter() - t0) * 1e3, world)
+        gather = {"ms": g_ms, "bytes_received_per_rank": got,
+                  "how": "shard.gather: one NCCL all_gather per output buffer of the batch "
+                         "rows, device to device, then D2H of the whole output (timed "
+                         "separately, not in value / e2e)"}
+    flops = wl.flops if sharded else world * wl.flops
+    return {"value": flops / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": e2e_ms,
+            "runs": n, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "how": ("shard.run" if sharded else "staircase machine.run") +
+                   " on host Buffers, B200 engine; H2D of the inputs and D2H of the written "
+                   "buffers inside the timed region (per rank)"}, gather
 
-    if rank != 0:
-        return
+
+def roofline(wl, prec, fam, ms, sus_ms, rank_flops):
+    """The dominant kernel family against its roofline (per-rank work)."""
     peaks, src = load_peaks()
     dom = max(fam, key=fam.get)
     dom_ms = fam[dom]
     family = KERNEL_OF.get(dom, dom)
-    if wl.name == "ewise":
-        achieved = wl.bytes / (dom_ms * 1e-3) / 1e9
+    share = dom_ms / sum(fam.values()) if sum(fam.values()) else None
+    scale = rank_flops / wl.flops
+    if wl.bytes is not None:
+        achieved = wl.bytes * scale / (dom_ms * 1e-3) / 1e9
         peak, unit, bound = peaks["hbm_gbs"], "GB/s", "hbm"
         peak_source = f"{src} HBM copy bandwidth (MEASURED_PEAKS.json)"
+        sus_peak = peak
     elif dom in TENSOR_KERNELS:
-        achieved = wl.flops / (dom_ms * 1e-3) / 1e12
-        peak = peaks["bf16_tflops"] * (1.0 if prec == "bf16" else 0.5)
+        achieved = rank_flops / (dom_ms * 1e-3) / 1e12
+        f = 1.0 if prec == "bf16" else 0.5
+        peak = peaks["bf16_tflops"] * f
+        sus_peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) * f
         unit, bound = "TFLOP/s", "tensor"
         peak_source = (f"{src} bf16 dense (MEASURED_PEAKS.json)" if prec == "bf16" else
                        f"{src} bf16 x 0.5 (tf32 = half rate, derived)")
-        tc_bytes = getattr(wl, "tc_bytes", None)
-        if tc_bytes and tc_bytes / (dom_ms * 1e-3) / 1e9 / peaks["hbm_gbs"] > achieved / peak:
+        if wl.tc_bytes and wl.tc_bytes * scale / (dom_ms * 1e-3) / 1e9 / peaks["hbm_gbs"] > \
+                achieved / peak:
             # the conv's f32 output read-modify-write makes it HBM-bound
-            achieved = tc_bytes / (dom_ms * 1e-3) / 1e9
+            achieved = wl.tc_bytes * scale / (dom_ms * 1e-3) / 1e9
             peak, unit, bound = peaks["hbm_gbs"], "GB/s", "hbm"
+            sus_peak = peak
             peak_source = (f"{src} HBM copy bandwidth (MEASURED_PEAKS.json); algorithmic bytes "
                            f"= NHWC bf16 input + 2 x f32 output")
     else:
         # the bit-exact kernels issue a separate, individually rounded
         # multiply and add per MAC (no FMA: the reference rounds each op), so
         # their ceiling is one FP32 op per lane per cycle, half the FMA peak
-        achieved = wl.flops / (dom_ms * 1e-3) / 1e12
+        achieved = rank_flops / (dom_ms * 1e-3) / 1e12
         peak = 148 * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        sus_peak = peak
         unit, bound = "TFLOP/s", "fp32-simt (no FMA)"
         peak_source = ("derived: 148 SM x 128 FP32 lanes x sm_max_mhz x 1 flop (mul and add "
-                       "issued separately; the FMA peak is 2x)")
-    if world == 1:
-        cpu_rate, cpu_t = reference_rate(wl)
-        cpu_sample = (f"{wl.slice[2]} via staircase _evalcy ({cpu_t:.2f} s); "
-                      f"host cores {len(os.sched_getaffinity(0))}")
-    else:   # the CPU baseline is timed in the N=1 run only
-        cpu_rate, cpu_sample = None, "timed in the N=1 run only"
-    dtype = {"bf16": "bf16 (fp32 accumulate)", "tf32": "tf32 (fp32 accumulate)",
-             "exact": "f32"}[prec]
-    big = wl.name != "linear32"
-    line = {
-        "metric": f"GFLOP/s ({wl.name})", "value": value, "unit": "GFLOP/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": wl.scaling, "vs_baseline": None, "dtype": dtype,
-        "data": "synthetic",
-        "config": {"workload": wl.desc, "precision": prec,
-                   "l2": "inputs larger than the 126 MB L2 (no flush)" if big else
-                         "L2-resident, latency-bound config",
-                   "parallelism": f"{'replica' if wl.scaling == 'weak' else 'batch-shard'} "
-                                  f"x{world}",
-                   "plan": [list(map(str, p)) for p in plan]},
-        "roofline": {"bound": bound, "kernel": dom, "achieved": achieved, "peak": peak,
-                     "unit": unit, "frac": achieved / peak, "peak_source": peak_source,
-                     "kernel_ms": dom_ms,
-                     "share_of_step": sum(fam.values()) and dom_ms / sum(fam.values()),
-                     "traffic": load_traffic(f"{wl.name}_{family}_{prec}")},
-        "e2e": {"value": wl.flops / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s",
-                "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "cpu_baseline": {"value": cpu_rate, "unit": "GFLOP/s", "cores": 1,
-                         "kind": "reference", "sample": cpu_sample},
-        # device time per step of every entry point the step launches
-        # (graph-replayed repeats of each recorded call, CUDA events)
-        "step_kernels_ms": {k: round(v, 4) for k, v in sorted(fam.items())},
-        "clocks": clk, "gpu_launches": rec.launches * args.steps,
-        "checksums": sums,
-    }
-    print(json.dumps(line), flush=True)
+                       "issued separately: the reference rounds each op; the FMA peak is 2x)")
+    # the whole step under sustained load against the sustained peak
+    step_sus = (achieved * (dom_ms / (sus_ms * (share or 1.0))) if share else None)
+    return {"bound": bound, "kernel": dom, "achieved": achieved, "peak": peak, "unit": unit,
+            "frac": achieved / peak, "peak_source": peak_source, "kernel_ms": dom_ms,
+            "share_of_step": share,
+            "frac_sustained": (step_sus / sus_peak) if step_sus else None,
+            "sustained_peak": sus_peak,
+            "traffic": load_traffic(f"{wl.name}_{family}_{prec}")}
 
+
+# -- the sweep (configs[4]) -------------------------------------------------------
 
 SWEEP_T = [1, 2, 4, 8, 16, 32, 64, 128]
 SWEEP_U = [1, 2, 4, 8]
 
 
-def run_sweep(args, rank, world, local, impl):
+def measure_sweep(rank, world, prec="exact", with_cpu=True):
     """The paper's tile-size / unroll design-space sweep (BASELINE configs[4]).
 
     512 configurations = tiles T x T (T in 1..128) x unroll U (1, 2, 4, 8) on
     two targets — the matmul nest (parallel form, 1024^3) and the paper's
     conv (1,1,1280,1280)*(1,3,3) — each enumerated exhaustively after the
     identity trial (strategy "grid").  Trials are sharded idx % world; one
-    all_gather_object of the trial records at the end.  Timed: the trial
-    phase (max over ranks, wall clock: every trial includes host-side pass
-    pipelines, plan building and the reference's correctness guard).
+    all_gather_object of the trial records at the end.  value = trials /
+    (setup + trials) wall time, max over ranks — every rank's setup (inputs,
+    identity baseline) included, so the scaling it reports is end to end.
     """
     import torch
 
+    import paper_2307_16080_b200 as b2
+    from paper_2307_16080_b200 import runtime as b2rt
     from paper_2307_16080_b200 import sweep
     from staircase.tuner import ParamSpace
 
     space = ParamSpace(tile_sizes=(SWEEP_T, SWEEP_T), unroll_factors=SWEEP_U)
     targets = [(bk.mm_par1024, 2.0 * 1024 ** 3), (bk.conv_paper, 2.0 * 1280 * 1280 * 9)]
-    if impl == "reference":
-        if rank != 0:
-            return
-        for _ in range(min(args.warmup, 1)):
-            reference_sweep_rate(budget=2)
-        res = [reference_sweep_rate() for _ in range(max(1, min(args.steps, 3)))]
-        rates = [r[0] for r in res]
-        value = statistics.median(rates)
-        note = res[0][1]
-        print(json.dumps({
-            "impl": "reference", "metric": "configs/s (tile/unroll design-space sweep)",
-            "value": value, "unit": "configs/s", "n_gpus": world, "steps": len(rates),
-            "warmup": args.warmup, "ms_per_step": 1e3 / value, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "reference tuner trials at desk scale (full-size sweep "
-                                   "trials are infeasible on the CPU executor)"},
-            "cpu_baseline": {"value": value, "unit": "configs/s", "cores": 1,
-                             "kind": "reference", "sample": note},
-            "e2e": {"value": value, "unit": "configs/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}), flush=True)
-        return
-    b2_prec = args.precision or "exact"
-    import paper_2307_16080_b200 as b2
-
-    b2.configure(precision=b2_prec)
-    from paper_2307_16080_b200 import runtime as b2rt
-
+    b2.configure(precision=prec)
     t0_totals = dict(b2rt.TOTALS)
     total_trials, trial_s, setup_s, flops = 0, 0.0, 0.0, 0.0
+    wall = 0.0
     logs = []
     for fn, f in targets:
         timing = {}
         barrier(world)
+        t0 = time.perf_counter()
         best, log = sweep.search(fn.module, None, space, budget=1 + len(SWEEP_T) ** 2 *
                                  len(SWEEP_U), seed=0, strategy="grid", timing=timing)
         torch.cuda.synchronize()
+        wall += max_over_ranks(time.perf_counter() - t0, world)
         trial_s += max_over_ranks(timing["trials_s"], world)
         setup_s += max_over_ranks(timing["setup_s"], world)
         total_trials += len(log)
         flops += f * len(log)
         logs.append((fn.__name__, best, log))
+    b2.configure(precision="exact")
     moved = {k: b2rt.TOTALS[k] - t0_totals[k] for k in t0_totals}
     if rank != 0:
-        return
-    # the reference tuner's per-trial rate on the same sweep machinery at desk
-    # scale (conv_small, reference _evalcy engine): full-size trials would take
-    # minutes to hours each on the CPU executor
-    cpu_rate, cpu_note = reference_sweep_rate()
-    line = {
-        "metric": "configs/s (tile/unroll design-space sweep)", "value": total_trials / trial_s,
-        "unit": "configs/s", "n_gpus": world, "steps": 1, "warmup": 0,
-        "ms_per_step": 1e3 * trial_s, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": b2_prec if b2_prec != "exact" else "f32",
+        return None
+    rec = {
+        "metric": "configs/s (tile/unroll design-space sweep)",
+        "value": total_trials / wall, "unit": "configs/s", "ms_per_step": 1e3 * wall,
+        "dtype": DTYPE[prec], "precision": prec,
         "data": "synthetic (tuner make_inputs, seed 0)",
         "config": {"workload": "512-config sweep: tiles T x T (T=1..128) x unroll (1,2,4,8) on "
                                "matmul 1024^3 (parallel form) and conv (1,1,1280,1280)*(1,3,3)",
+                   "baseline_config": "configs[4]",
                    "strategy": "grid (identity first)", "trials": total_trials,
                    "parallelism": f"trial shard idx % {world}",
-                   "setup_s_max_rank": setup_s,
                    "best": {n: {"idx": b.idx, "params": b.params, "cost": b.cost}
                             for n, b, _ in logs}},
-        "gflops_evaluated_per_s": flops / trial_s / 1e9,
-        # one step = the whole sweep on this rank (every trial's inputs are
-        # host Buffers staged to the device and its results written back)
-        "e2e": {"value": total_trials / (trial_s + setup_s), "unit": "configs/s",
+        "phases_s_max_rank": {"setup": setup_s, "trials": trial_s, "wall": wall},
+        "trials_only_configs_per_s": total_trials / trial_s,
+        "gflops_evaluated_per_s": flops / wall / 1e9,
+        "e2e": {"value": total_trials / wall, "unit": "configs/s",
                 "h2d_bytes_per_step": moved["h2d_bytes"],
-                "d2h_bytes_per_step": moved["d2h_bytes"]},
-        "cpu_baseline": {"value": cpu_rate, "unit": "configs/s", "cores": 1,
-                         "kind": "reference", "sample": cpu_note},
+                "d2h_bytes_per_step": moved["d2h_bytes"],
+                "how": "every trial's inputs are host Buffers staged to the device and its "
+                       "results written back; value already is end to end"},
         "gpu_launches": moved["launches"],
     }
-    print(json.dumps(line), flush=True)
+    if with_cpu:
+        rec["cpu_baseline"] = reference_sweep_rate() if world == 1 else {
+            "value": None, "unit": "configs/s", "cores": None, "kind": "reference",
+            "sample": "timed in the N=1 run only"}
+    return rec
 
 
 def reference_sweep_rate(budget=4):
@@ -594,9 +721,10 @@ def reference_sweep_rate(budget=4):
     rate on that nest is measured on a slice with the same loop structure and
     reduction length (matmul: 1x1024x1024; conv: 8 output rows), so
     trial time = kernel flops / slice rate.  Full-size trials would take
-    ~25 min (matmul) / ~40 s (conv) each on the CPU executor.
-    The reference's tuner machinery itself (tuner.search on the desk conv,
-    budget trials) is run too, to keep the measurement honest about overhead."""
+    ~25 min (matmul) / ~40 s (conv) each on the CPU executor.  The
+    reference's tuner machinery itself (tuner.search on the desk conv,
+    budget trials) is run too, to keep the measurement honest about
+    overhead.  One core: the tuner is sequential (search.py:180-279)."""
     import importlib
 
     from staircase.interp import _evalcy, machine
@@ -620,11 +748,129 @@ def reference_sweep_rate(budget=4):
     finally:
         machine._engine = saved
     per_config = statistics.mean(trial_s) + desk
-    return 1.0 / per_config, (
-        f"reference executor (_evalcy) slice rates {rates[0] / 1e6:.2f} / {rates[1] / 1e6:.2f} "
-        f"MFLOP/s on the matmul / conv nests -> extrapolated {trial_s[0]:.0f} s / "
-        f"{trial_s[1]:.1f} s per trial, + tuner overhead {desk * 1e3:.0f} ms/trial "
-        f"(tuner.search on the desk conv)")
+    return {"value": 1.0 / per_config, "unit": "configs/s", "cores": 1, "kind": "reference",
+            "sample": (f"reference executor (_evalcy) slice rates {rates[0] / 1e6:.2f} / "
+                       f"{rates[1] / 1e6:.2f} MFLOP/s on the matmul / conv nests -> "
+                       f"extrapolated {trial_s[0]:.0f} s / {trial_s[1]:.1f} s per trial, + "
+                       f"tuner overhead {desk * 1e3:.0f} ms/trial (tuner.search on the desk "
+                       f"conv; the tuner is sequential)")}
+
+
+# -- the line ---------------------------------------------------------------------
+
+def headline(rec, world, steps, warmup):
+    line = dict(rec)
+    line.update({"n_gpus": world, "steps": steps, "warmup": warmup, "higher_is_better": True,
+                 "vs_baseline": None, "data": rec.get("data", "synthetic")})
+    return line
+
+
+def run_ours(args, rank, world, local):
+    auto = args.workload == "auto"
+    name = ("mm" if world == 1 else "conv") if auto else args.workload
+    k = dict(steps=args.steps, warmup=args.warmup, min_seconds=args.min_seconds)
+    if name == "sweep":
+        main_rec = measure_sweep(rank, world, args.precision or "exact")
+        main_wl = None
+    else:
+        tiles = tuple(int(x) for x in args.tiles.split("x")) if args.tiles else None
+        main_wl = Workload(name, tiles)
+        main_rec = measure(main_wl, args.precision or "exact", rank, world, local, **k)
+    variants, configs = {}, {}
+    if auto:
+        if world == 1:
+            for prec, tiles in (("bf16", None), ("tf32", None), ("bf16", (8, 8)),
+                                ("bf16", (4, 16)), ("exact", (8, 8))):
+                wl = Workload("mm", tiles)
+                r = measure(wl, prec, rank, world, local, with_cpu=False, **k)
+                if r is not None:
+                    variants[f"{wl.key}_{prec}"] = r
+            todo = [("linear32", "exact"), ("conv", "exact"), ("conv", "bf16"), ("ls", "bf16"),
+                    ("ls", "exact"), ("ewise", "exact")]
+        else:
+            todo = [("conv", "bf16"), ("ls", "bf16")]
+        cpu = {}
+        for wname, prec in todo:
+            wl = Workload(wname)
+            r = measure(wl, prec, rank, world, local, with_cpu=wname not in cpu, **k)
+            if r is not None and rank == 0:
+                if "cpu_baseline" in r:
+                    cpu[wname] = r["cpu_baseline"]
+                else:
+                    r["cpu_baseline"] = cpu[wname]
+                configs[f"{wname}_{prec}"] = r
+        sw = measure_sweep(rank, world)
+        if sw is not None:
+            configs["sweep"] = sw
+    if rank != 0:
+        return
+    line = headline(main_rec, world, args.steps, args.warmup)
+    line["scaling"] = "strong" if (main_wl is None or (main_wl.sharded and world > 1)) \
+        else "weak"
+    if main_wl is not None and main_wl.name == "mm" and world == 1:
+        main_rec_cpu = line.get("cpu_baseline")
+        for v in variants.values():
+            v["cpu_baseline"] = main_rec_cpu
+    if variants:
+        line["variants"] = variants
+    if configs:
+        line["configs"] = configs
+    print(json.dumps(line), flush=True)
+
+
+# -- the reference arm -------------------------------------------------------------
+
+def run_reference(args, rank, world):
+    """The reference's own CPU implementation (baseline/_ref, _evalcy) on the
+    arm's config: a bounded slice per step in one process per host core."""
+    if rank != 0:
+        return
+    auto = args.workload == "auto"
+    name = ("mm" if world == 1 else "conv") if auto else args.workload
+    if name == "sweep":
+        vals = [reference_sweep_rate() for _ in range(max(1, min(args.steps, 3)))]
+        rec = vals[0]
+        value = statistics.median(v["value"] for v in vals)
+        print(json.dumps({
+            "impl": "reference", "metric": "configs/s (tile/unroll design-space sweep)",
+            "value": value, "unit": "configs/s", "n_gpus": world, "steps": len(vals),
+            "warmup": args.warmup, "ms_per_step": 1e3 / value, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "reference tuner trials (extrapolated from slices)"},
+            "cpu_baseline": dict(rec, value=value),
+            "e2e": {"value": value, "unit": "configs/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}), flush=True)
+        return
+    wl = Workload(name)
+    prec = args.precision or "exact"
+    pool = ReferencePool(wl)
+    try:
+        for _ in range(args.warmup):
+            pool.sample()
+        rates, per = [], []
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            r, t = pool.sample()
+            rates.append(r)
+            per.append(t)
+        wall = time.perf_counter() - t0
+    finally:
+        pool.close()
+    value = statistics.median(rates)
+    line = {
+        "impl": "reference", "metric": f"GFLOP/s ({wl.key}, {prec})", "value": value,
+        "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True,
+        "scaling": "strong" if wl.sharded and world > 1 else "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": wl.desc + " (reference CPU executor on a slice per core; rate "
+                                         "extrapolates)", "baseline_config": wl.config},
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": pool.cores,
+                         "kind": "reference", "sample": pool.describe(statistics.median(per))},
+        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
 
 
 def main():
@@ -633,14 +879,18 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="mm", choices=["mm", "conv", "ls", "linear32",
-                                                         "ewise", "sweep"])
+    ap.add_argument("--workload", default="auto",
+                    choices=["auto", "mm", "conv", "ls", "linear32", "ewise", "sweep"])
+    ap.add_argument("--tiles", default=None, help="e.g. 8x8: the mm nest tiled by the "
+                                                  "reference pass (parallel form)")
     ap.add_argument("--precision", default=None, choices=["bf16", "tf32", "exact"])
+    ap.add_argument("--min-seconds", type=float, default=1.0,
+                    help="length of the sustained and e2e timed regions")
     args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3   # the contract's minimum warm-up
     rank, world, local = dist_setup()
-    if args.workload == "sweep":
-        run_sweep(args, rank, world, local, args.impl)
-    elif args.impl == "reference":
+    if args.impl == "reference":
         run_reference(args, rank, world)
     else:
         run_ours(args, rank, world, local)

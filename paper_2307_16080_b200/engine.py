@@ -116,11 +116,12 @@ def _where(loc):
 class _Run:
     """One run() call: host walk of the entry tape + device regions."""
 
-    def __init__(self, program, ctx, backend=None):
+    def __init__(self, program, ctx, backend=None, shard=None):
         self.program = program
         self.ctx = ctx
         self.be = backend if backend is not None else DeviceBackend(stream_io=STREAM_IO)
         self.plan = []
+        self.shard = shard    # shard.Shard: run only this rank's batch rows
         self.pending = []     # queued MapItem / ContractItem, program order
 
     # -- host walk (mirrors interp/_evalpy.py:81-232 for top-level scalars) --
@@ -235,6 +236,12 @@ class _Run:
         except Unsupported as exc:
             self.flush_pending()
             raise E.ModeUnsupported(f"b200 engine: {exc}") from None
+        if self.shard is not None:   # batch-sharded run (shard.py)
+            try:
+                self.shard.restrict(r, accesses, getattr(self.be, "stage", None))
+            except E.ModeUnsupported:
+                self.flush_pending()
+                raise
         if _region_hook is not None:   # races.check_races: static race proof
             _region_hook(r, accesses)
         links, remainder = analysis.chain_of(r)
@@ -374,10 +381,11 @@ def _cmpi(p, a, b):
     return (a == b, a != b, a < b, a <= b, a > b, a >= b)[p]
 
 
-def run_tape(program, code, regs, tally, ctx, backend=None):
-    """Engine-protocol entry point (machine.py:112)."""
+def run_tape(program, code, regs, tally, ctx, backend=None, shard=None):
+    """Engine-protocol entry point (machine.py:112).  ``shard``: a
+    shard.Shard — execute only this rank's batch rows (shard.run)."""
     global last_plan
-    run = _Run(program, ctx, backend)
+    run = _Run(program, ctx, backend, shard)
     try:
         rets = run.exec_tape(code, regs, tally)
         run.flush_pending()
@@ -424,9 +432,13 @@ class Session:
     ``forget(buf)``).
     """
 
-    def __init__(self):
+    def __init__(self, shard=None):
         self.be = DeviceBackend()
         self.plan = []
+        # (rank, world): every run executes only this rank's batch rows
+        # (shard.py); the Session's device copies hold those rows
+        self.shard = shard
+        self.last_shard = None
 
     def _engine(self):
         sess = self
@@ -436,7 +448,12 @@ class Session:
 
             @staticmethod
             def run_tape(program, code, regs, tally, ctx):
-                run = _Run(program, ctx, sess.be)
+                sh = None
+                if sess.shard is not None:
+                    from .shard import Shard
+
+                    sh = sess.last_shard = Shard(*sess.shard)
+                run = _Run(program, ctx, sess.be, sh)
                 try:
                     rets = run.exec_tape(code, regs, tally)
                 finally:

@@ -52,32 +52,51 @@ def _size(buf):
     return math.prod(buf.shape)
 
 
-def _covers(m, buf):
-    """The map's store writes every element of buf exactly once."""
-    return math.prod(m.trips) == _size(buf)
+def _map_span(m, k):
+    """The element range [lo, hi) operand k of a map touches, when it is a
+    dense range walked once (one progression of unit stride over the box,
+    e.g. a whole buffer, a batch shard's rows or a tiled nest's origin +
+    offset loops), else None."""
+    w = _walk([(c, 0, t) for c, t in zip(m.coefs[k], m.trips) if t > 1])
+    if w is None or w[0] not in (0, 1):
+        return None
+    return m.bases[k], m.bases[k] + w[2]
+
+
+def _contract_span(g):
+    """The element range of C a contraction writes, when dense (rows of a
+    row-major C: the whole buffer or a batch shard's rows), else None."""
+    if g.strided and tuple(g.sC) == (g.N, 1):
+        return g.offC, g.offC + g.M * g.N
+    if g.M * g.N == _size(g.C):
+        # distinct outputs (match_contraction proves injectivity) as many as
+        # the buffer's elements: every element, whatever the index maps
+        return 0, _size(g.C)
+    return None
 
 
 def _fill(item):
-    """(buffer, value) if item is a full-buffer constant fill."""
+    """(buffer, value, span) if item is a dense constant fill."""
     if isinstance(item, MapItem) and item.m.kind == "fill" and len(item.m.buffers) == 1:
-        buf = item.m.buffers[0]
-        if _covers(item.m, buf):
-            return buf, item.m.consts[0]
+        span = _map_span(item.m, 0)
+        if span is not None:
+            return item.m.buffers[0], item.m.consts[0], span
     return None
 
 
 def _copy(item):
-    """(dst, src) if item is a full-buffer copy."""
+    """(dst, dst span, src, src span) if item is a dense copy."""
     if isinstance(item, MapItem) and item.m.kind == "copy" and len(item.m.buffers) == 2:
         src, dst = item.m.buffers
-        if _covers(item.m, dst) and src is not dst:
-            return dst, src
+        ss, ds = _map_span(item.m, 0), _map_span(item.m, 1)
+        if ss is not None and ds is not None and src is not dst:
+            return dst, ds, src, ss
     return None
 
 
-def _contract_covers(item, buf):
+def _contract_covers(item, buf, span):
     g = item.g
-    return g.C is buf and g.M * g.N == _size(buf)
+    return g.C is buf and _contract_span(g) == span
 
 
 def _walk(dims):
@@ -113,7 +132,9 @@ def _bias(citem, item):
         return None
     if o_ld is not g.C or o_st is not g.C or b_ld is g.C:
         return None
-    if m.bases[0] != m.bases[2] or m.coefs[0] != m.coefs[2] or not _covers(m, g.C):
+    if m.bases[0] != m.bases[2] or m.coefs[0] != m.coefs[2]:
+        return None
+    if _contract_span(g) is None or _map_span(m, 2) != _contract_span(g):
         return None
     if b_ld.dtype != g.C.dtype or m.bases[0] != g.offC:
         return None
@@ -140,11 +161,14 @@ def fuse(items):
         it = items[i]
         f = _fill(it)
         # fill(T); copy(O <- T); contract(O)  ->  fill(T); contract(O, init)
+        # (the copy reads only filled elements of T and writes exactly the
+        # contraction's output range)
         if f is not None and i + 2 < n:
             c = _copy(items[i + 1])
             nxt = items[i + 2]
-            if c is not None and c[1] is f[0] and isinstance(nxt, ContractItem) and \
-                    _contract_covers(nxt, c[0]) and nxt.g.dtype == "f32":
+            if c is not None and c[2] is f[0] and f[2][0] <= c[3][0] and c[3][1] <= f[2][1] \
+                    and isinstance(nxt, ContractItem) and _contract_covers(nxt, c[0], c[1]) \
+                    and nxt.g.dtype == "f32":
                 out.append(it)
                 nxt.init, nxt.init_value = 1, f[1]
                 nxt.fused += ["copy", "init"]
@@ -153,7 +177,7 @@ def fuse(items):
                 continue
         # fill(O); contract(O)  ->  contract(O, init)
         if f is not None and i + 1 < n and isinstance(items[i + 1], ContractItem) and \
-                _contract_covers(items[i + 1], f[0]) and items[i + 1].g.dtype == "f32":
+                _contract_covers(items[i + 1], f[0], f[2]) and items[i + 1].g.dtype == "f32":
             nxt = items[i + 1]
             nxt.init, nxt.init_value = 1, f[1]
             nxt.fused += ["fill"]
@@ -174,8 +198,10 @@ def fuse(items):
 
 
 def _dense_rows(buf, off, s, rows, cols):
-    """The operand is the whole buffer, row-major (rows x cols)."""
-    return off == 0 and tuple(s) == (cols, 1) and rows * cols == _size(buf)
+    """The operand is whole rows of a row-major buffer (rows x cols): all of
+    it, or a batch shard's rows."""
+    return tuple(s) == (cols, 1) and off % cols == 0 and off + rows * cols <= _size(buf) \
+        and cols > 0
 
 
 def plan_shadows(items):
@@ -201,7 +227,7 @@ def plan_shadows(items):
             if isinstance(c, ContractItem):
                 cg = c.g
                 if cg.A is pg.C and cg.strided and cg.C is not pg.C and cg.B is not pg.C and \
-                        cg.M == pg.M and cg.K == pg.N and \
+                        cg.M == pg.M and cg.K == pg.N and cg.offA == pg.offC and \
                         _dense_rows(cg.A, cg.offA, cg.sA, cg.M, cg.K):
                     p.shadow_out = c.shadow_in = True
                     break

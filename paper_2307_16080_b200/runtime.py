@@ -184,6 +184,9 @@ class Staging:
         self.d2h_bytes = 0
         self.panels = 0      # row panels run with pipelined copies (stream_rows)
         self._wb_event = None   # last streamed write-back (see stream_rows)
+        # batch shards (shard.py): id(Buffer) -> (r0, r1), the leading-dim rows
+        # this rank owns; only those rows are copied in and out
+        self.rows = {}
 
     @property
     def stream_ptr(self):
@@ -203,8 +206,16 @@ class Staging:
         ent = self.dev.get(id(buf))
         if ent is None or ent[0] is not buf:
             host = self.host(buf)
+            rows = self.rows.get(id(buf))
             if overwrite:
                 t = self.torch.empty_like(host, device="cuda")
+            elif rows is not None:
+                # a batch shard: this rank's rows only (the rest is never read)
+                pin_host(buf.data, host)
+                t = self.torch.empty_like(host, device="cuda")
+                h, d = self._row_views(buf, host, t, rows)
+                d.copy_(h)
+                self._count(h2d=h.numel() * h.element_size())
             else:
                 pin_host(buf.data, host)
                 t = host.to("cuda", non_blocking=False)
@@ -212,6 +223,13 @@ class Staging:
             ent = (buf, t)
             self.dev[id(buf)] = ent
         return ent[1]
+
+    @staticmethod
+    def _row_views(buf, host, dev, rows):
+        """The (host, device) views of leading-dim rows [r0, r1) of buf."""
+        r = buf.shape[0]
+        r0, r1 = rows
+        return host.view(r, -1)[r0:r1], dev.view(r, -1)[r0:r1]
 
     def mark_dirty(self, buf):
         self.dirty.add(id(buf))
@@ -229,6 +247,9 @@ class Staging:
                 continue   # marked but never staged: the device never touched it
             buf, t = self.dev[key]
             host = self.host(buf)
+            rows = self.rows.get(key)
+            if rows is not None:
+                host, t = self._row_views(buf, host, t, rows)
             host.copy_(t)
             self._count(d2h=host.numel() * host.element_size())
         self.dirty.clear()
@@ -250,7 +271,8 @@ class Staging:
         (registered in ``dev``); the current stream then waits for the
         write-backs, so later kernels cannot overwrite rows still being
         copied out.  ``panels``: [(r0, r1)] covering the leading dimension
-        (or ``rows`` equal slices of every buffer's flat storage).
+        (or ``rows`` equal slices of every buffer's flat storage); they may
+        cover a sub-range of the rows (a batch shard's).
         """
         torch = self.torch
         cur = torch.cuda.current_stream()
@@ -286,7 +308,7 @@ class Staging:
                 with torch.cuda.stream(down):
                     ho[r0:r1].copy_(to[r0:r1], non_blocking=True)
                 self._count(d2h=(r1 - r0) * to.shape[1] * esz)
-        assert panels[-1][1] == rows
+        assert panels[-1][1] <= rows
         if written_back:
             self._wb_event = torch.cuda.Event()
             self._wb_event.record(down)
@@ -531,10 +553,17 @@ def _row_major(buf):
     return tuple(buf.strides) == tuple(reversed(st))
 
 
-def _rows_of(buf, rows, cols):
-    """buf is exactly a dense row-major rows x cols block (leading dim = rows)."""
-    return (len(buf.shape) >= 1 and buf.shape[0] == rows and _row_major(buf) and
-            math.prod(buf.shape) == rows * cols)
+def _gemm_rows(buf, off, s, rows, cols):
+    """(r0, r1): the operand is rows r0 .. r1-1 of a row-major buffer whose
+    leading-dim rows are ``cols`` elements wide (stride (cols, 1)), else None."""
+    if tuple(s) != (cols, 1) or not buf.shape or not _row_major(buf) or cols <= 0:
+        return None
+    if math.prod(buf.shape[1:]) != cols or off % cols:
+        return None
+    r0 = off // cols
+    if r0 + rows > buf.shape[0]:
+        return None
+    return r0, r0 + rows
 
 
 def row_panels(rows, row_bytes, align):
@@ -655,18 +684,22 @@ class DeviceBackend:
                        getattr(g, "tiles", None))
         self.last_cta = cta
         bias_ptr = s.tensor(bias).data_ptr() + esz * bias_base if bias is not None else None
-        dense_c = (g.strided and g.offC == 0 and tuple(g.sC) == (g.N, 1) and
-                   _rows_of(g.C, g.M, g.N))
+        # C rows [c0, c1) of a row-major buffer of N-wide rows, all staged rows
+        # (the whole buffer, or a batch shard's rows)
+        crows = _gemm_rows(g.C, g.offC, g.sC, g.M, g.N) if g.strided else None
+        dense_c = crows is not None and self._owned(g.C, *crows)
         if (g.strided and g.dtype == "f32" and dense_c and
                 self._streaming(g.C, g.A, g.B, bias)):
-            stream_a = (not s.staged(g.A) and g.A is not g.B and g.offA == 0 and
-                        tuple(g.sA) == (g.K, 1) and _rows_of(g.A, g.M, g.K))
+            stream_a = (not s.staged(g.A) and g.A is not g.B and
+                        _gemm_rows(g.A, g.offA, g.sA, g.M, g.K) == crows and
+                        self._owned(g.A, *crows))
             panels = row_panels(g.M, 4 * (g.N * (1 if init else 2) + (g.K if stream_a else 0)),
                                 256)
             if panels is not None:
+                panels = [(crows[0] + a, crows[0] + b) for a, b in panels]
                 return self._gemm_streamed(g, precision, panels, stream_a, init, init_value,
                                            bias_ptr, bias_stride, shadow_out, shadow_in,
-                                           last_writer, cta)
+                                           last_writer, cta, crows[0])
         tA, tB = s.tensor(g.A), s.tensor(g.B)
         # a fused fill over all of a dense C: its old contents are never read
         tC = s.tensor(g.C, overwrite=bool(init) and dense_c and g.C is not g.A and
@@ -675,7 +708,8 @@ class DeviceBackend:
             a_packed = c16 = None
             if precision == "bf16" and tc_supported(precision, g.K):
                 sh = self._shadow
-                if shadow_in and sh is not None and sh[0] == (tA.data_ptr(), g.M, g.K):
+                if shadow_in and sh is not None and \
+                        sh[0] == (tA.data_ptr() + 4 * g.offA, g.M, g.K):
                     a_packed = sh[1]
                 if shadow_out and tc_supported(precision, g.N):
                     c16 = workspace(4 + (self._shadow_slot ^ 1), "bfloat16", g.M, g.N)
@@ -688,7 +722,7 @@ class DeviceBackend:
             self._shadow = None
             if c16 is not None:
                 self._shadow_slot ^= 1
-                self._shadow = ((tC.data_ptr(), g.M, g.N), c16)
+                self._shadow = ((tC.data_ptr() + 4 * g.offC, g.M, g.N), c16)
             self.last_shadow = (a_packed is not None, c16 is not None)
             return names
         return self._contract_tables(g, tA, tB, tC, init, init_value, bias_ptr, bias_stride)
@@ -708,11 +742,12 @@ class DeviceBackend:
         warnings.warn(msg, PrecisionFallback, stacklevel=3)
 
     def _gemm_streamed(self, g, precision, panels, stream_a, init, init_value, bias_ptr,
-                       bias_stride, shadow_out, shadow_in, last_writer, cta=None):
+                       bias_stride, shadow_out, shadow_in, last_writer, cta=None, row0=0):
         """C (+)= A.B over row panels of M with the host copies pipelined
         (Staging.stream_rows): panel p's GEMM overlaps the upload of panel
         p+1 and the write-back of panel p-1.  B is uploaded (and, on the
-        tensor-core path, packed) once."""
+        tensor-core path, packed) once.  ``panels``: absolute rows of C (and
+        of A when streamed), starting at C's first row ``row0``."""
         s = self.stage
         tB = s.tensor(g.B)
         a_packed = c16 = Bp = None
@@ -721,7 +756,7 @@ class DeviceBackend:
             tA = s.tensor(g.A)
             sh = self._shadow
             if (tc and precision == "bf16" and shadow_in and sh is not None and
-                    sh[0] == (tA.data_ptr(), g.M, g.K)):
+                    sh[0] == (tA.data_ptr() + 4 * g.offA, g.M, g.K)):
                 a_packed = sh[1]
         if tc:
             Bp = pack_b(s.lib, precision, tB.data_ptr() + 4 * g.offB, g.sB, g.N, g.K,
@@ -732,13 +767,14 @@ class DeviceBackend:
 
         def launch(r0, r1):
             tA, tC = s.dev[id(g.A)][1], s.dev[id(g.C)][1]
+            q0, q1 = r0 - row0, r1 - row0      # rows of the GEMM
             names[:] = launch_gemm(
-                s.lib, precision, tA.data_ptr() + 4 * (g.offA + r0 * g.sA[0]), g.sA,
+                s.lib, precision, tA.data_ptr() + 4 * (g.offA + q0 * g.sA[0]), g.sA,
                 tB.data_ptr() + 4 * g.offB, g.sB, tC.data_ptr() + 4 * (r0 * g.N), g.sC,
-                r1 - r0, g.N, g.K, s.stream_ptr, init=init, init_value=init_value,
+                q1 - q0, g.N, g.K, s.stream_ptr, init=init, init_value=init_value,
                 bias_ptr=bias_ptr, bias_stride=bias_stride, call=self.call,
-                c16=c16[r0:r1] if c16 is not None else None, b_packed=Bp,
-                a_packed=a_packed[r0:r1] if a_packed is not None else None, cta=cta)
+                c16=c16[q0:q1] if c16 is not None else None, b_packed=Bp,
+                a_packed=a_packed[q0:q1] if a_packed is not None else None, cta=cta)
 
         s.stream_rows(panels, [g.A] if stream_a else [], (g.C, not init), launch)
         if last_writer:
@@ -746,7 +782,7 @@ class DeviceBackend:
         self._shadow = None
         if c16 is not None:
             self._shadow_slot ^= 1
-            self._shadow = ((s.dev[id(g.C)][1].data_ptr(), g.M, g.N), c16)
+            self._shadow = ((s.dev[id(g.C)][1].data_ptr() + 4 * g.offC, g.M, g.N), c16)
         self.last_shadow = (a_packed is not None, c16 is not None)
         return (["pack_operand"] if tc else []) + names
 
@@ -767,28 +803,41 @@ class DeviceBackend:
                   P(bias_ptr) if bias_ptr else None, bias_stride, s.stream_ptr)
         return ["contract_exact"]
 
+    def _owned(self, buf, r0, r1):
+        """Rows [r0, r1) of buf are all the rows this run stages (the whole
+        buffer, or exactly a batch shard's rows)."""
+        rows = self.stage.rows.get(id(buf))
+        return (r0, r1) == (rows if rows is not None else (0, buf.shape[0]))
+
     def _conv_panels(self, cv, esz, init):
         """Image panels for a streamed conv, or (None, False)."""
         s = self.stage
+        n0, n1 = cv.n0, cv.n0 + cv.nb
         if not (self._streaming(cv.out, cv.inp, cv.ker) and _row_major(cv.out) and
-                cv.out.shape[0] == cv.nb):
+                self._owned(cv.out, n0, n1)):
             return None, False
         stream_in = (not s.staged(cv.inp) and cv.inp is not cv.ker and _row_major(cv.inp) and
-                     cv.inp.shape[0] == cv.nb)
+                     self._owned(cv.inp, n0, n1))
         row = esz * (cv.out.strides[0] * (1 if init else 2) +
                      (cv.inp.strides[0] if stream_in else 0))
-        return row_panels(cv.nb, row, 1), stream_in
+        panels = row_panels(cv.nb, row, 1)
+        if panels is not None:
+            panels = [(n0 + a, n0 + b) for a, b in panels]
+        return panels, stream_in
 
     def _conv_run(self, cv, esz, init, last_writer, launch):
-        """launch(inp_ptr, out_ptr, nb) over the whole batch, or over image
-        panels with the host copies pipelined (Staging.stream_rows)."""
+        """launch(inp_ptr, out_ptr, nb) over the conv's images [n0, n0 + nb),
+        or over image panels with the host copies pipelined
+        (Staging.stream_rows)."""
         s = self.stage
         panels, stream_in = self._conv_panels(cv, esz, init)
         if panels is None:
             inp = s.tensor(cv.inp)
             out = s.tensor(cv.out, overwrite=bool(init) and _row_major(cv.out) and
+                           self._owned(cv.out, cv.n0, cv.n0 + cv.nb) and
                            cv.out is not cv.inp and cv.out is not cv.ker)
-            launch(inp.data_ptr(), out.data_ptr(), cv.nb)
+            launch(inp.data_ptr() + esz * cv.n0 * cv.inp.strides[0],
+                   out.data_ptr() + esz * cv.n0 * cv.out.strides[0], cv.nb)
             return
         if not stream_in:
             s.tensor(cv.inp)

@@ -17,10 +17,12 @@ variables in nesting order).  Trip-1 variables are constants.  Then
     C[cM(m) + cN(n)] = C[..] + sum_k A[aM(m) + aK(k)] * B[bK(k) + bN(n)]
 
 where each offset function is a per-group table (mixed-radix enumeration of
-that group's variables).  A contraction with exactly one variable per group
-is a plain strided GEMM (and can use the tensor-core path); anything else
-(conv = implicit GEMM with M = (n, ho, wo), N = co, K = (ci, ki, kj), tiled
-nests whose M/N dims are origin + offset pairs, ...) uses offset tables.
+that group's variables).  A contraction whose every group walks one
+arithmetic progression in its operands — a single variable, or the origin +
+offset pair of a tiled nest (passes/tiling.py:56-80) — is a plain strided
+GEMM (and can use the tensor-core path; the tile sizes are kept to choose
+the CTA tile); anything else (conv = implicit GEMM with M = (n, ho, wo),
+N = co, K = (ci, ki, kj), ...) uses offset tables or the conv kernels.
 """
 from __future__ import annotations
 
@@ -278,7 +280,8 @@ class ConvView:
     """A contraction that is exactly conv_2d_nchw_fchw (valid, stride 1)."""
 
     __slots__ = ("nb", "c", "hp", "wp", "f", "ho", "wo", "kh", "kw", "inp", "ker", "out",
-                 "k_order")   # k_order: the reduction variables' roles in nest order
+                 "k_order",   # k_order: the reduction variables' roles in nest order
+                 "n0")        # first image (a batch shard's range starts there)
 
     def __repr__(self):
         return (f"ConvView(nb={self.nb}, c={self.c}, {self.hp}x{self.wp} -> f={self.f}, "
@@ -300,15 +303,22 @@ def conv_view(region, g, dtypes=("f32",)):
     if len(A.shape) != 4 or len(B.shape) != 4 or len(C.shape) != 4:
         return None
     sa, sb, sc = A.strides, B.strides, C.strides
-    # the operands' base offsets must be 0 (all loops start at 0)
-    if tuple(g.origins) != (0, 0, 0):
-        return None
+    offA, offB, offC = _offsets(region, g)
+    # every loop starts at 0, except that a single batch loop may start at
+    # n0 (a batch shard, shard.py): the operands' base offsets are then
+    # n0 whole images of the input and the output
+    n0 = 0
     for v in g.m_vars + g.n_vars + g.k_vars:
         lb, st, t = g.stat(v)
-        if lb != 0 or st < 1:
+        if st < 1:
             return None
+        if lb != 0:
+            if n0 or (offC.t.get(v.id, 0), offA.t.get(v.id, 0)) != (sc[0], sa[0]) or st != 1:
+                return None
+            n0 = lb
+    if tuple(g.origins) != (n0 * sa[0], 0, n0 * sc[0]):
+        return None
     # classify each variable by its coefficient signature
-    offA, offB, offC = _offsets(region, g)
     roles = {}
     for v in g.m_vars:
         sig = (offC.t.get(v.id, 0), offA.t.get(v.id, 0))
@@ -347,9 +357,14 @@ def conv_view(region, g, dtypes=("f32",)):
     cv.c, cv.kh, cv.kw = extent("ci"), extent("ki"), extent("kj")
     if None in (cv.nb, cv.f, cv.ho, cv.wo):
         return None
-    if A.shape[0] != cv.nb or A.shape[1] != cv.c or C.shape != (cv.nb, cv.f, cv.ho, cv.wo) or \
+    if n0 and len(roles.get("n", ())) != 1:
+        return None
+    if A.shape[0] != C.shape[0] or n0 + cv.nb > A.shape[0] or (not n0 and A.shape[0] != cv.nb):
+        return None
+    if A.shape[1] != cv.c or C.shape[1:] != (cv.f, cv.ho, cv.wo) or \
             B.shape != (cv.f, cv.c, cv.kh, cv.kw):
         return None
+    cv.n0 = n0
     cv.hp, cv.wp = A.shape[2], A.shape[3]
     if cv.hp < cv.ho + cv.kh - 1 or cv.wp < cv.wo + cv.kw - 1:
         return None

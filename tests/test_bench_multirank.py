@@ -1,12 +1,13 @@
 """bench.py's multi-rank plumbing on CPU (gloo, world size 2).
 
 The driver launches `bench.py --gpus N` under torch.distributed.run, one rank
-per GPU over NCCL; the only collectives are the timing max-over-ranks and one
-all-gather of per-rank checksums.  Here the same helpers run over
-gloo with two CPU processes: batch shards of the conv / Linear-stack
-workloads partition the batch exactly, max_over_ranks returns the slowest
-rank's time on every rank, and gather_checksums returns every rank's value in
-rank order.
+per GPU over NCCL; besides shard.gather (tests/test_shard.py) the only
+collectives are the timing max-over-ranks and one all-gather of per-rank
+checksums.  Here the same helpers run over gloo with two CPU
+processes: the conv / Linear-stack workloads are the global batch (sharded
+by paper_2307_16080_b200.shard at run time, contiguous halves), max_over_ranks
+returns the slowest rank's time on every rank, and gather_checksums returns
+every rank's value in rank order.
 """
 import os
 import socket
@@ -36,13 +37,18 @@ def _worker(rank, world, port, out_dir):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
     try:
-        conv, ls = bench.Workload("conv", world), bench.Workload("ls", world)
+        from paper_2307_16080_b200 import shard
+
+        conv, ls = bench.Workload("conv"), bench.Workload("ls")
         t = bench.max_over_ranks(1.0 + rank, world)
         sums = bench.gather_checksums(10.0 * rank + 0.5, world)
         bench.barrier(world)
+        nb = conv.fn.func_op.body().args[0].type.shape[0]
+        rows = ls.fn.func_op.body().args[0].type.shape[0]
         with open(os.path.join(out_dir, f"r{rank}.txt"), "w") as fh:
-            fh.write(repr((conv.shapes()[0][0], conv.flops, ls.shapes()[0][0], t, sums,
-                           conv.scaling, bench.Workload("mm", world).scaling)))
+            fh.write(repr((shard.chunk(nb, rank, world), conv.flops,
+                           shard.chunk(rows, rank, world), t, sums,
+                           conv.sharded, bench.Workload("mm").sharded)))
     finally:
         dist.destroy_process_group()
 
@@ -55,10 +61,10 @@ def test_two_rank_helpers_over_gloo():
     with tempfile.TemporaryDirectory() as d:
         mp.spawn(_worker, args=(2, _free_port(), d), nprocs=2, join=True)
         res = [eval(open(os.path.join(d, f"r{r}.txt")).read()) for r in range(2)]
-    full = bench.Workload("conv", 1)
-    for nb, flops, rows, t, sums, conv_scaling, mm_scaling in res:
-        assert nb == 128 and 2 * flops == full.flops      # the batch split exactly in two
-        assert rows == 32768
+    assert [r[0] for r in res] == [(0, 128), (128, 256)]          # contiguous image halves
+    assert [r[2] for r in res] == [(0, 32768), (32768, 65536)]    # contiguous row halves
+    for _, flops, _, t, sums, conv_sharded, mm_sharded in res:
+        assert flops == 2.0 * 256 * 64 * 56 * 56 * 64 * 9        # the global batch's work
         assert t == 2.0                                  # the slowest rank, on every rank
         assert sums == [0.5, 10.5]                       # rank order
-        assert (conv_scaling, mm_scaling) == ("strong", "weak")
+        assert (conv_sharded, mm_sharded) == (True, False)
