@@ -410,6 +410,12 @@ last_staging = None
 _region_hook = None   # callable(region, accesses) or None (races.check_races)
 
 
+def release_last_staging():
+    """Drop the last run's device copies (kept for device_copy)."""
+    global last_staging
+    last_staging = None
+
+
 def device_copy(buf):
     """The last run's device tensor of ``buf`` (same contents), or None."""
     st = last_staging

@@ -85,7 +85,10 @@ def _disk_put(key, image):
 def compile_kernel(src, name):
     """Compile (cached in memory and on disk) and return the opaque CUfunction."""
     key = cache_key(src)
-    fn = _CACHE.get(key)
+    # a CUfunction belongs to the context it was loaded in: key the in-memory
+    # cache by device too (the on-disk cubins are context-free)
+    mkey = (_device(), key)
+    fn = _CACHE.get(mkey)
     if fn is None:
         lib = load_library()
         image = _disk_get(key) if DISK else None
@@ -103,8 +106,17 @@ def compile_kernel(src, name):
         if fresh and DISK:
             _disk_put(key, image)
         fn = out.value
-        _CACHE[key] = fn
+        _CACHE[mkey] = fn
     return fn
+
+
+def _device():
+    try:
+        import torch
+
+        return torch.cuda.current_device() if torch.cuda.is_available() else -1
+    except Exception:
+        return -1
 
 
 def _flit(v):
@@ -124,8 +136,15 @@ def map_source(m):
     trips = list(m.trips)
     total = math.prod(trips) // (4 if vec else 1)
     name = "b200_map_jit"
+    # operands are per access, not per buffer: an in-place body (the bias
+    # nest's C is loaded and stored) passes one buffer as several pointers,
+    # so __restrict__ (no aliasing) is only true when every operand is a
+    # distinct buffer — otherwise the compiler could reorder a load above a
+    # store to the same address
+    distinct = len({id(b) for b in m.buffers}) == nops
+    qual = " __restrict__" if distinct else ""
     L = [f'extern "C" __global__ void __launch_bounds__(256) {name}(',
-         ", ".join(f"float* __restrict__ p{k}" for k in range(nops)) + ") {",
+         ", ".join(f"float*{qual} p{k}" for k in range(nops)) + ") {",
          f"  for (long long w = (long long)blockIdx.x * 256 + threadIdx.x; w < {total}LL;"
          f" w += (long long)gridDim.x * 256) {{",
          "    long long rem = w;"]

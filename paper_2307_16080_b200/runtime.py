@@ -358,17 +358,30 @@ def _copy_streams(torch):
 
 PRECISIONS = ("exact", "tf32", "bf16")
 _WORKSPACE = {}
+_RETIRED = []
 
 
 def workspace(slot, dtype, rows, cols):
-    """Cached device scratch for packed tensor-core operands."""
+    """Device scratch for packed tensor-core operands: one growable buffer
+    per (slot, dtype, device), returned as a rows x cols view of its front.
+
+    A buffer too small for a request is replaced by one of max(need, 2 x old)
+    elements, so a process that sees many shapes (streamed panels, conv
+    packs per image count, tuner trials) holds at most ~2x the largest
+    request per slot instead of one buffer per shape.  Replaced buffers are
+    retired, not freed: a Recording may still point into them (their total
+    is bounded by the geometric growth)."""
     torch = torch_mod()
-    key = (slot, dtype, rows, cols, torch.cuda.current_device())
+    key = (slot, dtype, torch.cuda.current_device())
+    need = max(1, rows * cols)
     t = _WORKSPACE.get(key)
-    if t is None:
-        t = torch.empty(rows, cols, dtype=getattr(torch, dtype), device="cuda")
+    if t is None or t.numel() < need:
+        if t is not None:
+            _RETIRED.append(t)
+        size = need if t is None else max(need, 2 * t.numel())
+        t = torch.empty(size, dtype=getattr(torch, dtype), device="cuda")
         _WORKSPACE[key] = t
-    return t
+    return t[:rows * cols].view(rows, cols)
 
 
 def tc_supported(precision, K):
@@ -680,8 +693,8 @@ class DeviceBackend:
                 self._fallback(precision, "index maps are not one strided GEMM")
             elif not tc_supported(precision, g.K):
                 self._fallback(precision, f"K={g.K} rows not 16-byte aligned")
-        cta = cta_tile(precision if g.strided and tc_supported(precision, g.K) else "exact",
-                       getattr(g, "tiles", None))
+        cta = cta_tile(precision if tc_supported(precision, g.K) else "exact",
+                       getattr(g, "tiles", None)) if g.strided and g.dtype == "f32" else None
         self.last_cta = cta
         bias_ptr = s.tensor(bias).data_ptr() + esz * bias_base if bias is not None else None
         # C rows [c0, c1) of a row-major buffer of N-wide rows, all staged rows

@@ -22,8 +22,11 @@ same way.  ``one_plus_one_es`` depends on earlier costs (search.py:226-234,
 (an extension) evaluates λ mutations of the parent per
 generation, sharded over the ranks, and equals (1+1)-ES at λ = 1.
 
-Trials run on the B200 engine (``install()`` is applied for the duration),
-which is what the reference ``run()`` inside ``_Session`` dispatches to.
+Trials run on the B200 engine: the session passes it to every run()
+explicitly (no module-global patching).  With several ranks, an exception in
+a trial is exchanged like a record and re-raised on every rank (the lowest
+index first, as the sequential reference would raise it), so no rank is
+left waiting in the all-gather.
 """
 from __future__ import annotations
 
@@ -111,14 +114,23 @@ def _fast_buffers_close(got, want):
 
 
 def _session_class():
+    """The reference trial session (tuner/search.py:151-201) bound to an
+    engine and with a vectorised equivalence guard.
+
+    ``__init__`` and ``trial`` restate the reference's (same baseline run,
+    pass pipeline, skip rules, guard and scoring) with two differences: every
+    run() goes to the session's engine explicitly — no patching of
+    ``machine._engine`` — and the guard is ``_state_matches`` below, the
+    reference predicate (search.py:115-127) evaluated on the device."""
     ensure_staircase()
     import importlib
 
     # the module (staircase.tuner re-exports the function under the same name)
     ref = importlib.import_module("staircase.tuner.search")
-
-    class Session(ref._Session):
-        """The reference trial session with a vectorised equivalence guard."""
+    from staircase.errors import PassFailure, StaircaseError, VerificationFailed
+    from staircase.interp import machine
+    from staircase.passes import run_pipeline
+    from staircase.tuner.space import Trial
 
     def _state_matches(got_results, got_args, want_results, want_args):
         from staircase.interp import Buffer
@@ -136,7 +148,61 @@ def _session_class():
                 return False
         return True
 
-    return Session, ref, _state_matches
+    class Session(ref._Session):
+        """The reference trial session on a given engine."""
+
+        def __init__(self, module, engine, func=None, seed=0, objective="model",
+                     pipeline_template=None, mode="sequential", workers=1):
+            if objective not in ("model", "wall"):
+                raise ValueError(f"unknown objective {objective!r}")
+            ref.verify_or_raise(module)
+            self.engine = engine
+            self.module = module
+            self.func_op = ref._find_func(module, func)
+            self.func = self.func_op.attributes["sym_name"].value
+            self.seed = seed
+            self.objective = objective
+            self.template = pipeline_template or ref.default_pipeline
+            self.mode = mode
+            self.workers = workers
+            self.inputs = ref.make_inputs(module, self.func, seed)
+            args = ref._copy_args(self.inputs)
+            results, stats = machine.run(module, self.func, args, mode="sequential",
+                                         engine=engine)
+            self.want_results = results
+            self.want_args = args
+            self.baseline_cost = self._score(stats)
+            self.baseline_stats = stats
+
+        def trial(self, idx, tiles, unroll):
+            params = {"tiles": [int(t) for t in tiles], "unroll": int(unroll)}
+            spec = self.template(params["tiles"], params["unroll"])
+            try:
+                work, _ = run_pipeline(self.module, spec)
+            except (PassFailure, VerificationFailed):
+                return Trial(idx, params, None, "skipped", self.seed)
+            try:
+                args = ref._copy_args(self.inputs)
+                results, stats = machine.run(work, self.func, args, mode=self.mode,
+                                             workers=self.workers, engine=self.engine)
+            finally:
+                if work in self.module.ctx.modules:
+                    self.module.ctx.modules.remove(work)
+            try:
+                ok = _state_matches(results, args, self.want_results, self.want_args)
+            finally:
+                # the guard was the last user of the trial's device copies
+                release = getattr(self.engine, "release_last_staging", None)
+                if release is not None:
+                    release()
+            if not ok:
+                raise StaircaseError(
+                    f"pipeline {spec!r} changed the results of @{self.func}; "
+                    "transformed kernels must match the untransformed run")
+            return Trial(idx, params, self._score(stats), "evaluated", self.seed,
+                         stats=ref._digest(stats))
+
+    return Session, ref
 
 
 def _params(space, budget, seed, strategy):
@@ -173,7 +239,6 @@ def search(kernel, pipeline_template=None, space=None, budget: int = 20, seed: i
     _WANT_DEV.clear()   # baseline device copies belong to one search
     ensure_staircase()
     from staircase.errors import EmptySpace
-    from staircase.interp import machine
     from staircase.tuner.space import Trial
 
     if space is None:
@@ -199,52 +264,70 @@ def search(kernel, pipeline_template=None, space=None, budget: int = 20, seed: i
         from . import engine as b200_engine
 
         engine = b200_engine
-    Session, ref, fast_match = _session_class()
-    saved_engine, saved_match = machine._engine, ref._state_matches
-    machine._engine = engine          # _Session.run() passes no engine= (search.py:170,190)
-    ref._state_matches = fast_match   # same predicate, vectorised
-    try:
-        module = ref._resolve_module(kernel)
-        session = Session(module, func=func, seed=seed, objective=objective,
-                          pipeline_template=pipeline_template, mode=mode, workers=workers)
-        if strategy == "one_plus_one_es":
-            # cost-dependent mutations: sequential by definition; every rank
-            # runs the same replica (no exchange needed)
-            best, log = _es(session, space, budget, seed)
-            return best, log
-        if strategy == "population_es":
-            t_trials = time.perf_counter()
-            best, log = _pop_es(session, space, budget, seed, lam, rank, world, dist)
-            if timing is not None:
-                timing.update(setup_s=t_trials - t_start,
-                              trials_s=time.perf_counter() - t_trials, gather_s=0.0,
-                              trials=sum(1 for t in log if t.idx % world == rank))
-            return best, log
-        identity = space.identity()
-        params = _params(space, budget, seed, strategy)
-        mine = []
-        t_trials = time.perf_counter()
-        for idx in range(budget):
-            if idx % world != rank:
-                continue
-            if idx == 0:
-                t = session.trial(0, identity["tiles"], identity["unroll"])
-            else:
-                tiles, unroll = params[idx]
-                t = session.trial(idx, tiles, unroll)
-            mine.append(_record(t))
-        t_gather = time.perf_counter()
-        records = sorted(_gather(dist, world, mine), key=lambda r: r[0])
-        if timing is not None:
-            timing.update(setup_s=t_trials - t_start, trials_s=t_gather - t_trials,
-                          gather_s=time.perf_counter() - t_gather, trials=len(mine))
-        log = [Trial(i, p, c, s, sd, stats=st) for i, p, c, s, sd, st in records]
-        evaluated = [t for t in log if t.status == "evaluated"]
-        best = min(evaluated, key=lambda t: (t.cost, t.idx))
+    Session, ref = _session_class()
+    module = ref._resolve_module(kernel)
+    session = Session(module, engine, func=func, seed=seed, objective=objective,
+                      pipeline_template=pipeline_template, mode=mode, workers=workers)
+    if strategy == "one_plus_one_es":
+        # cost-dependent mutations: sequential by definition; every rank
+        # runs the same replica (no exchange needed)
+        best, log = _es(session, space, budget, seed)
         return best, log
-    finally:
-        machine._engine = saved_engine
-        ref._state_matches = saved_match
+    if strategy == "population_es":
+        t_trials = time.perf_counter()
+        best, log = _pop_es(session, space, budget, seed, lam, rank, world, dist)
+        if timing is not None:
+            timing.update(setup_s=t_trials - t_start,
+                          trials_s=time.perf_counter() - t_trials, gather_s=0.0,
+                          trials=sum(1 for t in log if t.idx % world == rank))
+        return best, log
+    identity = space.identity()
+    params = _params(space, budget, seed, strategy)
+    mine = []
+    t_trials = time.perf_counter()
+    for idx in range(budget):
+        if idx % world != rank:
+            continue
+        tiles, unroll = ((identity["tiles"], identity["unroll"]) if idx == 0 else
+                         params[idx])
+        rec = _guarded(session, idx, tiles, unroll, world)
+        mine.append(rec)
+        if rec[3] == _FAILED:
+            break   # later trials of this rank cannot matter: idx order decides
+    t_gather = time.perf_counter()
+    records = _raise_first(sorted(_gather(dist, world, mine), key=lambda r: r[0]))
+    if timing is not None:
+        timing.update(setup_s=t_trials - t_start, trials_s=t_gather - t_trials,
+                      gather_s=time.perf_counter() - t_gather, trials=len(mine))
+    log = [Trial(i, p, c, s, sd, stats=st) for i, p, c, s, sd, st in records]
+    evaluated = [t for t in log if t.status == "evaluated"]
+    best = min(evaluated, key=lambda t: (t.cost, t.idx))
+    return best, log
+
+
+_FAILED = "__failed__"
+
+
+def _guarded(session, idx, tiles, unroll, world):
+    """One trial as a record; with several ranks an exception (the guard's
+    StaircaseError, an engine error) becomes a record too, so every rank
+    still reaches the all-gather instead of leaving the others blocked in
+    it.  _raise_first re-raises it on every rank."""
+    if world == 1:
+        return _record(session.trial(idx, tiles, unroll))
+    try:
+        return _record(session.trial(idx, tiles, unroll))
+    except Exception as exc:   # noqa: BLE001 — re-raised after the exchange
+        return (idx, None, None, _FAILED, None, exc)
+
+
+def _raise_first(records):
+    """Re-raise the exception of the lowest-index failed trial — the one the
+    sequential reference would have raised first — on every rank."""
+    for r in records:
+        if r[3] == _FAILED:
+            raise r[5]
+    return records
 
 
 def _gather(dist, world, mine):
@@ -270,18 +353,18 @@ def _pop_es(session, space, budget, seed, lam, rank, world, dist):
     from staircase.tuner.space import Trial
 
     identity = space.identity()
-    records = _gather(dist, world, [_record(session.trial(0, identity["tiles"],
-                                                          identity["unroll"]))]
-                      if rank == 0 else [])
+    records = _raise_first(_gather(dist, world, [
+        _guarded(session, 0, identity["tiles"], identity["unroll"], world)]
+        if rank == 0 else []))
     log = [Trial(i, p, c, s, sd, stats=st) for i, p, c, s, sd, st in records]
     rng = random.Random(seed)
     parent, parent_cost = dict(log[0].params), log[0].cost
     idx = 1
     while idx < budget:
         kids = [(idx + j, _mutate(space, parent, rng)) for j in range(min(lam, budget - idx))]
-        mine = [_record(session.trial(i, tiles, unroll))
+        mine = [_guarded(session, i, tiles, unroll, world)
                 for i, (tiles, unroll) in kids if i % world == rank]
-        gen = sorted(_gather(dist, world, mine), key=lambda r: r[0])
+        gen = _raise_first(sorted(_gather(dist, world, mine), key=lambda r: r[0]))
         gen = [Trial(i, p, c, s, sd, stats=st) for i, p, c, s, sd, st in gen]
         log.extend(gen)
         evaluated = [t for t in gen if t.status == "evaluated"]

@@ -237,8 +237,8 @@ def match_contraction(region, links, remainder, accesses):
     # K: the progression must also be the nest order (outer = larger stride),
     # the order every output's chain is rounded in
     kS = _progression(reversed(g.k_vars), (aA.offset, aB.offset), stat)
-    g.tiles = (_tile(g.m_vars, stat), _tile(g.n_vars, stat))
     g.strided = mS is not None and nS is not None and kS is not None
+    g.tiles = (_tile(g.m_vars, stat), _tile(g.n_vars, stat)) if g.strided else (None, None)
     if g.strided:
         g.sA = (mS[1], kS[0])
         g.sB = (kS[1], nS[1])
@@ -307,17 +307,16 @@ def conv_view(region, g, dtypes=("f32",)):
     # every loop starts at 0, except that a single batch loop may start at
     # n0 (a batch shard, shard.py): the operands' base offsets are then
     # n0 whole images of the input and the output
-    n0 = 0
+    n0 = g.origins[0] // sa[0] if sa[0] > 0 else 0
+    if n0 < 0 or tuple(g.origins) != (n0 * sa[0], 0, n0 * sc[0]):
+        return None
     for v in g.m_vars + g.n_vars + g.k_vars:
         lb, st, t = g.stat(v)
         if st < 1:
             return None
-        if lb != 0:
-            if n0 or (offC.t.get(v.id, 0), offA.t.get(v.id, 0)) != (sc[0], sa[0]) or st != 1:
-                return None
-            n0 = lb
-    if tuple(g.origins) != (n0 * sa[0], 0, n0 * sc[0]):
-        return None
+        if lb != 0 and ((offC.t.get(v.id, 0), offA.t.get(v.id, 0)) != (sc[0], sa[0]) or
+                        st != 1 or lb != n0):
+            return None
     # classify each variable by its coefficient signature
     roles = {}
     for v in g.m_vars:
@@ -357,9 +356,9 @@ def conv_view(region, g, dtypes=("f32",)):
     cv.c, cv.kh, cv.kw = extent("ci"), extent("ki"), extent("kj")
     if None in (cv.nb, cv.f, cv.ho, cv.wo):
         return None
-    if n0 and len(roles.get("n", ())) != 1:
+    if n0 and len(roles.get("n", ())) > 1:
         return None
-    if A.shape[0] != C.shape[0] or n0 + cv.nb > A.shape[0] or (not n0 and A.shape[0] != cv.nb):
+    if n0 + cv.nb > A.shape[0] or n0 + cv.nb > C.shape[0]:
         return None
     if A.shape[1] != cv.c or C.shape[1:] != (cv.f, cv.ho, cv.wo) or \
             B.shape != (cv.f, cv.c, cv.kh, cv.kw):

@@ -283,3 +283,36 @@ def conv_tc_smoke(inp: MemRef[(2, 64, 18, 30), F32], ker: MemRef[(64, 64, 3, 3),
             for ki in range(0, 3):
                 for kj in range(0, 3):
                     out[n, co, ho, wo] += inp[n, ci, ho + ki, wo + kj] * ker[co, ci, ki, kj]
+
+
+@staged
+def store_then_load(x: MemRef[(64, 128), F32], y: MemRef[(64, 128), F32],
+                    z: MemRef[(64, 128), F32]):
+    # a store followed by a load of the same element inside one point: the
+    # JIT map kernel must not treat the two y operands as non-aliasing
+    for i, j in parallel((0, 0), (64, 128)):
+        y[i, j] = constant(3.0, F32)
+        z[i, j] = y[i, j] * x[i, j]
+
+
+@staged
+def conv_ones8(input: MemRef[(1, 1, 8, 8), F64], kernel: MemRef[(1, 1, 3, 3), F64],
+               output: MemRef[(1, 1, 6, 6), F64]):
+    # SPEC.md:568 "conv2d on input 1x1x8x8 ones, kernel 1x3x3 ones -> interior
+    # outputs 9.0" (valid conv: every output is interior)
+    for n, co, ho, wo in parallel((0, 0, 0, 0), (1, 1, 6, 6)):
+        for ci in range(0, 1):
+            for ki in range(0, 3):
+                for kj in range(0, 3):
+                    output[n, co, ho, wo] += input[n, ci, ho + ki, wo + kj] * kernel[co, ci, ki, kj]
+
+
+@staged
+def conv_ones64(inp: MemRef[(2, 64, 10, 30), F32], ker: MemRef[(64, 64, 3, 3), F32],
+                out: MemRef[(2, 64, 8, 28), F32]):
+    # the same known answer through the tcgen05 conv (C = F = 64): 9 * 64
+    for n, co, ho, wo in parallel((0, 0, 0, 0), (2, 64, 8, 28)):
+        for ci in range(0, 64):
+            for ki in range(0, 3):
+                for kj in range(0, 3):
+                    out[n, co, ho, wo] += inp[n, ci, ho + ki, wo + kj] * ker[co, ci, ki, kj]

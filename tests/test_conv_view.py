@@ -63,3 +63,32 @@ def test_single_channel_conv_is_a_conv(monkeypatch):
     cv = templates.conv_view(None, g, ("f32",))
     assert cv is not None
     assert (cv.nb, cv.c, cv.f, cv.ho, cv.wo, cv.kh, cv.kw) == (1, 1, 1, 1280, 1280, 3, 3)
+
+
+@pytest.mark.parametrize("rank,world,rows", [(0, 2, (0, 2)), (1, 2, (2, 4)), (3, 4, (3, 4)),
+                                             (1, 3, (1, 2))])
+def test_batch_shard_conv_is_a_conv(rank, world, rows, monkeypatch):
+    """A batch shard (shard.py) restricts the conv's batch loop to rows
+    [r0, r1): still conv_2d_nchw_fchw, over nb = r1 - r0 images from n0 = r0
+    (a one-image shard has no batch variable left: n0 comes from the
+    operands' base offsets)."""
+    import corpus
+    from paper_2307_16080_b200 import engine, shard, templates
+    from vm_sim import SimBackend
+
+    got = []
+    orig = templates.match_contraction
+
+    def wrap(*a, **k):
+        g = orig(*a, **k)
+        got.append(g)
+        return g
+
+    monkeypatch.setattr(engine.templates, "match_contraction", wrap)
+    fn = corpus.conv_mid          # (4, 16, 34, 34) * (8, 16, 3, 3)
+    shard.run(fn.module, fn.__name__, harness.make_args(fn, 0), rank=rank, world=world,
+              backend=SimBackend())
+    (g,) = [x for x in got if x is not None]
+    cv = templates.conv_view(None, g, ("f32",))
+    assert cv is not None
+    assert (cv.n0, cv.nb, cv.c, cv.f, cv.ho, cv.wo) == (rows[0], rows[1] - rows[0], 16, 8, 32, 32)

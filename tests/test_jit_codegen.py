@@ -82,3 +82,37 @@ def test_disk_kernel_cache_round_trip(tmp_path, monkeypatch):
     assert jit.cache_key(src) != key            # options are part of the key
     (tmp_path / "bad.cubin").write_bytes(b"not an elf")
     assert jit._disk_get("bad") is None
+
+
+def test_aliasing_operands_are_not_restrict(monkeypatch):
+    """Operands are per access: a body that stores y and then loads y passes
+    y twice, so the generated kernel must not declare its pointers
+    __restrict__ (jit.py restrict aliasing); kernels whose
+    operands are distinct buffers keep it."""
+    from paper_2307_16080_b200 import jit
+
+    maps = []
+    for fn in (corpus.store_then_load, corpus.ewise_ops, corpus.saxpy_f32):
+        maps += [m for m in _maps(fn, monkeypatch) if m is not None]
+    seen = set()
+    for m in maps:
+        distinct = len({id(b) for b in m.buffers}) == len(m.buffers)
+        assert ("__restrict__" in jit.map_source(m)[0]) == distinct
+        seen.add(distinct)
+    assert seen == {True, False}
+
+
+def _maps(fn, monkeypatch):
+    from paper_2307_16080_b200 import engine, templates
+
+    got = []
+    orig = templates.match_map
+
+    def wrap(*a, **k):
+        m = orig(*a, **k)
+        got.append(m)
+        return m
+
+    monkeypatch.setattr(engine.templates, "match_map", wrap)
+    harness.run_engine(SimEngine(), fn, None, "sequential", 0)
+    return got

@@ -215,3 +215,61 @@ def test_population_es_world2_gloo_equals_world1():
             assert load(os.path.join(d, f"log{rank}.jsonl")) == log1
             idx, cost = open(os.path.join(d, f"best{rank}.txt")).read().split()
             assert int(idx) == best1.idx and float(cost) == best1.cost
+
+
+def _failing_template(tiles, unroll):
+    """A pipeline template that fails on two grid points (idx 3 and 6 of the
+    grid over SPACE_ARGS) — the sharded search must raise the idx-3 error on
+    every rank instead of leaving a rank blocked in the all-gather."""
+    from staircase.tuner.search import default_pipeline
+
+    if (list(tiles), unroll) in (([1, 1], 4), ([1, 2], 4)):
+        raise RuntimeError(f"template failure at tiles={list(tiles)} unroll={unroll}")
+    return default_pipeline(tiles, unroll)
+
+
+def _fail_worker(rank, world, port, out_dir):
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path[:0] = [here, os.path.dirname(here)]
+    import conftest  # noqa: F401
+    import torch.distributed as dist
+
+    import corpus as c
+    import oracle as o
+    import test_sweep as ts
+    from paper_2307_16080_b200 import sweep
+    from staircase.tuner import ParamSpace
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        try:
+            sweep.search(c.conv_small.module, ts._failing_template, ParamSpace(**SPACE_ARGS),
+                         budget=10, seed=0, strategy="grid", engine=o)
+            msg = "no error"
+        except RuntimeError as exc:
+            msg = str(exc)
+        with open(os.path.join(out_dir, f"err{rank}.txt"), "w") as fh:
+            fh.write(msg)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_world2_trial_error_raises_on_every_rank():
+    import torch.multiprocessing as mp
+
+    oracle.build()
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_fail_worker, args=(2, _free_port(), d), nprocs=2, join=True)
+        msgs = [open(os.path.join(d, f"err{r}.txt")).read() for r in range(2)]
+    first = "template failure at tiles=[1, 1] unroll=4"
+    assert msgs == [first, first]
+    # the sequential search raises the same error
+    from paper_2307_16080_b200 import sweep
+    from staircase.tuner import ParamSpace
+
+    with pytest.raises(RuntimeError, match=r"tiles=\[1, 1\] unroll=4"):
+        sweep.search(corpus.conv_small.module, _failing_template, ParamSpace(**SPACE_ARGS),
+                     budget=10, seed=0, strategy="grid", engine=oracle)
