@@ -25,7 +25,7 @@ namespace {
 
 enum {
   V_END = 0, V_CONST, V_BINF, V_BINI, V_CMPF, V_CMPI, V_CAST, V_LOAD, V_STORE,
-  V_MOV, V_TEST, V_NEXT, V_JUMP, V_IFF, V_PCHECK, V_NOP
+  V_MOV, V_TEST, V_NEXT, V_JUMP, V_IFF, V_PCHECK, V_NOP, V_ZERO
 };
 
 constexpr int kMaxRegs = 256;
@@ -242,6 +242,18 @@ __global__ void __launch_bounds__(kThreads) vm_kernel(VmParams p) {
               goto fault;
             }
           pc += 1 + nd;
+          break;
+        }
+        case V_ZERO: {
+          // memref.alloc inside the region: a fresh zero-filled buffer
+          // (reference _evalpy.py:209-210) — the region's scratch slot
+          const int dt = fl & 3;
+          const b200_buffer &b = sbuf[sprog[pc + 1]];
+          const int64_t n = sprog[pc + 2];
+          const int64_t bytes = n * (dt == 0 || dt == 2 ? 4 : 8);
+          unsigned char *q = static_cast<unsigned char *>(b.ptr);
+          for (int64_t i = 0; i < bytes; ++i) q[i] = 0;
+          pc += 3;
           break;
         }
         default:  // V_NOP (counting only)

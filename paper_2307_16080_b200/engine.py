@@ -246,7 +246,9 @@ class _Run:
             _region_hook(r, accesses)
         links, remainder = analysis.chain_of(r)
         safe = analysis.statically_in_bounds(r, accesses) and not analysis.invalid_steps(r)
-        band = analysis.choose_band(r, links, accesses) if safe else []
+        # a region with memref.alloc runs on one thread: its scratch buffer
+        # is the reference's sequence of fresh buffers (lift._leaf ALLOC)
+        band = analysis.choose_band(r, links, accesses) if safe and not r.has_alloc else []
         st = analysis.static_tally(r.tree)
         written = {a.slot for a in accesses if a.write}
         for slot in written:

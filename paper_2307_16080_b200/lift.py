@@ -353,11 +353,42 @@ def _lift_block(program, code, start, end, fr, region):
             out.append(node)
             pc += 1
             continue
-        if op in (CALL, RETURN):
-            raise Unsupported("func.call / return inside a loop region")
+        if op == CALL:
+            out.extend(_inline_call(program, ins, fr, region))
+            pc += 1
+            continue
+        if op == RETURN:
+            raise Unsupported("return inside a loop region")
         out.append(_leaf(ins, fr, region))
         pc += 1
     return out
+
+
+MAX_INLINE = 8
+
+
+def _inline_call(program, ins, fr, region):
+    """func.call inside a loop region, inlined (reference _evalpy.py:216-223:
+    a fresh register file for the callee, its RETURN operands copied to the
+    caller's result registers).  The CALL and the callee's RETURN stay in the
+    tree as tally-only leaves (the reference counts both).  Callees with a
+    RETURN anywhere but at the end, or nested deeper than MAX_INLINE
+    (recursion), are not lifted."""
+    depth = getattr(fr, "depth", 0)
+    if depth >= MAX_INLINE:
+        raise Unsupported("func.call nesting too deep inside a loop region")
+    callee = program.funcs[ins[2]]
+    ccode = callee.code
+    if not ccode or ccode[-1][0] != RETURN or any(c[0] == RETURN for c in ccode[:-1]):
+        raise Unsupported("a callee with an early return inside a loop region")
+    cf = _Frame(region)
+    cf.depth = depth + 1
+    for dst, src in zip(callee.arg_regs, ins[3]):
+        cf.map[dst] = fr.get(src)
+    body = _lift_block(program, ccode, 0, len(ccode) - 1, cf, region)
+    for dst, r in zip(ins[1], ccode[-1][1]):
+        fr.map[dst] = cf.get(r)
+    return [Ins(CALL)] + body + [Ins(RETURN)]
 
 
 def _leaf(ins, fr, region):
@@ -401,8 +432,21 @@ def _leaf(ins, fr, region):
         n.idx = tuple(fr.get(r) for r in ins[3])
         n.loc = ins[4]
     elif op == ALLOC:
+        # memref.alloc inside a loop: a fresh zero-filled Buffer every time it
+        # executes (reference _evalpy.py:209-210).  It becomes a region
+        # scratch buffer that the VM zero-fills at this instruction; the
+        # engine runs such regions on one thread (no band), so one scratch
+        # buffer is exactly the reference's sequence of fresh buffers.
+        from staircase.interp.buffer import Buffer
+
         region.has_alloc = True
-        raise Unsupported("memref.alloc inside a loop region")
+        buf = Buffer(ins[2], ins[3])
+        n.dst = fr.define(ins[1])
+        n.value = buf
+        region.env[n.dst] = buf
+        region.kind[n.dst] = "buf"
+        region.buf_slot[id(buf)] = len(region.buffers)
+        region.buffers.append(buf)
     elif op == DEALLOC:
         n.a = fr.get(ins[1])
     elif op == GPUID:

@@ -29,7 +29,8 @@ import os
 
 from . import jit
 from .vmcode import (V_BINF, V_BINI, V_CAST, V_CMPF, V_CMPI, V_CONST, V_END, V_IFF,
-                     V_JUMP, V_LOAD, V_MOV, V_NEXT, V_NOP, V_PCHECK, V_STORE, V_TEST)
+                     V_JUMP, V_LOAD, V_MOV, V_NEXT, V_NOP, V_PCHECK, V_STORE, V_TEST,
+                     V_ZERO)
 
 ENABLED = os.environ.get("B200_NATIVE", "1") != "0"
 KTALLY = 25
@@ -83,6 +84,8 @@ def _decode(words):
             size = 2
         elif op == V_PCHECK:
             size = 1 + fl
+        elif op == V_ZERO:
+            size = 3
         else:
             raise ValueError(f"unknown VM opcode {op} at {pc}")
         out.append((pc, op, tag, fl, words[pc + 1:pc + size]))
@@ -256,6 +259,9 @@ def _stmt(pc, op, fl, a, buffers, count):
     if op == V_PCHECK:
         conds = " || ".join(f"(i64)R{r} <= 0" for r in a[:fl]) or "false"
         return f"if ({conds}) {{ report(ERR, 3, -1, 0, 0, -1); goto fault; }}"
+    if op == V_ZERO:   # memref.alloc in the region: zero-fill its scratch buffer
+        T = _CTYPE[fl & 3]
+        return f"for (i64 z = 0; z < {a[1]}LL; ++z) (({T} *)P[{a[0]}])[z] = 0;"
     raise ValueError(f"unknown VM opcode {op}")
 
 

@@ -21,14 +21,14 @@ from __future__ import annotations
 
 import struct
 
-from .lift import (BINF, BINI, CAST, CMPF, CMPI, CONST, DEALLOC, GPUID, JUMP,
-                   LAUNCH, LOAD, LOOP_INIT_A, LOOP_INIT_S, LOOP_NEXT_I,
+from .lift import (ALLOC, BINF, BINI, CALL, CAST, CMPF, CMPI, CONST, DEALLOC, GPUID, JUMP,
+                   RETURN, LAUNCH, LOAD, LOOP_INIT_A, LOOP_INIT_S, LOOP_NEXT_I,
                    LOOP_NEXT_R, LOOP_TEST_I, LOOP_TEST_R, PARALLEL, RETURN_GPU,
                    STORE, IF_FALSE, If, Ins, Launch, Loop, Par, Unsupported)
 
 # VM opcodes (csrc/vm.cu)
 V_END, V_CONST, V_BINF, V_BINI, V_CMPF, V_CMPI, V_CAST, V_LOAD, V_STORE, V_MOV, \
-    V_TEST, V_NEXT, V_JUMP, V_IFF, V_PCHECK, V_NOP = range(16)
+    V_TEST, V_NEXT, V_JUMP, V_IFF, V_PCHECK, V_NOP, V_ZERO = range(17)
 
 DTYPE_CODE = {"f32": 0, "f64": 1, "i32": 2, "i64": 3}
 MAX_REGS = 256
@@ -141,8 +141,18 @@ class _Enc:
         elif op == GPUID:
             self.head(V_MOV, tag)
             self.w.extend([n.dst, n.a])
-        elif op in (JUMP, DEALLOC, RETURN_GPU):
+        elif op in (JUMP, DEALLOC, RETURN_GPU, CALL, RETURN):
             self.head(V_NOP, tag)
+        elif op == ALLOC:
+            # fresh zero-filled scratch (lift._leaf): V_ZERO slot, elements
+            buf = n.value
+            size = 1
+            for d in buf.shape:
+                size *= d
+            if size >= 1 << 31:
+                raise Unsupported("memref.alloc too large for the VM")
+            self.head(V_ZERO, tag, DTYPE_CODE[buf.dtype])
+            self.w.extend([self.r.buf_slot[id(buf)], size])
         else:
             raise Unsupported(f"VM cannot encode opcode {op}")
 

@@ -11,7 +11,7 @@ import struct
 import numpy as np
 
 V_END, V_CONST, V_BINF, V_BINI, V_CMPF, V_CMPI, V_CAST, V_LOAD, V_STORE, V_MOV, \
-    V_TEST, V_NEXT, V_JUMP, V_IFF, V_PCHECK, V_NOP = range(16)
+    V_TEST, V_NEXT, V_JUMP, V_IFF, V_PCHECK, V_NOP, V_ZERO = range(17)
 
 _NP = {"f32": np.float32, "f64": np.float64, "i32": np.int32, "i64": np.int64}
 
@@ -253,6 +253,9 @@ class SimBackend:
                     if I(w[pc + 1 + k]) <= 0:
                         return (3, -1, 0, 0, -1)
                 pc += 1 + nd
+            elif op == V_ZERO:
+                bufs[w[pc + 1]][0][:w[pc + 2]] = 0
+                pc += 3
             else:
                 pc += 1
 
