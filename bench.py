@@ -400,7 +400,8 @@ TENSOR_KERNELS = ("b200_gemm_tc", "b200_conv2d_tc")
 # entry points that run the same kernel family (timed together)
 ALIASES = {"b200_gemm_tc_shadow": "b200_gemm_tc", "b200_gemm_tc_kn": "b200_gemm_tc",
            "b200_gemm_f32_exact_tiled": "b200_gemm_f32_exact"}
-DTYPE = {"bf16": "bf16 (fp32 accumulate)", "tf32": "tf32 (fp32 accumulate)", "exact": "f32"}
+DTYPE = {"bf16": "bf16 (fp32 accumulate)", "tf32": "tf32 (fp32 accumulate)", "exact": "f32",
+         "f32x3": "f32 (3xTF32 split, fp32 accumulate; within fp32 rel 1e-5)"}
 
 
 def _timed(fn, stream, min_steps, min_seconds):
@@ -604,12 +605,14 @@ def roofline(wl, prec, fam, ms, sus_ms, rank_flops):
         sus_peak = peak
     elif dom in TENSOR_KERNELS:
         achieved = rank_flops / (dom_ms * 1e-3) / 1e12
-        f = 1.0 if prec == "bf16" else 0.5
+        f = {"bf16": 1.0, "tf32": 0.5, "f32x3": 0.5 / 3}[prec]
         peak = peaks["bf16_tflops"] * f
         sus_peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) * f
         unit, bound = "TFLOP/s", "tensor"
-        peak_source = (f"{src} bf16 dense (MEASURED_PEAKS.json)" if prec == "bf16" else
-                       f"{src} bf16 x 0.5 (tf32 = half rate, derived)")
+        peak_source = {"bf16": f"{src} bf16 dense (MEASURED_PEAKS.json)",
+                       "tf32": f"{src} bf16 x 0.5 (tf32 = half rate, derived)",
+                       "f32x3": f"{src} bf16 x 0.5 / 3 (derived: each fp32-accurate product is "
+                                f"3 tf32 products at half the bf16 rate)"}[prec]
         if wl.tc_bytes and wl.tc_bytes * scale / (dom_ms * 1e-3) / 1e9 / peaks["hbm_gbs"] > \
                 achieved / peak:
             # the conv's f32 output read-modify-write makes it HBM-bound
@@ -779,14 +782,14 @@ def run_ours(args, rank, world, local):
     variants, configs = {}, {}
     if auto:
         if world == 1:
-            for prec, tiles in (("bf16", None), ("tf32", None), ("bf16", (8, 8)),
-                                ("bf16", (4, 16)), ("exact", (8, 8))):
+            for prec, tiles in (("f32x3", None), ("bf16", None), ("tf32", None),
+                                ("bf16", (8, 8)), ("bf16", (4, 16)), ("exact", (8, 8))):
                 wl = Workload("mm", tiles)
                 r = measure(wl, prec, rank, world, local, with_cpu=False, **k)
                 if r is not None:
                     variants[f"{wl.key}_{prec}"] = r
             todo = [("linear32", "exact"), ("conv", "exact"), ("conv", "bf16"), ("ls", "bf16"),
-                    ("ls", "exact"), ("ewise", "exact")]
+                    ("ls", "f32x3"), ("ls", "exact"), ("ewise", "exact")]
         else:
             todo = [("conv", "bf16"), ("ls", "bf16")]
         cpu = {}
@@ -883,7 +886,7 @@ def main():
                     choices=["auto", "mm", "conv", "ls", "linear32", "ewise", "sweep"])
     ap.add_argument("--tiles", default=None, help="e.g. 8x8: the mm nest tiled by the "
                                                   "reference pass (parallel form)")
-    ap.add_argument("--precision", default=None, choices=["bf16", "tf32", "exact"])
+    ap.add_argument("--precision", default=None, choices=["bf16", "tf32", "f32x3", "exact"])
     ap.add_argument("--min-seconds", type=float, default=1.0,
                     help="length of the sustained and e2e timed regions")
     args = ap.parse_args()

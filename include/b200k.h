@@ -148,6 +148,11 @@ int b200_map_f32(const int32_t *prog, int32_t n_words, const float *consts, int3
  * Operand packing for the tensor-core contraction: dst[r][c] (dense
  * row-major, i.e. K-major for the GEMM) = round(src[r*s_row + c*s_col]),
  * kind 0 -> bf16 (RN), kind 1 -> tf32 held in f32 (RN, low 13 bits zero).
+ * kinds 2 / 3: the split pack of the fp32-accurate "f32x3" path (3xTF32):
+ * with hi = tf32(x), lo = tf32(x - hi), each dst row holds 3 * cols
+ * values, [hi | hi | lo] (kind 2, the A operand) or [hi | lo | hi]
+ * (kind 3, B^T), so a kind-1 b200_gemm_tc over K' = 3K sums
+ * hiA.hiB + hiA.loB + loA.hiB.
  * Used to stage A (rows = M) and B^T (rows = N) of a recognised matmul nest,
  * whatever the nest's index maps (reference tests/kernels.py:24-38).
  */

@@ -184,12 +184,80 @@ __device__ __forceinline__ float cvt<float>(float v) {
   return __uint_as_float(u);
 }
 
+// Split packing for the fp32-accurate "f32x3" contraction (3xTF32): x =
+// hi + lo + d with hi = tf32(x), lo = tf32(x - hi) (x - hi is exact in f32),
+// |d| <= 2^-22 |x|.  A row of the packed operand holds three K-segments, so
+// one tf32 GEMM over K' = 3K sums hiA.hiB + hiA.loB + loA.hiB (the dropped
+// loA.loB is <= 2^-22 |ab|): SPLIT 1 writes [hi | hi | lo] (the A operand),
+// SPLIT 2 writes [hi | lo | hi] (B^T).  SPLIT 0 is the plain pack.
+template <int SPLIT>
+__device__ __forceinline__ void seg_offsets(int64_t cols, int64_t &hi0, int64_t &hi1,
+                                            int64_t &lo) {
+  if (SPLIT == 1) hi0 = 0, hi1 = cols, lo = 2 * cols;
+  else hi0 = 0, hi1 = 2 * cols, lo = cols;
+}
+
+// 8 consecutive converted elements of row r, columns c .. c + 7 (16-byte
+// aligned destination rows of pitch ld)
+template <typename T, int SPLIT>
+__device__ __forceinline__ void store8(T *__restrict__ dst, int64_t r, int64_t c, int64_t cols,
+                                       int64_t ld, const float v[8]) {
+  if constexpr (SPLIT == 0) {
+    if (sizeof(T) == 2) {
+      __nv_bfloat162 o[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) o[j] = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+      *reinterpret_cast<uint4 *>(dst + r * ld + c) = *reinterpret_cast<uint4 *>(o);
+    } else {
+      float4 *d = reinterpret_cast<float4 *>(reinterpret_cast<float *>(dst) + r * ld + c);
+      d[0] = make_float4(cvt<float>(v[0]), cvt<float>(v[1]), cvt<float>(v[2]), cvt<float>(v[3]));
+      d[1] = make_float4(cvt<float>(v[4]), cvt<float>(v[5]), cvt<float>(v[6]), cvt<float>(v[7]));
+    }
+  } else {
+    float hi[8], lo[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      hi[j] = cvt<float>(v[j]);
+      lo[j] = cvt<float>(__fsub_rn(v[j], hi[j]));
+    }
+    int64_t o_hi0, o_hi1, o_lo;
+    seg_offsets<SPLIT>(cols, o_hi0, o_hi1, o_lo);
+    float *row = reinterpret_cast<float *>(dst) + r * ld + c;
+    const float4 h0 = make_float4(hi[0], hi[1], hi[2], hi[3]);
+    const float4 h1 = make_float4(hi[4], hi[5], hi[6], hi[7]);
+    const float4 l0 = make_float4(lo[0], lo[1], lo[2], lo[3]);
+    const float4 l1 = make_float4(lo[4], lo[5], lo[6], lo[7]);
+    reinterpret_cast<float4 *>(row + o_hi0)[0] = h0;
+    reinterpret_cast<float4 *>(row + o_hi0)[1] = h1;
+    reinterpret_cast<float4 *>(row + o_hi1)[0] = h0;
+    reinterpret_cast<float4 *>(row + o_hi1)[1] = h1;
+    reinterpret_cast<float4 *>(row + o_lo)[0] = l0;
+    reinterpret_cast<float4 *>(row + o_lo)[1] = l1;
+  }
+}
+
+template <typename T, int SPLIT>
+__device__ __forceinline__ void store1(T *__restrict__ dst, int64_t r, int64_t c, int64_t cols,
+                                       int64_t ld, float v) {
+  if constexpr (SPLIT == 0) {
+    dst[r * ld + c] = cvt<T>(v);
+  } else {
+    const float hi = cvt<float>(v), lo = cvt<float>(__fsub_rn(v, hi));
+    int64_t o_hi0, o_hi1, o_lo;
+    seg_offsets<SPLIT>(cols, o_hi0, o_hi1, o_lo);
+    float *row = reinterpret_cast<float *>(dst) + r * ld + c;
+    row[o_hi0] = hi;
+    row[o_hi1] = hi;
+    row[o_lo] = lo;
+  }
+}
+
 // Row-contiguous source (s_col == 1, rows 16-byte aligned): 8 elements per
 // thread, 2 x 128-bit loads -> one 128-bit (bf16) or two (tf32) stores.
-template <typename T>
+template <typename T, int SPLIT = 0>
 __global__ void __launch_bounds__(256) pack_rows_kernel(const float *__restrict__ src, int64_t s_row,
                                                         T *__restrict__ dst, int64_t rows,
-                                                        int64_t cols) {
+                                                        int64_t cols, int64_t ld) {
   const int64_t per_row = cols / 8;
   const int64_t total = rows * per_row;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
@@ -197,25 +265,19 @@ __global__ void __launch_bounds__(256) pack_rows_kernel(const float *__restrict_
     const int64_t r = i / per_row, c = (i % per_row) * 8;
     const float4 *s = reinterpret_cast<const float4 *>(src + r * s_row + c);
     float4 a = __ldcs(s), b = __ldcs(s + 1);
-    if (sizeof(T) == 2) {
-      __nv_bfloat162 o[4] = {__floats2bfloat162_rn(a.x, a.y), __floats2bfloat162_rn(a.z, a.w),
-                             __floats2bfloat162_rn(b.x, b.y), __floats2bfloat162_rn(b.z, b.w)};
-      *reinterpret_cast<uint4 *>(dst + r * cols + c) = *reinterpret_cast<uint4 *>(o);
-    } else {
-      float4 *d = reinterpret_cast<float4 *>(dst + r * cols + c);
-      d[0] = make_float4(cvt<float>(a.x), cvt<float>(a.y), cvt<float>(a.z), cvt<float>(a.w));
-      d[1] = make_float4(cvt<float>(b.x), cvt<float>(b.y), cvt<float>(b.z), cvt<float>(b.w));
-    }
+    const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    store8<T, SPLIT>(dst, r, c, cols, ld, v);
   }
 }
 
 // Column-contiguous source (s_row == 1): a 64 x 64 tile transposed through
 // shared memory; 128-bit coalesced loads along the source rows and 128-bit
 // coalesced stores along the destination rows.
-template <typename T>
+template <typename T, int SPLIT = 0>
 __global__ void __launch_bounds__(256) pack_transpose_kernel(const float *__restrict__ src,
                                                              int64_t s_col, T *__restrict__ dst,
-                                                             int64_t rows, int64_t cols) {
+                                                             int64_t rows, int64_t cols,
+                                                             int64_t ld) {
   __shared__ float tile[64][65];  // [c][r]
   const int64_t r0 = (int64_t)blockIdx.x * 64, c0 = (int64_t)blockIdx.y * 64;
   const int t = threadIdx.x;
@@ -251,27 +313,18 @@ __global__ void __launch_bounds__(256) pack_transpose_kernel(const float *__rest
 #pragma unroll
     for (int j = 0; j < 8; ++j) v[j] = tile[cc + j][rr];
     if (c + 7 < cols && ((cols % 8) == 0)) {
-      if (sizeof(T) == 2) {
-        __nv_bfloat162 o[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) o[j] = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
-        *reinterpret_cast<uint4 *>(dst + r * cols + c) = *reinterpret_cast<uint4 *>(o);
-      } else {
-        float4 *d = reinterpret_cast<float4 *>(dst + r * cols + c);
-        d[0] = make_float4(cvt<float>(v[0]), cvt<float>(v[1]), cvt<float>(v[2]), cvt<float>(v[3]));
-        d[1] = make_float4(cvt<float>(v[4]), cvt<float>(v[5]), cvt<float>(v[6]), cvt<float>(v[7]));
-      }
+      store8<T, SPLIT>(dst, r, c, cols, ld, v);
     } else {
       for (int j = 0; j < 8; ++j)
-        if (c + j < cols) dst[r * cols + c + j] = cvt<T>(v[j]);
+        if (c + j < cols) store1<T, SPLIT>(dst, r, c + j, cols, ld, v[j]);
     }
   }
 }
 
 // General strides: 32x32 tiles through shared memory.
-template <typename T>
+template <typename T, int SPLIT = 0>
 __global__ void pack_kernel(const float *__restrict__ src, int64_t s_row, int64_t s_col,
-                            T *__restrict__ dst, int64_t rows, int64_t cols) {
+                            T *__restrict__ dst, int64_t rows, int64_t cols, int64_t ld) {
   __shared__ float tile[32][33];
   const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
@@ -286,13 +339,14 @@ __global__ void pack_kernel(const float *__restrict__ src, int64_t s_row, int64_
   __syncthreads();
   for (int i = ty; i < 32; i += 8) {
     const int64_t r = r0 + i, c = c0 + tx;
-    if (r < rows && c < cols) dst[r * cols + c] = cvt<T>(tile[i][tx]);
+    if (r < rows && c < cols) store1<T, SPLIT>(dst, r, c, cols, ld, tile[i][tx]);
   }
 }
 
-template <typename T>
+template <typename T, int SPLIT = 0>
 int pack(const float *src, int64_t s_row, int64_t s_col, T *dst, int64_t rows, int64_t cols,
          cudaStream_t s) {
+  const int64_t ld = SPLIT ? 3 * cols : cols;
   const bool aligned = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) &&
                        ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
   if (s_col == 1 && aligned && cols % 8 == 0 && s_row % 4 == 0) {
@@ -300,13 +354,13 @@ int pack(const float *src, int64_t s_row, int64_t s_col, T *dst, int64_t rows, i
     int64_t blocks = (work + 255) / 256;
     const int64_t cap = (int64_t)num_sms() * 8;
     if (blocks > cap) blocks = cap;
-    pack_rows_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(src, s_row, dst, rows, cols);
+    pack_rows_kernel<T, SPLIT><<<(unsigned)blocks, 256, 0, s>>>(src, s_row, dst, rows, cols, ld);
   } else if (s_row == 1 && aligned && s_col % 4 == 0) {
     dim3 grid((unsigned)((rows + 63) / 64), (unsigned)((cols + 63) / 64));
-    pack_transpose_kernel<T><<<grid, 256, 0, s>>>(src, s_col, dst, rows, cols);
+    pack_transpose_kernel<T, SPLIT><<<grid, 256, 0, s>>>(src, s_col, dst, rows, cols, ld);
   } else {
     dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
-    pack_kernel<T><<<grid, dim3(32, 8), 0, s>>>(src, s_row, s_col, dst, rows, cols);
+    pack_kernel<T, SPLIT><<<grid, dim3(32, 8), 0, s>>>(src, s_row, s_col, dst, rows, cols, ld);
   }
   return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
 }
@@ -319,6 +373,11 @@ extern "C" int b200_pack_operand(int32_t kind, const float *src, int64_t s_row, 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (kind == 0)
     return pack<__nv_bfloat16>(src, s_row, s_col, static_cast<__nv_bfloat16 *>(dst), rows, cols, s);
+  if (kind == 2)
+    return pack<float, 1>(src, s_row, s_col, static_cast<float *>(dst), rows, cols, s);
+  if (kind == 3)
+    return pack<float, 2>(src, s_row, s_col, static_cast<float *>(dst), rows, cols, s);
+  if (kind != 1) return B200_EINVAL;
   return pack<float>(src, s_row, s_col, static_cast<float *>(dst), rows, cols, s);
 }
 

@@ -45,9 +45,12 @@ from .runtime import DeviceBackend
 ENGINE_NAME = "b200"
 
 # Contraction precision.  "exact" (default): fp32 per-op rounding on the FP32
-# pipes, bit-identical to the reference.  "tf32" / "bf16": operands rounded to
-# tf32 / bf16 and contracted on the tcgen05 tensor cores with fp32
-# accumulation (tolerance: DESIGN.md, tests/test_gpu_tc.py).
+# pipes, bit-identical to the reference.  "f32x3": f32 operands split into
+# tf32 hi + lo parts, three tf32 products per term on the tensor cores —
+# fp32-accurate (within rel 1e-5 of the reference, tests/test_gpu_f32x3.py),
+# not bit-identical.  "tf32" / "bf16": operands rounded to tf32 / bf16 and
+# contracted on the tcgen05 tensor cores with fp32 accumulation (tolerance:
+# DESIGN.md, tests/tcbound.py).
 PRECISION = os.environ.get("B200_PRECISION", "exact")
 # Cross-region fusion of queued plans (B200_FUSE=0 disables, for A/B tests).
 FUSE = os.environ.get("B200_FUSE", "1") != "0"
@@ -72,7 +75,9 @@ def configure(precision=None, fuse=None, shadow=None, strict=None):
     if strict is not None:
         STRICT = bool(strict)
     if precision is not None:
-        if precision not in ("exact", "tf32", "bf16"):
+        from .runtime import PRECISIONS
+
+        if precision not in PRECISIONS:
             raise ValueError(f"unknown precision {precision!r}")
         PRECISION = precision
     if fuse is not None:

@@ -356,7 +356,11 @@ def _copy_streams(torch):
     return _COPY_STREAMS[dev]
 
 
-PRECISIONS = ("exact", "tf32", "bf16")
+# exact: per-op f32 rounding on the FP32 pipes (bit-identical to the
+# reference); f32x3: fp32-accurate on the tensor cores (3xTF32 split, within
+# the fp32 tolerance, not bit-identical); tf32 / bf16: rounded operands.
+PRECISIONS = ("exact", "f32x3", "tf32", "bf16")
+TC_PRECISIONS = ("bf16", "tf32", "f32x3")
 _WORKSPACE = {}
 _RETIRED = []
 
@@ -385,8 +389,9 @@ def workspace(slot, dtype, rows, cols):
 
 
 def tc_supported(precision, K):
-    """tcgen05 path needs 16-byte TMA rows of packed K (bf16: K%8, tf32: K%4)."""
-    return precision in ("bf16", "tf32") and K > 0 and \
+    """tcgen05 path needs 16-byte TMA rows of packed K (bf16: K%8, tf32 and
+    f32x3 — 3K tf32 values per row — K%4)."""
+    return precision in TC_PRECISIONS and K > 0 and \
         (K * (2 if precision == "bf16" else 4)) % 16 == 0
 
 
@@ -452,7 +457,7 @@ def cta_tile(precision, tiles):
     if tm is None and tn is None:
         return None
     tm, tn = tm or 1, tn or 1
-    if precision in ("bf16", "tf32"):
+    if precision in TC_PRECISIONS:
         return (128, 256) if tn >= 2 * tm else (256, 256)
     if tm * tn <= 16:
         return (64, 64)
@@ -500,12 +505,15 @@ def launch_gemm(lib, precision, a_ptr, sA, b_ptr, sB, c_ptr, sC, M, N, K, stream
         variant = 1 if cta == (128, 256) else 2
     kind = 0 if precision == "bf16" else 1
     dt = "bfloat16" if kind == 0 else "float32"
+    split = precision == "f32x3"      # packed rows hold 3 K-segments (gemm_tc.cu)
+    KP = 3 * K if split else K
     names = []
     if a_packed is not None:
         Ap = a_packed
     else:
-        Ap = workspace(0, dt, M, K)
-        call("b200_pack_operand", kind, P(a_ptr), sA[0], sA[1], P(Ap.data_ptr()), M, K, stream)
+        Ap = workspace(0, dt, M, KP)
+        call("b200_pack_operand", 2 if split else kind, P(a_ptr), sA[0], sA[1],
+             P(Ap.data_ptr()), M, K, stream)
         names.append("pack_operand")
     if b_packed is not None:
         Bp, kn = b_packed if isinstance(b_packed, tuple) else (b_packed, False)
@@ -518,7 +526,9 @@ def launch_gemm(lib, precision, a_ptr, sA, b_ptr, sB, c_ptr, sC, M, N, K, stream
              M, N, K, init, init_value, P(bias_ptr) if bias_ptr else None, bias_stride,
              P(c16.data_ptr()) if c16 is not None else None, N if c16 is not None else 0,
              stream)
-    elif c16 is not None:
+        return names + [f"gemm_tc_{precision}"]
+    K = KP
+    if c16 is not None:
         call("b200_gemm_tc_shadow", kind, P(Ap.data_ptr()), P(Bp.data_ptr()), P(c_ptr), sC[0],
              sC[1], M, N, K, init, init_value, P(bias_ptr) if bias_ptr else None, bias_stride,
              P(c16.data_ptr()), N, stream)
@@ -541,6 +551,12 @@ def pack_b(lib, precision, b_ptr, sB, N, K, stream, call=None, allow_kn=True):
     operand of b200_gemm_tc."""
     call = call or _direct_call(lib)
     kind = 0 if precision == "bf16" else 1
+    if precision == "f32x3":
+        # B^T as N rows of [hi | lo | hi] (3K tf32 values)
+        Bp = workspace(1, "float32", N, 3 * K)
+        call("b200_pack_operand", 3, ctypes.c_void_p(b_ptr), sB[1], sB[0],
+             ctypes.c_void_p(Bp.data_ptr()), N, K, stream)
+        return Bp, False
     if GEMM_KN and allow_kn and kind == 0 and sB[1] == 1 and N % 64 == 0:
         Bp = workspace(1, "bfloat16", K, N)
         call("b200_pack_operand", kind, ctypes.c_void_p(b_ptr), sB[0], sB[1],
