@@ -35,7 +35,7 @@ from __future__ import annotations
 import math
 import os
 
-from . import analysis, fusion, templates, vmcode
+from . import analysis, fusion, plancache, templates, vmcode
 from .host import errors as _errors
 from .lift import (ALLOC, BINF, BINI, CALL, CAST, CMPF, CMPI, CONST, DEALLOC, IF_FALSE,
                    JUMP, LAUNCH, LOAD, LOOP_INIT_A, LOOP_INIT_S, PARALLEL, RETURN,
@@ -64,6 +64,10 @@ STREAM_IO = os.environ.get("B200_STREAM_IO", "1") != "0"
 # unaligned K, conv shape outside the tcgen05 kernel) runs exact f32 with a
 # runtime.PrecisionFallback warning; strict makes it PrecisionUnavailable.
 STRICT = os.environ.get("B200_STRICT", "0") == "1"
+# Per-region plan cache (plancache.py): a repeated run of the same tape
+# region with the same scalar values and buffer geometry skips lifting,
+# analysis and matching (B200_PLAN_CACHE=0 disables, for A/B tests).
+PLAN_CACHE = os.environ.get("B200_PLAN_CACHE", "1") != "0"
 
 # kernel choice of the last run (tests and bench inspect these)
 last_plan = []
@@ -224,6 +228,15 @@ class _Run:
 
     # -- regions ---------------------------------------------------------------
     def region(self, code, start, end, regs, tally):
+        key = None
+        if PLAN_CACHE and self.shard is None and _region_hook is None:
+            rkey = (plancache.region_key(self.program, code, start, end), self.ctx.mode,
+                    PRECISION, FUSE, SHADOW)
+            key = plancache.lookup_key(rkey, regs)
+            hit = plancache.get(key)
+            if hit is not None:
+                self.replay(hit, regs, tally)
+                return
         E = _errors()
         try:
             r = lift_region(self.program, code, start, end, regs)
@@ -259,37 +272,69 @@ class _Run:
         for slot in written:
             self.be.mark_dirty(r.buffers[slot])
 
+        store = key is None and PLAN_CACHE and self.shard is None and _region_hook is None
         if safe and st is not None:
             g = templates.match_contraction(r, links, remainder, accesses)
             if g is not None:
                 _add(tally, st)
                 self.pending.append(fusion.ContractItem(g))
+                if store:
+                    plancache.put(rkey, regs, r, plancache.Plan("contract", st, written, g))
                 return
             mm = templates.match_map(r, links, remainder, accesses, band)
             if mm is not None:
                 _add(tally, st)
                 self.pending.append(fusion.MapItem(mm))
+                if store:
+                    plancache.put(rkey, regs, r, plancache.Plan("map", st, written, mm))
                 return
 
         # generic tier: the device tape VM (runs in order after queued plans)
-        self.flush_pending({id(r.buffers[slot]) for slot in written})
         count = st is None
         try:
             prog = vmcode.encode(r, links, remainder, band, count, checked=not safe)
         except Unsupported as exc:
+            self.flush_pending()
             raise E.ModeUnsupported(f"b200 engine: {exc}") from None
-        dev_tally, fault = self.be.vm(r, prog, checked=not safe)
+        chain = analysis.chain_tally(links)[0] if count else None
+        entry = ("vm", len(band), "checked" if not safe else "unchecked",
+                 "count" if count else "static")
+        plan = plancache.Plan("vm", st, written, prog, chain=chain, entry=entry,
+                              checked=not safe)
+        if store:
+            plancache.put(rkey, regs, r, plan)
+        self.run_vm(r, plan, tally)
+
+    def run_vm(self, r, plan, tally):
+        """Execute a VM plan after the queued plans; tally; raise its fault."""
+        self.flush_pending({id(r.buffers[slot]) for slot in plan.written})
+        prog = plan.item
+        dev_tally, fault = self.be.vm(r, prog, checked=plan.checked)
         if fault is not None:
             self.be.flush()
             self.raise_fault(r, prog, fault)
-        if count:
-            chain, _ = analysis.chain_tally(links)
-            _add(tally, chain)
+        if plan.chain is not None:
+            _add(tally, plan.chain)
             _add(tally, dev_tally)
         else:
-            _add(tally, st)
-        self.plan.append(("vm", len(band), "checked" if not safe else "unchecked",
-                          "count" if count else "static"))
+            _add(tally, plan.st)
+        self.plan.append(plan.entry)
+
+    def replay(self, hit, regs, tally):
+        """A cached region plan (plancache) bound to this run's registers."""
+        plan, shell = hit
+        r = plancache.bind(shell, regs)
+        for slot in plan.written:
+            self.be.mark_dirty(r.buffers[slot])
+        if plan.kind == "contract":
+            _add(tally, plan.st)
+            self.pending.append(fusion.ContractItem(
+                plancache.rebind_contract(plan.item, r, plan.slots)))
+        elif plan.kind == "map":
+            _add(tally, plan.st)
+            self.pending.append(fusion.MapItem(plancache.rebind_map(plan.item, r, plan.slots)))
+        else:
+            self.run_vm(r, plan, tally)
 
     def flush_pending(self, trigger_writes=()):
         """Execute the queued plans.  ``trigger_writes``: ids of the buffers

@@ -183,6 +183,7 @@ class Region:
         self.has_if = False
         self.has_alloc = False
         self.has_launch = False
+        self.outer = []         # (outer tape register, vreg) in first-read order
 
     def new_vreg(self):
         v = self.n_vregs
@@ -244,6 +245,7 @@ def lift_region(program, code, start, end, regs):
         frame.map[reg] = v
         val = env_map[reg]
         region.env[v] = val
+        region.outer.append((reg, v))
         if isinstance(val, Buffer):
             region.kind[v] = "buf"
             if id(val) not in region.buf_slot:

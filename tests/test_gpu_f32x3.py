@@ -50,10 +50,11 @@ def _f32_chain(c0, a, b):
     return c
 
 
-def _check(got, want, mag, label):
+def _check(got, want, mag, label, K):
     err = np.abs(got.astype(np.float64) - want.astype(np.float64))
     norm = float((err / mag).max())
-    conftest.TC_ERRORS.append((label + " (f32x3: |err| / sum|ab|, bound 1e-5)", 0, norm))
+    conftest.TC_ERRORS.append((label, K, norm,
+                               "f32x3: |got-want| / sum|ab| vs the reference chain, bound 1e-5"))
     assert (err <= TOL * mag).all(), f"{label}: max normalised error {norm:.3g}"
     return norm
 
@@ -87,7 +88,7 @@ def test_mm4096_f32x3_within_fp32_tolerance(tiles):
     want = _f32_chain(C0[i, k], A[i, :], B[:, k].T)
     mag = np.abs(A[i, :].astype(np.float64) * B[:, k].T.astype(np.float64)).sum(axis=1) + \
         np.abs(C0[i, k])
-    _check(C[i, k], want, mag, f"mm4096 f32x3 tiles={tiles}")
+    _check(C[i, k], want, mag, f"mm4096 f32x3 tiles={tiles}", 4096)
 
 
 @pytest.mark.parametrize("shape", [(96, 200, 160), (130, 72, 148), (256, 256, 1024)])
@@ -120,7 +121,7 @@ def mmx(A: MemRef[({M}, {K}), F32], B: MemRef[({K}, {N}), F32], C: MemRef[({M}, 
     B = np.array(want[1].data, dtype=np.float64).reshape(K, N)
     C0 = np.array(harness.make_args(fn, 3)[2].data, dtype=np.float64).reshape(M, N)
     mag = np.abs(A) @ np.abs(B) + np.abs(C0)
-    _check(_np(args[2]), _np(want[2]), mag, f"mm {M}x{N}x{K} f32x3")
+    _check(_np(args[2]), _np(want[2]), mag, f"mm {M}x{N}x{K} f32x3", K)
 
 
 def test_split_pack_layout():
