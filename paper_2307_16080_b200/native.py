@@ -93,16 +93,58 @@ def _decode(words):
     return out
 
 
-def vm_source(prog, buffers, env_regs):
+_RECORD = r"""
+// race recorder (races.py): per buffer element, the first writing point W,
+// the first reading point R1 and the first reading point other than R1, R2
+// (INT64_MAX = none); pass 0 fills W / R1, pass 1 R2, pass 2 emits the
+// reference recorder's conflicts (interp/races.py:52-76) as events
+// (point, sequence, kind, other point, slot, offset)
+__device__ __forceinline__ void emit_ev(i64 *EV, u64 *NEV, i64 cap, i64 q, i64 seq, i64 kind,
+                                        i64 other, i64 slot, i64 off) {
+  const u64 k = atomicAdd(NEV, 1ULL);
+  if ((i64)k < cap) {
+    i64 *e = EV + 6 * k;
+    e[0] = q; e[1] = seq; e[2] = kind; e[3] = other; e[4] = slot; e[5] = off;
+  }
+}
+__device__ __forceinline__ void rec(int pass, int slot, i64 off, int wr, i64 q, i64 seq,
+                                    i64 *const *SH, i64 *EV, u64 *NEV, i64 cap) {
+  i64 *W = SH[3 * slot], *R1 = SH[3 * slot + 1], *R2 = SH[3 * slot + 2];
+  if (pass == 0) {
+    if (wr) atomicMin((long long *)&W[off], (long long)q);
+    else atomicMin((long long *)&R1[off], (long long)q);
+    return;
+  }
+  if (pass == 1) {
+    if (!wr && R1[off] != q) atomicMin((long long *)&R2[off], (long long)q);
+    return;
+  }
+  const i64 w = W[off];
+  if (w < q) emit_ev(EV, NEV, cap, q, seq, 0, w, slot, off);
+  if (wr) {
+    const i64 r1 = R1[off], r2 = R2[off];
+    if (r1 < q) emit_ev(EV, NEV, cap, q, seq, 1, r1, slot, off);
+    if (r2 < q) emit_ev(EV, NEV, cap, q, seq, 2, r2, slot, off);
+  }
+}
+"""
+
+
+def vm_source(prog, buffers, env_regs, record=False):
     """CUDA C for a VMProgram over ``buffers`` (slot order).
 
     ``env_regs``: the init registers holding host values (loaded from the
     kernel's ``env`` argument, in prog.init_regs order); every other init
     register is a program constant and is embedded.  Returns (source,
     kernel name, env list of (reg, index into init_vals)).
+
+    ``record``: the race recorder variant (races.py): loads and stores only
+    report their addresses to ``rec`` (point = the band index, in
+    row-major order) — valid for programs whose addresses and control flow
+    do not depend on loaded data, which races.py checks.
     """
-    count = prog.count
-    name = "b200_vm_native"
+    count = prog.count and not record
+    name = "b200_vm_record" if record else "b200_vm_native"
     used = set()
     insts = _decode(prog.words)
     for _, op, _, fl, a in insts:
@@ -135,9 +177,15 @@ def vm_source(prog, buffers, env_regs):
         else:
             consts.append((reg, val))
 
-    L = [_PRELUDE, f'extern "C" __global__ void __launch_bounds__({THREADS}) {name}(',
-         "    void *const *__restrict__ P, const i64 *__restrict__ ENV, u64 *__restrict__ TALLY,"
-         " VmErr *__restrict__ ERR) {"]
+    if record:
+        L = [_PRELUDE, _RECORD,
+             f'extern "C" __global__ void __launch_bounds__({THREADS}) {name}(',
+             "    void *const *__restrict__ P, const i64 *__restrict__ ENV, i64 *const *SH,"
+             " i64 *EV, u64 *NEV, const i64 CAP, const int PASS, VmErr *__restrict__ ERR) {"]
+    else:
+        L = [_PRELUDE, f'extern "C" __global__ void __launch_bounds__({THREADS}) {name}(',
+             "    void *const *__restrict__ P, const i64 *__restrict__ ENV, u64 *__restrict__ TALLY,"
+             " VmErr *__restrict__ ERR) {"]
     regs = sorted(used | {r for r, _ in consts} | {r for r, _ in env})
     L.append("  u64 " + ", ".join(f"R{r} = 0" for r in regs) + ";" if regs else "")
     if count:
@@ -147,6 +195,8 @@ def vm_source(prog, buffers, env_regs):
     total = math.prod(b[3] for b in prog.band) if prog.band else 1
     L.append(f"  for (i64 pt = (i64)blockIdx.x * {THREADS} + threadIdx.x; pt < {total}LL;"
              f" pt += (i64)gridDim.x * {THREADS}) {{")
+    if record:
+        L.append("    i64 seq = 0;")
     for reg, val in consts:
         L.append(f"    R{reg} = 0x{val & 0xFFFFFFFFFFFFFFFF:x}ULL;")
     for reg, _ in env:
@@ -161,7 +211,7 @@ def vm_source(prog, buffers, env_regs):
             line.append(f"L{pc}:;")
         if count and tag >= 0:
             line.append(f"c{tag}++;")
-        line.append(_stmt(pc, op, fl, a, buffers, count))
+        line.append(_stmt(pc, op, fl, a, buffers, count, record))
         L.append("    " + " ".join(line))
     L.append("  next_point:;")
     L.append("  }")
@@ -178,7 +228,7 @@ def vm_source(prog, buffers, env_regs):
     return "\n".join(L) + "\n", name, env
 
 
-def _stmt(pc, op, fl, a, buffers, count):
+def _stmt(pc, op, fl, a, buffers, count, record=False):
     if op == V_END:
         return "goto next_point;"
     if op == V_NOP:
@@ -222,6 +272,12 @@ def _stmt(pc, op, fl, a, buffers, count):
                              f"goto fault; }}")
             terms.append(f"(i64)R{ir} * {buf.strides[k]}LL")
         off = " + ".join(terms) if terms else "0"
+        if record:
+            parts.append(f"rec(PASS, {slot}, {off}, {int(op == V_STORE)}, pt, seq++, SH, EV, NEV,"
+                         f" CAP);")
+            if op == V_LOAD:
+                parts.append(f"R{reg} = 0;")
+            return "{ " + " ".join(parts) + " }"
         T = _CTYPE[dt]
         p = f"(({T} *)P[{slot}])[{off}]"
         if op == V_LOAD:
