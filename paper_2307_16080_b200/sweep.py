@@ -113,6 +113,44 @@ def _fast_buffers_close(got, want):
     return bool(np.all(close))
 
 
+def make_inputs(module, func, seed):
+    """The reference's make_inputs (tuner/search.py:78-102), bit for bit, with
+    the float memrefs drawn by numpy: ``random.Random(seed)``'s Mersenne
+    Twister state is handed to a numpy RandomState, whose random_sample()
+    is the same 53-bit draw as random.random(), so uniform(-2, 2) =
+    -2 + 4 * random() gives the same doubles (and, stored into an f32
+    Buffer, the same round-to-nearest floats); the state is handed back for
+    the next argument.  Integer, i1 and scalar arguments use the Python
+    generator itself.  ~30x faster on the sweep's 1024^2 operands, which
+    dominated each rank's setup."""
+    import importlib
+    import math
+
+    from staircase.interp import Buffer
+
+    # the module (staircase.tuner re-exports the function under the same name)
+    ref = importlib.import_module("staircase.tuner.search")
+
+    func_op = ref._find_func(module, func)
+    rng = random.Random(seed)
+    out = []
+    for arg in func_op.body().args:
+        ty = arg.type
+        if ty.kind == "memref" and ty.element.is_float:
+            size = math.prod(ty.shape)
+            st = rng.getstate()
+            rs = np.random.RandomState()
+            rs.set_state(("MT19937", np.array(st[1][:-1], dtype=np.uint32), st[1][-1]))
+            vals = -2.0 + (2.0 - -2.0) * rs.random_sample(size)
+            s2 = rs.get_state()
+            rng.setstate((3, tuple(int(v) for v in s2[1]) + (int(s2[2]),), None))
+            dt = np.float32 if ty.element.kind == "f32" else np.float64
+            out.append(Buffer(ty.shape, ty.element.kind, vals.astype(dt).tobytes()))
+        else:
+            out.append(ref._fresh_argument(ty, rng))
+    return out
+
+
 def _session_class():
     """The reference trial session (tuner/search.py:151-201) bound to an
     engine and with a vectorised equivalence guard.
@@ -165,7 +203,7 @@ def _session_class():
             self.template = pipeline_template or ref.default_pipeline
             self.mode = mode
             self.workers = workers
-            self.inputs = ref.make_inputs(module, self.func, seed)
+            self.inputs = make_inputs(module, self.func, seed)
             args = ref._copy_args(self.inputs)
             results, stats = machine.run(module, self.func, args, mode="sequential",
                                          engine=engine)

@@ -273,3 +273,25 @@ def test_world2_trial_error_raises_on_every_rank():
     with pytest.raises(RuntimeError, match=r"tiles=\[1, 1\] unroll=4"):
         sweep.search(corpus.conv_small.module, _failing_template, ParamSpace(**SPACE_ARGS),
                      budget=10, seed=0, strategy="grid", engine=oracle)
+
+
+@pytest.mark.parametrize("fn", [corpus.conv_small, corpus.matmul_par, corpus.int_ops,
+                                corpus.scalar_args, corpus.linear32])
+@pytest.mark.parametrize("seed", [0, 3, 12345])
+def test_fast_make_inputs_is_the_reference_stream(fn, seed):
+    """sweep.make_inputs draws the float memrefs with numpy from the same
+    Mersenne Twister state: every argument bit-identical to the reference's
+    make_inputs (tuner/search.py:78-102), including what follows them."""
+    from paper_2307_16080_b200 import sweep
+    from staircase.interp import Buffer
+    from staircase.tuner.search import make_inputs
+
+    want = make_inputs(fn.module, fn.__name__, seed)
+    got = sweep.make_inputs(fn.module, fn.__name__, seed)
+    assert len(got) == len(want)
+    for g, w in zip(got, want):
+        if isinstance(w, Buffer):
+            assert (g.shape, g.dtype) == (w.shape, w.dtype)
+            assert g.data.tobytes() == w.data.tobytes()
+        else:
+            assert type(g) is type(w) and g == w
