@@ -1,6 +1,6 @@
 """The reference's command line, executed on the B200 backend.
 
-    python -m paper_2307_16080_b200 [--precision exact|tf32|bf16] <staircase CLI arguments>
+    python -m paper_2307_16080_b200 [--precision exact|f32x3|tf32|bf16] <staircase CLI arguments>
 
 e.g. ``python -m paper_2307_16080_b200 run --input k.sir --func matmul --args a.json
 b.json c.json --out outdir`` or ``python -m paper_2307_16080_b200 tune --input

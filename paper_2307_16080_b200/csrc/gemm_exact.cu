@@ -92,8 +92,15 @@ struct MinBlocks {
 // VEC (strided f32 only): A k-contiguous and B n-contiguous with 16-byte
 // aligned rows and K, N multiples of 4 — the tiles are staged with 16-byte
 // global loads (A transposed into As by four scalar stores, B stored as is).
-template <typename T, typename Addr, int BM, int BN, int TM, int TN, bool VEC = false>
-__global__ void __launch_bounds__(kThreads, MinBlocks<T, TM, TN>::value)
+// Shared staging of one CTA: A (k-major, padded) and B double buffers.
+template <typename T, int BM, int BN>
+constexpr size_t smem_bytes() {
+  return (size_t)2 * BK * ((BM + 16 / sizeof(T)) + BN) * sizeof(T);
+}
+
+template <typename T, typename Addr, int BM, int BN, int TM, int TN, bool VEC = false,
+          int MINB = MinBlocks<T, TM, TN>::value>
+__global__ void __launch_bounds__(kThreads, MINB)
     contract_exact_kernel(Args<T, Addr> g) {
   constexpr int PAD = 16 / sizeof(T);
   constexpr int LA = BM * BK / kThreads;  // A elements staged per thread
@@ -102,8 +109,11 @@ __global__ void __launch_bounds__(kThreads, MinBlocks<T, TM, TN>::value)
   constexpr int TX = BN / TN;              // threads along n
   static_assert((BM / TM) * (BN / TN) == kThreads, "tile / thread mismatch");
   static_assert(kThreads % BM == 0 && kThreads % BN == 0, "fixed-row staging");
-  __shared__ __align__(16) T As[2][BK][BM + PAD];
-  __shared__ __align__(16) T Bs[2][BK][BN];
+  static_assert(BM % 64 == 0 || !VEC, "VEC staging: rows t / 4 + 64 i");
+  // dynamic shared memory (tiles above 48 KB of staging need the opt-in)
+  extern __shared__ __align__(16) unsigned char smem_dyn[];
+  auto As = reinterpret_cast<T (*)[BK][BM + PAD]>(smem_dyn);
+  auto Bs = reinterpret_cast<T (*)[BK][BN]>(smem_dyn + (size_t)2 * BK * (BM + PAD) * sizeof(T));
 
   int64_t m0, n0;
   if (g.ntn > 0) {
@@ -295,21 +305,40 @@ __global__ void __launch_bounds__(kThreads, MinBlocks<T, TM, TN>::value)
   }
 }
 
-template <typename T, typename Addr, int BM, int BN, int TM, int TN, bool VEC = false>
+template <typename T, typename Addr, int BM, int BN, int TM, int TN, bool VEC, int MINB>
+void *kernel_ptr() {
+  auto k = contract_exact_kernel<T, Addr, BM, BN, TM, TN, VEC, MINB>;
+  constexpr size_t smem = smem_bytes<T, BM, BN>();
+  if (smem > 48 * 1024) {
+    static bool done = false;   // opt in once per instantiation
+    if (!done) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      done = true;
+    }
+  }
+  return reinterpret_cast<void *>(k);
+}
+
+template <typename T, typename Addr, int BM, int BN, int TM, int TN, bool VEC = false,
+          int MINB = MinBlocks<T, TM, TN>::value>
 int launch_tile(const Args<T, Addr> &g, void *stream) {
   dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM));
   if (grid.y > 65535u) return B200_EINVAL;
-  contract_exact_kernel<T, Addr, BM, BN, TM, TN, VEC>
-      <<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(g);
+  kernel_ptr<T, Addr, BM, BN, TM, TN, VEC, MINB>();
+  contract_exact_kernel<T, Addr, BM, BN, TM, TN, VEC, MINB>
+      <<<grid, kThreads, smem_bytes<T, BM, BN>(), static_cast<cudaStream_t>(stream)>>>(g);
   return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
 }
 
-template <typename T, typename Addr, int BM, int BN, int TM, int TN, bool VEC = false>
+template <typename T, typename Addr, int BM, int BN, int TM, int TN, bool VEC = false,
+          int MINB = MinBlocks<T, TM, TN>::value>
 int launch_linear(const Args<T, Addr> &g, int64_t blocks, void *stream) {
   if (blocks <= 0) return B200_OK;
   if (blocks >= (int64_t(1) << 31)) return B200_EINVAL;
-  contract_exact_kernel<T, Addr, BM, BN, TM, TN, VEC>
-      <<<(unsigned)blocks, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(g);
+  kernel_ptr<T, Addr, BM, BN, TM, TN, VEC, MINB>();
+  contract_exact_kernel<T, Addr, BM, BN, TM, TN, VEC, MINB>
+      <<<(unsigned)blocks, kThreads, smem_bytes<T, BM, BN>(),
+         static_cast<cudaStream_t>(stream)>>>(g);
   return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
 }
 
@@ -364,6 +393,10 @@ int launch(const Args<float, Addr> &g, void *stream) {
   if (g.M * g.N <= 64 * 64) return launch_tile<float, Addr, 32, 32, 2, 2>(g, stream);
   if (big_ctas < 148) return launch_tile<float, Addr, 64, 64, 4, 4>(g, stream);
   if (g.N <= 64) return launch_tile<float, Addr, 256, 64, 8, 8>(g, stream);
+  // (measured at 4096^3, tools/probe_exact.py: one CTA per SM with 255
+  // registers — 128x128, 128x256 at 8x16 or 256x128 at 16x8 per thread —
+  // ran 7-17 % slower than two 128-register CTAs: the FMUL -> FADD and LDS
+  // latencies need the second CTA's warps more than the extra registers)
   if constexpr (std::is_same<Addr, Strided>::value)
     if (vec_ok(g)) return launch_128<Addr, true>(g, stream);
   return launch_128<Addr, false>(g, stream);
