@@ -15,8 +15,8 @@ ensure_staircase()
 
 from . import engine  # noqa: E402
 from .engine import (ENGINE_NAME, ExecContext, Session, configure, install,  # noqa: E402
-                     run_tape)
+                     run_tape, settings, uninstall, using)
 from .races import check_races  # noqa: E402
 
-__all__ = ["engine", "install", "configure", "run_tape", "ExecContext", "Session",
-           "ENGINE_NAME", "check_races"]
+__all__ = ["engine", "install", "uninstall", "configure", "using", "settings", "run_tape",
+           "ExecContext", "Session", "ENGINE_NAME", "check_races"]

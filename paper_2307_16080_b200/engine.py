@@ -32,8 +32,10 @@ Install globally (the tuner calls run() without engine=, search.py:170,190):
 """
 from __future__ import annotations
 
+import contextlib
 import math
 import os
+import threading
 
 from . import analysis, fusion, plancache, templates, vmcode
 from .host import errors as _errors
@@ -44,51 +46,117 @@ from .runtime import DeviceBackend
 
 ENGINE_NAME = "b200"
 
-# Contraction precision.  "exact" (default): fp32 per-op rounding on the FP32
-# pipes, bit-identical to the reference.  "f32x3": f32 operands split into
-# tf32 hi + lo parts, three tf32 products per term on the tensor cores —
-# fp32-accurate (within rel 1e-5 of the reference, tests/test_gpu_f32x3.py),
-# not bit-identical.  "tf32" / "bf16": operands rounded to tf32 / bf16 and
-# contracted on the tcgen05 tensor cores with fp32 accumulation (tolerance:
-# DESIGN.md, tests/tcbound.py).
-PRECISION = os.environ.get("B200_PRECISION", "exact")
-# Cross-region fusion of queued plans (B200_FUSE=0 disables, for A/B tests).
-FUSE = os.environ.get("B200_FUSE", "1") != "0"
-# bf16 shadows of contraction outputs read as the next contraction's A
-# (fusion.plan_shadows; B200_SHADOW=0 disables, for A/B tests).
-SHADOW = os.environ.get("B200_SHADOW", "1") != "0"
-# Row-panel pipelining of the host copies of large contractions / convs
-# (runtime.Staging.stream_rows; B200_STREAM_IO=0 disables, for A/B tests).
-STREAM_IO = os.environ.get("B200_STREAM_IO", "1") != "0"
-# A bf16 / tf32 request a contraction cannot honour (no strided GEMM view,
-# unaligned K, conv shape outside the tcgen05 kernel) runs exact f32 with a
-# runtime.PrecisionFallback warning; strict makes it PrecisionUnavailable.
-STRICT = os.environ.get("B200_STRICT", "0") == "1"
-# Per-region plan cache (plancache.py): a repeated run of the same tape
-# region with the same scalar values and buffer geometry skips lifting,
-# analysis and matching (B200_PLAN_CACHE=0 disables, for A/B tests).
-PLAN_CACHE = os.environ.get("B200_PLAN_CACHE", "1") != "0"
+# Execution knobs.  Process-wide defaults come from the environment and
+# configure(); using(...) overrides them for the calling thread only, so
+# concurrent callers (threads, the tuner) never see each other's settings.
+#
+# precision: contraction arithmetic.  "exact" (default): fp32 per-op
+#   rounding on the FP32 pipes, bit-identical to the reference.  "f32x3": f32
+#   operands split into tf32 hi + lo parts, three tf32 products per term on
+#   the tensor cores — fp32-accurate (within rel 1e-5 of the reference,
+#   tests/test_gpu_f32x3.py), not bit-identical.  "tf32" / "bf16": operands
+#   rounded to tf32 / bf16 and contracted on the tcgen05 tensor cores with
+#   fp32 accumulation (tolerance: DESIGN.md, tests/tcbound.py).
+# fuse: cross-region fusion of queued plans (B200_FUSE=0 disables, A/B tests).
+# shadow: bf16 shadows of contraction outputs read as the next contraction's
+#   A (fusion.plan_shadows; B200_SHADOW=0 disables).
+# stream_io: row-panel pipelining of the host copies of large contractions /
+#   convs (runtime.Staging.stream_rows; B200_STREAM_IO=0 disables).
+# strict: a bf16 / tf32 request a contraction cannot honour (no strided GEMM
+#   view, unaligned K, conv shape outside the tcgen05 kernel) runs exact f32
+#   with a runtime.PrecisionFallback warning; strict makes it
+#   PrecisionUnavailable.
+# plan_cache: per-region plan cache (plancache.py): a repeated run of the
+#   same tape region with the same scalar values and buffer geometry skips
+#   lifting, analysis and matching (B200_PLAN_CACHE=0 disables).
+_defaults = {
+    "precision": os.environ.get("B200_PRECISION", "exact"),
+    "fuse": os.environ.get("B200_FUSE", "1") != "0",
+    "shadow": os.environ.get("B200_SHADOW", "1") != "0",
+    "stream_io": os.environ.get("B200_STREAM_IO", "1") != "0",
+    "strict": os.environ.get("B200_STRICT", "0") == "1",
+    "plan_cache": os.environ.get("B200_PLAN_CACHE", "1") != "0",
+}
+# per-thread state: using() overrides, the last run's plan and device copies,
+# the race checker's region hook
+_tls = threading.local()
+# module attributes kept for callers that read them (engine.PRECISION, ...):
+# each resolves to the calling thread's effective value (PEP 562)
+_KNOB_ATTRS = {"PRECISION": "precision", "FUSE": "fuse", "SHADOW": "shadow",
+               "STREAM_IO": "stream_io", "STRICT": "strict", "PLAN_CACHE": "plan_cache"}
 
-# kernel choice of the last run (tests and bench inspect these)
-last_plan = []
+
+def _validated(kw):
+    bad = set(kw) - set(_defaults)
+    if bad:
+        raise TypeError(f"unknown engine setting(s) {sorted(bad)}")
+    out = {}
+    for k, v in kw.items():
+        if v is None:
+            continue
+        if k == "precision":
+            from .runtime import PRECISIONS
+
+            if v not in PRECISIONS:
+                raise ValueError(f"unknown precision {v!r}")
+            out[k] = v
+        else:
+            out[k] = bool(v)
+    return out
 
 
-def configure(precision=None, fuse=None, shadow=None, strict=None):
-    """Select the contraction precision / fusion for subsequent runs."""
-    global PRECISION, FUSE, SHADOW, STRICT
-    if strict is not None:
-        STRICT = bool(strict)
-    if precision is not None:
-        from .runtime import PRECISIONS
+def settings():
+    """The calling thread's effective settings (a fresh dict)."""
+    eff = dict(_defaults)
+    eff.update(getattr(_tls, "overrides", None) or {})
+    return eff
 
-        if precision not in PRECISIONS:
-            raise ValueError(f"unknown precision {precision!r}")
-        PRECISION = precision
-    if fuse is not None:
-        FUSE = bool(fuse)
-    if shadow is not None:
-        SHADOW = bool(shadow)
-    return {"precision": PRECISION, "fuse": FUSE, "shadow": SHADOW, "strict": STRICT}
+
+def configure(precision=None, fuse=None, shadow=None, strict=None, stream_io=None,
+              plan_cache=None):
+    """Set the process-wide defaults for subsequent runs (threads inside a
+    using() block keep their overrides)."""
+    _defaults.update(_validated(dict(precision=precision, fuse=fuse, shadow=shadow,
+                                     strict=strict, stream_io=stream_io,
+                                     plan_cache=plan_cache)))
+    return {k: _defaults[k] for k in ("precision", "fuse", "shadow", "strict")}
+
+
+@contextlib.contextmanager
+def using(**kw):
+    """Override settings for the calling thread inside the block:
+
+        with engine.using(precision="bf16", strict=True):
+            machine.run(module, "matmul", args, engine=engine)
+    """
+    prev = getattr(_tls, "overrides", None)
+    _tls.overrides = {**(prev or {}), **_validated(kw)}
+    try:
+        yield settings()
+    finally:
+        _tls.overrides = prev
+
+
+@contextlib.contextmanager
+def region_hook(fn):
+    """Call ``fn(region, accesses)`` for every region this thread's runs lift
+    (races.check_races' static proof)."""
+    prev = getattr(_tls, "region_hook", None)
+    _tls.region_hook = fn
+    try:
+        yield
+    finally:
+        _tls.region_hook = prev
+
+
+def __getattr__(name):
+    if name in _KNOB_ATTRS:
+        return settings()[_KNOB_ATTRS[name]]
+    if name == "last_plan":     # kernel choice of this thread's last run
+        return getattr(_tls, "last_plan", [])
+    if name == "last_staging":
+        return getattr(_tls, "last_staging", None)
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")
 
 
 class ExecContext:
@@ -128,7 +196,10 @@ class _Run:
     def __init__(self, program, ctx, backend=None, shard=None):
         self.program = program
         self.ctx = ctx
-        self.be = backend if backend is not None else DeviceBackend(stream_io=STREAM_IO)
+        self.cfg = settings()
+        self.hook = getattr(_tls, "region_hook", None)
+        self.be = (backend if backend is not None
+                   else DeviceBackend(stream_io=self.cfg["stream_io"]))
         self.plan = []
         self.shard = shard    # shard.Shard: run only this rank's batch rows
         self.pending = []     # queued MapItem / ContractItem, program order
@@ -229,9 +300,11 @@ class _Run:
     # -- regions ---------------------------------------------------------------
     def region(self, code, start, end, regs, tally):
         key = None
-        if PLAN_CACHE and self.shard is None and _region_hook is None:
+        cfg = self.cfg
+        cacheable = cfg["plan_cache"] and self.shard is None and self.hook is None
+        if cacheable:
             rkey = (plancache.region_key(self.program, code, start, end), self.ctx.mode,
-                    PRECISION, FUSE, SHADOW)
+                    cfg["precision"], cfg["fuse"], cfg["shadow"])
             key = plancache.lookup_key(rkey, regs)
             hit = plancache.get(key)
             if hit is not None:
@@ -260,8 +333,8 @@ class _Run:
             except E.ModeUnsupported:
                 self.flush_pending()
                 raise
-        if _region_hook is not None:   # races.check_races: static race proof
-            _region_hook(r, accesses)
+        if self.hook is not None:   # races.check_races: static race proof
+            self.hook(r, accesses)
         links, remainder = analysis.chain_of(r)
         safe = analysis.statically_in_bounds(r, accesses) and not analysis.invalid_steps(r)
         # a region with memref.alloc runs on one thread: its scratch buffer
@@ -272,7 +345,7 @@ class _Run:
         for slot in written:
             self.be.mark_dirty(r.buffers[slot])
 
-        store = key is None and PLAN_CACHE and self.shard is None and _region_hook is None
+        store = key is None and cacheable
         if safe and st is not None:
             g = templates.match_contraction(r, links, remainder, accesses)
             if g is not None:
@@ -341,8 +414,8 @@ class _Run:
         the region that forced the flush will write (already marked dirty)."""
         if not self.pending:
             return
-        items = fusion.fuse(self.pending) if FUSE else self.pending
-        if SHADOW:
+        items = fusion.fuse(self.pending) if self.cfg["fuse"] else self.pending
+        if self.cfg["shadow"]:
             fusion.plan_shadows(items)
         self.pending = []
         # last_writer[i]: no later queued plan (nor the triggering region)
@@ -360,7 +433,7 @@ class _Run:
                 later.update(id(b) for b in it.m.buffers)
         for it, last in zip(items, last_writer):
             if isinstance(it, fusion.ContractItem):
-                kernels = self.be.contract(it.g, PRECISION, init=it.init,
+                kernels = self.be.contract(it.g, self.cfg["precision"], init=it.init,
                                            init_value=it.init_value, bias=it.bias,
                                            bias_base=it.bias_base,
                                            bias_stride=it.bias_stride,
@@ -436,7 +509,6 @@ def _cmpi(p, a, b):
 def run_tape(program, code, regs, tally, ctx, backend=None, shard=None):
     """Engine-protocol entry point (machine.py:112).  ``shard``: a
     shard.Shard — execute only this rank's batch rows (shard.run)."""
-    global last_plan
     run = _Run(program, ctx, backend, shard)
     try:
         rets = run.exec_tape(code, regs, tally)
@@ -446,31 +518,25 @@ def run_tape(program, code, regs, tally, ctx, backend=None, shard=None):
             run.flush_pending()
             run.be.flush()
         finally:
-            last_plan = run.plan
+            _tls.last_plan = run.plan
         raise
     run.be.flush()
-    last_plan = run.plan
-    global last_staging
+    _tls.last_plan = run.plan
     # the run's device copies (== the host Buffers after the flush): kept
-    # until the next run so a caller can post-process on the device (the
-    # sweep's equivalence guard, sweep.py)
-    last_staging = getattr(run.be, "stage", None)
+    # until this thread's next run so a caller can post-process on the
+    # device (the sweep's equivalence guard, sweep.py)
+    _tls.last_staging = getattr(run.be, "stage", None)
     return rets
 
 
-last_staging = None
-_region_hook = None   # callable(region, accesses) or None (races.check_races)
-
-
 def release_last_staging():
-    """Drop the last run's device copies (kept for device_copy)."""
-    global last_staging
-    last_staging = None
+    """Drop this thread's last run's device copies (kept for device_copy)."""
+    _tls.last_staging = None
 
 
 def device_copy(buf):
     """The last run's device tensor of ``buf`` (same contents), or None."""
-    st = last_staging
+    st = getattr(_tls, "last_staging", None)
     if st is None or not hasattr(st, "dev"):
         return None
     ent = st.dev.get(id(buf))
@@ -549,8 +615,15 @@ class Session:
         self.be.flush()
 
 
+_previous_engine = None
+
+
 def install():
-    """Make this engine the default of staircase.interp.machine.run()."""
+    """Make this engine the default of staircase.interp.machine.run().
+
+    machine.ENGINE_NAME (computed once at import, machine.py:34) is updated
+    too, so the reference's reports name the engine that actually runs."""
+    global _previous_engine
     from .host import ensure_staircase
 
     ensure_staircase()
@@ -558,8 +631,24 @@ def install():
 
     from staircase.interp import machine
 
-    machine._engine = sys.modules[__name__]
+    me = sys.modules[__name__]
+    if machine._engine is not me:
+        _previous_engine = (machine._engine, machine.ENGINE_NAME)
+    machine._engine = me
+    machine.ENGINE_NAME = ENGINE_NAME
     return machine
 
 
-__all__ = ["ExecContext", "run_tape", "install", "configure", "ENGINE_NAME"]
+def uninstall():
+    """Restore the engine install() replaced."""
+    global _previous_engine
+    from staircase.interp import machine
+
+    if _previous_engine is not None:
+        machine._engine, machine.ENGINE_NAME = _previous_engine
+        _previous_engine = None
+    return machine
+
+
+__all__ = ["ExecContext", "run_tape", "install", "uninstall", "configure", "using",
+           "settings", "region_hook", "ENGINE_NAME"]

@@ -235,13 +235,11 @@ def check_races(module, func_name, args, engine=None):
         else:
             found.extend(got)
 
-    b2engine._region_hook = hook
     try:
-        machine.run(module, func_name, copies, mode="gpu_emulated", engine=eng)
+        with b2engine.region_hook(hook):
+            machine.run(module, func_name, copies, mode="gpu_emulated", engine=eng)
     except Exception:
         fallback.append(True)   # let the reference reproduce whatever happened
-    finally:
-        b2engine._region_hook = None
     if fallback:
         return reference_check(module, func_name, args)
     out, seen = [], set()

@@ -37,14 +37,10 @@ def _run(fn, precision, stream, monkeypatch):
     import paper_2307_16080_b200 as b2
     from paper_2307_16080_b200 import engine, runtime
 
-    monkeypatch.setattr(engine, "STREAM_IO", stream)
     monkeypatch.setattr(runtime, "STREAM_MIN_BYTES", 1)
     monkeypatch.setattr(runtime, "STREAM_PANEL_BYTES", 1 << 12)
-    b2.configure(precision=precision)
-    try:
+    with engine.using(precision=precision, stream_io=stream):
         _, bufs, tally, _ = harness.run_engine(b2.engine, fn, None, "sequential", 5)
-    finally:
-        b2.configure(precision="exact")
     return bufs, tally, list(engine.last_plan), engine.last_staging.panels
 
 

@@ -131,11 +131,8 @@ def test_recordable_regions(name, ok):
     args = harness.make_args(fn, 3)
     labels = {id(a): f"arg{i}" for i, a in enumerate(args)}
     seen = []
-    engine._region_hook = lambda r, acc: seen.append(races.recordable(r, acc, labels))
-    try:
+    with engine.region_hook(lambda r, acc: seen.append(races.recordable(r, acc, labels))):
         harness.run_engine(SimEngine(), fn, None, "gpu_emulated", 3, args=args)
-    finally:
-        engine._region_hook = None
     assert seen == [ok]
     del analysis
 
@@ -150,11 +147,8 @@ def test_data_dependent_scatter_is_not_recordable():
     module, args = scatter_module(), scatter_args()
     labels = {id(a): f"arg{i}" for i, a in enumerate(args)}
     seen = []
-    engine._region_hook = lambda r, acc: seen.append(races.recordable(r, acc, labels))
-    try:
+    with engine.region_hook(lambda r, acc: seen.append(races.recordable(r, acc, labels))):
         machine.run(module, "scatter", args, mode="gpu_emulated", engine=SimEngine())
-    finally:
-        engine._region_hook = None
     assert seen == [False]
     got = races.check_races(module, "scatter", scatter_args(), engine=SimEngine())
     from staircase.interp.races import check_races
@@ -171,11 +165,8 @@ def test_record_kernel_compiles(name):
     fn = _kernels()[name]
     args = harness.make_args(fn, 3)
     got = []
-    engine._region_hook = lambda r, acc: got.append((r, acc))
-    try:
+    with engine.region_hook(lambda r, acc: got.append((r, acc))):
         harness.run_engine(SimEngine(), fn, None, "gpu_emulated", 3, args=args)
-    finally:
-        engine._region_hook = None
     (r, acc), = got
     links, remainder = analysis.chain_of(r)
     band = [v.id for v in r.tree[0].vars]
