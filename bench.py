@@ -383,6 +383,45 @@ def load_peaks():
             "sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md)"
 
 
+_TF32_PEAK = {}
+
+
+def tf32_peak():
+    """Dense tf32 tensor-core peak measured here (MEASURED_PEAKS.json has
+    bf16 only): cuBLAS fp32 GEMM with tf32 allowed, 8192^3, best of 10 after
+    warm-up, CUDA events (burst, like the bf16 figure it sits beside).
+    Cached for the process; None without a GPU."""
+    if "v" in _TF32_PEAK:
+        return _TF32_PEAK["v"]
+    import torch
+
+    v = None
+    if torch.cuda.is_available():
+        prev = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = True
+        try:
+            n = 8192
+            a = torch.randn(n, n, device="cuda")
+            b = torch.randn(n, n, device="cuda")
+            for _ in range(3):
+                torch.matmul(a, b)
+            best = None
+            for _ in range(10):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                torch.matmul(a, b)
+                e1.record()
+                e1.synchronize()
+                ms = e0.elapsed_time(e1)
+                best = ms if best is None else min(best, ms)
+            v = 2.0 * n ** 3 / (best * 1e-3) / 1e12
+            del a, b
+        finally:
+            torch.backends.cuda.matmul.allow_tf32 = prev
+    _TF32_PEAK["v"] = v
+    return v
+
+
 def load_traffic(key):
     """dram bytes per launch of the dominant kernel from the committed ncu summary."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
@@ -605,14 +644,25 @@ def roofline(wl, prec, fam, ms, sus_ms, rank_flops):
         sus_peak = peak
     elif dom in TENSOR_KERNELS:
         achieved = rank_flops / (dom_ms * 1e-3) / 1e12
-        f = {"bf16": 1.0, "tf32": 0.5, "f32x3": 0.5 / 3}[prec]
-        peak = peaks["bf16_tflops"] * f
-        sus_peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) * f
+        tf = tf32_peak() if prec in ("tf32", "f32x3") else None
+        if tf is not None:
+            # tf32 rate measured in this run (cuBLAS tf32 8192^3, burst)
+            f = {"tf32": 1.0, "f32x3": 1.0 / 3}[prec]
+            peak = tf * f
+            sus_peak = peak * peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) / \
+                peaks["bf16_tflops"]
+            peak_source = {"tf32": "measured in this run: cuBLAS tf32 GEMM 8192^3 (burst)",
+                           "f32x3": "measured in this run: cuBLAS tf32 GEMM 8192^3 (burst) / 3 "
+                                    "(each fp32-accurate product is 3 tf32 products)"}[prec]
+        else:
+            f = {"bf16": 1.0, "tf32": 0.5, "f32x3": 0.5 / 3}[prec]
+            peak = peaks["bf16_tflops"] * f
+            sus_peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) * f
+            peak_source = {"bf16": f"{src} bf16 dense (MEASURED_PEAKS.json)",
+                           "tf32": f"{src} bf16 x 0.5 (tf32 = half rate, derived)",
+                           "f32x3": f"{src} bf16 x 0.5 / 3 (derived: each fp32-accurate product "
+                                    f"is 3 tf32 products at half the bf16 rate)"}[prec]
         unit, bound = "TFLOP/s", "tensor"
-        peak_source = {"bf16": f"{src} bf16 dense (MEASURED_PEAKS.json)",
-                       "tf32": f"{src} bf16 x 0.5 (tf32 = half rate, derived)",
-                       "f32x3": f"{src} bf16 x 0.5 / 3 (derived: each fp32-accurate product is "
-                                f"3 tf32 products at half the bf16 rate)"}[prec]
         if wl.tc_bytes and wl.tc_bytes * scale / (dom_ms * 1e-3) / 1e9 / peaks["hbm_gbs"] > \
                 achieved / peak:
             # the conv's f32 output read-modify-write makes it HBM-bound

@@ -305,6 +305,166 @@ __global__ void __launch_bounds__(kThreads, MINB)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Whole-tile strided f32 kernel (the 4096^3 / Linear-stack shapes): M, N
+// multiples of 128, K a multiple of 32, A k-contiguous and B n-contiguous
+// with 16-byte aligned rows.  Same arithmetic as contract_exact_kernel (one
+// __fmul_rn and one __fadd_rn per MAC, k ascending), different staging:
+//   * both operands arrive by cp.async (16-byte, L2-only) in a 3-stage ring
+//     of BK = 32 slices — no staging registers, one barrier per 32 k;
+//   * A stays row-major in shared memory ([m][k], rows padded to 36 floats so
+//     the two rows a warp reads sit 16 banks apart) and is read AK k at a
+//     time per row (LDS.64 / LDS.128), B is read as two LDS.128 per k;
+//   * no bounds tests and 32-bit shared addressing in the main loop.
+// The generic kernel spent ~190 issue slots per 16-k slice on 64-bit index
+// and bounds arithmetic (SASS; ~11 % of all issued instructions at 4096^3).
+constexpr int FBM = 128, FBN = 128, FBK = 32, FSTAGES = 3, FAPAD = 36;
+constexpr size_t kFullStageA = (size_t)FBM * FAPAD * 4;
+constexpr size_t kFullStageB = (size_t)FBK * FBN * 4;
+constexpr size_t kFullSmem = FSTAGES * (kFullStageA + kFullStageB);
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const float *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+
+template <int AK>
+__global__ void __launch_bounds__(kThreads, 2) gemm_exact_full_kernel(Args<float, Strided> g) {
+  extern __shared__ __align__(16) unsigned char smem_dyn[];
+  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dyn));
+  const float *As = reinterpret_cast<const float *>(smem_dyn);
+  const float *Bs = reinterpret_cast<const float *>(smem_dyn + FSTAGES * kFullStageA);
+  const uint32_t sA0 = sbase, sB0 = sbase + (uint32_t)(FSTAGES * kFullStageA);
+
+  int64_t m0, n0;
+  if (g.ntn > 0) {
+    const int64_t tl = g.tile_base + blockIdx.x;
+    m0 = (tl / g.ntn) * FBM;
+    n0 = (tl % g.ntn) * FBN;
+  } else {
+    m0 = (int64_t)blockIdx.y * FBM;
+    n0 = (int64_t)blockIdx.x * FBN;
+  }
+  const int t = threadIdx.x;
+  const int tx = t % 16, ty = t / 16;
+
+  // copy assignments: A chunk c = t + 256 i -> row c / 8, k quad c % 8;
+  // B chunk c -> k row c / 32, n quad c % 32
+  const float *ga = g.A + (m0 + t / 8) * g.ad.sAm + 4 * (t % 8);
+  const int64_t ga_step = 32 * g.ad.sAm;   // rows t/8 + 32 i
+  const float *gb = g.B + (int64_t)(t / 32) * g.ad.sBk + n0 + 4 * (t % 32);
+  const int64_t gb_step = 8 * g.ad.sBk;    // k rows t/32 + 8 i
+  const uint32_t da = (uint32_t)(((t / 8) * FAPAD + 4 * (t % 8)) * 4);
+  const uint32_t db = (uint32_t)(((t / 32) * FBN + 4 * (t % 32)) * 4);
+  auto load = [&](int64_t k0, int st) {
+    const uint32_t a = sA0 + (uint32_t)(st * kFullStageA) + da;
+    const uint32_t b = sB0 + (uint32_t)(st * kFullStageB) + db;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) cp_async16(a + i * 32 * FAPAD * 4, ga + i * ga_step + k0);
+    const float *pb = gb + k0 * g.ad.sBk;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) cp_async16(b + i * 8 * FBN * 4, pb + i * gb_step);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t m = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t n = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+      acc[i][j] = g.init ? g.init_value : g.C[g.ad.c(m, n)];
+    }
+  }
+
+  const int64_t ktiles = g.K / FBK;
+#pragma unroll
+  for (int s = 0; s < FSTAGES - 1; ++s) {
+    if (s < ktiles) load(s * FBK, s);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  // this thread's first A row / B column inside a stage
+  const int arow = ty * 4, bcol = tx * 4;
+  int st = 0;
+#pragma unroll 1
+  for (int64_t kt = 0; kt < ktiles; ++kt) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(FSTAGES - 2) : "memory");
+    __syncthreads();   // stage st complete for every thread; stage st-1 drained
+    {
+      const int64_t kn = kt + FSTAGES - 1;
+      const int ls = st == 0 ? FSTAGES - 1 : st - 1;
+      if (kn < ktiles) load(kn * FBK, ls);
+      else asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    const float *as = As + st * (kFullStageA / 4);
+    const float *bs = Bs + st * (kFullStageB / 4);
+#pragma unroll 2
+    for (int kq = 0; kq < FBK; kq += AK) {
+      float a[8][AK];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float *p = as + (i < 4 ? arow + i : 64 + arow + i - 4) * FAPAD + kq;
+        if constexpr (AK == 4) {
+          const float4 v = *reinterpret_cast<const float4 *>(p);
+          a[i][0] = v.x, a[i][1] = v.y, a[i][2] = v.z, a[i][3] = v.w;
+        } else {
+          const float2 v = *reinterpret_cast<const float2 *>(p);
+          a[i][0] = v.x, a[i][1] = v.y;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < AK; ++u) {
+        const float4 b0 = *reinterpret_cast<const float4 *>(bs + (kq + u) * FBN + bcol);
+        const float4 b1 = *reinterpret_cast<const float4 *>(bs + (kq + u) * FBN + 64 + bcol);
+        const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(a[i][u], b[j]));
+      }
+    }
+    st = st + 1 == FSTAGES ? 0 : st + 1;
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t m = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t n = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+      float v = acc[i][j];
+      if (g.bias) v = __fadd_rn(v, __ldg(g.bias + n * g.bias_stride));
+      g.C[g.ad.c(m, n)] = v;
+    }
+  }
+}
+
+inline bool full_ok(const Args<float, Strided> &g) {
+  const auto &a = g.ad;
+  return a.sAk == 1 && a.sBn == 1 && g.M % FBM == 0 && g.N % FBN == 0 && g.K % FBK == 0 &&
+         g.K > 0 && a.sAm % 4 == 0 && a.sBk % 4 == 0 &&
+         (reinterpret_cast<uintptr_t>(g.A) & 15) == 0 &&
+         (reinterpret_cast<uintptr_t>(g.B) & 15) == 0 && g.M / FBM <= 65535;
+}
+
+int launch_full(const Args<float, Strided> &g, void *stream) {
+  static int ak = -1;
+  if (ak < 0) {
+    const char *e = getenv("B200_GEMM_EXACT_AK");   // dev A/B knob
+    ak = (e && atoi(e) == 2) ? 2 : 4;
+  }
+  auto k = ak == 2 ? gemm_exact_full_kernel<2> : gemm_exact_full_kernel<4>;
+  static bool attr[2] = {false, false};
+  if (!attr[ak == 2]) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFullSmem);
+    attr[ak == 2] = true;
+  }
+  dim3 grid((unsigned)(g.N / FBN), (unsigned)(g.M / FBM));
+  k<<<grid, kThreads, kFullSmem, static_cast<cudaStream_t>(stream)>>>(g);
+  return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
+}
+
 template <typename T, typename Addr, int BM, int BN, int TM, int TN, bool VEC, int MINB>
 void *kernel_ptr() {
   auto k = contract_exact_kernel<T, Addr, BM, BN, TM, TN, VEC, MINB>;
@@ -397,8 +557,10 @@ int launch(const Args<float, Addr> &g, void *stream) {
   // registers — 128x128, 128x256 at 8x16 or 256x128 at 16x8 per thread —
   // ran 7-17 % slower than two 128-register CTAs: the FMUL -> FADD and LDS
   // latencies need the second CTA's warps more than the extra registers)
-  if constexpr (std::is_same<Addr, Strided>::value)
+  if constexpr (std::is_same<Addr, Strided>::value) {
+    if (full_ok(g) && !getenv("B200_GEMM_EXACT_OLD")) return launch_full(g, stream);
     if (vec_ok(g)) return launch_128<Addr, true>(g, stream);
+  }
   return launch_128<Addr, false>(g, stream);
 }
 
@@ -409,6 +571,8 @@ int launch_cta(const Args<float, Strided> &g, int cta_m, int cta_n, void *stream
   if (g.M < 0 || g.N < 0 || g.K < 0) return B200_EINVAL;
   if (g.M == 0 || g.N == 0) return B200_OK;
   const bool vec = vec_ok(g);
+  if (cta_m == 128 && cta_n == 128 && full_ok(g) && !getenv("B200_GEMM_EXACT_OLD"))
+    return launch_full(g, stream);
   if (cta_m == 128 && cta_n == 128)
     return vec ? launch_tile<float, Strided, 128, 128, 8, 8, true>(g, stream)
                : launch_tile<float, Strided, 128, 128, 8, 8>(g, stream);

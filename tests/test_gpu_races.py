@@ -50,9 +50,9 @@ def test_recorder_large_racy_accumulate(monkeypatch):
 
     src = """
 @staged
-def acc2d(x: MemRef[(64, 48), F32], acc: MemRef[(6,), F32]):
-    for i, j in parallel((0, 0), (64, 48)):
-        acc[j % 6] = acc[j % 6] + x[i, j]
+def acc2d(x: MemRef[(128, 48), F32], acc: MemRef[(6,), F32]):
+    for i, j in parallel((0, 0), (128, 6)):
+        acc[j] = acc[j] + x[i, j * 8]
 """
     fn = bk._capture_from_source(src, "acc2d", {}, "races_big")
     args = harness.make_args(fn, 2)
