@@ -22,6 +22,13 @@ same way.  ``one_plus_one_es`` depends on earlier costs (search.py:226-234,
 (an extension) evaluates λ mutations of the parent per
 generation, sharded over the ranks, and equals (1+1)-ES at λ = 1.
 
+``objective="device"`` (an extension) scores a trial by the device time of
+the launch sequence the engine chose for it (recorded, replayed between CUDA
+events): on the B200 the reference's ``"wall"`` (``stats.wall_time``, the
+whole host-side run()) is dominated by lifting and planning and barely sees
+the tile choice, while the tile sizes select the CTA tile of the
+contraction kernels (runtime.cta_tile), which the device time does see.
+
 Trials run on the B200 engine: the session passes it to every run()
 explicitly (no module-global patching).  With several ranks, an exception in
 a trial is exchanged like a record and re-raised on every rank (the lowest
@@ -191,8 +198,11 @@ def _session_class():
 
         def __init__(self, module, engine, func=None, seed=0, objective="model",
                      pipeline_template=None, mode="sequential", workers=1):
-            if objective not in ("model", "wall"):
+            if objective not in ("model", "wall", "device"):
                 raise ValueError(f"unknown objective {objective!r}")
+            if objective == "device" and engine is not _b200_engine():
+                raise ValueError("objective 'device' times the B200 engine's kernels; "
+                                 "it needs engine=paper_2307_16080_b200.engine")
             ref.verify_or_raise(module)
             self.engine = engine
             self.module = module
@@ -209,8 +219,41 @@ def _session_class():
                                          engine=engine)
             self.want_results = results
             self.want_args = args
-            self.baseline_cost = self._score(stats)
+            self.baseline_cost = (self._device_ms(module) if objective == "device"
+                                  else self._score(stats))
             self.baseline_stats = stats
+
+        def _device_ms(self, module):
+            """objective="device": the device time (ms) of the launch
+            sequence the engine runs for ``module`` on this session's inputs
+            — recorded once on resident copies, then replayed (1 warm-up,
+            median of DEVICE_REPS) between CUDA events on the launch stream.
+            Unlike the reference's "wall" (stats.wall_time: the whole run()
+            on the host, dominated here by lifting and planning), this
+            separates tile choices that select different kernels / CTA
+            tiles.  Not log-equal to anything in the reference (timing)."""
+            import torch
+
+            from .engine import Session as DeviceSession
+
+            sess = DeviceSession()
+            rec = sess.record(module, self.func, ref._copy_args(self.inputs),
+                              mode=self.mode, workers=self.workers)
+            if not rec.calls:
+                return 0.0
+            stream = torch.cuda.current_stream()
+            rec.replay()
+            times = []
+            for _ in range(DEVICE_REPS):
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                rec.replay()
+                e1.record(stream)
+                e1.synchronize()
+                times.append(e0.elapsed_time(e1))
+            times.sort()
+            return times[len(times) // 2]
 
         def trial(self, idx, tiles, unroll):
             params = {"tiles": [int(t) for t in tiles], "unroll": int(unroll)}
@@ -223,6 +266,7 @@ def _session_class():
                 args = ref._copy_args(self.inputs)
                 results, stats = machine.run(work, self.func, args, mode=self.mode,
                                              workers=self.workers, engine=self.engine)
+                dev_ms = self._device_ms(work) if self.objective == "device" else None
             finally:
                 if work in self.module.ctx.modules:
                     self.module.ctx.modules.remove(work)
@@ -237,10 +281,19 @@ def _session_class():
                 raise StaircaseError(
                     f"pipeline {spec!r} changed the results of @{self.func}; "
                     "transformed kernels must match the untransformed run")
-            return Trial(idx, params, self._score(stats), "evaluated", self.seed,
-                         stats=ref._digest(stats))
+            cost = dev_ms if dev_ms is not None else self._score(stats)
+            return Trial(idx, params, cost, "evaluated", self.seed, stats=ref._digest(stats))
 
     return Session, ref
+
+
+DEVICE_REPS = 5
+
+
+def _b200_engine():
+    from . import engine
+
+    return engine
 
 
 def _params(space, budget, seed, strategy):

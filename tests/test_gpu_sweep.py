@@ -36,3 +36,27 @@ def test_population_es_on_b200_equals_its_definition():
                              strategy="population_es", lam=8, rank=0, world=1)
     assert log == _pop_es_spec(corpus.conv_small.module, 17, 6, 8)
     assert best.cost <= log[0].cost
+
+
+def test_device_objective_sees_the_tile_choice():
+    """objective="device": costs are device milliseconds of each trial's
+    launch sequence; the log's statuses and params equal the model run's
+    (same guard, same skips), and the tile sizes, which select the CTA tile
+    of the exact GEMM, show up as different costs."""
+    import bench_kernels as bk
+    from staircase.tuner import ParamSpace
+
+    from paper_2307_16080_b200 import sweep
+
+    space = ParamSpace(tile_sizes=([1, 8, 32], [1, 8, 32]), unroll_factors=[1])
+    kw = dict(budget=10, seed=0, strategy="grid", rank=0, world=1)
+    _, log_m = sweep.search(bk.mm_par1024.module, None, space, **kw)
+    best, log_d = sweep.search(bk.mm_par1024.module, None, space, objective="device", **kw)
+    assert [(t.idx, t.params, t.status) for t in log_d] == \
+        [(t.idx, t.params, t.status) for t in log_m]
+    costs = [t.cost for t in log_d if t.status == "evaluated"]
+    assert all(0 < c < 1e3 for c in costs)
+    # 2 * 1024^3 flops at >= 5 TFLOP/s: well under a millisecond each
+    assert min(costs) < 0.5
+    assert best.cost == min(costs)
+    assert len({round(c, 2) for c in costs}) > 1
