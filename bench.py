@@ -52,6 +52,8 @@ import subprocess
 import sys
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -486,6 +488,10 @@ def measure(wl, prec, rank, world, local, steps, warmup, min_seconds, with_cpu=T
     plan = list(sess.plan)
     rows = sess.last_shard.rows if sharded else None
     torch.cuda.synchronize()
+    # the recorded run applied the nest once: check sampled outputs against
+    # the host recomputation before the replays accumulate further
+    acc_rec = (accuracy(wl, prec, dev_args, sess.tensor(dev_args[-1]))
+               if rank == 0 and not sharded else None)
     stream = torch.cuda.current_stream()
     for _ in range(warmup):
         rec.replay(lib)
@@ -567,6 +573,8 @@ def measure(wl, prec, rank, world, local, steps, warmup, min_seconds, with_cpu=T
     if rank == 0:
         rec_out["roofline"] = roofline(wl, prec, fam, ms, sus_ms, rate_flops)
         rec_out["step_kernels_ms"] = {k: round(v, 4) for k, v in sorted(fam.items())}
+        if acc_rec is not None:
+            rec_out["accuracy"] = acc_rec
         if e2e is not None:
             rec_out["e2e"] = e2e
         if gather is not None:
@@ -576,6 +584,79 @@ def measure(wl, prec, rank, world, local, steps, warmup, min_seconds, with_cpu=T
                 "value": None, "unit": "GFLOP/s", "cores": None, "kind": "reference",
                 "sample": "timed in the N=1 run only"}
     return rec_out
+
+
+def _round_bf16(x):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(
+        torch.bfloat16).float().numpy()
+
+
+def _round_tf32(x):
+    """Round to nearest even at 10 mantissa bits (b200_pack_operand kind 1)."""
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.int32).astype(np.int64)
+    u = (u + 0xFFF + ((u >> 13) & 1)) & ~0x1FFF
+    return u.astype(np.uint32).view(np.float32).reshape(np.shape(x))
+
+
+def accuracy(wl, prec, host, out_dev, samples=64):
+    """Sampled accuracy of one application of the nest (mm and conv).
+
+    ``host``: the untouched host inputs; ``out_dev``: the device output after
+    one run.  exact: the reference's chain (one f32 multiply and one f32 add
+    per MAC, reduction in nest order) recomputed with numpy float32 ops —
+    counts bit-identical samples.  bf16 / tf32: float64 sums of the rounded
+    operands; max_norm_err = max |got - want| / (2^-24 sqrt(K) sum|ab|), the
+    tests' bound is 8 (tests/tcbound.py).  f32x3: the same normalised error
+    against unrounded operands."""
+    if wl.name not in ("mm", "conv"):
+        return None
+    f32 = np.float32
+    arr = [np.frombuffer(b.data, dtype=f32).reshape(b.shape) for b in host]
+    rng = np.random.default_rng(12345)
+    out = out_dev.view(-1)
+    if wl.name == "mm":
+        A, B, C0 = arr
+        M, K = A.shape
+        N = B.shape[1]
+        ii, jj = rng.integers(0, M, samples), rng.integers(0, N, samples)
+        a, b, c0 = A[ii, :], B[:, jj].T, C0[ii, jj]
+        flat = ii * N + jj
+    else:
+        X, W, O0 = arr
+        nb, fo, ho, wo = O0.shape
+        _, C, KH, KW = W.shape
+        n_, f_, h_, w_ = (rng.integers(0, e, samples) for e in (nb, fo, ho, wo))
+        # operands in the reference's reduction order (ci, ki, kj)
+        a = np.stack([X[n_[s], :, h_[s]:h_[s] + KH, w_[s]:w_[s] + KW].reshape(-1)
+                      for s in range(samples)])
+        b = np.stack([W[f_[s]].reshape(-1) for s in range(samples)])
+        c0 = O0[n_, f_, h_, w_]
+        flat = ((n_ * fo + f_) * ho + h_) * wo + w_
+        K = C * KH * KW
+    import torch
+
+    got = out[torch.from_numpy(flat).to(out.device)].cpu().numpy().astype(np.float64)
+    if prec == "exact":
+        acc = c0.astype(f32).copy()
+        for k in range(a.shape[1]):
+            acc = (acc + (a[:, k] * b[:, k]).astype(f32)).astype(f32)
+        same = int((acc.astype(np.float64) == got).sum())
+        return {"samples": samples, "bit_identical": same,
+                "check": "reference f32 chain (mul, add per MAC in nest order) on sampled "
+                         "outputs of one run"}
+    rnd = {"bf16": _round_bf16, "tf32": _round_tf32}.get(prec, lambda x: x)
+    ra, rb = rnd(a).astype(np.float64), rnd(b).astype(np.float64)
+    prod = ra * rb
+    want = c0.astype(np.float64) + prod.sum(axis=1)
+    mag = np.abs(prod).sum(axis=1)
+    norm = np.abs(got - want) / (2.0 ** -24 * math.sqrt(K) * mag + 1e-300)
+    return {"samples": samples, "K": K, "max_norm_err": float(norm.max()),
+            "bound": 8.0,
+            "check": ("|got - want| / (2^-24 sqrt(K) sum|ab|) on sampled outputs of one run; "
+                      "want = float64 sum of the " +
+                      ("unrounded" if prec == "f32x3" else prec + "-rounded") + " operands")}
 
 
 def _e2e(wl, rank, world, sharded, min_seconds):
@@ -695,6 +776,7 @@ def roofline(wl, prec, fam, ms, sus_ms, rank_flops):
 
 SWEEP_T = [1, 2, 4, 8, 16, 32, 64, 128]
 SWEEP_U = [1, 2, 4, 8]
+SWEEP_WEIGHTS = (1, 1)
 
 
 def measure_sweep(rank, world, prec="exact", with_cpu=True):
@@ -703,10 +785,14 @@ def measure_sweep(rank, world, prec="exact", with_cpu=True):
     512 configurations = tiles T x T (T in 1..128) x unroll U (1, 2, 4, 8) on
     two targets — the matmul nest (parallel form, 1024^3) and the paper's
     conv (1,1,1280,1280)*(1,3,3) — each enumerated exhaustively after the
-    identity trial (strategy "grid").  Trials are sharded idx % world; one
-    all_gather_object of the trial records at the end.  value = trials /
-    (setup + trials) wall time, max over ranks — every rank's setup (inputs,
-    identity baseline) included, so the scaling it reports is end to end.
+    identity trial (strategy "grid").  sweep.search_many splits the ranks
+    into one group per target (equal: the targets' trials take the same host
+    time);
+    inside a group trials are sharded idx % group size; all_gather_object of
+    the trial records per group, then of the per-target results.  value =
+    trials / wall time, max over ranks — every rank's setup (inputs, identity
+    baseline) and the gathers included, so the scaling it reports is end to
+    end.  A 2-trial warm-up search runs first (engine paths, CUDA context).
     """
     import torch
 
@@ -719,22 +805,27 @@ def measure_sweep(rank, world, prec="exact", with_cpu=True):
     targets = [(bk.mm_par1024, 2.0 * 1024 ** 3), (bk.conv_paper, 2.0 * 1280 * 1280 * 9)]
     b2.configure(precision=prec)
     t0_totals = dict(b2rt.TOTALS)
-    total_trials, trial_s, setup_s, flops = 0, 0.0, 0.0, 0.0
-    wall = 0.0
-    logs = []
-    for fn, f in targets:
-        timing = {}
-        barrier(world)
-        t0 = time.perf_counter()
-        best, log = sweep.search(fn.module, None, space, budget=1 + len(SWEEP_T) ** 2 *
-                                 len(SWEEP_U), seed=0, strategy="grid", timing=timing)
-        torch.cuda.synchronize()
-        wall += max_over_ranks(time.perf_counter() - t0, world)
-        trial_s += max_over_ranks(timing["trials_s"], world)
-        setup_s += max_over_ranks(timing["setup_s"], world)
-        total_trials += len(log)
-        flops += f * len(log)
-        logs.append((fn.__name__, best, log))
+    budget = 1 + len(SWEEP_T) ** 2 * len(SWEEP_U)
+    for fn, _ in targets:   # warm-up (not timed)
+        sweep.search(fn.module, None, space, budget=2, seed=1, strategy="grid", rank=0,
+                     world=1)
+    torch.cuda.synchronize()
+    timing = {}
+    barrier(world)
+    t0 = time.perf_counter()
+    # one rank group per target (sweep.search_many): a rank builds one
+    # target's inputs and baseline; equal groups — the two targets' trials
+    # took the same host time at N=1 (0.69 / 0.70 s, profiles/r02_sweep_*)
+    res = sweep.search_many([fn.module for fn, _ in targets], None, space, budget=budget,
+                            seed=0, strategy="grid", weights=SWEEP_WEIGHTS, timing=timing)
+    torch.cuda.synchronize()
+    wall = max_over_ranks(time.perf_counter() - t0, world)
+    trial_s = max_over_ranks(timing.get("trials_s", 0.0), world)
+    setup_s = max_over_ranks(timing.get("setup_s", 0.0), world)
+    total_trials = sum(len(log) for _, log in res)
+    flops = sum(f * len(log) for (_, f), (_, log) in zip(targets, res))
+    logs = [(fn.__name__, best, log) for (fn, _), (best, log) in zip(targets, res)]
+    groups = sweep.rank_groups(SWEEP_WEIGHTS, world)
     b2.configure(precision="exact")
     moved = {k: b2rt.TOTALS[k] - t0_totals[k] for k in t0_totals}
     if rank != 0:
@@ -748,17 +839,24 @@ def measure_sweep(rank, world, prec="exact", with_cpu=True):
                                "matmul 1024^3 (parallel form) and conv (1,1,1280,1280)*(1,3,3)",
                    "baseline_config": "configs[4]",
                    "strategy": "grid (identity first)", "trials": total_trials,
-                   "parallelism": f"trial shard idx % {world}",
+                   "parallelism": (f"target groups {groups} (ranks per target), trials "
+                                   f"idx % group size inside a group"),
                    "best": {n: {"idx": b.idx, "params": b.params, "cost": b.cost}
                             for n, b, _ in logs}},
         "phases_s_max_rank": {"setup": setup_s, "trials": trial_s, "wall": wall},
+        "rank0_per_target_s": {targets[k][0].__name__: {key: round(v, 4) for key, v in t.items()
+                                                        if isinstance(v, float)}
+                               for k, t in timing.get("per_kernel", {}).items()},
         "trials_only_configs_per_s": total_trials / trial_s,
         "gflops_evaluated_per_s": flops / wall / 1e9,
         "e2e": {"value": total_trials / wall, "unit": "configs/s",
                 "h2d_bytes_per_step": moved["h2d_bytes"],
                 "d2h_bytes_per_step": moved["d2h_bytes"],
-                "how": "every trial's inputs are host Buffers staged to the device and its "
-                       "results written back; value already is end to end"},
+                "how": "each rank draws the seeded inputs on the host (make_inputs), runs the "
+                       "baseline through machine.run on host Buffers and uploads the inputs "
+                       "once; every trial then runs on device clones of them and is checked on "
+                       "the device; setup (inputs + baseline + upload) and the final all-gather "
+                       "are inside value, so value already is end to end"},
         "gpu_launches": moved["launches"],
     }
     if with_cpu:

@@ -247,6 +247,18 @@ int b200_conv2d_exact(int32_t dtype, const void *in, const int64_t *in_strides, 
                       double init_value, void *stream);
 
 /*
+ * The tuner's seeded inputs (replaces the per-element
+ * [rng.uniform(-2.0, 2.0) for _ in range(size)] of _fresh_argument,
+ * reference pkg/src/staircase/tuner/search.py:78-90).  HOST code: `state` is
+ * the 624-word MT19937 state of a Python random.Random (getstate()[1][:624]),
+ * `*pos` its index (getstate()[1][624]); writes n values lo + (hi - lo) *
+ * random() as f32 (round to nearest) or f64 into host memory `out` and
+ * advances state / pos exactly as n Python draws would.
+ */
+int b200_mt_uniform(uint32_t *state, int32_t *pos, int64_t n, double lo, double hi, void *out,
+                    int32_t dtype);
+
+/*
  * Runtime specialisation (NVRTC, sm_100a): compile generated CUDA C `src`
  * and return the kernel `kernel` as an opaque handle in *fn.  The engine
  * generates straight-line kernels for region shapes whose generic execution

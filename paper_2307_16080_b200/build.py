@@ -18,7 +18,8 @@ OUT = os.path.join(PKG, "libb200k.so")
 BUILD = os.path.join(PKG, "_build")
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
-              "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
+              "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
+              "-Xptxas", "-v",
               "--expt-relaxed-constexpr"]
 
 

@@ -48,6 +48,7 @@ _I64 = ctypes.c_int64
 _F32 = ctypes.c_float
 
 SIGNATURES = {
+    "b200_mt_uniform": [_P, _P, _I64, ctypes.c_double, ctypes.c_double, _P, _I32],
     "b200_vm_run": [_P, _I32, _P, _P, _I32, _I32, _P, _I32, _I32, _P, _P, _P, _P,
                     _I32, _P, _P, _P],
     "b200_gemm_f32_exact": [_P, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64, _I64,
@@ -194,6 +195,12 @@ class Staging:
 
     def host(self, buf):
         return self.torch.frombuffer(buf.data, dtype=getattr(self.torch, _TORCH_DT[buf.dtype]))
+
+    def adopt(self, buf, tensor):
+        """Use ``tensor`` (same dtype and element count) as the device copy of
+        ``buf``: nothing is uploaded (sweep trials start from device clones
+        of resident inputs)."""
+        self.dev[id(buf)] = (buf, tensor)
 
     def staged(self, buf):
         ent = self.dev.get(id(buf))

@@ -83,7 +83,7 @@ def _isfinite(a):
     return torch.isfinite(a) if isinstance(a, torch.Tensor) else np.isfinite(a)
 
 
-def _fast_buffers_close(got, want):
+def _fast_buffers_close(got, want, dev_of=None):
     """Vectorised twin of the reference guard's element test
     (math.isclose(g, w, rel_tol=1e-6, abs_tol=1e-9) over every element,
     tuner/search.py:128-138): the same predicate, evaluated on the GPU on
@@ -95,7 +95,7 @@ def _fast_buffers_close(got, want):
         return False
     from . import engine
 
-    tg = engine.device_copy(got)
+    tg = (dev_of or engine.device_copy)(got)
     if tg is not None:
         import torch
 
@@ -145,17 +145,69 @@ def make_inputs(module, func, seed):
         ty = arg.type
         if ty.kind == "memref" and ty.element.is_float:
             size = math.prod(ty.shape)
-            st = rng.getstate()
-            rs = np.random.RandomState()
-            rs.set_state(("MT19937", np.array(st[1][:-1], dtype=np.uint32), st[1][-1]))
-            vals = -2.0 + (2.0 - -2.0) * rs.random_sample(size)
-            s2 = rs.get_state()
-            rng.setstate((3, tuple(int(v) for v in s2[1]) + (int(s2[2]),), None))
             dt = np.float32 if ty.element.kind == "f32" else np.float64
-            out.append(Buffer(ty.shape, ty.element.kind, vals.astype(dt).tobytes()))
+            out.append(_buffer_from(ty.shape, ty.element.kind, _uniform(rng, size, dt)))
         else:
             out.append(ref._fresh_argument(ty, rng))
     return out
+
+
+def _uniform(rng, size, dt):
+    """[rng.uniform(-2.0, 2.0) for _ in range(size)] as a numpy array of dt,
+    leaving ``rng`` where that loop would: the native generator
+    (b200_mt_uniform, host code) when the library loads, else a numpy
+    RandomState seeded with the same Mersenne Twister state (random_sample()
+    is the same 53-bit draw as random.random())."""
+    st = rng.getstate()
+    words = np.array(st[1][:-1], dtype=np.uint32)
+    out = np.empty(size, dtype=dt)
+    lib = _native()
+    if lib is not None:
+        import ctypes
+
+        pos = ctypes.c_int32(st[1][-1])
+        rc = lib.b200_mt_uniform(words.ctypes.data, ctypes.byref(pos), size, -2.0, 2.0,
+                                 out.ctypes.data, 0 if dt == np.float32 else 1)
+        if rc != 0:
+            raise RuntimeError(f"b200_mt_uniform failed ({rc})")
+        rng.setstate((3, tuple(words.tolist()) + (pos.value,), None))
+        return out
+    rs = np.random.RandomState()
+    rs.set_state(("MT19937", words, st[1][-1]))
+    vals = rs.random_sample(size)
+    vals *= 2.0 - -2.0      # same rounding as -2 + (2 - -2) * random()
+    vals += -2.0
+    s2 = rs.get_state()
+    rng.setstate((3, tuple(s2[1].tolist()) + (int(s2[2]),), None))
+    out[...] = vals
+    return out
+
+
+def _native():
+    try:
+        from .runtime import load_library
+
+        return load_library()
+    except Exception:   # no library built: the numpy path draws the same values
+        return None
+
+
+def _buffer_from(shape, dtype, values):
+    """A staircase Buffer holding ``values`` (a numpy array of the Buffer's
+    element type), filled with one copy (Buffer(shape, dtype, bytes) makes
+    three)."""
+    from array import array
+
+    from staircase.interp import Buffer
+    from staircase.interp.buffer import _TYPECODES, row_major_strides
+
+    b = Buffer.__new__(Buffer)
+    b.shape = tuple(int(x) for x in shape)
+    b.strides = row_major_strides(b.shape)
+    b.dtype = dtype
+    b.data = array(_TYPECODES[dtype])
+    b.data.frombytes(memoryview(np.ascontiguousarray(values)).cast("B"))
+    return b
 
 
 def _session_class():
@@ -177,19 +229,19 @@ def _session_class():
     from staircase.passes import run_pipeline
     from staircase.tuner.space import Trial
 
-    def _state_matches(got_results, got_args, want_results, want_args):
+    def _state_matches(got_results, got_args, want_results, want_args, dev_of=None):
         from staircase.interp import Buffer
 
         if len(got_results) != len(want_results):
             return False
         for g, w in zip(got_results, want_results):
             if isinstance(w, Buffer):
-                if not _fast_buffers_close(g, w):
+                if not _fast_buffers_close(g, w, dev_of):
                     return False
             elif not ref._values_close(g, w):
                 return False
         for g, w in zip(got_args, want_args):
-            if isinstance(w, Buffer) and not _fast_buffers_close(g, w):
+            if isinstance(w, Buffer) and not _fast_buffers_close(g, w, dev_of):
                 return False
         return True
 
@@ -219,9 +271,43 @@ def _session_class():
                                          engine=engine)
             self.want_results = results
             self.want_args = args
+            # resident trial inputs (B200 engine): every trial starts from
+            # device clones of one upload instead of host copies + uploads
+            self._masters = None
+            if engine is _b200_engine() and RESIDENT:
+                import torch
+
+                from staircase.interp import Buffer
+
+                self._masters = [
+                    torch.frombuffer(bytearray(a.data), dtype=getattr(torch, _TORCH_DT[a.dtype]))
+                    .to("cuda") if isinstance(a, Buffer) else None for a in self.inputs]
             self.baseline_cost = (self._device_ms(module) if objective == "device"
                                   else self._score(stats))
             self.baseline_stats = stats
+
+        def _resident_args(self):
+            """(device Session, trial arguments) for a resident trial: Buffer
+            shells share the input arrays (read only: a Session never writes
+            back) and their device copies are clones of the resident inputs —
+            the trial sees exactly the reference's fresh copies
+            (search.py:105-106), without a host copy or an upload."""
+            from staircase.interp import Buffer
+
+            from .engine import Session as DeviceSession
+
+            sess = DeviceSession()
+            args = []
+            for a, m in zip(self.inputs, self._masters):
+                if isinstance(a, Buffer):
+                    shell = Buffer.__new__(Buffer)
+                    shell.shape, shell.strides, shell.dtype = a.shape, a.strides, a.dtype
+                    shell.data = a.data
+                    sess.be.stage.adopt(shell, m.clone())
+                    args.append(shell)
+                else:
+                    args.append(a)
+            return sess, args
 
         def _device_ms(self, module):
             """objective="device": the device time (ms) of the launch
@@ -236,9 +322,11 @@ def _session_class():
 
             from .engine import Session as DeviceSession
 
-            sess = DeviceSession()
-            rec = sess.record(module, self.func, ref._copy_args(self.inputs),
-                              mode=self.mode, workers=self.workers)
+            if self._masters is not None:
+                sess, args = self._resident_args()
+            else:
+                sess, args = DeviceSession(), ref._copy_args(self.inputs)
+            rec = sess.record(module, self.func, args, mode=self.mode, workers=self.workers)
             if not rec.calls:
                 return 0.0
             stream = torch.cuda.current_stream()
@@ -262,16 +350,27 @@ def _session_class():
                 work, _ = run_pipeline(self.module, spec)
             except (PassFailure, VerificationFailed):
                 return Trial(idx, params, None, "skipped", self.seed)
+            dev_of = None
             try:
-                args = ref._copy_args(self.inputs)
-                results, stats = machine.run(work, self.func, args, mode=self.mode,
-                                             workers=self.workers, engine=self.engine)
+                if self._masters is not None:
+                    sess, args = self._resident_args()
+                    results, stats = sess.run(work, self.func, args, mode=self.mode,
+                                              workers=self.workers)
+                    stage = sess.be.stage
+
+                    def dev_of(buf):
+                        ent = stage.dev.get(id(buf))
+                        return ent[1] if ent is not None and ent[0] is buf else None
+                else:
+                    args = ref._copy_args(self.inputs)
+                    results, stats = machine.run(work, self.func, args, mode=self.mode,
+                                                 workers=self.workers, engine=self.engine)
                 dev_ms = self._device_ms(work) if self.objective == "device" else None
             finally:
                 if work in self.module.ctx.modules:
                     self.module.ctx.modules.remove(work)
             try:
-                ok = _state_matches(results, args, self.want_results, self.want_args)
+                ok = _state_matches(results, args, self.want_results, self.want_args, dev_of)
             finally:
                 # the guard was the last user of the trial's device copies
                 release = getattr(self.engine, "release_last_staging", None)
@@ -288,6 +387,10 @@ def _session_class():
 
 
 DEVICE_REPS = 5
+# resident trial inputs on the B200 engine (B200_SWEEP_RESIDENT=0: every trial
+# copies its inputs on the host and uploads them, as the reference copies)
+RESIDENT = __import__("os").environ.get("B200_SWEEP_RESIDENT", "1") != "0"
+_TORCH_DT = {"f32": "float32", "f64": "float64", "i32": "int32", "i64": "int64"}
 
 
 def _b200_engine():
@@ -314,7 +417,7 @@ def _params(space, budget, seed, strategy):
 
 def search(kernel, pipeline_template=None, space=None, budget: int = 20, seed: int = 0,
            strategy: str = "random", *, func=None, objective="model", mode="sequential",
-           workers=1, engine=None, rank=None, world=None, timing=None, lam=8):
+           workers=1, engine=None, rank=None, world=None, timing=None, lam=8, group=None):
     """``tuner.search`` with trials sharded over torch.distributed ranks.
 
     Returns ``(best, log)`` exactly like the reference; ``log`` is sorted by
@@ -323,6 +426,8 @@ def search(kernel, pipeline_template=None, space=None, budget: int = 20, seed: i
     generation (see ``_pop_es``).  ``timing`` (a dict), if given,
     receives this rank's ``setup_s`` (inputs + baseline run), ``trials_s``
     (its share of the trials), ``gather_s`` and ``trials`` (count).
+    ``group``: a torch.distributed process group to shard over (with
+    ``rank`` / ``world`` its own rank and size; search_many uses it).
     """
     import time
 
@@ -366,7 +471,7 @@ def search(kernel, pipeline_template=None, space=None, budget: int = 20, seed: i
         return best, log
     if strategy == "population_es":
         t_trials = time.perf_counter()
-        best, log = _pop_es(session, space, budget, seed, lam, rank, world, dist)
+        best, log = _pop_es(session, space, budget, seed, lam, rank, world, dist, group)
         if timing is not None:
             timing.update(setup_s=t_trials - t_start,
                           trials_s=time.perf_counter() - t_trials, gather_s=0.0,
@@ -386,7 +491,7 @@ def search(kernel, pipeline_template=None, space=None, budget: int = 20, seed: i
         if rec[3] == _FAILED:
             break   # later trials of this rank cannot matter: idx order decides
     t_gather = time.perf_counter()
-    records = _raise_first(sorted(_gather(dist, world, mine), key=lambda r: r[0]))
+    records = _raise_first(sorted(_gather(dist, world, mine, group), key=lambda r: r[0]))
     if timing is not None:
         timing.update(setup_s=t_trials - t_start, trials_s=t_gather - t_trials,
                       gather_s=time.perf_counter() - t_gather, trials=len(mine))
@@ -394,6 +499,83 @@ def search(kernel, pipeline_template=None, space=None, budget: int = 20, seed: i
     evaluated = [t for t in log if t.status == "evaluated"]
     best = min(evaluated, key=lambda t: (t.cost, t.idx))
     return best, log
+
+
+def rank_groups(weights, world):
+    """Ranks for each of several sweeps (search_many): contiguous groups,
+    sizes proportional to ``weights`` (largest remainders), at least one
+    rank each.  With fewer ranks than sweeps, sweep k runs alone on rank
+    k % world."""
+    n = len(weights)
+    if world < n:
+        return [[k % world] for k in range(n)]
+    total = float(sum(weights)) or 1.0
+    raw = [world * w / total for w in weights]
+    size = [max(1, int(r)) for r in raw]
+    while sum(size) > world:   # the max(1, .) floors overshot: take from the largest
+        size[max(range(n), key=lambda k: (size[k], -k))] -= 1
+    order = sorted(range(n), key=lambda k: (-(raw[k] - int(raw[k])), k))
+    i = 0
+    while sum(size) < world:
+        size[order[i % n]] += 1
+        i += 1
+    out, r0 = [], 0
+    for k in range(n):
+        out.append(list(range(r0, r0 + size[k])))
+        r0 += size[k]
+    return out
+
+
+def search_many(kernels, pipeline_template=None, space=None, budget: int = 20, seed: int = 0,
+                strategy: str = "random", *, weights=None, rank=None, world=None, timing=None,
+                **kw):
+    """Several sweeps at once (the paper's design space over more than one
+    kernel), partitioned across the ranks: each kernel gets its own group of
+    ranks (rank_groups, sizes proportional to ``weights``, default equal)
+    whose members shard that kernel's trials ``idx % group size`` — so a
+    rank builds one kernel's inputs and baseline instead of every kernel's
+    (the per-kernel setup is replicated only inside a group).  Returns
+    ``[(best, log), ...]`` in kernel order, identical on every rank and equal
+    to ``search`` of each kernel alone.  ``timing`` receives this rank's
+    kernel index and its search() phases."""
+    import time
+
+    dist = _dist()
+    if rank is None:
+        rank = dist.get_rank() if dist else 0
+    if world is None:
+        world = dist.get_world_size() if dist else 1
+    n = len(kernels)
+    groups = rank_groups(weights or [1] * n, world)
+    pgs = [None] * n
+    if dist is not None and world > 1:
+        made = {}
+        for k, g in enumerate(groups):   # every rank creates every group, same order
+            key = tuple(g)
+            if key not in made:
+                made[key] = dist.new_group(list(g)) if len(g) > 1 else None
+            pgs[k] = made[key]
+    mine = {}
+    for k, g in enumerate(groups):
+        if rank not in g:
+            continue
+        t = {} if timing is not None else None
+        t0 = time.perf_counter()
+        mine[k] = search(kernels[k], pipeline_template, space, budget, seed, strategy,
+                         rank=g.index(rank), world=len(g), group=pgs[k], timing=t, **kw)
+        if timing is not None:
+            timing.setdefault("kernels", []).append(k)
+            for key, v in (t or {}).items():
+                timing[key] = timing.get(key, 0) + v
+            timing["wall_s"] = timing.get("wall_s", 0.0) + time.perf_counter() - t0
+            timing.setdefault("per_kernel", {})[k] = dict(t or {}, wall_s=time.perf_counter() - t0)
+    # every rank learns every kernel's result from the group leaders
+    leaders = {k: v for k, v in mine.items() if groups[k][0] == rank}
+    parts = _gather(dist, world, [leaders]) if dist is not None and world > 1 else [leaders]
+    out = {}
+    for part in parts:
+        out.update(part)
+    return [out[k] for k in range(n)]
 
 
 _FAILED = "__failed__"
@@ -421,15 +603,15 @@ def _raise_first(records):
     return records
 
 
-def _gather(dist, world, mine):
+def _gather(dist, world, mine, group=None):
     if dist is not None and world > 1:
         gathered = [None] * world
-        dist.all_gather_object(gathered, mine)
+        dist.all_gather_object(gathered, mine, group=group)
         return [r for part in gathered for r in part]
     return list(mine)
 
 
-def _pop_es(session, space, budget, seed, lam, rank, world, dist):
+def _pop_es(session, space, budget, seed, lam, rank, world, dist, group=None):
     """(1+λ)-ES (an extension of search.py:226-234,261-279).
 
     Each generation draws λ children of the current parent with the
@@ -446,7 +628,7 @@ def _pop_es(session, space, budget, seed, lam, rank, world, dist):
     identity = space.identity()
     records = _raise_first(_gather(dist, world, [
         _guarded(session, 0, identity["tiles"], identity["unroll"], world)]
-        if rank == 0 else []))
+        if rank == 0 else [], group))
     log = [Trial(i, p, c, s, sd, stats=st) for i, p, c, s, sd, st in records]
     rng = random.Random(seed)
     parent, parent_cost = dict(log[0].params), log[0].cost
@@ -455,7 +637,7 @@ def _pop_es(session, space, budget, seed, lam, rank, world, dist):
         kids = [(idx + j, _mutate(space, parent, rng)) for j in range(min(lam, budget - idx))]
         mine = [_guarded(session, i, tiles, unroll, world)
                 for i, (tiles, unroll) in kids if i % world == rank]
-        gen = _raise_first(sorted(_gather(dist, world, mine), key=lambda r: r[0]))
+        gen = _raise_first(sorted(_gather(dist, world, mine, group), key=lambda r: r[0]))
         gen = [Trial(i, p, c, s, sd, stats=st) for i, p, c, s, sd, st in gen]
         log.extend(gen)
         evaluated = [t for t in gen if t.status == "evaluated"]

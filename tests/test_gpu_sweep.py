@@ -60,3 +60,21 @@ def test_device_objective_sees_the_tile_choice():
     assert min(costs) < 0.5
     assert best.cost == min(costs)
     assert len({round(c, 2) for c in costs}) > 1
+
+
+@pytest.mark.parametrize("fn", [corpus.conv_rows, corpus.matmul_par, corpus.linear32])
+def test_resident_trials_equal_host_copied_trials(fn, monkeypatch):
+    """Trials that start from device clones of the resident inputs produce the
+    log of trials that copy and upload their inputs (the reference's
+    _copy_args), including the baseline and the guard's verdicts."""
+    from staircase.tuner import ParamSpace
+
+    from paper_2307_16080_b200 import sweep
+
+    space = ParamSpace(tile_sizes=([1, 2, 4, 8],) * 2, unroll_factors=[1, 2])
+    kw = dict(budget=12, seed=3, strategy="grid", rank=0, world=1)
+    monkeypatch.setattr(sweep, "RESIDENT", False)
+    _, host_log = sweep.search(fn.module, None, space, **kw)
+    monkeypatch.setattr(sweep, "RESIDENT", True)
+    _, dev_log = sweep.search(fn.module, None, space, **kw)
+    assert dev_log == host_log

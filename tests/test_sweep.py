@@ -295,3 +295,127 @@ def test_fast_make_inputs_is_the_reference_stream(fn, seed):
             assert g.data.tobytes() == w.data.tobytes()
         else:
             assert type(g) is type(w) and g == w
+
+
+def test_device_objective_needs_the_b200_engine():
+    """objective="device" times the B200 engine's recorded kernels; any other
+    engine is refused up front (like the reference's unknown-objective check)."""
+    from vm_sim import SimEngine
+
+    from paper_2307_16080_b200 import sweep
+
+    with pytest.raises(ValueError, match="device"):
+        sweep.search(corpus.conv_small.module, None, _space(), budget=2, seed=0,
+                     objective="device", engine=SimEngine(), rank=0, world=1)
+    with pytest.raises(ValueError, match="objective"):
+        sweep.search(corpus.conv_small.module, None, _space(), budget=2, seed=0,
+                     objective="cycles", engine=SimEngine(), rank=0, world=1)
+
+
+def test_rank_groups():
+    from paper_2307_16080_b200.sweep import rank_groups
+
+    assert rank_groups([1, 1], 1) == [[0], [0]]
+    assert rank_groups([1, 1], 2) == [[0], [1]]
+    assert rank_groups([1, 1], 3) == [[0, 1], [2]]
+    assert rank_groups([1, 1], 8) == [[0, 1, 2, 3], [4, 5, 6, 7]]
+    assert rank_groups([5, 3], 8) == [[0, 1, 2, 3, 4], [5, 6, 7]]
+    assert rank_groups([1, 100], 4) == [[0], [1, 2, 3]]
+    assert rank_groups([1, 1, 1], 2) == [[0], [1], [0]]
+    for w in range(1, 12):
+        for wts in ([1, 1], [3, 1], [1, 2, 3]):
+            g = rank_groups(wts, w)
+            assert all(g) and all(0 <= r < w for grp in g for r in grp)
+            if w >= len(wts):
+                assert sorted(r for grp in g for r in grp) == list(range(w))
+
+
+def _many_worker(rank, world, port, out_dir):
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path[:0] = [here, os.path.dirname(here)]
+    import conftest  # noqa: F401  (path + staircase shim)
+    import torch.distributed as dist
+
+    import corpus as c
+    import oracle as o
+    from paper_2307_16080_b200 import sweep
+    from staircase.tuner import ParamSpace
+    from staircase.tuner.log import persist
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        res = sweep.search_many([c.conv_small.module, c.conv_rows.module], None,
+                                ParamSpace(**SPACE_ARGS), budget=10, seed=4, strategy="grid",
+                                engine=o)
+        for k, (best, log) in enumerate(res):
+            persist(log, os.path.join(out_dir, f"log{rank}_{k}.jsonl"))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_search_many_gloo_equals_single_searches(world):
+    """Two kernels swept at once over 2 and 3 gloo ranks (one group per
+    kernel; at 3 the first group shards its trials over two ranks): every
+    rank returns each kernel's log exactly as a world-1 search of it."""
+    import torch.multiprocessing as mp
+    from staircase.tuner import ParamSpace
+    from staircase.tuner.log import load
+
+    from paper_2307_16080_b200 import sweep
+
+    oracle.build()
+    want = [sweep.search(m, None, ParamSpace(**SPACE_ARGS), budget=10, seed=4,
+                         strategy="grid", engine=oracle, rank=0, world=1)[1]
+            for m in (corpus.conv_small.module, corpus.conv_rows.module)]
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_many_worker, args=(world, _free_port(), d), nprocs=world, join=True)
+        for rank in range(world):
+            for k in range(2):
+                assert load(os.path.join(d, f"log{rank}_{k}.jsonl")) == want[k]
+
+
+@pytest.mark.parametrize("native", [True, False])
+def test_uniform_stream_is_pythons(native, monkeypatch):
+    """make_inputs' float draws (native b200_mt_uniform, or the numpy
+    fallback) equal [rng.uniform(-2, 2) ...] bit for bit across many twists,
+    from odd start positions, and leave the generator in the same state."""
+    import random
+
+    import numpy as np
+
+    from paper_2307_16080_b200 import sweep
+
+    if not native:
+        monkeypatch.setattr(sweep, "_native", lambda: None)
+    r1, r2 = random.Random(7), random.Random(7)
+    for n in (1, 311, 624, 1249, 20011):
+        r1.random()
+        r2.random()
+        for dt in (np.float64, np.float32):
+            got = sweep._uniform(r1, n, dt)
+            want = np.array([r2.uniform(-2.0, 2.0) for _ in range(n)]).astype(dt)
+            assert got.tobytes() == want.tobytes()
+            assert r1.getstate() == r2.getstate()
+
+
+def test_make_inputs_equals_reference():
+    import importlib
+
+    from paper_2307_16080_b200 import sweep
+
+    ref = importlib.import_module("staircase.tuner.search")
+    for fn in (corpus.conv_small, corpus.matmul_par, corpus.int_ops, corpus.scalar_args,
+               corpus.linear32):
+        for seed in (0, 9):
+            got, want = sweep.make_inputs(fn.module, None, seed), ref.make_inputs(
+                fn.module, None, seed)
+            for g, w in zip(got, want):
+                if hasattr(w, "data"):
+                    assert (g.shape, g.strides, g.dtype) == (w.shape, w.strides, w.dtype)
+                    assert g.data.tobytes() == w.data.tobytes()
+                else:
+                    assert g == w
