@@ -727,14 +727,22 @@ def roofline(wl, prec, fam, ms, sus_ms, rank_flops):
         achieved = rank_flops / (dom_ms * 1e-3) / 1e12
         tf = tf32_peak() if prec in ("tf32", "f32x3") else None
         if tf is not None:
-            # tf32 rate measured in this run (cuBLAS tf32 8192^3, burst)
+            # tf32 ceiling: the larger of cuBLAS tf32 measured in this run
+            # (8192^3, burst) and half the measured bf16 peak (the tensor
+            # cores' tf32 rate is half their bf16 rate) — our own tf32
+            # kernels ran above cuBLAS' tf32 (r02), so cuBLAS alone is no
+            # ceiling
+            half = peaks["bf16_tflops"] * 0.5
+            base = max(tf, half)
             f = {"tf32": 1.0, "f32x3": 1.0 / 3}[prec]
-            peak = tf * f
+            peak = base * f
             sus_peak = peak * peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) / \
                 peaks["bf16_tflops"]
-            peak_source = {"tf32": "measured in this run: cuBLAS tf32 GEMM 8192^3 (burst)",
-                           "f32x3": "measured in this run: cuBLAS tf32 GEMM 8192^3 (burst) / 3 "
-                                    "(each fp32-accurate product is 3 tf32 products)"}[prec]
+            which = (f"cuBLAS tf32 GEMM 8192^3 measured in this run ({tf:.1f})" if tf >= half
+                     else f"{src} bf16 x 0.5 ({half:.1f}; cuBLAS tf32 measured in this run: "
+                          f"{tf:.1f})")
+            peak_source = which + (" / 3 (each fp32-accurate product is 3 tf32 products)"
+                                   if prec == "f32x3" else "")
         else:
             f = {"bf16": 1.0, "tf32": 0.5, "f32x3": 0.5 / 3}[prec]
             peak = peaks["bf16_tflops"] * f
