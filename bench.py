@@ -97,6 +97,8 @@ class Workload:
             # algorithmic DRAM bytes of b200_conv2d_tc: the NHWC bf16 input
             # once, the f32 output read and written (out += conv)
             self.tc_bytes = 256 * 58 * 58 * 64 * 2 + 2 * 256 * 64 * 56 * 56 * 4
+            # the fused kernel reads the f32 NCHW input itself
+            self.tc_fused_bytes = 256 * 58 * 58 * 64 * 4 + 2 * 256 * 64 * 56 * 56 * 4
             self.config = "configs[2]"
         elif name == "ls":
             self.fn = bk.make_linear_stack(65536)
@@ -436,8 +438,9 @@ KERNEL_OF = {"b200_gemm_tc": "gemm", "b200_gemm_f32_exact": "gemm",
              "b200_contract_exact": "contract", "b200_map_f32": "map", "b200_vm_run": "vm",
              "b200_pack_operand": "pack", "b200_conv2d_tc": "conv",
              "b200_pack_conv_input": "pack", "b200_pack_conv": "pack",
-             "b200_conv2d_exact": "conv", "b200_jit_launch": "map"}
-TENSOR_KERNELS = ("b200_gemm_tc", "b200_conv2d_tc")
+             "b200_conv2d_exact": "conv", "b200_jit_launch": "map",
+             "b200_conv2d_tc_fused": "conv", "b200_pack_conv_weight": "pack"}
+TENSOR_KERNELS = ("b200_gemm_tc", "b200_conv2d_tc", "b200_conv2d_tc_fused")
 # entry points that run the same kernel family (timed together)
 ALIASES = {"b200_gemm_tc_shadow": "b200_gemm_tc", "b200_gemm_tc_kn": "b200_gemm_tc",
            "b200_gemm_f32_exact_tiled": "b200_gemm_f32_exact"}
@@ -752,14 +755,17 @@ def roofline(wl, prec, fam, ms, sus_ms, rank_flops):
                            "f32x3": f"{src} bf16 x 0.5 / 3 (derived: each fp32-accurate product "
                                     f"is 3 tf32 products at half the bf16 rate)"}[prec]
         unit, bound = "TFLOP/s", "tensor"
-        if wl.tc_bytes and wl.tc_bytes * scale / (dom_ms * 1e-3) / 1e9 / peaks["hbm_gbs"] > \
+        tcb = getattr(wl, "tc_fused_bytes", None) if dom == "b200_conv2d_tc_fused" else \
+            wl.tc_bytes
+        if tcb and tcb * scale / (dom_ms * 1e-3) / 1e9 / peaks["hbm_gbs"] > \
                 achieved / peak:
             # the conv's f32 output read-modify-write makes it HBM-bound
-            achieved = wl.tc_bytes * scale / (dom_ms * 1e-3) / 1e9
+            achieved = tcb * scale / (dom_ms * 1e-3) / 1e9
             peak, unit, bound = peaks["hbm_gbs"], "GB/s", "hbm"
             sus_peak = peak
             peak_source = (f"{src} HBM copy bandwidth (MEASURED_PEAKS.json); algorithmic bytes "
-                           f"= NHWC bf16 input + 2 x f32 output")
+                           + ("= f32 NCHW input + 2 x f32 output" if dom == "b200_conv2d_tc_fused"
+                              else "= NHWC bf16 input + 2 x f32 output"))
     else:
         # the bit-exact kernels issue a separate, individually rounded
         # multiply and add per MAC (no FMA: the reference rounds each op), so

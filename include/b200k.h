@@ -228,6 +228,19 @@ int b200_conv2d_tc(const void *in_nhwc, const void *wt, float *out, const int64_
                    int64_t nb, int64_t cp, int64_t hp, int64_t wp, int64_t f, int64_t ho,
                    int64_t wo, int64_t kh, int64_t kw, int32_t init, float init_value,
                    void *stream);
+/*
+ * b200_conv2d_tc without the input repack: `in` is the NCHW f32 input
+ * (element strides in_strides[4], HOST array; dense planes: w stride 1,
+ * h stride = wp, 16-byte channel and image strides), read by TMA in raw
+ * f32 row spans and converted to the bf16 NHWC patch inside the kernel by a
+ * converter warpgroup.  `wt` as for b200_conv2d_tc (b200_pack_conv_weight,
+ * cp = c rounded up to 64).  3x3 merged-tap tiling only (F in {32, 64});
+ * B200_EUNSUPPORTED otherwise, and the caller packs instead.
+ */
+int b200_conv2d_tc_fused(const float *in, const int64_t *in_strides, const void *wt, float *out,
+                         const int64_t *out_strides, int64_t nb, int64_t c, int64_t hp,
+                         int64_t wp, int64_t f, int64_t ho, int64_t wo, int64_t kh, int64_t kw,
+                         int32_t init, float init_value, void *stream);
 
 /*
  * Bit-exact direct convolution (conv_2d_nchw_fchw, valid, stride 1;

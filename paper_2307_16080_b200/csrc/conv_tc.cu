@@ -51,6 +51,7 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include "../../include/b200k.h"
 #include "tc_common.cuh"
@@ -62,7 +63,11 @@ namespace {
 constexpr int kMaxStages = 6;             // patch pipeline depth (runtime, smem permitting)
 constexpr int kMaxOut = 3;                // staged output blocks (runtime)
 constexpr int kThreads = 384;              // 4 control warps + 2 epilogue warpgroups
+constexpr int kConvThreads = 128;          // fused: + 1 converter warpgroup (warps 12-15)
+constexpr int kMaxRaw = 8;                 // fused: raw f32 chunk buffers (runtime, smem permitting)
+constexpr int kRawCh = 8;                  // fused: channels per raw chunk
 constexpr size_t kSmemMax = 232448;
+int *b200_conv_trace_host = nullptr;
 
 // Tile geometry of tiling R.  ROWLEN: pixels per patch row = per M row group
 // (M = 128 = TH * ROWLEN); TW: output columns per tile — R > 1 loses the
@@ -92,7 +97,23 @@ struct ConvGeo {
   int init;
   float init_value;
   unsigned long long *stats;   // dev: per-role wait cycles (B200_CONV_STATS), or null
+  // fused (NCHW f32 input read by the kernel): a raw chunk is ONE TMA box
+  // over the input viewed as [N][C][H / 2][2 W] (row pairs: a 16-byte
+  // multiple pitch where single rows are not): `npair` row pairs x `blen`
+  // pixels (W + prow, rounded to 4) x kRawCh channels; `rstages` buffers of
+  // `raw_bytes`
+  int blen, npair, raw_bytes, rstages, c;
+  // dev: per-CTA progress counters in mapped host memory (B200_CONV_TRACE),
+  // [cta][8]: producer units, converter patches, mma patches, epilogue
+  // tiles, loader tiles; or null
+  volatile int *trace;
 };
+#define TRACE(slot, v)                                           \
+  do {                                                           \
+    if (g.trace) {                                               \
+      g.trace[blockIdx.x * 8 + (slot)] = (v);                    \
+    }                                                            \
+  } while (0)
 
 // dev instrumentation: cycles spent in a wait, per role slot
 #define TIMED(slot, stmt)                          \
@@ -149,8 +170,8 @@ __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-template <int F, int R>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int F, int R, bool FUSED = false>
+__global__ void __launch_bounds__(kThreads + (FUSED ? kConvThreads : 0), 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tma_in,
                    const __grid_constant__ CUtensorMap tma_w,
                    const __grid_constant__ CUtensorMap tma_out, float *__restrict__ out,
@@ -174,8 +195,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t sP = base + nslices * SLICE;                 // stages x patch
   const uint32_t sO = sP + stages * pstage;                   // nout x OUTBUF
   float *gO = reinterpret_cast<float *>(gbase + (sO - base));
-  uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + (sO - base) + g.nout * OUTBUF);
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * kMaxStages + 5 + 2 * kMaxOut);
+  const uint32_t sR = sO + g.nout * OUTBUF;                   // fused: rstages raw chunks
+  const float *gR = reinterpret_cast<const float *>(gbase + (sR - base));
+  uint64_t *bars = reinterpret_cast<uint64_t *>(
+      gbase + (sR - base) + (FUSED ? g.rstages * g.raw_bytes : 0));
+  uint32_t *tmem_slot =
+      reinterpret_cast<uint32_t *>(bars + 2 * kMaxStages + 5 + 2 * kMaxOut + 2 * kMaxRaw);
   const uint32_t bar0 = smem_u32(bars);
   auto full = [&](int s) { return bar0 + 8u * s; };
   auto empty = [&](int s) { return bar0 + 8u * (kMaxStages + s); };
@@ -184,6 +209,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t wbar = bar0 + 8u * (2 * kMaxStages + 4);
   auto ofull = [&](int b) { return bar0 + 8u * (2 * kMaxStages + 5 + b); };
   auto oempty = [&](int b) { return bar0 + 8u * (2 * kMaxStages + 5 + kMaxOut + b); };
+  auto rfull = [&](int r) { return bar0 + 8u * (2 * kMaxStages + 5 + 2 * kMaxOut + r); };
+  auto rempty = [&](int r) {
+    return bar0 + 8u * (2 * kMaxStages + 5 + 2 * kMaxOut + kMaxRaw + r);
+  };
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -191,9 +220,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const long long t_start = clock64();
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < stages; ++s) {
-      mbar_init(full(s), 1);
+      // fused: the converter warps fill a patch stage and each arrives
+      mbar_init(full(s), FUSED ? kConvThreads / 32 : 1);
       mbar_init(empty(s), 1);
     }
+    if (FUSED)
+      for (int r = 0; r < g.rstages; ++r) {
+        mbar_init(rfull(r), 1);
+        mbar_init(rempty(r), 1);   // the one converter warp that owns the chunk
+      }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull(a), 1);
       mbar_init(tempty(a), 256);
@@ -228,6 +263,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     w0 = (int32_t)((r - ty * twt) * g.tw);
   };
 
+  // this CTA's tile sequence: strided tiles, or (fused) whole row bands — a
+  // band's tw_tiles tiles back to back, so its input rows are loaded and
+  // converted once for all of them
+  const int64_t twt64 = g.tw_tiles;
+  const int64_t nbands = g.tiles / twt64;
+  auto tile_at = [&](int64_t i) -> int64_t {   // -1: no more tiles
+    if (!FUSED) {
+      const int64_t t = blockIdx.x + i * (int64_t)gridDim.x;
+      return t < g.tiles ? t : -1;
+    }
+    const int64_t band = blockIdx.x + (i / twt64) * (int64_t)gridDim.x;
+    return band < nbands ? band * twt64 + i % twt64 : -1;
+  };
+
   if (warp == 0) {
     if (lane == 0) {
       // resident weights: slice (ki, kj, cb) = rows f of columns
@@ -244,10 +293,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       int s = 0;
       uint32_t ph = 0;
-      for (int64_t t = blockIdx.x; t < g.tiles; t += gridDim.x) {
+      int64_t rq = 0;   // fused: raw chunk stream index
+      for (int64_t i = 0, t; (t = tile_at(i)) >= 0; ++i) {
         int32_t n, h0, w0;
         tile_coords(t, n, h0, w0);
         for (int cb = 0; cb < g.cblocks; ++cb) {
+          if (FUSED) {
+            // raw f32 chunks of kRawCh channels, once per row band (its
+            // first tile): one box of whole row pairs h0 / 2 .. + npair - 1.
+            // Chunk q of the stream goes to converter warp q % 4's own ring
+            // (rstages / 4 buffers): a buffer is only ever waited on by one
+            // warp, in order — the mbarrier parity test cannot tell use k
+            // from use k - 2, so two warps sharing a buffer would race
+            if (i % twt64 != 0) continue;
+            const int pw = g.rstages / 4;
+            for (int j = 0; j < 64 / kRawCh; ++j) {
+              const int64_t q = (rq++);
+              const int64_t k = q / 4;
+              const int rb = (int)(q % 4) * pw + (int)(k % pw);
+              const uint32_t rph = (uint32_t)((k / pw) & 1);
+              TIMED(0, mbar_wait(rempty(rb), rph ^ 1));
+              mbar_expect_tx(rfull(rb), (uint32_t)g.raw_bytes);
+              tma_load_4d(&tma_in, rfull(rb), sR + rb * g.raw_bytes, 0, h0 / 2,
+                          cb * 64 + j * kRawCh, n);
+              TRACE(0, (int)(q + 1));
+            }
+            continue;
+          }
           TIMED(0, mbar_wait(empty(s), ph ^ 1));
           mbar_expect_tx(full(s), (uint32_t)g.patch_bytes);
           tma_load_4d(&tma_in, full(s), sP + s * pstage, cb * 64, w0, h0, n);
@@ -266,7 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t ph = 0;
       int acc = 0;
       uint32_t aph = 0;
-      for (int64_t t = blockIdx.x; t < g.tiles; t += gridDim.x) {
+      for (int64_t i = 0, t; (t = tile_at(i)) >= 0; ++i) {
         TIMED(2, mbar_wait(tempty(acc), aph ^ 1));
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + (uint32_t)(acc * N);
@@ -310,6 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           umma_commit(empty(s));
           if (++s == stages) { s = 0; ph ^= 1; }
+          TRACE(2, (int)i * 4 + cb + 1);
         }
         umma_commit(tfull(acc));
         if (++acc == 2) { acc = 0; aph ^= 1; }
@@ -322,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // is only handed over once its last store has drained)
       int b = 0;
       uint32_t ph = 0;
-      for (int64_t t = blockIdx.x; t < g.tiles; t += gridDim.x) {
+      for (int64_t i = 0, t; (t = tile_at(i)) >= 0; ++i) {
         int32_t n, h0, w0;
         tile_coords(t, n, h0, w0);
         mbar_wait(oempty(b), ph ^ 1);
@@ -333,7 +406,72 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_load_4d(&tma_out, ofull(b), sO + b * OUTBUF, w0, h0, 0, n);
         }
         if (++b == g.nout) { b = 0; ph ^= 1; }
+
       }
+    }
+  } else if (FUSED && warp >= 12) {
+    // converter warpgroup: raw f32 [kRawCh][npair][blen] chunks -> the bf16
+    // patch stage ([ph][ROWLEN px][64 ch], 128-byte pixel rows, 128B swizzle:
+    // the 16-byte channel group k of pixel p sits at k ^ (p & 7)).  The four
+    // warps convert different chunks at once — chunk q of the stream goes to
+    // warp q % 4 — so their load-to-store latencies overlap; a warp releases
+    // its raw buffer alone (rempty count 1) and the patch is full once all
+    // four have arrived.  Lane task = a pixel pair of one patch row: 8 LDS.64
+    // (channel rows of the chunk), 8 packs, two 16-byte stores.  Patch row y
+    // is row pair y / 2 at offset (y % 2) W; W even keeps pairs 8-byte aligned.
+    const int cw = warp - 12;
+    constexpr int NCH = 64 / kRawCh;   // chunks per 64-channel patch (cblocks == 1)
+    const int npairs = g.ph * ROWLEN / 2;
+    const int cstride = g.npair * g.blen;   // floats between a chunk's channels
+    const int twt = (int)twt64;
+    int s = 0;
+    uint32_t ph = 0;
+    int64_t bi = 0;   // band index of this CTA's stream
+    for (int64_t i = 0, t; (t = tile_at(i)) >= 0; i += twt, ++bi) {
+      // the band's tiles take the next twt patch stages
+      for (int k = 0, ss = s; k < twt; ++k) {
+        mbar_wait(empty(ss), (ss >= s ? ph : ph ^ 1) ^ 1);
+        if (++ss == stages) ss = 0;
+      }
+      for (int j = cw; j < NCH; j += 4) {
+        const int64_t q = bi * NCH + j;   // q % 4 == cw: this warp's ring
+        const int64_t k = q / 4;
+        const int pw = g.rstages / 4;
+        const int rs = cw * pw + (int)(k % pw);
+        mbar_wait(rfull(rs), (uint32_t)((k / pw) & 1));
+        const float *raw = gR + rs * (g.raw_bytes / 4);
+        for (int tx = 0, ss = s; tx < twt; ++tx) {
+          unsigned char *patch = gbase + (sP - base) + ss * pstage;
+          const int w0 = tx * g.tw;
+          for (int tp = lane; tp < npairs; tp += 32) {
+            const int p = 2 * tp;
+            const int y = p / ROWLEN, x = p % ROWLEN;
+            const float *src = raw + (y >> 1) * g.blen + (y & 1) * (int)g.wp + w0 + x;
+            __nv_bfloat162 v0[4], v1[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const float2 a = *reinterpret_cast<const float2 *>(src + (2 * c) * cstride);
+              const float2 b = *reinterpret_cast<const float2 *>(src + (2 * c + 1) * cstride);
+              v0[c] = __floats2bfloat162_rn(a.x, b.x);
+              v1[c] = __floats2bfloat162_rn(a.y, b.y);
+            }
+            *reinterpret_cast<uint4 *>(patch + p * 128 + ((j ^ (p & 7)) << 4)) =
+                *reinterpret_cast<uint4 *>(v0);
+            *reinterpret_cast<uint4 *>(patch + (p + 1) * 128 + ((j ^ ((p + 1) & 7)) << 4)) =
+                *reinterpret_cast<uint4 *>(v1);
+          }
+          if (++ss == stages) ss = 0;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(rempty(rs));
+      }
+      fence_proxy_async();   // generic-proxy stores -> the tensor cores' reads
+      __syncwarp();
+      for (int k = 0; k < twt; ++k) {
+        if (lane == 0) mbar_arrive(full(s));
+        if (++s == stages) { s = 0; ph ^= 1; }
+      }
+      if (lane == 0) TRACE(cw == 0 ? 1 : 4 + cw, (int)(i + twt));
     }
   } else if (warp >= 4) {
     // two epilogue warpgroups: warp w reads TMEM lanes 32 * (w % 4) + [0, 32)
@@ -349,7 +487,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t aph = 0;
     int ob = 0;
     uint32_t oph = 0;
-    for (int64_t t = blockIdx.x; t < g.tiles; t += gridDim.x) {
+    for (int64_t i = 0, t; (t = tile_at(i)) >= 0; ++i) {
       int32_t n, h0, w0;
       tile_coords(t, n, h0, w0);
       const bool valid = lane_ok && h0 + hr < g.ho && w0 + wc < g.wo;
@@ -404,6 +542,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(tempty(acc));
       if (++acc == 2) { acc = 0; aph ^= 1; }
+      if (threadIdx.x == 128) TRACE(3, (int)i * 2 + 1);
       if (g.nout > 0) {
         // the block goes back by one TMA store (out-of-range rows/columns
         // clipped); buffer ob - 1 is released once its own store has read it
@@ -412,12 +551,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (threadIdx.x == 128) {
           tma_store_4d(&tma_out, sO + ob * OUTBUF, w0, h0, 0, n);
           bulk_commit();
-          if (t != blockIdx.x) {
+          if (g.nout == 1) {
+            // a single buffer: the next tile's load waits for this store
+            bulk_wait_read<0>();
+            mbar_arrive(oempty(0));
+          } else if (i != 0) {
             bulk_wait_read<1>();
             mbar_arrive(oempty(ob == 0 ? g.nout - 1 : ob - 1));
           }
         }
         if (++ob == g.nout) { ob = 0; oph ^= 1; }
+        if (threadIdx.x == 128) TRACE(3, (int)i * 2 + 2);
       }
     }
     if (g.nout > 0 && threadIdx.x == 128) bulk_wait_all();
@@ -740,25 +884,48 @@ int conv_merge(int64_t f, int64_t kw) {
 // output blocks of `outbuf` bytes, barriers, alignment).  Mirrored by
 // runtime.conv_tc_supported (2 stages, no staged output blocks).
 size_t conv_smem(int64_t f, int64_t kh, int64_t kw, int64_t cp, int64_t pstage, int stages,
-                 int nout, int64_t outbuf) {
-  return 1024 + kh * kw * (cp / 64) * f * 128 + stages * pstage + nout * outbuf + 256;
+                 int nout, int64_t outbuf, int64_t raw_bytes = 0, int rstages = 0) {
+  return 1024 + kh * kw * (cp / 64) * f * 128 + stages * pstage + nout * outbuf +
+         rstages * raw_bytes + 512;   // barriers (39 x 8 bytes) + the TMEM slot
 }
 
-template <int F, int R>
-int launch_conv(const void *in_nhwc, const void *wt, float *out, ConvGeo &g, cudaStream_t s) {
+// FUSED: `in` is the NCHW f32 input itself (dense planes; see
+// b200_conv2d_tc_fused), read by TMA as [N][C][H * W] and converted in the
+// kernel; otherwise `in` is the NHWC bf16 repack.
+template <int F, int R, bool FUSED = false>
+int launch_conv(const void *in, const int64_t *in_strides, const void *wt, float *out,
+                ConvGeo &g, cudaStream_t s) {
   using T = Tiling<F, R>;
-  auto smem_of = [&](int stages, int nout) {
-    return conv_smem(F, g.kh, g.kw, g.cp, g.pstage, stages, nout, T::OUTBUF);
+  const int64_t raw = FUSED ? g.raw_bytes : 0;
+  // fused: at least 2 raw chunk buffers; the staged output blocks are capped
+  // at 2 so the rest of shared memory deepens the raw ring (its TMA loads
+  // are what hides the input's latency)
+  const int rmin = FUSED ? 4 : 0;
+  auto smem_of = [&](int stages, int nout, int rst = -1) {
+    return conv_smem(F, g.kh, g.kw, g.cp, g.pstage, stages, nout, T::OUTBUF, raw,
+                     rst < 0 ? rmin : rst);
   };
   CUtensorMap mi, mw, mo;
-  cuuint64_t di[4] = {(cuuint64_t)g.cp, (cuuint64_t)g.wp, (cuuint64_t)g.hp, (cuuint64_t)g.nb};
-  cuuint64_t si[3] = {(cuuint64_t)(g.cp * 2), (cuuint64_t)(g.wp * g.cp * 2),
-                      (cuuint64_t)(g.hp * g.wp * g.cp * 2)};
-  // the whole patch of one 64-channel block per box, rows of 128 B, swizzled
-  cuuint32_t bi[4] = {64, (cuuint32_t)g.prow, (cuuint32_t)g.ph, 1};
-  if (!make_map_4d(&mi, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, in_nhwc, di, si, bi,
-                   CU_TENSOR_MAP_SWIZZLE_128B))
-    return B200_ELAUNCH;
+  if (FUSED) {
+    // [N][C][H / 2][2 W] f32: row pairs of 8 W bytes (16-byte multiples)
+    cuuint64_t di[4] = {(cuuint64_t)(2 * g.wp), (cuuint64_t)(g.hp / 2), (cuuint64_t)g.c,
+                        (cuuint64_t)g.nb};
+    cuuint64_t si[3] = {(cuuint64_t)(2 * g.wp * 4), (cuuint64_t)(in_strides[1] * 4),
+                        (cuuint64_t)(in_strides[0] * 4)};
+    cuuint32_t bi[4] = {(cuuint32_t)g.blen, (cuuint32_t)g.npair, (cuuint32_t)kRawCh, 1};
+    if (!make_map_4d(&mi, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, in, di, si, bi,
+                     CU_TENSOR_MAP_SWIZZLE_NONE))
+      return B200_ELAUNCH;
+  } else {
+    cuuint64_t di[4] = {(cuuint64_t)g.cp, (cuuint64_t)g.wp, (cuuint64_t)g.hp, (cuuint64_t)g.nb};
+    cuuint64_t si[3] = {(cuuint64_t)(g.cp * 2), (cuuint64_t)(g.wp * g.cp * 2),
+                        (cuuint64_t)(g.hp * g.wp * g.cp * 2)};
+    // the whole patch of one 64-channel block per box, rows of 128 B, swizzled
+    cuuint32_t bi[4] = {64, (cuuint32_t)g.prow, (cuuint32_t)g.ph, 1};
+    if (!make_map_4d(&mi, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, in, di, si, bi,
+                     CU_TENSOR_MAP_SWIZZLE_128B))
+      return B200_ELAUNCH;
+  }
   if (!make_map(&mw, 0, wt, F, g.kh * g.kw * g.cp, F)) return B200_ELAUNCH;
   if (smem_of(2, 0) > kSmemMax) return B200_EUNSUPPORTED;
   // output blocks staged through shared memory (TMA load, in-place update,
@@ -777,25 +944,45 @@ int launch_conv(const void *in_nhwc, const void *wt, float *out, ConvGeo &g, cud
     if (make_map_4d(&mo, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, out, dout, sout, bout,
                     CU_TENSOR_MAP_SWIZZLE_NONE)) {
       const char *env = getenv("B200_CONV_NOUT");   // dev knob
-      g.nout = env ? atoi(env) : kMaxOut;
+      g.nout = env ? atoi(env) : (FUSED ? 2 : kMaxOut);
       if (g.nout > kMaxOut) g.nout = kMaxOut;
       while (g.nout > 0 && smem_of(2, g.nout) > kSmemMax) --g.nout;
     }
   }
   if (g.nout == 0) mo = mi;   // unused placeholder
   g.stages = kMaxStages;
-  while (smem_of(g.stages, g.nout) > kSmemMax) --g.stages;
-  const size_t smem = smem_of(g.stages, g.nout);
+  if (FUSED) {
+    const char *env = getenv("B200_CONV_RAW");   // dev knob
+    g.rstages = env ? atoi(env) : kMaxRaw;
+    if (g.rstages > kMaxRaw) g.rstages = kMaxRaw;
+    g.rstages &= ~3;   // one ring per converter warp
+    while (g.rstages > 4 && smem_of(2, g.nout, g.rstages) > kSmemMax) g.rstages -= 4;
+    if (g.rstages < 4) g.rstages = 4;
+  }
+  while (smem_of(g.stages, g.nout, g.rstages) > kSmemMax) --g.stages;
+  const size_t smem = smem_of(g.stages, g.nout, g.rstages);
+  if (FUSED && g.stages < g.tw_tiles) return B200_EUNSUPPORTED;   // a band's patches
   int ctas = num_sms();
-  if (g.tiles < ctas) ctas = (int)g.tiles;
-  cudaFuncSetAttribute(conv_tc_kernel<F, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const int64_t units = FUSED ? g.tiles / g.tw_tiles : g.tiles;   // fused: row bands
+  if (units < ctas) ctas = (int)units;
+  cudaFuncSetAttribute(conv_tc_kernel<F, R, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
+  if (getenv("B200_CONV_TRACE")) {   // dev: progress counters the host can read while it runs
+    static int *host_trace = nullptr;
+    if (!host_trace) cudaHostAlloc(&host_trace, 8 * 1024 * sizeof(int), cudaHostAllocMapped);
+    memset(host_trace, 0, 8 * 1024 * sizeof(int));
+    int *dev = nullptr;
+    cudaHostGetDevicePointer(&dev, host_trace, 0);
+    g.trace = dev;
+    b200_conv_trace_host = host_trace;
+  }
   const bool stats = getenv("B200_CONV_STATS") != nullptr;   // dev: print role wait cycles
   if (stats) {
     cudaMalloc(&g.stats, 16 * sizeof(unsigned long long));
     cudaMemsetAsync(g.stats, 0, 16 * sizeof(unsigned long long), s);
   }
-  conv_tc_kernel<F, R><<<ctas, kThreads, smem, s>>>(mi, mw, mo, out, g);
+  conv_tc_kernel<F, R, FUSED>
+      <<<ctas, kThreads + (FUSED ? kConvThreads : 0), smem, s>>>(mi, mw, mo, out, g);
   if (stats) {
     unsigned long long h[16];
     cudaMemcpyAsync(h, g.stats, sizeof(h), cudaMemcpyDeviceToHost, s);
@@ -806,9 +993,9 @@ int launch_conv(const void *in_nhwc, const void *wt, float *out, ConvGeo &g, cud
             "conv stats (kcycles/CTA): producer total %.1f wait-empty %.1f | mma total %.1f "
             "wait-full %.1f wait-tempty %.1f | epilogue total %.1f wait-tfull %.1f "
             "wait-out %.1f | "
-            "R %d stages %d staged output blocks %d tiles %lld\n",
+            "R %d stages %d staged output blocks %d raw stages %d tiles %lld\n",
             h[8] / c / 1e3, h[0] / c / 1e3, h[9] / c / 1e3, h[1] / c / 1e3, h[2] / c / 1e3,
-            h[10] / c / 1e3, h[3] / c / 1e3, h[4] / c / 1e3, R, g.stages, g.nout,
+            h[10] / c / 1e3, h[3] / c / 1e3, h[4] / c / 1e3, R, g.stages, g.nout, g.rstages,
             (long long)g.tiles);
   }
   return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
@@ -928,14 +1115,13 @@ extern "C" int b200_pack_conv_weight(const float *src, const int64_t *sstr, void
   return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
 }
 
-extern "C" int b200_conv2d_tc(const void *in_nhwc, const void *wt, float *out,
-                              const int64_t *out_strides, int64_t nb, int64_t cp, int64_t hp,
-                              int64_t wp, int64_t f, int64_t ho, int64_t wo, int64_t kh,
-                              int64_t kw, int32_t init, float init_value, void *stream) {
-  if (cp % 64 || ho <= 0 || wo <= 0 || kh <= 0 || kw <= 0 || ho + kh - 1 > hp ||
-      wo + kw - 1 > wp)
-    return B200_EINVAL;
-  ConvGeo g{};
+namespace {
+// Tile / patch geometry shared by both entry points; false: outside the
+// kernel's 32-bit index limits.
+bool conv_geo(ConvGeo &g, const int64_t *out_strides, int64_t nb, int64_t cp, int64_t hp,
+              int64_t wp, int64_t f, int64_t ho, int64_t wo, int64_t kh, int64_t kw, int32_t init,
+              float init_value) {
+  g = ConvGeo{};
   g.nb = nb; g.cp = cp; g.hp = hp; g.wp = wp; g.f = f; g.ho = ho; g.wo = wo;
   g.kh = kh; g.kw = kw; g.init = init; g.init_value = init_value;
   g.so_n = out_strides[0]; g.so_f = out_strides[1];
@@ -954,17 +1140,69 @@ extern "C" int b200_conv2d_tc(const void *in_nhwc, const void *wt, float *out,
   g.patch_bytes = g.ph * g.prow * 128;
   g.pstage = (g.patch_bytes + 1023) & ~1023;
   // 32-bit tile indices and per-pixel channel offsets in the kernel
-  if (g.ph > 256 || g.prow > 256 || g.tiles + 2 * 148 >= (int64_t(1) << 31) ||
-      out_strides[1] < 0 || out_strides[1] * f >= (int64_t(1) << 31))
+  return !(g.ph > 256 || g.prow > 256 || g.tiles + 2 * 148 >= (int64_t(1) << 31) ||
+           out_strides[1] < 0 || out_strides[1] * f >= (int64_t(1) << 31));
+}
+}  // namespace
+
+extern "C" int b200_conv2d_tc(const void *in_nhwc, const void *wt, float *out,
+                              const int64_t *out_strides, int64_t nb, int64_t cp, int64_t hp,
+                              int64_t wp, int64_t f, int64_t ho, int64_t wo, int64_t kh,
+                              int64_t kw, int32_t init, float init_value, void *stream) {
+  if (cp % 64 || ho <= 0 || wo <= 0 || kh <= 0 || kw <= 0 || ho + kh - 1 > hp ||
+      wo + kw - 1 > wp)
+    return B200_EINVAL;
+  ConvGeo g;
+  if (!conv_geo(g, out_strides, nb, cp, hp, wp, f, ho, wo, kh, kw, init, init_value))
     return B200_EUNSUPPORTED;
+  const int R = conv_merge(f, kw);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   switch (f * 16 + R) {
-    case 32 * 16 + 1: return launch_conv<32, 1>(in_nhwc, wt, out, g, s);
-    case 64 * 16 + 1: return launch_conv<64, 1>(in_nhwc, wt, out, g, s);
-    case 128 * 16 + 1: return launch_conv<128, 1>(in_nhwc, wt, out, g, s);
-    case 32 * 16 + 3: return launch_conv<32, 3>(in_nhwc, wt, out, g, s);
-    case 64 * 16 + 3: return launch_conv<64, 3>(in_nhwc, wt, out, g, s);
-    case 32 * 16 + 5: return launch_conv<32, 5>(in_nhwc, wt, out, g, s);
+    case 32 * 16 + 1: return launch_conv<32, 1>(in_nhwc, nullptr, wt, out, g, s);
+    case 64 * 16 + 1: return launch_conv<64, 1>(in_nhwc, nullptr, wt, out, g, s);
+    case 128 * 16 + 1: return launch_conv<128, 1>(in_nhwc, nullptr, wt, out, g, s);
+    case 32 * 16 + 3: return launch_conv<32, 3>(in_nhwc, nullptr, wt, out, g, s);
+    case 64 * 16 + 3: return launch_conv<64, 3>(in_nhwc, nullptr, wt, out, g, s);
+    case 32 * 16 + 5: return launch_conv<32, 5>(in_nhwc, nullptr, wt, out, g, s);
     default: return B200_EUNSUPPORTED;
   }
 }
+
+extern "C" int b200_conv2d_tc_fused(const float *in, const int64_t *in_strides, const void *wt,
+                                    float *out, const int64_t *out_strides, int64_t nb,
+                                    int64_t c, int64_t hp, int64_t wp, int64_t f, int64_t ho,
+                                    int64_t wo, int64_t kh, int64_t kw, int32_t init,
+                                    float init_value, void *stream) {
+  if (c <= 0 || ho <= 0 || wo <= 0 || kh <= 0 || kw <= 0 || ho + kh - 1 > hp ||
+      wo + kw - 1 > wp)
+    return B200_EINVAL;
+  const int64_t cp = (c + 63) / 64 * 64;
+  ConvGeo g;
+  if (!conv_geo(g, out_strides, nb, cp, hp, wp, f, ho, wo, kh, kw, init, init_value))
+    return B200_EUNSUPPORTED;
+  const int R = conv_merge(f, kw);
+  // dense planes read as [N][C][H * W] f32: unit pixel stride, rows back to
+  // back, 16-byte channel / image strides and base (TMA)
+  if (R == 1 || in_strides[3] != 1 || in_strides[2] != wp || in_strides[1] % 4 ||
+      in_strides[0] % 4 || (reinterpret_cast<uintptr_t>(in) & 15) || hp * wp >= (int64_t(1) << 31))
+    return B200_EUNSUPPORTED;
+  // one TMA box per raw chunk over row pairs ([N][C][H / 2][2 W]): H and W
+  // even (pair pitch 8 W bytes), box starts (w0, h0 / 2) on 16-byte
+  // boundaries (a misaligned TMA box start faults — measured, "illegal
+  // instruction"): tile origins are (4 h, 28 w), so 16 | 112 and h0 is even
+  g.c = (int)c;
+  g.blen = (int)(2 * wp);   // whole row pairs: a band's tiles share the chunk
+  g.npair = (g.ph + 1) / 2;
+  if (hp % 2 || wp % 2 || g.blen > 256 || g.th % 2 || g.cblocks != 1 || g.tw_tiles > 2)
+    return B200_EUNSUPPORTED;
+  g.raw_bytes = kRawCh * g.npair * g.blen * 4;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  switch (f * 16 + R) {
+    case 32 * 16 + 3: return launch_conv<32, 3, true>(in, in_strides, wt, out, g, s);
+    case 64 * 16 + 3: return launch_conv<64, 3, true>(in, in_strides, wt, out, g, s);
+    default: return B200_EUNSUPPORTED;
+  }
+}
+
+// dev: the mapped progress counters of the last B200_CONV_TRACE launch
+extern "C" int *b200_conv_trace(void) { return b200_conv_trace_host; }

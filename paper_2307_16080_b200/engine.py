@@ -451,6 +451,8 @@ class _Run:
                 note = getattr(self.be, "last_note", None)
                 if note:
                     fused.append(note)
+                if "pack_conv_weight" in kernels:   # b200_conv2d_tc_fused
+                    fused.append("input converted in-kernel")
                 self.plan.append((kernels[-1], g.M, g.N, g.K) +
                                  ((tuple(fused),) if fused else ()))
             else:

@@ -69,6 +69,8 @@ SIGNATURES = {
     "b200_pack_conv": [_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _P, _P, _P, _I64, _I64, _I64,
                        _P],
     "b200_pack_conv_weight": [_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _P],
+    "b200_conv2d_tc_fused": [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64,
+                             _I64, _I32, _F32, _P],
     "b200_conv2d_tc": [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64,
                        _I32, _F32, _P],
     "b200_conv2d_exact": [_I32, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64,
@@ -416,6 +418,43 @@ def conv_tc_supported(cv):
     patch = -(-(ph * prow * 128) // 1024) * 1024
     smem = 1024 + cv.kh * cv.kw * (cp // 64) * cv.f * 128 + 2 * patch + 256
     return smem <= 232448 and ph <= 256 and prow <= 256
+
+
+# The fused conv reads and converts the f32 input inside the conv kernel;
+# its shared memory (resident weights + staged output blocks + bf16 patches +
+# raw f32 chunks) leaves two patch stages, so a row band's conversion cannot
+# overlap the previous band's MMAs: at ResNet's N = 256 it is 160 us against
+# 152 for pack + conv (tools/probe_conv_fused.py), while small batches, where
+# the separate pack launch's fixed cost dominates, gain 20-30 % (nb 4: 13 vs
+# 17 us, nb 8: 14 vs 18).  It therefore takes batches up to this size.
+FUSED_CONV_MAX_IMAGES = int(os.environ.get("B200_CONV_FUSED_MAX", "32"))
+
+
+def conv_tc_fused_ok(cv):
+    """b200_conv2d_tc_fused applies (mirrors csrc/conv_tc.cu's checks): the
+    merged 3x3 tiling (F 32 / 64), C <= 64, at most two 28-column tiles per
+    row band (W - 2 <= 56, the band's rows are one TMA box), dense NCHW planes
+    (unit w stride, rows back to back, 16-byte channel / image strides),
+    even H and W, and shared memory for the
+    weights, two patch stages and four raw chunks (one per converter warp;
+    one TMA box over row pairs per 8 channels: H and W even).  B200_CONV_UNFUSED=1 forces the repack
+    path (A/B)."""
+    if os.environ.get("B200_CONV_UNFUSED") == "1":
+        return False
+    if not (cv.kw == 3 and cv.f in (32, 64)) or cv.nb > FUSED_CONV_MAX_IMAGES:
+        return False
+    st = cv.inp.strides
+    if st[3] != 1 or st[2] != cv.wp or st[1] % 4 or st[0] % 4 or cv.hp * cv.wp >= 2 ** 31:
+        return False
+    ph, prow = 4 + cv.kh - 1, 32
+    blen = 2 * cv.wp                           # whole row pairs per 8-channel chunk
+    if cv.hp % 2 or cv.wp % 2 or blen > 256 or cv.c > 64 or -(-cv.wo // 28) > 2:
+        return False
+    raw = 8 * ((ph + 1) // 2) * blen * 4
+    cp = -(-cv.c // 64) * 64
+    patch = -(-(ph * prow * 128) // 1024) * 1024
+    smem = 1024 + cv.kh * cv.kw * (cp // 64) * cv.f * 128 + 2 * patch + 4 * raw + 512
+    return smem <= 232448
 
 
 def conv_exact_supported(cv, esz):
@@ -921,6 +960,19 @@ class DeviceBackend:
             self.recording.keep.append((sin, sw, sout))
         self.keep(sin, sw, sout)
         first = [True]   # the first input pack also packs the weights (one launch)
+        if conv_tc_fused_ok(cv):
+            # the input is read as f32 and converted inside the conv kernel
+            def launch_fused(inp_ptr, out_ptr, nb):
+                if first[0]:
+                    first[0] = False
+                    self.call("b200_pack_conv_weight", P(ker.data_ptr()), sw,
+                              P(xw.data_ptr()), cv.f, cv.c, cv.kh, cv.kw, cp, s.stream_ptr)
+                self.call("b200_conv2d_tc_fused", P(inp_ptr), sin, P(xw.data_ptr()),
+                          P(out_ptr), sout, nb, cv.c, cv.hp, cv.wp, cv.f, cv.ho, cv.wo, cv.kh,
+                          cv.kw, init, init_value, s.stream_ptr)
+
+            self._conv_run(cv, 4, init, last_writer, launch_fused)
+            return ["pack_conv_weight", "conv2d_tc_bf16"]
 
         def launch(inp_ptr, out_ptr, nb):
             xin = workspace(2, "bfloat16", nb * cv.hp * cv.wp, cp)
