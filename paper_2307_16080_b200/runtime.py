@@ -267,7 +267,8 @@ class Staging:
             self._wb_event.synchronize()
             self._wb_event = None
 
-    def stream_rows(self, panels, ins, out, launch, written_back=True, rows=None):
+    def stream_rows(self, panels, ins, out, launch, written_back=True, rows=None,
+                    concurrent=1):
         """Run ``launch(r0, r1)`` over row panels with the host copies overlapped.
 
         The row-major buffers in ``ins`` (uploaded, panel by panel, on a copy
@@ -281,12 +282,20 @@ class Staging:
         write-backs, so later kernels cannot overwrite rows still being
         copied out.  ``panels``: [(r0, r1)] covering the leading dimension
         (or ``rows`` equal slices of every buffer's flat storage); they may
-        cover a sub-range of the rows (a batch shard's).
+        cover a sub-range of the rows (a batch shard's).  ``concurrent`` > 1:
+        panel kernels go round-robin to that many side streams, so the small
+        grids of consecutive panels share the GPU (compute-bound kernels
+        whose panel grids are under a wave); rows of different panels are
+        disjoint, so they may run in any order.
         """
         torch = self.torch
         cur = torch.cuda.current_stream()
         up, down = _copy_streams(torch)
         up.wait_stream(cur)     # device storage may be recycled from earlier kernels
+        comp = _compute_streams(torch, concurrent) if concurrent > 1 else [cur]
+        for cs in comp:
+            if cs is not cur:
+                cs.wait_stream(cur)
         obuf, oup = out
         lead = rows
         rows = rows or obuf.shape[0]
@@ -300,24 +309,29 @@ class Staging:
             views.append((host.view(r, -1), t.view(r, -1)))
         hin, (ho, to) = views[:-1], views[-1]
         esz = to.element_size()
-        for r0, r1 in panels:
+        for p, (r0, r1) in enumerate(panels):
             with torch.cuda.stream(up):
                 for (h, t) in hin + ([(ho, to)] if oup else []):
                     t[r0:r1].copy_(h[r0:r1], non_blocking=True)
                     self._count(h2d=(r1 - r0) * t.shape[1] * esz)
             ev = torch.cuda.Event()
             ev.record(up)
-            cur.wait_event(ev)
-            launch(r0, r1)
+            cs = comp[p % len(comp)]
+            cs.wait_event(ev)
+            with torch.cuda.stream(cs):
+                launch(r0, r1)
             self.panels += 1
             if written_back:
                 done = torch.cuda.Event()
-                done.record(cur)
+                done.record(cs)
                 down.wait_event(done)
                 with torch.cuda.stream(down):
                     ho[r0:r1].copy_(to[r0:r1], non_blocking=True)
                 self._count(d2h=(r1 - r0) * to.shape[1] * esz)
         assert panels[-1][1] <= rows
+        for cs in comp:
+            if cs is not cur:
+                cur.wait_stream(cs)
         if written_back:
             self._wb_event = torch.cuda.Event()
             self._wb_event.record(down)
@@ -355,6 +369,17 @@ class Staging:
 TOTALS = {"launches": 0, "h2d_bytes": 0, "d2h_bytes": 0}
 
 _COPY_STREAMS = {}
+
+
+_COMPUTE_STREAMS = {}
+
+
+def _compute_streams(torch, k):
+    """k side streams of the current device for concurrent panel kernels."""
+    key = (torch.cuda.current_device(), k)
+    if key not in _COMPUTE_STREAMS:
+        _COMPUTE_STREAMS[key] = [torch.cuda.Stream() for _ in range(k)]
+    return _COMPUTE_STREAMS[key]
 
 
 def _copy_streams(torch):
@@ -641,11 +666,12 @@ def _gemm_rows(buf, off, s, rows, cols):
     return r0, r0 + rows
 
 
-def row_panels(rows, row_bytes, align):
+def row_panels(rows, row_bytes, align, count=None):
     total = rows * row_bytes
     if total < STREAM_MIN_BYTES or rows < 2 * align:
         return None
-    p = max(2, min(8, total // STREAM_PANEL_BYTES))
+    p = count or max(2, min(8, total // STREAM_PANEL_BYTES))
+    p = max(2, min(p, rows // align))
     step = -(-rows // p)
     step = -(-step // align) * align
     return [(r, min(rows, r + step)) for r in range(0, rows, step)]
@@ -768,13 +794,19 @@ class DeviceBackend:
             stream_a = (not s.staged(g.A) and g.A is not g.B and
                         _gemm_rows(g.A, g.offA, g.sA, g.M, g.K) == crows and
                         self._owned(g.A, *crows))
+            # the exact kernels are compute-bound (4096^3: 4.5 ms against
+            # 4.7 ms of copies): eight panels, whose sub-wave grids run
+            # three at a time on side streams, so the copies hide behind
+            # the GEMM; the tensor-core path is copy-bound (default panels)
+            exact = not tc_supported(precision, g.K)
             panels = row_panels(g.M, 4 * (g.N * (1 if init else 2) + (g.K if stream_a else 0)),
-                                256)
+                                256, count=8 if exact else None)
             if panels is not None:
                 panels = [(crows[0] + a, crows[0] + b) for a, b in panels]
                 return self._gemm_streamed(g, precision, panels, stream_a, init, init_value,
                                            bias_ptr, bias_stride, shadow_out, shadow_in,
-                                           last_writer, cta, crows[0])
+                                           last_writer, cta, crows[0],
+                                           concurrent=3 if exact else 1)
         tA, tB = s.tensor(g.A), s.tensor(g.B)
         # a fused fill over all of a dense C: its old contents are never read
         tC = s.tensor(g.C, overwrite=bool(init) and dense_c and g.C is not g.A and
@@ -817,7 +849,8 @@ class DeviceBackend:
         warnings.warn(msg, PrecisionFallback, stacklevel=3)
 
     def _gemm_streamed(self, g, precision, panels, stream_a, init, init_value, bias_ptr,
-                       bias_stride, shadow_out, shadow_in, last_writer, cta=None, row0=0):
+                       bias_stride, shadow_out, shadow_in, last_writer, cta=None, row0=0,
+                       concurrent=1):
         """C (+)= A.B over row panels of M with the host copies pipelined
         (Staging.stream_rows): panel p's GEMM overlaps the upload of panel
         p+1 and the write-back of panel p-1.  B is uploaded (and, on the
@@ -827,6 +860,11 @@ class DeviceBackend:
         tB = s.tensor(g.B)
         a_packed = c16 = Bp = None
         tc = tc_supported(precision, g.K)
+        if concurrent > 1 and not tc and cta is None:
+            # concurrent panels share the GPU: keep the whole-tile 128 x 128
+            # kernel (by its own size rule a panel's sub-wave grid would
+            # pick small tiles)
+            cta = (128, 128)
         if not stream_a:
             tA = s.tensor(g.A)
             sh = self._shadow
@@ -851,7 +889,8 @@ class DeviceBackend:
                 c16=c16[q0:q1] if c16 is not None else None, b_packed=Bp,
                 a_packed=a_packed[q0:q1] if a_packed is not None else None, cta=cta)
 
-        s.stream_rows(panels, [g.A] if stream_a else [], (g.C, not init), launch)
+        s.stream_rows(panels, [g.A] if stream_a else [], (g.C, not init), launch,
+                      concurrent=concurrent)
         if last_writer:
             s.dirty.discard(id(g.C))
         self._shadow = None
