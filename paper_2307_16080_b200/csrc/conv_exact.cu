@@ -31,7 +31,10 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "../../include/b200k.h"
+#include "tc_common.cuh"
 
 namespace {
 
@@ -508,6 +511,170 @@ __global__ void __launch_bounds__(kThreads) conv_runs_kernel(ConvArgs<T> g, int 
   }
 }
 
+// TMA-fed runs kernel (f32, 3x3; the default where its tensor maps apply,
+// B200_CONV_EXACT_TMA=0 selects conv_runs_kernel): the same tile, lane
+// mapping and arithmetic, staged differently — each 8-channel chunk is two
+// TMA boxes issued by thread 0 (the input as whole row pairs of the
+// [N][C][H/2][2W] view: single rows of W floats are not 16-byte multiples;
+// the transposed weights as [8 x 9][64]) into a 3-stage ring tracked by
+// mbarriers.  No per-element copy addressing (division by the patch
+// geometry per element in conv_runs_kernel's staging) and no CTA-wide
+// barrier: a warp waits only for the chunk it reads, thread 0 refills a
+// stage once all eight warps released it.  The patch row pitch is W (rows of
+// a pair are back to back), so the ring holds full rows.
+constexpr int TSTG = 3;
+
+template <int PXW>
+__global__ void __launch_bounds__(kThreads) conv_runs_tma_kernel(
+    const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tw,
+    ConvArgs<float> g) {
+  using namespace b200tc;
+  constexpr int KH = 3, KW = 3, TAPS = 9, TWR = 8 * PXW, RUN = PXW + KW - 1;
+  constexpr int PH = PTH + KH - 1;                 // 6 rows = 3 pairs
+  constexpr int W_ELEMS = CC * TAPS * FT;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  unsigned char *gbase = smem_raw + (base - smem_u32(smem_raw));
+  const int W = g.wp;
+  const int in_elems = CC * PH * W;                // [CC][3 pairs][2W]
+  const uint32_t in_bytes = (uint32_t)in_elems * 4u;
+  const uint32_t in_stage = (in_bytes + 127u) & ~127u;
+  const float *in_s = reinterpret_cast<const float *>(gbase);
+  const float *w_s = reinterpret_cast<const float *>(gbase + TSTG * in_stage);
+  const uint32_t sIn = base, sW = base + TSTG * in_stage;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + TSTG * (in_stage + W_ELEMS * 4));
+  const uint32_t bar0 = smem_u32(bars);
+  auto full = [&](int st) { return bar0 + 8u * st; };
+  auto empty = [&](int st) { return bar0 + 8u * (TSTG + st); };
+
+  const int t = threadIdx.x, warp = t / 32, lane = t % 32;
+  const int r = lane / 8, cg = lane % 8;
+  int tile = blockIdx.x;
+  const int tw_i = tile % g.tw_tiles;
+  tile /= g.tw_tiles;
+  const int th_i = tile % g.th_tiles;
+  const int n = tile / g.th_tiles;
+  const int h0 = th_i * PTH, w0 = tw_i * TWR;
+  const int f0 = blockIdx.y * FT;
+  const int fw = f0 + warp * FX;
+  const int chunks = (g.c + CC - 1) / CC;
+  auto issue = [&](int k) {
+    const int st = k % TSTG;
+    mbar_expect_tx(full(st), in_bytes + (uint32_t)W_ELEMS * 4u);
+    // input: pairs h0 / 2 .. + 2 of channels k CC .. + CC - 1 (zero past C / H)
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(sIn + st * in_stage),
+        "l"(reinterpret_cast<uint64_t>(&tin)), "r"(full(st)), "r"(0), "r"(h0 / 2),
+        "r"(k * CC), "r"(n)
+        : "memory");
+    tma_load_2d(&tw, full(st), sW + st * (uint32_t)(W_ELEMS * 4), f0, k * CC * TAPS);
+  };
+  if (t == 0) {
+    for (int st = 0; st < TSTG; ++st) {
+      mbar_init(full(st), 1);
+      mbar_init(empty(st), kThreads / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (t == 0)
+    for (int k = 0; k < TSTG && k < chunks; ++k) issue(k);
+
+  float acc[PXW][FX];
+  const int ho = h0 + r, wo0 = w0 + PXW * cg;
+#pragma unroll
+  for (int j = 0; j < FX; ++j) {
+    const int ff = fw + j;
+    const float *o =
+        g.out + (int64_t)n * g.so[0] + (int64_t)ff * g.so[1] + (int64_t)ho * g.so[2];
+#pragma unroll
+    for (int u = 0; u < PXW; ++u) {
+      const int wo = wo0 + u;
+      acc[u][j] = (!g.init && ho < g.ho && wo < g.wo && ff < g.f) ? o[(int64_t)wo * g.so[3]]
+                                                                  : g.init_value;
+    }
+  }
+
+  for (int k = 0; k < chunks; ++k) {
+    const int st = k % TSTG;
+    const uint32_t ph = (uint32_t)((k / TSTG) & 1);
+    mbar_wait(full(st), ph);
+    const float *is = in_s + st * (in_stage / 4) + r * W + w0 + PXW * cg;
+    const float *ws = w_s + st * W_ELEMS + warp * FX;
+    const int cn = min(CC, g.c - k * CC);
+    for (int cc = 0; cc < cn; ++cc) {
+#pragma unroll
+      for (int ki = 0; ki < KH; ++ki) {
+        float x[RUN];
+        const float *row = is + (cc * PH + ki) * W;
+#pragma unroll
+        for (int u = 0; u < RUN; ++u) x[u] = row[u];
+        const float *wrow = ws + (cc * TAPS + ki * KW) * FT;
+#pragma unroll
+        for (int kj = 0; kj < KW; ++kj) {
+          float wv[FX];
+#pragma unroll
+          for (int j = 0; j < FX; ++j) wv[j] = wrow[kj * FT + j];
+#pragma unroll
+          for (int u = 0; u < PXW; ++u)
+#pragma unroll
+            for (int j = 0; j < FX; ++j)
+              acc[u][j] = __fadd_rn(acc[u][j], __fmul_rn(x[u + kj], wv[j]));
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty(st));
+    if (t == 0 && k + TSTG < chunks) {
+      mbar_wait(empty(st), ph);   // every warp is done with this chunk
+      issue(k + TSTG);
+    }
+  }
+
+  if (ho >= g.ho) return;
+#pragma unroll
+  for (int j = 0; j < FX; ++j) {
+    const int ff = fw + j;
+    if (ff >= g.f) continue;
+    float *o = g.out + (int64_t)n * g.so[0] + (int64_t)ff * g.so[1] + (int64_t)ho * g.so[2];
+#pragma unroll
+    for (int u = 0; u < PXW; ++u)
+      if (wo0 + u < g.wo) o[(int64_t)(wo0 + u) * g.so[3]] = acc[u][j];
+  }
+}
+
+// The runs-TMA kernel's tensor maps, or false where they do not apply
+// (dense even-sized planes with 16-byte strides, rows of <= 128 floats, F a
+// multiple of 4, 16-byte aligned bases).
+bool runs_tma_maps(CUtensorMap *tin, CUtensorMap *tw, const float *in, const int64_t *si,
+                   const float *wt, int64_t nb, int64_t c, int64_t hp, int64_t wp, int64_t f) {
+  using namespace b200tc;
+  if (si[3] != 1 || si[2] != wp || wp % 2 || hp % 2 || 2 * wp > 256 || si[1] % 4 ||
+      si[0] % 4 || f % 4 || (reinterpret_cast<uintptr_t>(in) & 15) ||
+      (reinterpret_cast<uintptr_t>(wt) & 15))
+    return false;
+  EncodeTiled enc = get_encode();
+  if (!enc) return false;
+  const cuuint64_t di[4] = {(cuuint64_t)(2 * wp), (cuuint64_t)(hp / 2), (cuuint64_t)c,
+                            (cuuint64_t)nb};
+  const cuuint64_t sti[3] = {(cuuint64_t)(2 * wp * 4), (cuuint64_t)(si[1] * 4),
+                             (cuuint64_t)(si[0] * 4)};
+  const cuuint32_t bi[4] = {(cuuint32_t)(2 * wp), 3, (cuuint32_t)CC, 1};
+  const cuuint32_t e4[4] = {1, 1, 1, 1};
+  const cuuint64_t dw[2] = {(cuuint64_t)f, (cuuint64_t)(c * 9)};
+  const cuuint64_t stw[1] = {(cuuint64_t)(f * 4)};
+  const cuuint32_t bw[2] = {(cuuint32_t)FT, (cuuint32_t)(CC * 9)};
+  return enc(tin, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(in), di, sti, bi, e4,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+             CUDA_SUCCESS &&
+         enc(tw, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(wt), dw, stw, bw, e4,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+             CUDA_SUCCESS;
+}
+
 // FCHW weights (any strides) -> [C][KH * KW][F], f fastest.
 template <typename T>
 __global__ void transpose_w_kernel(const T *__restrict__ w, int64_t s0, int64_t s1, int64_t s2,
@@ -570,6 +737,23 @@ int launch(const void *in, const int64_t *si, const void *w, const int64_t *sw, 
     gr.th_tiles = (int)((ho + PTH - 1) / PTH);
     gr.tw_tiles = (int)((wo + 55) / 56);
     dim3 rgrid((unsigned)(nb * gr.th_tiles * gr.tw_tiles), (unsigned)((f + FT - 1) / FT));
+    const char *tv = getenv("B200_CONV_EXACT_TMA");   // dev A/B: "0" = cp.async staging
+    if constexpr (std::is_same<T, float>::value) {
+      CUtensorMap tin, tw;
+      if (!(tv && tv[0] == '0') &&
+          runs_tma_maps(&tin, &tw, static_cast<const float *>(in), si,
+                        static_cast<const float *>(w_work), nb, c, hp, wp, f)) {
+        const size_t in_stage = ((size_t)CC * (PTH + 2) * wp * 4 + 127) / 128 * 128;
+        const size_t tsmem = 1024 + TSTG * (in_stage + (size_t)CC * 9 * FT * 4) + 64;
+        if (tsmem <= 227 * 1024) {
+          auto kernel = conv_runs_tma_kernel<7>;
+          cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)tsmem);
+          kernel<<<rgrid, kThreads, tsmem, s>>>(tin, tw, gr);
+          return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
+        }
+      }
+    }
     auto kernel = conv_runs_kernel<T, 3, 3, 7>;
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem);
     kernel<<<rgrid, kThreads, rsmem, s>>>(gr, vec_in, vec_w);
