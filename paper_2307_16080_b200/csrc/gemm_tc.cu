@@ -399,8 +399,14 @@ int gemm_tc(int32_t kind, const void *A, const void *Bt, float *C, int64_t sCm, 
     const int64_t pair_tiles = ((M + 255) / 256) * ((N + 255) / 256);
     variant = pair_tiles >= sms / 2 ? 2 : 1;
   }
-  if (Bkn) return launch_gemm_tc2(kind, A, nullptr, ep, M, N, K, max_ctas / 2, s, Bkn);
-  if (variant == 2) return launch_gemm_tc2(kind, A, Bt, ep, M, N, K, max_ctas / 2, s);
+  if (Bkn) return launch_gemm_tc2(kind, A, nullptr, ep, M, N, K, max_ctas / 2, s, Bkn, false);
+  if (variant == 2) return launch_gemm_tc2(kind, A, Bt, ep, M, N, K, max_ctas / 2, s, nullptr,
+                                           false);
+  // variant 3: 128 x 256 CTA tiles as cta_group::1 MMAs in 2-CTA clusters
+  // sharing the B tile by multicast (gemm_tc2.cu SOLO); variant 1: the
+  // stand-alone single-CTA kernel below
+  if (variant == 3 && !getenv("B200_TC_SOLO_OFF"))
+    return launch_gemm_tc2(kind, A, Bt, ep, M, N, K, max_ctas / 2, s, nullptr, true);
   CUtensorMap ma, mb;
   if (!make_map(&ma, kind, A, M, K, BM) || !make_map(&mb, kind, Bt, N, K, BN))
     return B200_ELAUNCH;

@@ -54,17 +54,42 @@ constexpr int PTHREADS = 256;
 // barriers.  The shadow variant trades one operand stage for two staged
 // shadow chunks (the shadow's TMA stores are coalesced; per-thread row
 // stores of 64 B were not).
-template <bool SH>
+// SOLO (the 128 x 256 CTA tile of (4, 16)-style tilings): each CTA of the
+// cluster runs its own cta_group::1 MMAs on its 128 rows and the cluster's
+// whole 256-column B tile, whose two halves the two CTAs load once and
+// multicast to both — a stage holds all 256 rows of B^T.
+template <bool SH, bool SOLO = false>
 struct Lay {
-  static constexpr int STAGES = SH ? 4 : 5;
+  static constexpr int PBS = SOLO ? 2 * PB : PB;   // B bytes per stage
+  static constexpr int STAGES = SOLO ? 3 : (SH ? 4 : 5);
   static constexpr int NSBUF = SH ? 2 : 0;
-  static constexpr size_t C_OFF = (size_t)STAGES * (PA + PB);
+  static constexpr size_t C_OFF = (size_t)STAGES * (PA + PBS);
   static constexpr size_t S_OFF = C_OFF + NCBUF * CBUF;
   static constexpr size_t BIAS_OFF = S_OFF + NSBUF * SBUF;
   static constexpr size_t BAR_OFF = BIAS_OFF + BIASB;
   static constexpr size_t SMEM = 1024 + BAR_OFF + 256;
 };
 static_assert(Lay<false>::SMEM <= 232448 && Lay<true>::SMEM <= 232448, "smem");
+static_assert(Lay<false, true>::SMEM <= 232448 && Lay<true, true>::SMEM <= 232448, "smem");
+
+// TMA load multicast to every CTA of `mask` (same shared offsets; each
+// destination's barrier at `bar` receives its bytes)
+__device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap *map, uint32_t bar, uint32_t dst,
+                                               int32_t c0, int32_t c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+// single-CTA MMA commit arriving on the same barrier in every CTA of `mask`
+__device__ __forceinline__ void umma_commit_mc(uint32_t bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(bar),
+      "h"(mask)
+      : "memory");
+}
 
 struct Sched {
   int64_t tiles, nt, kb_total, ncl;
@@ -104,7 +129,7 @@ __device__ __forceinline__ bool get_item(const Sched &s, int64_t cid, int64_t i,
   return true;
 }
 
-template <int KIND, bool SH, bool BMN>
+template <int KIND, bool SH, bool BMN, bool SOLO = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tma_a,
                     const __grid_constant__ CUtensorMap tma_b,
@@ -112,8 +137,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
                     const __grid_constant__ CUtensorMap tma_c,
                     const __grid_constant__ CUtensorMap tma_s, int use_tma_c, Epi ep, int64_t M,
                     int64_t N, Sched sch) {
-  using L = Lay<SH>;
+  using L = Lay<SH, SOLO>;
   constexpr int PSTAGES = L::STAGES;
+  static_assert(!(SOLO && BMN), "SOLO reads B K-major");
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   unsigned char *gbase = smem_raw + (base - smem_u32(smem_raw));
@@ -147,11 +173,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < PSTAGES; ++s) {
       mbar_init(full(s), 1);
-      mbar_init(empty(s), 1);
+      // SOLO: a stage's B halves come from both CTAs, so both MMAs release it
+      mbar_init(empty(s), SOLO ? 2 : 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull(a), 1);
-      mbar_init(tempty(a), 256);
+      mbar_init(tempty(a), SOLO ? 128 : 256);
     }
     for (int b = 0; b < NCBUF; ++b) mbar_init(cbar(b), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -159,10 +186,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(512));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    if (SOLO) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(512));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(512));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
   }
   tc_fence_before();
   cluster_sync();
@@ -186,6 +220,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
         const uint32_t bytes = BMN ? 2u * (PA + nbox * CHB) : 2u * (PA + brows * 128);
         const int32_t m0 = (int32_t)(it.m0 + rank * 128);
         const int32_t n0 = (int32_t)(it.n0 + rank * brows);
+        if (SOLO) {
+          // own A rows; this CTA's half of the item's B^T rows to both CTAs
+          const int32_t nh = (int32_t)(it.n0 + rank * brows);
+          for (int64_t kb = 0; kb < kb_total; ++kb) {
+            mbar_wait(empty(s), ph ^ 1);
+            mbar_expect_tx(full(s), (uint32_t)(PA + 2 * brows * 128));
+            tma_load_2d(&tma_a, full(s), sA + s * PA, (int32_t)(kb * BK), m0);
+            tma_load_2d_mc(mb, full(s), sB + s * L::PBS + rank * (uint32_t)(brows * 128),
+                           (int32_t)(kb * BK), nh, (uint16_t)0x3);
+            if (++s == PSTAGES) { s = 0; ph ^= 1; }
+          }
+          continue;
+        }
         for (int64_t kb = 0; kb < kb_total; ++kb) {
           mbar_wait(empty(s), ph ^ 1);
           if (leader) mbar_expect_tx(full(s), bytes);
@@ -203,7 +250,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (leader && lane == 0) {
+    if (SOLO && lane == 0) {
+      // every CTA: 128 x ncols from its own A rows and the shared B tile;
+      // a stage is released to both producers (their multicasts wrote it)
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      Item it;
+      for (int64_t i = 0; get_item(sch, cid, i, it); ++i) {
+        const uint32_t idesc = make_idesc(KIND, 128, it.ncols);
+        mbar_wait(tempty(acc), aph ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + (uint32_t)(acc * 256);
+        for (int64_t kb = 0; kb < kb_total; ++kb) {
+          mbar_wait(full(s), ph);
+          tc_fence_after();
+          const uint32_t a_addr = sA + s * PA, b_addr = sB + s * L::PBS;
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k)
+            umma<KIND, 1>(tmem_d, smem_desc(a_addr + 32 * k), smem_desc(b_addr + 32 * k), idesc,
+                          (kb | k) != 0);
+          umma_commit_mc(empty(s), 0x3);
+          if (++s == PSTAGES) { s = 0; ph ^= 1; }
+        }
+        umma_commit(tfull(acc));
+        if (++acc == 2) { acc = 0; aph ^= 1; }
+      }
+    } else if (!SOLO && leader && lane == 0) {
       int s = 0;
       uint32_t ph = 0;
       int acc = 0;
@@ -316,7 +390,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
       }
       g += 8 - nchunks;  // keep one 8-chunk slot per item (only the last item is narrower)
       tc_fence_before();
-      mbar_arrive_cluster(acc == 0 ? lead_tempty0 : lead_tempty1);
+      if (SOLO)
+        mbar_arrive(tempty(acc));   // this CTA's own accumulator
+      else
+        mbar_arrive_cluster(acc == 0 ? lead_tempty0 : lead_tempty1);
       if (++acc == 2) { acc = 0; aph ^= 1; }
     }
     if (lead_t && use_tma_c) bulk_wait_all();
@@ -325,19 +402,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
   cluster_sync();
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(512));
+    if (SOLO)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(512));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(512));
   }
 }
 
 }  // namespace
 
-template <int KIND, bool SH, bool BMN = false>
+template <int KIND, bool SH, bool BMN = false, bool SOLO = false>
 int launch(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mbs,
            const CUtensorMap &mc, const CUtensorMap &ms, int use_tma_c, const Epi &ep, int64_t M,
            int64_t N, const Sched &sch, int clusters, cudaStream_t s) {
-  constexpr size_t smem = Lay<SH>::SMEM;
-  auto kernel = gemm_tc2_kernel<KIND, SH, BMN>;
+  constexpr size_t smem = Lay<SH, SOLO>::SMEM;
+  auto kernel = gemm_tc2_kernel<KIND, SH, BMN, SOLO>;
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   kernel<<<2 * clusters, PTHREADS, smem, s>>>(ma, mb, mbs, mc, ms, use_tma_c, ep, M, N, sch);
   return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
@@ -364,7 +445,8 @@ bool make_map_kn(CUtensorMap *map, int kind, const void *B, int64_t K, int64_t N
 }
 
 int launch_gemm_tc2(int kind, const void *A, const void *Bt, const Epi &ep, int64_t M, int64_t N,
-                    int64_t K, int max_clusters, cudaStream_t s, const void *Bkn) {
+                    int64_t K, int max_clusters, cudaStream_t s, const void *Bkn, bool solo) {
+  if (solo && Bkn) return B200_EUNSUPPORTED;
   // MN-major operands are a 16-bit-type feature: tf32 B read MN-major came
   // out wrong on the B200 (tools/probe_gemm_kn.py --kind 1), so kind 0 only
   if (Bkn && (kind != 0 || N % 64 != 0)) return B200_EUNSUPPORTED;
@@ -413,6 +495,17 @@ int launch_gemm_tc2(int kind, const void *A, const void *Bt, const Epi &ep, int6
     return sh ? launch<0, true, true>(ma, mb, mbs, mc, ms, use_tma_c, ep, M, N, sch, clusters, s)
               : launch<0, false, true>(ma, mb, mbs, mc, ms, use_tma_c, ep, M, N, sch, clusters,
                                        s);
+  if (solo) {
+    if (kind == 0)
+      return sh ? launch<0, true, false, true>(ma, mb, mbs, mc, ms, use_tma_c, ep, M, N, sch,
+                                               clusters, s)
+                : launch<0, false, false, true>(ma, mb, mbs, mc, ms, use_tma_c, ep, M, N, sch,
+                                                clusters, s);
+    return sh ? launch<1, true, false, true>(ma, mb, mbs, mc, ms, use_tma_c, ep, M, N, sch,
+                                             clusters, s)
+              : launch<1, false, false, true>(ma, mb, mbs, mc, ms, use_tma_c, ep, M, N, sch,
+                                              clusters, s);
+  }
   if (kind == 0)
     return sh ? launch<0, true>(ma, mb, mbs, mc, ms, use_tma_c, ep, M, N, sch, clusters, s)
               : launch<0, false>(ma, mb, mbs, mc, ms, use_tma_c, ep, M, N, sch, clusters, s);

@@ -467,8 +467,10 @@ inline int num_sms() {
 }
 
 // 2-CTA launcher (gemm_tc2.cu).  Bkn (bf16 only): B as a K x N row-major
-// tensor read MN-major, instead of the K-major N x K pack Bt.
+// tensor read MN-major, instead of the K-major N x K pack Bt.  solo: 128 x
+// 256 CTA tiles with cta_group::1 MMAs, the cluster's B tile multicast.
 int launch_gemm_tc2(int kind, const void *A, const void *Bt, const Epi &ep, int64_t M, int64_t N,
-                    int64_t K, int max_clusters, cudaStream_t s, const void *Bkn = nullptr);
+                    int64_t K, int max_clusters, cudaStream_t s, const void *Bkn = nullptr,
+                    bool solo = false);
 
 }  // namespace b200tc

@@ -573,7 +573,7 @@ def launch_gemm(lib, precision, a_ptr, sA, b_ptr, sB, c_ptr, sC, M, N, K, stream
              P(bias_ptr) if bias_ptr else None, bias_stride, stream)
         return ["gemm_f32_exact"]
     if cta is not None:
-        variant = 1 if cta == (128, 256) else 2
+        variant = 3 if cta == (128, 256) else 2
     kind = 0 if precision == "bf16" else 1
     dt = "bfloat16" if kind == 0 else "float32"
     split = precision == "f32x3"      # packed rows hold 3 K-segments (gemm_tc.cu)
@@ -589,8 +589,10 @@ def launch_gemm(lib, precision, a_ptr, sA, b_ptr, sB, c_ptr, sC, M, N, K, stream
     if b_packed is not None:
         Bp, kn = b_packed if isinstance(b_packed, tuple) else (b_packed, False)
     else:
+        # the MN-major B (b200_gemm_tc_kn) is a CTA-pair-only read: not for
+        # the 128 x 256 CTA tile (variants 1 and 3)
         Bp, kn = pack_b(lib, precision, b_ptr, sB, N, K, stream, call,
-                        allow_kn=variant != 1)
+                        allow_kn=variant not in (1, 3))
         names.append("pack_operand")
     if kn:
         call("b200_gemm_tc_kn", kind, P(Ap.data_ptr()), P(Bp.data_ptr()), P(c_ptr), sC[0], sC[1],
