@@ -170,7 +170,13 @@ __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-template <int F, int R, bool FUSED = false>
+// PAIR (fused only, launched as 2-CTA clusters): the two column tiles of a
+// row band run on the two CTAs of a cluster as ONE cta_group::2 MMA
+// (M = 2 x 128 pixels, N = KW x F): each CTA keeps only half of the stacked
+// weight rows (B is split along N across the pair), which frees the shared
+// memory for a third patch stage; each CTA converts its own tile's patch
+// from its own copy of the band; the leader issues the MMAs.
+template <int F, int R, bool FUSED = false, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads + (FUSED ? kConvThreads : 0), 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tma_in,
                    const __grid_constant__ CUtensorMap tma_w,
@@ -191,8 +197,9 @@ __global__ void __launch_bounds__(kThreads + (FUSED ? kConvThreads : 0), 1)
   const int nslices = taps * g.cblocks;
   const int stages = g.stages;
   const uint32_t pstage = (uint32_t)g.pstage;
-  const uint32_t sB = base;                                   // nslices x SLICE
-  const uint32_t sP = base + nslices * SLICE;                 // stages x patch
+  constexpr int WSL = PAIR ? SLICE / 2 : SLICE;  // this CTA's bytes of a weight slice
+  const uint32_t sB = base;                                   // nslices x WSL
+  const uint32_t sP = base + nslices * WSL;                   // stages x patch
   const uint32_t sO = sP + stages * pstage;                   // nout x OUTBUF
   float *gO = reinterpret_cast<float *>(gbase + (sO - base));
   const uint32_t sR = sO + g.nout * OUTBUF;                   // fused: rstages raw chunks
@@ -218,10 +225,13 @@ __global__ void __launch_bounds__(kThreads + (FUSED ? kConvThreads : 0), 1)
   const int lane = threadIdx.x % 32;
   long long st[5] = {0, 0, 0, 0, 0};
   const long long t_start = clock64();
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0;
+  const bool leader = rank == 0;
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < stages; ++s) {
       // fused: the converter warps fill a patch stage and each arrives
-      mbar_init(full(s), FUSED ? kConvThreads / 32 : 1);
+      // (PAIR: both CTAs' converters, on the leader's barrier)
+      mbar_init(full(s), FUSED ? (PAIR ? 2 : 1) * kConvThreads / 32 : 1);
       mbar_init(empty(s), 1);
     }
     if (FUSED)
@@ -231,7 +241,7 @@ __global__ void __launch_bounds__(kThreads + (FUSED ? kConvThreads : 0), 1)
       }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull(a), 1);
-      mbar_init(tempty(a), 256);
+      mbar_init(tempty(a), PAIR ? 512 : 256);   // PAIR: both CTAs' epilogues, on the leader
     }
     for (int b = 0; b < g.nout; ++b) {
       mbar_init(ofull(b), 1);
@@ -241,13 +251,20 @@ __global__ void __launch_bounds__(kThreads + (FUSED ? kConvThreads : 0), 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(TCOLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(TCOLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(TCOLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   // 32-bit tile decomposition (tiles < 2^31, checked on the host): 64-bit
@@ -269,6 +286,10 @@ __global__ void __launch_bounds__(kThreads + (FUSED ? kConvThreads : 0), 1)
   const int64_t twt64 = g.tw_tiles;
   const int64_t nbands = g.tiles / twt64;
   auto tile_at = [&](int64_t i) -> int64_t {   // -1: no more tiles
+    if (PAIR) {   // band cid + i * clusters; this CTA's column tile = its rank
+      const int64_t band = blockIdx.x / 2 + i * (int64_t)(gridDim.x / 2);
+      return band < nbands ? band * twt64 + rank : -1;
+    }
     if (!FUSED) {
       const int64_t t = blockIdx.x + i * (int64_t)gridDim.x;
       return t < g.tiles ? t : -1;
@@ -283,12 +304,29 @@ __global__ void __launch_bounds__(kThreads + (FUSED ? kConvThreads : 0), 1)
       // [(ki * KW + kj) * cp + cb * 64, +64); R == 1 orders slices
       // (tap, cb), R > 1 orders them (ki, cb, kj) so that the KW slices of
       // one (ki, cb) stack into the N = KW * F rows of a single B operand
-      mbar_expect_tx(wbar, (uint32_t)(nslices * SLICE));
-      for (int tap = 0; tap < taps; ++tap) {
-        const int ki = tap / (int)g.kw, kj = tap % (int)g.kw;
-        for (int cb = 0; cb < g.cblocks; ++cb) {
-          const int slot = R == 1 ? tap * g.cblocks + cb : (ki * g.cblocks + cb) * R + kj;
-          tma_load_2d(&tma_w, wbar, sB + slot * SLICE, (int32_t)(tap * g.cp + cb * 64), 0);
+      if (PAIR) {
+        // this CTA's half of each (ki, cb) group's stacked rows (kj, f):
+        // half-slices hs = 2 kj + (f >= F / 2) in [rank R, rank R + R),
+        // counted on the leader's weight barrier (both halves)
+        if (leader) mbar_expect_tx(wbar, (uint32_t)(nslices * SLICE));
+        const uint32_t lw = map_to_rank(wbar, 0);
+        for (int ki = 0; ki < (int)g.kh; ++ki)
+          for (int cb = 0; cb < g.cblocks; ++cb)
+            for (int h = 0; h < R; ++h) {
+              const int hs = (int)rank * R + h, kj = hs / 2, hf = hs % 2;
+              const int tap = ki * (int)g.kw + kj;
+              tma_load_2d_pair(&tma_w, lw,
+                               sB + (ki * g.cblocks + cb) * R * WSL + h * (F / 2) * 128,
+                               (int32_t)(tap * g.cp + cb * 64), hf * (F / 2));
+            }
+      } else {
+        mbar_expect_tx(wbar, (uint32_t)(nslices * SLICE));
+        for (int tap = 0; tap < taps; ++tap) {
+          const int ki = tap / (int)g.kw, kj = tap % (int)g.kw;
+          for (int cb = 0; cb < g.cblocks; ++cb) {
+            const int slot = R == 1 ? tap * g.cblocks + cb : (ki * g.cblocks + cb) * R + kj;
+            tma_load_2d(&tma_w, wbar, sB + slot * SLICE, (int32_t)(tap * g.cp + cb * 64), 0);
+          }
         }
       }
       int s = 0;
@@ -305,7 +343,7 @@ __global__ void __launch_bounds__(kThreads + (FUSED ? kConvThreads : 0), 1)
             // (rstages / 4 buffers): a buffer is only ever waited on by one
             // warp, in order — the mbarrier parity test cannot tell use k
             // from use k - 2, so two warps sharing a buffer would race
-            if (i % twt64 != 0) continue;
+            if (!PAIR && i % twt64 != 0) continue;
             const int pw = g.rstages / 4;
             for (int j = 0; j < 64 / kRawCh; ++j) {
               const int64_t q = (rq++);
@@ -328,7 +366,41 @@ __global__ void __launch_bounds__(kThreads + (FUSED ? kConvThreads : 0), 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (PAIR && lane == 0 && leader) {
+      // one cta_group::2 MMA per (ki, 16 channels): A = each CTA's own
+      // patch (M 2 x 128), B = the (ki, cb) group's stacked rows split across
+      // the pair (N / 2 per CTA); commits reach both CTAs
+      constexpr uint32_t idesc = make_idesc(0, 256, N);
+      mbar_wait_cluster(wbar, 0);
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      for (int64_t i = 0, t; (t = tile_at(i)) >= 0; ++i) {
+        TIMED(2, mbar_wait_cluster(tempty(acc), aph ^ 1));
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + (uint32_t)(acc * N);
+        for (int cb = 0; cb < g.cblocks; ++cb) {
+          TIMED(1, mbar_wait_cluster(full(s), ph));
+          tc_fence_after();
+          const uint64_t a0 = desc_sw128(sP + s * pstage, 1024);
+          uint32_t acc_flag = cb != 0;
+          for (int ki = 0; ki < (int)g.kh; ++ki) {
+            const uint64_t ad = a0 + (uint64_t)ki * g.prow * 8;
+            const uint64_t bd = desc_sw128(sB + (ki * g.cblocks + cb) * R * WSL, 1024);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              umma<0, 2>(tmem_d, ad + 2 * k, bd + 2 * k, idesc, acc_flag);
+              acc_flag = 1;
+            }
+          }
+          umma_commit_pair(empty(s), 0x3);
+          if (++s == stages) { s = 0; ph ^= 1; }
+        }
+        umma_commit_pair(tfull(acc), 0x3);
+        if (++acc == 2) { acc = 0; aph ^= 1; }
+      }
+    } else if (!PAIR && lane == 0) {
       constexpr uint32_t idesc = make_idesc(0, 128, N);
       // 8-pixel M groups: one patch row apart (R == 1), or back to back
       // (R > 1: two groups per 16-pixel patch row)
@@ -423,7 +495,9 @@ __global__ void __launch_bounds__(kThreads + (FUSED ? kConvThreads : 0), 1)
     constexpr int NCH = 64 / kRawCh;   // chunks per 64-channel patch (cblocks == 1)
     const int npairs = g.ph * ROWLEN / 2;
     const int cstride = g.npair * g.blen;   // floats between a chunk's channels
-    const int twt = (int)twt64;
+    // the band's tiles this CTA converts: all of them, or (PAIR) its own
+    const int twt = PAIR ? 1 : (int)twt64;
+    const int tx0 = PAIR ? (int)rank : 0;
     int s = 0;
     uint32_t ph = 0;
     int64_t bi = 0;   // band index of this CTA's stream
@@ -442,7 +516,7 @@ __global__ void __launch_bounds__(kThreads + (FUSED ? kConvThreads : 0), 1)
         const float *raw = gR + rs * (g.raw_bytes / 4);
         for (int tx = 0, ss = s; tx < twt; ++tx) {
           unsigned char *patch = gbase + (sP - base) + ss * pstage;
-          const int w0 = tx * g.tw;
+          const int w0 = (tx0 + tx) * g.tw;
           for (int tp = lane; tp < npairs; tp += 32) {
             const int p = 2 * tp;
             const int y = p / ROWLEN, x = p % ROWLEN;
@@ -468,7 +542,12 @@ __global__ void __launch_bounds__(kThreads + (FUSED ? kConvThreads : 0), 1)
       fence_proxy_async();   // generic-proxy stores -> the tensor cores' reads
       __syncwarp();
       for (int k = 0; k < twt; ++k) {
-        if (lane == 0) mbar_arrive(full(s));
+        if (lane == 0) {
+          if (PAIR)
+            mbar_arrive_cluster(map_to_rank(full(s), 0));   // the leader issues the MMA
+          else
+            mbar_arrive(full(s));
+        }
         if (++s == stages) { s = 0; ph ^= 1; }
       }
       if (lane == 0) TRACE(cw == 0 ? 1 : 4 + cw, (int)(i + twt));
@@ -492,7 +571,10 @@ __global__ void __launch_bounds__(kThreads + (FUSED ? kConvThreads : 0), 1)
       tile_coords(t, n, h0, w0);
       const bool valid = lane_ok && h0 + hr < g.ho && w0 + wc < g.wo;
       float *const o = out + n * g.so_n + (h0 + hr) * g.so_h + (w0 + wc) * g.so_w;
-      TIMED(3, mbar_wait(tfull(acc), aph));
+      if (PAIR)
+        TIMED(3, mbar_wait_cluster(tfull(acc), aph));
+      else
+        TIMED(3, mbar_wait(tfull(acc), aph));
       tc_fence_after();
       // staged: this pixel's [c][row][col] slot of the TMA-loaded block,
       // updated in place and stored back by TMA
@@ -540,7 +622,10 @@ __global__ void __launch_bounds__(kThreads + (FUSED ? kConvThreads : 0), 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(tempty(acc));
+      if (PAIR)
+        mbar_arrive_cluster(map_to_rank(tempty(acc), 0));
+      else
+        mbar_arrive(tempty(acc));
       if (++acc == 2) { acc = 0; aph ^= 1; }
       if (threadIdx.x == 128) TRACE(3, (int)i * 2 + 1);
       if (g.nout > 0) {
@@ -582,11 +667,15 @@ __global__ void __launch_bounds__(kThreads + (FUSED ? kConvThreads : 0), 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync(); else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(TCOLS));
+    if (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(TCOLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(TCOLS));
   }
 }
 
@@ -884,15 +973,17 @@ int conv_merge(int64_t f, int64_t kw) {
 // output blocks of `outbuf` bytes, barriers, alignment).  Mirrored by
 // runtime.conv_tc_supported (2 stages, no staged output blocks).
 size_t conv_smem(int64_t f, int64_t kh, int64_t kw, int64_t cp, int64_t pstage, int stages,
-                 int nout, int64_t outbuf, int64_t raw_bytes = 0, int rstages = 0) {
-  return 1024 + kh * kw * (cp / 64) * f * 128 + stages * pstage + nout * outbuf +
+                 int nout, int64_t outbuf, int64_t raw_bytes = 0, int rstages = 0,
+                 bool pair = false) {
+  return 1024 + kh * kw * (cp / 64) * f * 128 / (pair ? 2 : 1) + stages * pstage +
+         nout * outbuf +
          rstages * raw_bytes + 512;   // barriers (39 x 8 bytes) + the TMEM slot
 }
 
 // FUSED: `in` is the NCHW f32 input itself (dense planes; see
 // b200_conv2d_tc_fused), read by TMA as [N][C][H * W] and converted in the
 // kernel; otherwise `in` is the NHWC bf16 repack.
-template <int F, int R, bool FUSED = false>
+template <int F, int R, bool FUSED = false, bool PAIR = false>
 int launch_conv(const void *in, const int64_t *in_strides, const void *wt, float *out,
                 ConvGeo &g, cudaStream_t s) {
   using T = Tiling<F, R>;
@@ -903,7 +994,7 @@ int launch_conv(const void *in, const int64_t *in_strides, const void *wt, float
   const int rmin = FUSED ? 4 : 0;
   auto smem_of = [&](int stages, int nout, int rst = -1) {
     return conv_smem(F, g.kh, g.kw, g.cp, g.pstage, stages, nout, T::OUTBUF, raw,
-                     rst < 0 ? rmin : rst);
+                     rst < 0 ? rmin : rst, PAIR);
   };
   CUtensorMap mi, mw, mo;
   if (FUSED) {
@@ -926,7 +1017,8 @@ int launch_conv(const void *in, const int64_t *in_strides, const void *wt, float
                      CU_TENSOR_MAP_SWIZZLE_128B))
       return B200_ELAUNCH;
   }
-  if (!make_map(&mw, 0, wt, F, g.kh * g.kw * g.cp, F)) return B200_ELAUNCH;
+  // PAIR: each CTA loads half-slices of F / 2 rows
+  if (!make_map(&mw, 0, wt, F, g.kh * g.kw * g.cp, PAIR ? F / 2 : F)) return B200_ELAUNCH;
   if (smem_of(2, 0) > kSmemMax) return B200_EUNSUPPORTED;
   // output blocks staged through shared memory (TMA load, in-place update,
   // TMA store) when the NCHW output is a legal tensor map: 16-byte aligned
@@ -961,12 +1053,16 @@ int launch_conv(const void *in, const int64_t *in_strides, const void *wt, float
   }
   while (smem_of(g.stages, g.nout, g.rstages) > kSmemMax) --g.stages;
   const size_t smem = smem_of(g.stages, g.nout, g.rstages);
-  if (FUSED && g.stages < g.tw_tiles) return B200_EUNSUPPORTED;   // a band's patches
+  if (FUSED && !PAIR && g.stages < g.tw_tiles) return B200_EUNSUPPORTED;   // a band's patches
   int ctas = num_sms();
   const int64_t units = FUSED ? g.tiles / g.tw_tiles : g.tiles;   // fused: row bands
-  if (units < ctas) ctas = (int)units;
-  cudaFuncSetAttribute(conv_tc_kernel<F, R, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)smem);
+  if (PAIR) {
+    ctas = 2 * (int)(units < num_sms() / 2 ? units : num_sms() / 2);   // clusters of 2
+  } else if (units < ctas) {
+    ctas = (int)units;
+  }
+  cudaFuncSetAttribute(conv_tc_kernel<F, R, FUSED, PAIR>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (getenv("B200_CONV_TRACE")) {   // dev: progress counters the host can read while it runs
     static int *host_trace = nullptr;
     if (!host_trace) cudaHostAlloc(&host_trace, 8 * 1024 * sizeof(int), cudaHostAllocMapped);
@@ -981,8 +1077,24 @@ int launch_conv(const void *in, const int64_t *in_strides, const void *wt, float
     cudaMalloc(&g.stats, 16 * sizeof(unsigned long long));
     cudaMemsetAsync(g.stats, 0, 16 * sizeof(unsigned long long), s);
   }
-  conv_tc_kernel<F, R, FUSED>
-      <<<ctas, kThreads + (FUSED ? kConvThreads : 0), smem, s>>>(mi, mw, mo, out, g);
+  if (PAIR) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)ctas);
+    cfg.blockDim = dim3(kThreads + kConvThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, conv_tc_kernel<F, R, FUSED, PAIR>, mi, mw, mo, out, g);
+  } else {
+    conv_tc_kernel<F, R, FUSED>
+        <<<ctas, kThreads + (FUSED ? kConvThreads : 0), smem, s>>>(mi, mw, mo, out, g);
+  }
   if (stats) {
     unsigned long long h[16];
     cudaMemcpyAsync(h, g.stats, sizeof(h), cudaMemcpyDeviceToHost, s);
@@ -1197,9 +1309,21 @@ extern "C" int b200_conv2d_tc_fused(const float *in, const int64_t *in_strides, 
     return B200_EUNSUPPORTED;
   g.raw_bytes = kRawCh * g.npair * g.blen * 4;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // the CTA-pair variant (opt-in, B200_CONV_PAIR=1) needs both column tiles
+  // of every band.  Measured at N = 256: 217 us against 160 for one CTA per
+  // band — the freed shared memory buys a third patch stage, but the pair's
+  // MMA couples the two CTAs' epilogues (the leader waits for the slower
+  // one's TMEM release: 116 of 183 kcycles) and their output-block loads
+  // queue behind each other (epilogue wait-out 105 vs 43 kcycles)
+  const char *pe = getenv("B200_CONV_PAIR");
+  const bool pair = g.tw_tiles == 2 && pe && pe[0] == '1';
   switch (f * 16 + R) {
-    case 32 * 16 + 3: return launch_conv<32, 3, true>(in, in_strides, wt, out, g, s);
-    case 64 * 16 + 3: return launch_conv<64, 3, true>(in, in_strides, wt, out, g, s);
+    case 32 * 16 + 3:
+      return pair ? launch_conv<32, 3, true, true>(in, in_strides, wt, out, g, s)
+                  : launch_conv<32, 3, true>(in, in_strides, wt, out, g, s);
+    case 64 * 16 + 3:
+      return pair ? launch_conv<64, 3, true, true>(in, in_strides, wt, out, g, s)
+                  : launch_conv<64, 3, true>(in, in_strides, wt, out, g, s);
     default: return B200_EUNSUPPORTED;
   }
 }

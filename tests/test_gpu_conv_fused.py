@@ -57,7 +57,11 @@ def _run_both(nb, c, f, ho, wo, init=0, seed=0):
     (4, 32, 32, 20, 30), (5, 64, 32, 56, 56), (3, 48, 64, 16, 24), (2, 64, 64, 12, 20),
 ])
 @pytest.mark.parametrize("init", [0, 1])
-def test_fused_equals_repack_path(nb, c, f, ho, wo, init):
+@pytest.mark.parametrize("pair", ["0", "1"])
+def test_fused_equals_repack_path(nb, c, f, ho, wo, init, pair, monkeypatch):
+    """pair "1": the opt-in CTA-pair variant (B200_CONV_PAIR=1: the band's two
+    column tiles as one cta_group::2 MMA, weights split across the pair)."""
+    monkeypatch.setenv("B200_CONV_PAIR", pair)
     rc, a, b = _run_both(nb, c, f, ho, wo, init)
     assert rc == 0
     assert bool((a == b).all()), f"max diff {(a - b).abs().max().item()}"
