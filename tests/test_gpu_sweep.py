@@ -78,3 +78,30 @@ def test_resident_trials_equal_host_copied_trials(fn, monkeypatch):
     monkeypatch.setattr(sweep, "RESIDENT", True)
     _, dev_log = sweep.search(fn.module, None, space, **kw)
     assert dev_log == host_log
+
+
+def test_guard_failure_raises_the_reference_error(monkeypatch):
+    """Resident trials (device clones, guard on the device): a baseline that
+    no trial can match must raise the reference's StaircaseError."""
+    from staircase.errors import StaircaseError
+    from staircase.tuner import ParamSpace
+
+    from paper_2307_16080_b200 import sweep
+
+    orig = sweep._session_class
+
+    def patched():
+        S, ref = orig()
+
+        class Perturbed(S):
+            def __init__(self, *a, **k):
+                super().__init__(*a, **k)
+                self.want_args[-1].data[0] += 1.0   # the baseline output, one element
+
+        return Perturbed, ref
+
+    monkeypatch.setattr(sweep, "_session_class", patched)
+    space = ParamSpace(tile_sizes=([1, 2, 4],) * 2, unroll_factors=[1, 2])
+    with pytest.raises(StaircaseError, match="changed the results"):
+        sweep.search(corpus.matmul_par.module, None, space, budget=6, seed=0,
+                     strategy="grid", rank=0, world=1)
