@@ -59,15 +59,40 @@ extern "C" int b200_mt_uniform(uint32_t *state, int32_t *pos, int64_t n, double 
   // (hi - lo) * r then + lo, two rounded double ops as CPython evaluates
   // them (the build passes -ffp-contract=off to the host compiler)
   const double span = hi - lo;
-  for (int64_t i = 0; i < n; ++i) {
-    const uint32_t a = draw(state, p) >> 5, b = draw(state, p) >> 6;
-    const double r = ((double)a * 67108864.0 + (double)b) * (1.0 / 9007199254740992.0);
+  auto value = [&](uint32_t a, uint32_t b) {
+    const double r = ((double)(a >> 5) * 67108864.0 + (double)(b >> 6)) *
+                     (1.0 / 9007199254740992.0);
     const double scaled = span * r;
-    const double v = lo + scaled;
+    return lo + scaled;
+  };
+  auto store = [&](int64_t i, double v) {
     if (dtype == B200_F32)
       static_cast<float *>(out)[i] = (float)v;
     else
       static_cast<double *>(out)[i] = v;
+  };
+  int64_t i = 0;
+  // whole blocks: twist, temper all 624 words at once (a vectorisable loop),
+  // then turn word pairs into values; a value whose two draws straddle a
+  // block boundary is assembled by the scalar path
+  uint32_t tw[kN];
+  while (i < n) {
+    if (p == kN && n - i >= kN / 2) {
+      twist(state);
+      for (int k = 0; k < kN; ++k) {
+        uint32_t y = state[k];
+        y ^= y >> 11;
+        y ^= (y << 7) & 0x9d2c5680u;
+        y ^= (y << 15) & 0xefc60000u;
+        y ^= y >> 18;
+        tw[k] = y;
+      }
+      for (int k = 0; k < kN / 2; ++k) store(i + k, value(tw[2 * k], tw[2 * k + 1]));
+      i += kN / 2;
+      continue;   // p stays kN: the next block twists again
+    }
+    const uint32_t a = draw(state, p), b = draw(state, p);
+    store(i++, value(a, b));
   }
   *pos = p;
   return B200_OK;
