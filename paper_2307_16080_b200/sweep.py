@@ -39,6 +39,7 @@ from __future__ import annotations
 
 import itertools
 import math
+import os
 import random
 
 import numpy as np
@@ -389,7 +390,7 @@ def _session_class():
 DEVICE_REPS = 5
 # resident trial inputs on the B200 engine (B200_SWEEP_RESIDENT=0: every trial
 # copies its inputs on the host and uploads them, as the reference copies)
-RESIDENT = __import__("os").environ.get("B200_SWEEP_RESIDENT", "1") != "0"
+RESIDENT = os.environ.get("B200_SWEEP_RESIDENT", "1") != "0"
 _TORCH_DT = {"f32": "float32", "f64": "float64", "i32": "int32", "i64": "int64"}
 
 
