@@ -272,6 +272,16 @@ int b200_mt_uniform(uint32_t *state, int32_t *pos, int64_t n, double lo, double 
                     int32_t dtype);
 
 /*
+ * A strided host <-> device block copy (cudaMemcpy2DAsync): `rows` rows of
+ * `width` bytes, row pitches `dpitch` / `spitch` bytes; kind 1 = host to
+ * device, 2 = device to host; enqueued on `stream`.  Used to stream column
+ * panels of B and (row, column) blocks of C around the exact GEMM (replaces
+ * the per-run Buffer upload / write-back of interp/buffer.py for those).
+ */
+int b200_copy2d(void *dst, int64_t dpitch, const void *src, int64_t spitch, int64_t width,
+                int64_t rows, int32_t kind, void *stream);
+
+/*
  * Runtime specialisation (NVRTC, sm_100a): compile generated CUDA C `src`
  * and return the kernel `kernel` as an opaque handle in *fn.  The engine
  * generates straight-line kernels for region shapes whose generic execution

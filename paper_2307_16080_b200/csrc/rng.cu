@@ -97,3 +97,23 @@ extern "C" int b200_mt_uniform(uint32_t *state, int32_t *pos, int64_t n, double 
   *pos = p;
   return B200_OK;
 }
+
+// Strided host <-> device block copies for the streamed GEMMs (one
+// cudaMemcpy2DAsync per block: column panels of B and (row, column) blocks of
+// C are not contiguous, and a framework copy of a non-contiguous host view
+// would first gather it on the host).  kind 1: host -> device, 2: device ->
+// host; pitches and width in bytes; host memory page-locked for overlap.
+#include <cuda_runtime.h>
+
+extern "C" int b200_copy2d(void *dst, int64_t dpitch, const void *src, int64_t spitch,
+                           int64_t width, int64_t rows, int32_t kind, void *stream) {
+  if (!dst || !src || width < 0 || rows < 0 || dpitch < width || spitch < width ||
+      (kind != 1 && kind != 2))
+    return B200_EINVAL;
+  if (width == 0 || rows == 0) return B200_OK;
+  const cudaError_t e = cudaMemcpy2DAsync(
+      dst, (size_t)dpitch, src, (size_t)spitch, (size_t)width, (size_t)rows,
+      kind == 1 ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost,
+      static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? B200_OK : B200_ELAUNCH;
+}

@@ -49,6 +49,7 @@ _F32 = ctypes.c_float
 
 SIGNATURES = {
     "b200_mt_uniform": [_P, _P, _I64, ctypes.c_double, ctypes.c_double, _P, _I32],
+    "b200_copy2d": [_P, _I64, _P, _I64, _I64, _I64, _I32, _P],
     "b200_vm_run": [_P, _I32, _P, _P, _I32, _I32, _P, _I32, _I32, _P, _P, _P, _P,
                     _I32, _P, _P, _P],
     "b200_gemm_f32_exact": [_P, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64, _I64,
@@ -644,6 +645,8 @@ def pack_b(lib, precision, b_ptr, sB, N, K, stream, call=None, allow_kn=True):
 # Host-copy pipelining (Staging.stream_rows): only when the streamed bytes
 # are worth several panels; each panel ~32 MB of traffic, 2..8 panels.
 STREAM_MIN_BYTES = 48 << 20
+# exact GEMMs stream B by column panels too (B200_STREAM_2D=0: row panels only)
+STREAM_2D = os.environ.get("B200_STREAM_2D", "1") != "0"
 STREAM_PANEL_BYTES = 32 << 20
 
 
@@ -805,6 +808,12 @@ class DeviceBackend:
                                 256, count=8 if exact else None)
             if panels is not None:
                 panels = [(crows[0] + a, crows[0] + b) for a, b in panels]
+                if (exact and stream_a and STREAM_2D and not s.staged(g.B) and
+                        g.B is not bias and g.B is not g.A and crows[0] == 0 and
+                        _gemm_rows(g.B, g.offB, g.sB, g.K, g.N) == (0, g.K) and
+                        self._owned(g.B, 0, g.K) and g.N % 256 == 0):
+                    return self._gemm_streamed_2d(g, init, init_value, bias, bias_base,
+                                                  bias_stride, last_writer)
                 return self._gemm_streamed(g, precision, panels, stream_a, init, init_value,
                                            bias_ptr, bias_stride, shadow_out, shadow_in,
                                            last_writer, cta, crows[0],
@@ -849,6 +858,96 @@ class DeviceBackend:
         if engine.STRICT:
             raise PrecisionUnavailable(msg)
         warnings.warn(msg, PrecisionFallback, stacklevel=3)
+
+    def _gemm_streamed_2d(self, g, init, init_value, bias, bias_base, bias_stride,
+                          last_writer, mpanels=4, npanels=2, concurrent=3):
+        """Exact C (+)= A.B with A, B and C streamed in blocks: B in column
+        panels, A in row panels, C in (row, column) blocks.  The first GEMM
+        block waits only for B's first column panel, A's first rows and C's
+        first block (44 of 192 MiB at 4096^3) instead of all of B; blocks run
+        three at a time on side streams (whole-tile 128 x 128 kernel) while
+        later blocks upload and finished ones write back.  Each output keeps
+        its full k-chain: bit-identical to the unblocked kernel."""
+        s = self.stage
+        torch = s.torch
+        env = os.environ.get("B200_STREAM_2D_SHAPE")   # dev A/B: "m,n,concurrent"
+        if env:
+            mpanels, npanels, concurrent = (int(v) for v in env.split(","))
+        cur = torch.cuda.current_stream()
+        up, down = _copy_streams(torch)
+        up.wait_stream(cur)
+        comp = _compute_streams(torch, concurrent)
+        for cs in comp:
+            cs.wait_stream(cur)
+        views = {}
+        for name, buf in (("A", g.A), ("B", g.B), ("C", g.C)):
+            host = s.host(buf)
+            pin_host(buf.data, host)
+            t = torch.empty_like(host, device="cuda")
+            s.dev[id(buf)] = (buf, t)
+            views[name] = (host.view(buf.shape[0], -1), t.view(buf.shape[0], -1))
+        (hA, tA), (hB, tB), (hC, tC) = views["A"], views["B"], views["C"]
+        M, N, K = g.M, g.N, g.K
+        ms = -(-M // mpanels)
+        ms = -(-ms // 128) * 128
+        rows = [(r, min(M, r + ms)) for r in range(0, M, ms)]
+        ns = N // npanels // 128 * 128 or N
+        cols = [(c, min(N, c + ns) if c + ns < N else N) for c in range(0, N, ns)]
+        cols = [(c0, c1) for c0, c1 in cols if c0 < c1]
+        if cols[-1][1] < N:
+            cols[-1] = (cols[-1][0], N)
+        bias_t = s.tensor(bias) if bias is not None else None
+        P = ctypes.c_void_p
+        esz = 4
+        k = 0
+        lib = s.lib
+        upp = ctypes.c_void_p(up.cuda_stream)
+        downp = ctypes.c_void_p(down.cuda_stream)
+
+        def block(dst, src, c0, c1, r0, r1, kind, stream):
+            # rows r0..r1-1, columns c0..c1-1 of two N-wide row-major views
+            check(lib.b200_copy2d(P(dst.data_ptr() + esz * (r0 * N + c0)), N * esz,
+                                  P(src.data_ptr() + esz * (r0 * N + c0)), N * esz,
+                                  (c1 - c0) * esz, r1 - r0, kind, stream), "b200_copy2d")
+
+        for j, (c0, c1) in enumerate(cols):
+            block(tB, hB, c0, c1, 0, K, 1, upp)
+            s._count(h2d=K * (c1 - c0) * esz)
+            for r0, r1 in rows:
+                if j == 0:
+                    with torch.cuda.stream(up):
+                        tA[r0:r1].copy_(hA[r0:r1], non_blocking=True)
+                    s._count(h2d=(r1 - r0) * K * esz)
+                if not init:
+                    block(tC, hC, c0, c1, r0, r1, 1, upp)
+                    s._count(h2d=(r1 - r0) * (c1 - c0) * esz)
+                ev = torch.cuda.Event()
+                ev.record(up)
+                cs = comp[k % len(comp)]
+                k += 1
+                cs.wait_event(ev)
+                with torch.cuda.stream(cs):
+                    bp = (bias_t.data_ptr() + esz * (bias_base + c0 * bias_stride)
+                          if bias_t is not None else None)
+                    self.call("b200_gemm_f32_exact_tiled", P(tA[r0].data_ptr()), K, 1,
+                              P(tB[0, c0:].data_ptr()), N, 1, P(tC[r0, c0:].data_ptr()), N, 1,
+                              r1 - r0, c1 - c0, K, init, init_value, P(bp) if bp else None,
+                              bias_stride, 128, 128, ctypes.c_void_p(cs.cuda_stream))
+                    done = torch.cuda.Event()
+                    done.record(cs)
+                down.wait_event(done)
+                block(hC, tC, c0, c1, r0, r1, 2, downp)
+                s._count(d2h=(r1 - r0) * (c1 - c0) * esz)
+                s.panels += 1
+        for cs in comp:
+            cur.wait_stream(cs)
+        s._wb_event = torch.cuda.Event()
+        s._wb_event.record(down)
+        cur.wait_event(s._wb_event)
+        if last_writer:
+            s.dirty.discard(id(g.C))
+        self._shadow = None
+        return ["gemm_f32_exact"]
 
     def _gemm_streamed(self, g, precision, panels, stream_a, init, init_value, bias_ptr,
                        bias_stride, shadow_out, shadow_in, last_writer, cta=None, row0=0,

@@ -96,3 +96,22 @@ def test_streamed_write_back_before_a_later_writer_matches_the_oracle(monkeypatc
     assert t_got == t_want
     for g, w in zip(got, want):
         assert g.data.tobytes() == w.data.tobytes()
+
+
+@pytest.mark.parametrize("name", ["mm1024", "ls512"])
+def test_block_streamed_exact_gemm_equals_row_panels(name, monkeypatch):
+    """The exact GEMM streamed in (row, column) blocks (B by column panels,
+    runtime._gemm_streamed_2d) equals the row-panel pipeline and the
+    unstreamed run bit for bit, tally included."""
+    from paper_2307_16080_b200 import runtime
+
+    fn = _fn(name)
+    want, t_want, plan_want, _ = _run(fn, "exact", False, monkeypatch)
+    monkeypatch.setattr(runtime, "STREAM_2D", False)
+    rows, t_rows, _, p_rows = _run(fn, "exact", True, monkeypatch)
+    monkeypatch.setattr(runtime, "STREAM_2D", True)
+    blocks, t_blocks, plan, p_blocks = _run(fn, "exact", True, monkeypatch)
+    assert p_rows >= 2 and p_blocks >= 2
+    assert plan == plan_want and t_blocks == t_rows == t_want
+    for g, r, w in zip(blocks, rows, want):
+        assert g.data.tobytes() == r.data.tobytes() == w.data.tobytes()
