@@ -808,7 +808,7 @@ class DeviceBackend:
                                 256, count=8 if exact else None)
             if panels is not None:
                 panels = [(crows[0] + a, crows[0] + b) for a, b in panels]
-                if (exact and stream_a and STREAM_2D and not s.staged(g.B) and
+                if (exact and stream_a and STREAM_2D and not s.rows and not s.staged(g.B) and
                         g.B is not bias and g.B is not g.A and crows[0] == 0 and
                         _gemm_rows(g.B, g.offB, g.sB, g.K, g.N) == (0, g.K) and
                         self._owned(g.B, 0, g.K) and g.N % 256 == 0):
