@@ -282,6 +282,16 @@ int b200_copy2d(void *dst, int64_t dpitch, const void *src, int64_t spitch, int6
                 int64_t rows, int32_t kind, void *stream);
 
 /*
+ * The tuner's equivalence guard (replaces the per-element
+ * math.isclose(got, want, rel_tol=1e-6, abs_tol=1e-9) loop of
+ * reference tuner/search.py:128-138): adds to *bad (device counter) the
+ * number of the n elements of `got` (B200_F32 / B200_F64, device) that are not
+ * close to `want` (device, f64).
+ */
+int b200_guard_close(int32_t dtype, const void *got, const double *want, int64_t n,
+                     double rel_tol, double abs_tol, unsigned long long *bad, void *stream);
+
+/*
  * Runtime specialisation (NVRTC, sm_100a): compile generated CUDA C `src`
  * and return the kernel `kernel` as an opaque handle in *fn.  The engine
  * generates straight-line kernels for region shapes whose generic execution

@@ -182,3 +182,53 @@ extern "C" int b200_map_f32(const int32_t *prog, int32_t n_words, const float *c
   dispatch_nl(p, vector != 0, nd == 1, nload, (unsigned)blocks, s);
   return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
 }
+
+// ---------------------------------------------------------------------------
+// The tuner's equivalence guard on the device (sweep.py): counts the
+// elements of a trial's buffer that are NOT math.isclose(got, want,
+// rel_tol, abs_tol) (reference tuner/search.py:128-138): equal values
+// (infinities included) are close; otherwise both must be finite and
+// |got - want| <= max(rel_tol * max(|got|, |want|), abs_tol); NaN is never
+// close.  got: f32 or f64 (the trial's device copy), want: f64 (the
+// baseline, cached on the device); the count is atomically added to *bad.
+namespace {
+
+template <typename T>
+__global__ void guard_close_kernel(const T *__restrict__ got, const double *__restrict__ want,
+                                   int64_t n, double rel, double abs_tol,
+                                   unsigned long long *bad) {
+  unsigned long long mine = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double g = (double)got[i], w = want[i];
+    bool ok = g == w;
+    if (!ok && isfinite(g) && isfinite(w)) {
+      const double tol = fmax(rel * fmax(fabs(g), fabs(w)), abs_tol);
+      ok = fabs(g - w) <= tol;
+    }
+    mine += ok ? 0 : 1;
+  }
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_down_sync(0xffffffffu, mine, o);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(bad, mine);
+}
+
+}  // namespace
+
+extern "C" int b200_guard_close(int32_t dtype, const void *got, const double *want, int64_t n,
+                                double rel_tol, double abs_tol, unsigned long long *bad,
+                                void *stream) {
+  if (n < 0 || (n > 0 && (!got || !want || !bad))) return B200_EINVAL;
+  if (n == 0) return B200_OK;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (dtype == B200_F32)
+    guard_close_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(
+        static_cast<const float *>(got), want, n, rel_tol, abs_tol, bad);
+  else if (dtype == B200_F64)
+    guard_close_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(
+        static_cast<const double *>(got), want, n, rel_tol, abs_tol, bad);
+  else
+    return B200_EINVAL;
+  return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
+}

@@ -50,6 +50,7 @@ _F32 = ctypes.c_float
 SIGNATURES = {
     "b200_mt_uniform": [_P, _P, _I64, ctypes.c_double, ctypes.c_double, _P, _I32],
     "b200_copy2d": [_P, _I64, _P, _I64, _I64, _I64, _I32, _P],
+    "b200_guard_close": [_I32, _P, _P, _I64, ctypes.c_double, ctypes.c_double, _P, _P],
     "b200_vm_run": [_P, _I32, _P, _P, _I32, _I32, _P, _I32, _I32, _P, _P, _P, _P,
                     _I32, _P, _P, _P],
     "b200_gemm_f32_exact": [_P, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64, _I64,

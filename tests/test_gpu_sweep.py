@@ -105,3 +105,39 @@ def test_guard_failure_raises_the_reference_error(monkeypatch):
     with pytest.raises(StaircaseError, match="changed the results"):
         sweep.search(corpus.matmul_par.module, None, space, budget=6, seed=0,
                      strategy="grid", rank=0, world=1)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_native_guard_is_math_isclose(dtype):
+    """b200_guard_close counts exactly the elements math.isclose(g, w,
+    rel_tol=1e-6, abs_tol=1e-9) rejects (reference tuner/search.py:128-138),
+    special values included."""
+    import ctypes
+    import math
+
+    import numpy as np
+    import torch
+
+    from paper_2307_16080_b200 import runtime
+
+    inf, nan = float("inf"), float("nan")
+    pairs = [(1.0, 1.0), (1.0, 1.0 + 1e-7), (1.0, 1.0 + 1e-5), (0.0, 5e-10), (0.0, 2e-9),
+             (-0.0, 0.0), (inf, inf), (-inf, inf), (inf, 1e308), (nan, nan), (nan, 1.0),
+             (1e30, 1e30 * (1 + 5e-7)), (1e30, 1e30 * (1 + 2e-6)), (-3.5, -3.5), (2.0, -2.0)]
+    rng = np.random.default_rng(1)
+    extra = rng.uniform(-2, 2, 2000)
+    pairs += [(float(v), float(v) * (1 + d)) for v, d in zip(extra, rng.uniform(-3e-6, 3e-6,
+                                                                          2000))]
+    npdt = np.float32 if dtype == "f32" else np.float64
+    g = np.array([p[0] for p in pairs], dtype=npdt)
+    w = np.array([p[1] for p in pairs], dtype=npdt).astype(np.float64)
+    want_bad = sum(not math.isclose(float(a), float(b), rel_tol=1e-6, abs_tol=1e-9)
+                   for a, b in zip(g.astype(np.float64), w))
+    tg, tw = torch.from_numpy(g).cuda(), torch.from_numpy(w).cuda()
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    P = ctypes.c_void_p
+    rc = runtime.load_library().b200_guard_close(
+        0 if dtype == "f32" else 1, P(tg.data_ptr()), P(tw.data_ptr()), tg.numel(), 1e-6, 1e-9,
+        P(bad.data_ptr()), P(torch.cuda.current_stream().cuda_stream))
+    assert rc == 0
+    assert int(bad.item()) == want_bad > 0

@@ -38,7 +38,7 @@ def main():
         prof.disable()
         print(f"== {fn.__name__}: {budget} trials, trials {timing.get('trials_s'):.3f} s",
               flush=True)
-        pstats.Stats(prof).sort_stats("cumulative").print_stats(28)
+        pstats.Stats(prof).sort_stats(os.environ.get("SORT", "cumulative")).print_stats(int(os.environ.get("TOP", "28")))
 
 
 if __name__ == "__main__":
