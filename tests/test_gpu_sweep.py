@@ -96,7 +96,12 @@ def test_guard_failure_raises_the_reference_error(monkeypatch):
         class Perturbed(S):
             def __init__(self, *a, **k):
                 super().__init__(*a, **k)
-                self.want_args[-1].data[0] += 1.0   # the baseline output, one element
+                w = self.want_args[-1]               # the baseline output, one element
+                ent = sweep._WANT_DEV.get(id(w))
+                if ent is not None:                  # kept on the device (resident)
+                    ent[1].view(-1)[0] += 1.0
+                else:
+                    w.data[0] += 1.0
 
         return Perturbed, ref
 
