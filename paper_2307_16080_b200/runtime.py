@@ -452,9 +452,10 @@ def conv_tc_supported(cv):
 # raw f32 chunks) leaves two patch stages, so a row band's conversion cannot
 # overlap the previous band's MMAs: at ResNet's N = 256 it is 160 us against
 # 152 for pack + conv (tools/probe_conv_fused.py), while small batches, where
-# the separate pack launch's fixed cost dominates, gain 20-30 % (nb 4: 13 vs
-# 17 us, nb 8: 14 vs 18).  It therefore takes batches up to this size.
-FUSED_CONV_MAX_IMAGES = int(os.environ.get("B200_CONV_FUSED_MAX", "32"))
+# the separate pack launch's fixed cost dominates, gain 15-30 % (nb 4: 13 vs
+# 17 us, nb 8: 14.5 vs 17.3; nb 16: 21.2 vs 19.8, the crossover).  It
+# therefore takes batches up to this size.
+FUSED_CONV_MAX_IMAGES = int(os.environ.get("B200_CONV_FUSED_MAX", "8"))
 
 
 def conv_tc_fused_ok(cv):

@@ -42,9 +42,9 @@ def _cv(**kw):
 
 
 @pytest.mark.parametrize("kw,ok", [
-    ({}, True), (dict(nb=33), False), (dict(f=128), False), (dict(kw=5, kh=5), False),
+    ({}, True), (dict(nb=9), False), (dict(f=128), False), (dict(kw=5, kh=5), False),
     (dict(c=100), False), (dict(hp=57, ho=55), False), (dict(wp=90, wo=88), False),
-    (dict(c=48), True), (dict(f=32, nb=32), True),
+    (dict(c=48), True), (dict(f=32, nb=4), True),
 ])
 def test_fused_conv_routing(kw, ok, monkeypatch):
     from paper_2307_16080_b200 import runtime
