@@ -2,7 +2,7 @@
 (N=256, C=F=64, 56x56, 3x3), timed with CUDA events; prints a hash of the
 output so staging variants (B200_CONV_EXACT_TMA=0/1) can be compared.
 
-    python tools/probe_conv_exact.py [NB]
+    python tools/probe_conv_exact.py [NB [INIT]]    (INIT 0: out += conv, as the bench)
 """
 import ctypes
 import hashlib
@@ -18,6 +18,7 @@ def main():
     from paper_2307_16080_b200 import runtime
 
     nb = int(sys.argv[1]) if len(sys.argv) > 1 else 256
+    init = int(sys.argv[2]) if len(sys.argv) > 2 else 0
     c = f = 64
     ho = wo = 56
     lib = runtime.load_library()
@@ -34,7 +35,7 @@ def main():
     def run():
         runtime.check(lib.b200_conv2d_exact(0, P(x.data_ptr()), xs, P(w.data_ptr()), ws,
                                             P(work.data_ptr()), P(out.data_ptr()), os_, nb, c,
-                                            ho + 2, wo + 2, f, ho, wo, 3, 3, 1,
+                                            ho + 2, wo + 2, f, ho, wo, 3, 3, init,
                                             ctypes.c_double(0.0), s), "conv")
 
     run()
