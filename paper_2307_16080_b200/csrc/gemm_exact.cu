@@ -616,8 +616,8 @@ inline bool full_ok(const Args<float, Strided> &g) {
 }
 
 int launch_full(const Args<float, Strided> &g, void *stream) {
-  static const bool tma = !(getenv("B200_GEMM_EXACT_TMA") &&
-                            getenv("B200_GEMM_EXACT_TMA")[0] == '0');   // dev A/B
+  const char *tv = getenv("B200_GEMM_EXACT_TMA");   // dev A/B: "0" = cp.async kernel
+  const bool tma = !(tv && tv[0] == '0');
   if (tma && g.ntn == 0) {
     const int rc = launch_tma(g, stream);
     if (rc != 1) return rc;   // 1: a tensor map the driver refused -> the cp.async kernel
