@@ -168,7 +168,9 @@ int b200_pack_operand(int32_t kind, const float *src, int64_t s_row, int64_t s_c
  * recognised matmul / Linear contraction when the engine precision is bf16
  * or tf32 (accumulation-order tolerance).  max_ctas <= 0 uses
  * one persistent CTA per SM.  variant: 0 auto, 1 single-CTA 128x256 tiles,
- * 2 CTA-pair 256x256 tiles (tcgen05 cta_group::2).
+ * 2 CTA-pair 256x256 tiles (tcgen05 cta_group::2), 3 128x256 tiles as
+ * cta_group::1 MMAs in 2-CTA clusters sharing the B tile by TMA multicast
+ * (the engine's choice for the reference's (4, 16) tiling).
  */
 int b200_gemm_tc(int32_t kind, const void *A, const void *Bt, float *C, int64_t sCm,
                  int64_t sCn, int64_t M, int64_t N, int64_t K, int32_t init,

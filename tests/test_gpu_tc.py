@@ -70,7 +70,7 @@ def _run(kind, M, N, K, init=0, bias=False, trans_b=False, seed=0, max_ctas=0, v
     return err, bound, Ap, Bp, A, Bsrc
 
 
-@pytest.mark.parametrize("variant", [1, 2], ids=["cta1", "cta2"])
+@pytest.mark.parametrize("variant", [1, 2, 3], ids=["cta1", "cta2", "solo"])
 @pytest.mark.parametrize("kind", [0, 1], ids=["bf16", "tf32"])
 @pytest.mark.parametrize("shape", [(128, 256, 64), (256, 512, 256), (300, 520, 200),
                                    (1024, 1024, 1024), (2048, 1536, 512)])
@@ -83,7 +83,7 @@ def test_gemm_tc_accuracy(kind, shape, variant):
     assert bad == 0, f"{bad} outputs outside the bound; max err {err.max().item()}"
 
 
-@pytest.mark.parametrize("variant", [1, 2], ids=["cta1", "cta2"])
+@pytest.mark.parametrize("variant", [1, 2, 3], ids=["cta1", "cta2", "solo"])
 @pytest.mark.parametrize("kind", [0, 1], ids=["bf16", "tf32"])
 def test_gemm_tc_epilogue_modes(kind, variant):
     err, bound, *_ = _run(kind, 512, 512, 128, init=1, bias=True, trans_b=True,
@@ -101,7 +101,7 @@ def test_pack_rounding_exact():
     assert torch.equal(Bp, Bsrc.t().contiguous())
 
 
-@pytest.mark.parametrize("variant", [1, 2], ids=["cta1", "cta2"])
+@pytest.mark.parametrize("variant", [1, 2, 3], ids=["cta1", "cta2", "solo"])
 def test_gemm_tc_few_ctas_persistent_loop(variant):
     # fewer CTAs than tiles: every CTA loops over several tiles (TMEM ping-pong)
     err, bound, *_ = _run(0, 1024, 1024, 256, max_ctas=4, variant=variant)
