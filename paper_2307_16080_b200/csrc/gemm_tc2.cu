@@ -47,6 +47,10 @@ constexpr int PA = 128 * 128;   // A half: 128 rows x 128 B
 constexpr int PB = 128 * 128;   // B half: 128 rows x 128 B
 constexpr int CBUF = 128 * 128; // C chunk: 128 rows x 32 fp32
 constexpr int NCBUF = 4;
+#ifndef B200_SOLO_STAGES
+#define B200_SOLO_STAGES 4
+#endif
+constexpr int SOLO_STAGES = B200_SOLO_STAGES;
 constexpr int SBUF = 128 * 64;  // bf16 shadow chunk: 128 rows x 32 bf16
 constexpr int BIASB = 256 * 4;  // the tile's bias values
 constexpr int PTHREADS = 256;
@@ -61,10 +65,13 @@ constexpr int PTHREADS = 256;
 template <bool SH, bool SOLO = false>
 struct Lay {
   static constexpr int PBS = SOLO ? 2 * PB : PB;   // B bytes per stage
-  static constexpr int STAGES = SOLO ? 3 : (SH ? 4 : 5);
+  // SOLO: 48 KB stages; four of them leave room for two C chunks only (the
+  // epilogue of a K = 4096 tile is a small share of its 24 us)
+  static constexpr int STAGES = SOLO ? (SH ? 3 : SOLO_STAGES) : (SH ? 4 : 5);
+  static constexpr int NCB = SOLO && STAGES == 4 ? 2 : NCBUF;
   static constexpr int NSBUF = SH ? 2 : 0;
   static constexpr size_t C_OFF = (size_t)STAGES * (PA + PBS);
-  static constexpr size_t S_OFF = C_OFF + NCBUF * CBUF;
+  static constexpr size_t S_OFF = C_OFF + NCB * CBUF;
   static constexpr size_t BIAS_OFF = S_OFF + NSBUF * SBUF;
   static constexpr size_t BAR_OFF = BIAS_OFF + BIASB;
   static constexpr size_t SMEM = 1024 + BAR_OFF + 256;
@@ -139,6 +146,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
                     int64_t N, Sched sch) {
   using L = Lay<SH, SOLO>;
   constexpr int PSTAGES = L::STAGES;
+  constexpr int NCB = L::NCB;
   static_assert(!(SOLO && BMN), "SOLO reads B K-major");
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -151,7 +159,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
   unsigned char *gS = gbase + L::S_OFF;
   float *sBias = reinterpret_cast<float *>(gbase + L::BIAS_OFF);
   uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + L::BAR_OFF);
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * PSTAGES + 4 + NCBUF);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * PSTAGES + 4 + NCB);
   const uint32_t bar0 = smem_u32(bars);
   auto full = [&](int s) { return bar0 + 8u * s; };
   auto empty = [&](int s) { return bar0 + 8u * (PSTAGES + s); };
@@ -180,7 +188,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
       mbar_init(tfull(a), 1);
       mbar_init(tempty(a), SOLO ? 128 : 256);
     }
-    for (int b = 0; b < NCBUF; ++b) mbar_init(cbar(b), 1);
+    for (int b = 0; b < NCB; ++b) mbar_init(cbar(b), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
@@ -321,12 +329,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
     auto issue_load = [&](int64_t g) {
       int32_t col, row;
       if (!chunk_coords(g, col, row)) return;
-      const int b = (int)(g % NCBUF);
+      const int b = (int)(g % NCB);
       mbar_expect_tx(cbar(b), CBUF);
       tma_load_2d(&tma_c, cbar(b), sC + b * CBUF, col, row);
     };
     if (load_c && lead_t)
-      for (int64_t g = 0; g < NCBUF - 1; ++g) issue_load(g);
+      for (int64_t g = 0; g < NCB - 1; ++g) issue_load(g);
     int acc = 0;
     uint32_t aph = 0;
     int64_t g = 0;
@@ -360,13 +368,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
         tmem_ld32(trow + (uint32_t)(c * 32), r);
         const int64_t nb = it.n0 + c * 32;
         if (use_tma_c) {
-          const int b = (int)(g % NCBUF);
+          const int b = (int)(g % NCB);
           if (load_c) {
-            mbar_wait(cbar(b), (uint32_t)((g / NCBUF) & 1));
+            mbar_wait(cbar(b), (uint32_t)((g / NCB) & 1));
           } else {
             // no C load: make sure the store of chunk g-4 (shadow: g-2) has
             // left this buffer
-            if (lead_t) bulk_wait_read<SH ? 1 : NCBUF - 1>();
+            if (lead_t) bulk_wait_read<SH ? 1 : NCB - 1>();
             named_bar_sync(1, 128);
           }
           const int sb = (int)(g & 1);
@@ -381,7 +389,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHREADS, 1)
             bulk_commit();
             if (load_c) {
               bulk_wait_read<1>();  // store of chunk g-1 has read buffer (g+3) % 4
-              issue_load(g + NCBUF - 1);
+              issue_load(g + NCB - 1);
             }
           }
         } else {
