@@ -86,6 +86,7 @@ def collect_accesses(region):
 
 def statically_in_bounds(region, accesses):
     """True iff no access can go out of bounds (exact for affine indices)."""
+    memo = {}   # variable ranges, shared by every index of the region
     for a in accesses:
         buf = region.buffers[a.slot]
         if len(a.idx) != len(buf.shape):
@@ -93,7 +94,7 @@ def statically_in_bounds(region, accesses):
         for i, extent in zip(a.idx, buf.shape):
             if i is None:
                 return False
-            r = aff_range(region, i)
+            r = aff_range(region, i, memo)
             if r is None:
                 return False
             if r is EMPTY or r[1] < r[0]:
@@ -156,7 +157,9 @@ def _mixed_radix_injective(terms, span):
     return True
 
 
-def band_ok(region, accesses, band_ids, written):
+def band_ok(region, accesses, band_ids, written, memo=None):
+    if memo is None:
+        memo = {}
     for slot in written:
         accs = [a for a in accesses if a.slot == slot]
         if any(a.offset is None for a in accs):
@@ -171,7 +174,7 @@ def band_ok(region, accesses, band_ids, written):
                 return False
             rest = Aff(a.offset.c, {k: v for k, v in a.offset.t.items()
                                     if k not in band_ids})
-            r = aff_range(region, rest)
+            r = aff_range(region, rest, memo)
             if r is None:
                 return False
             if r is EMPTY:
@@ -197,6 +200,7 @@ def choose_band(region, links, accesses):
     other dimension is in the band.  Returned in nest order."""
     written = sorted({a.slot for a in accesses if a.write})
     order = [v.id for link in links for v in link.vars]
+    memo = {}   # variable ranges: fixed for the region, shared by every trial band
     band = []
     changed = True
     while changed:
@@ -205,7 +209,7 @@ def choose_band(region, links, accesses):
             if vid in band:
                 continue
             trial = sorted(band + [vid], key=order.index)
-            if band_ok(region, accesses, trial, written):
+            if band_ok(region, accesses, trial, written, memo):
                 band = trial
                 changed = True
     return band
