@@ -454,7 +454,7 @@ constexpr size_t kTmaStageA = (size_t)FBM * FBK * 4;   // 16 KB
 constexpr size_t kTmaStageB = (size_t)FBK * FBN * 4;   // 16 KB
 constexpr size_t kTmaSmem = 1024 + TSTAGES * (kTmaStageA + kTmaStageB) + 64;
 
-template <int AK, int UNR = 2>
+template <int AK, int UNR = 2, bool EAGER = false>
 __global__ void __launch_bounds__(kThreads, 2)
     gemm_exact_tma_kernel(const __grid_constant__ CUtensorMap tma_a,
                           const __grid_constant__ CUtensorMap tma_b, Args<float, Strided> g) {
@@ -515,10 +515,21 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
   }
   const int arow = ty * 4, bcol = tx * 4;
+  // stage / phase counters instead of kt % TSTAGES (a 64-bit division on the
+  // integer pipe the FMULs / FADDs share)
+  int st = 0, pst = TSTAGES - 1;
+  uint32_t ph = 0, pph = 1;
+  const int nk = (int)ktiles;
 #pragma unroll 1
-  for (int64_t kt = 0; kt < ktiles; ++kt) {
-    const int st = (int)(kt % TSTAGES);
-    const uint32_t ph = (uint32_t)((kt / TSTAGES) & 1);
+  for (int kt = 0; kt < nk; ++kt) {
+    // thread 0 refills the stage every warp released one chunk ago (chunk
+    // kt - 1 -> kt + TSTAGES - 1): waiting one chunk late lets warp 0 run a
+    // chunk ahead of the slowest warp instead of stalling on it
+    if (EAGER) {
+    } else if (t == 0 && kt > 0 && kt - 1 + TSTAGES < nk) {
+      mbar_wait(empty(pst), pph);
+      issue(kt - 1 + TSTAGES);
+    }
     mbar_wait(full(st), ph);
     const float *as = As + st * (kTmaStageA / 4);
     const float *bs = Bs + st * (kTmaStageB / 4);
@@ -549,10 +560,13 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty(st));
-    if (t == 0 && kt + TSTAGES < ktiles) {
+    if (EAGER && t == 0 && kt + TSTAGES < nk) {
       mbar_wait(empty(st), ph);   // every warp is done with this stage
       issue(kt + TSTAGES);
     }
+    pst = st;
+    pph = ph;
+    if (++st == TSTAGES) { st = 0; ph ^= 1; }
   }
 
 #pragma unroll
@@ -594,10 +608,14 @@ int launch_tma(const Args<float, Strided> &g, void *stream) {
   if (!make_exact_maps(&ma, &mb, g)) return 1;   // not applicable: the caller falls back
   // (measured at 4096^3: <AK 4, unroll 2> 31.4 TFLOP/s, <2, 2> 31.3, <4, 4>
   // 29.9 — it spills)
-  auto k = gemm_exact_tma_kernel<4, 2>;
+  const char *ev = getenv("B200_GEMM_EXACT_EAGER");   // dev A/B: refill right after release
+  auto k = ev && ev[0] == '1' ? gemm_exact_tma_kernel<4, 2, true> : gemm_exact_tma_kernel<4, 2>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+    cudaFuncSetAttribute(gemm_exact_tma_kernel<4, 2>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+    cudaFuncSetAttribute(gemm_exact_tma_kernel<4, 2, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
     attr = true;
   }
   const int64_t tiles = (g.M / FBM) * (g.N / FBN);
