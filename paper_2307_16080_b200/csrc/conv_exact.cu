@@ -596,9 +596,16 @@ __global__ void __launch_bounds__(kThreads) conv_runs_tma_kernel(
     }
   }
 
+  // stage / phase counters; thread 0 refills the stage every warp released
+  // one chunk earlier (as in gemm_exact_tma_kernel), so warp 0 runs up to a
+  // chunk ahead of the slowest warp instead of stalling on it
+  int st = 0, pst = TSTG - 1;
+  uint32_t ph = 0, pph = 1;
   for (int k = 0; k < chunks; ++k) {
-    const int st = k % TSTG;
-    const uint32_t ph = (uint32_t)((k / TSTG) & 1);
+    if (t == 0 && k > 0 && k - 1 + TSTG < chunks) {
+      mbar_wait(empty(pst), pph);
+      issue(k - 1 + TSTG);
+    }
     mbar_wait(full(st), ph);
     const float *is = in_s + st * (in_stage / 4) + r * W + w0 + PXW * cg;
     const float *ws = w_s + st * W_ELEMS + warp * FX;
@@ -626,10 +633,9 @@ __global__ void __launch_bounds__(kThreads) conv_runs_tma_kernel(
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty(st));
-    if (t == 0 && k + TSTG < chunks) {
-      mbar_wait(empty(st), ph);   // every warp is done with this chunk
-      issue(k + TSTG);
-    }
+    pst = st;
+    pph = ph;
+    if (++st == TSTG) { st = 0; ph ^= 1; }
   }
 
   if (ho >= g.ho) return;
