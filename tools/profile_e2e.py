@@ -23,7 +23,7 @@ def main():
     from staircase.interp import machine
 
     name = sys.argv[1] if len(sys.argv) > 1 else "mm"
-    wl = bench.Workload(name, 1)
+    wl = bench.Workload(name)
     b2.configure(precision=sys.argv[2] if len(sys.argv) > 2 else wl.default_precision)
     host = bench.host_inputs(wl.fn)
     fn = wl.fn
