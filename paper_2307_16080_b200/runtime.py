@@ -862,19 +862,28 @@ class DeviceBackend:
         warnings.warn(msg, PrecisionFallback, stacklevel=3)
 
     def _gemm_streamed_2d(self, g, init, init_value, bias, bias_base, bias_stride,
-                          last_writer, mpanels=4, npanels=2, concurrent=3):
+                          last_writer, mpanels=4, npanels=2, concurrent=3, kslices=4):
         """Exact C (+)= A.B with A, B and C streamed in blocks: B in column
-        panels, A in row panels, C in (row, column) blocks.  The first GEMM
-        block waits only for B's first column panel, A's first rows and C's
-        first block (44 of 192 MiB at 4096^3) instead of all of B; blocks run
-        three at a time on side streams (whole-tile 128 x 128 kernel) while
-        later blocks upload and finished ones write back.  Each output keeps
-        its full k-chain: bit-identical to the unblocked kernel."""
+        panels, A in row panels, C in (row, column) blocks, and each block's
+        contraction in `kslices` K slices, so a block's first slice computes
+        while the rest of its A rows / B columns upload.  The first launch
+        waits for 20 of 192 MiB at 4096^3 (C's first block, a quarter of A's
+        first rows and of B's first columns) instead of 56; blocks run three at a
+        time on side streams (whole-tile 128 x 128 kernel) while later blocks
+        upload and finished ones write back.  A block's slices run in K order
+        on one stream, the first with the nest's init (fill value or C), the
+        rest continuing from C in memory, the bias on the last: every output
+        keeps its full ascending k-chain, bit-identical to the unblocked
+        kernel.  Through run() at 4096^3: 6.55 ms per run with whole-K
+        blocks, 6.39 with 2 slices, 6.20 with 4 (the copies alone take 4.89;
+        tools/gpu/kslice.sh)."""
         s = self.stage
         torch = s.torch
-        env = os.environ.get("B200_STREAM_2D_SHAPE")   # dev A/B: "m,n,concurrent"
+        env = os.environ.get("B200_STREAM_2D_SHAPE")   # dev A/B: "m,n,concurrent[,kslices]"
         if env:
-            mpanels, npanels, concurrent = (int(v) for v in env.split(","))
+            v = [int(x) for x in env.split(",")]
+            mpanels, npanels, concurrent = v[:3]
+            kslices = v[3] if len(v) > 3 else kslices
         cur = torch.cuda.current_stream()
         up, down = _copy_streams(torch)
         up.wait_stream(cur)
@@ -912,29 +921,46 @@ class DeviceBackend:
                                   P(src.data_ptr() + esz * (r0 * N + c0)), N * esz,
                                   (c1 - c0) * esz, r1 - r0, kind, stream), "b200_copy2d")
 
+        # K slices: multiples of 32 (the whole-tile kernel's stage depth)
+        kl = -(-K // kslices)
+        kl = -(-kl // 32) * 32
+        ks = [(k0, min(K, k0 + kl)) for k0 in range(0, K, kl)]
+        a_rows = {}   # A row panel -> K slices uploaded
+
+        def block_a(r0, r1, k0, k1):
+            # rows r0..r1-1, columns k0..k1-1 of A (K-wide rows)
+            check(lib.b200_copy2d(P(tA.data_ptr() + esz * (r0 * K + k0)), K * esz,
+                                  P(hA.data_ptr() + esz * (r0 * K + k0)), K * esz,
+                                  (k1 - k0) * esz, r1 - r0, 1, upp), "b200_copy2d")
+
         for j, (c0, c1) in enumerate(cols):
-            block(tB, hB, c0, c1, 0, K, 1, upp)
-            s._count(h2d=K * (c1 - c0) * esz)
             for r0, r1 in rows:
-                if j == 0:
-                    with torch.cuda.stream(up):
-                        tA[r0:r1].copy_(hA[r0:r1], non_blocking=True)
-                    s._count(h2d=(r1 - r0) * K * esz)
                 if not init:
                     block(tC, hC, c0, c1, r0, r1, 1, upp)
                     s._count(h2d=(r1 - r0) * (c1 - c0) * esz)
-                ev = torch.cuda.Event()
-                ev.record(up)
                 cs = comp[k % len(comp)]
                 k += 1
-                cs.wait_event(ev)
+                for si, (k0, k1) in enumerate(ks):
+                    if j == 0 and a_rows.get(r0, 0) <= si:
+                        block_a(r0, r1, k0, k1)
+                        s._count(h2d=(r1 - r0) * (k1 - k0) * esz)
+                        a_rows[r0] = si + 1
+                    if r0 == rows[0][0]:   # B's column panel j, slice by slice
+                        block(tB, hB, c0, c1, k0, k1, 1, upp)
+                        s._count(h2d=(k1 - k0) * (c1 - c0) * esz)
+                    ev = torch.cuda.Event()
+                    ev.record(up)
+                    cs.wait_event(ev)
+                    first, last = si == 0, si == len(ks) - 1
+                    with torch.cuda.stream(cs):
+                        bp = (bias_t.data_ptr() + esz * (bias_base + c0 * bias_stride)
+                              if bias_t is not None and last else None)
+                        self.call("b200_gemm_f32_exact_tiled", P(tA[r0, k0:].data_ptr()), K, 1,
+                                  P(tB[k0, c0:].data_ptr()), N, 1, P(tC[r0, c0:].data_ptr()), N,
+                                  1, r1 - r0, c1 - c0, k1 - k0, init if first else 0,
+                                  init_value, P(bp) if bp else None, bias_stride, 128, 128,
+                                  ctypes.c_void_p(cs.cuda_stream))
                 with torch.cuda.stream(cs):
-                    bp = (bias_t.data_ptr() + esz * (bias_base + c0 * bias_stride)
-                          if bias_t is not None else None)
-                    self.call("b200_gemm_f32_exact_tiled", P(tA[r0].data_ptr()), K, 1,
-                              P(tB[0, c0:].data_ptr()), N, 1, P(tC[r0, c0:].data_ptr()), N, 1,
-                              r1 - r0, c1 - c0, K, init, init_value, P(bp) if bp else None,
-                              bias_stride, 128, 128, ctypes.c_void_p(cs.cuda_stream))
                     done = torch.cuda.Event()
                     done.record(cs)
                 down.wait_event(done)

@@ -98,13 +98,18 @@ def test_streamed_write_back_before_a_later_writer_matches_the_oracle(monkeypatc
         assert g.data.tobytes() == w.data.tobytes()
 
 
+@pytest.mark.parametrize("shape", [None, "4,2,3,1", "2,2,2,3", "4,2,3,5"])
 @pytest.mark.parametrize("name", ["mm1024", "ls512"])
-def test_block_streamed_exact_gemm_equals_row_panels(name, monkeypatch):
-    """The exact GEMM streamed in (row, column) blocks (B by column panels,
-    runtime._gemm_streamed_2d) equals the row-panel pipeline and the
-    unstreamed run bit for bit, tally included."""
+def test_block_streamed_exact_gemm_equals_row_panels(name, shape, monkeypatch):
+    """The exact GEMM streamed in (row, column) blocks and K slices (B by
+    column panels, runtime._gemm_streamed_2d; shape = row panels, column
+    panels, streams, K slices) equals the row-panel pipeline and the
+    unstreamed run bit for bit, tally included — init, fill and bias only on
+    a block's first / last K slice."""
     from paper_2307_16080_b200 import runtime
 
+    if shape:
+        monkeypatch.setenv("B200_STREAM_2D_SHAPE", shape)
     fn = _fn(name)
     want, t_want, plan_want, _ = _run(fn, "exact", False, monkeypatch)
     monkeypatch.setattr(runtime, "STREAM_2D", False)
