@@ -229,7 +229,10 @@ class Staging:
                 self._count(h2d=h.numel() * h.element_size())
             else:
                 pin_host(buf.data, host)
-                t = host.to("cuda", non_blocking=False)
+                # asynchronous on the current stream: the Buffer's storage
+                # outlives the run and is only written by the final flush
+                # (pageable storage is staged by the driver before it returns)
+                t = host.to("cuda", non_blocking=True)
                 self._count(h2d=host.numel() * host.element_size())
             ent = (buf, t)
             self.dev[id(buf)] = ent
@@ -253,6 +256,10 @@ class Staging:
 
     def flush(self):
         torch = self.torch
+        if self._wb_event is not None:
+            # streamed write-backs first: a buffer written again after its
+            # streamed write-back is copied below, and must land last
+            torch.cuda.current_stream().wait_event(self._wb_event)
         for key in list(self.dirty):
             if key not in self.dev:
                 continue   # marked but never staged: the device never touched it
@@ -280,9 +287,9 @@ class Staging:
         p's kernels wait only for panel p's uploads, and panel p's write-back
         overlaps the uploads and kernels of the panels after it (PCIe is full
         duplex: both directions run at once).  Every buffer ends staged
-        (registered in ``dev``); the current stream then waits for the
-        write-backs, so later kernels cannot overwrite rows still being
-        copied out.  ``panels``: [(r0, r1)] covering the leading dimension
+        (registered in ``dev``); later regions do not wait for the
+        write-backs (a chained layer's write-back of its output overlaps the
+        next layer), flush() does.  ``panels``: [(r0, r1)] covering the leading dimension
         (or ``rows`` equal slices of every buffer's flat storage); they may
         cover a sub-range of the rows (a batch shard's).  ``concurrent`` > 1:
         panel kernels go round-robin to that many side streams, so the small
@@ -292,6 +299,10 @@ class Staging:
         """
         torch = self.torch
         cur = torch.cuda.current_stream()
+        if STREAM_TRACE is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(cur)
+            STREAM_TRACE.append(("stream_rows entry (current stream)", e))
         up, down = _copy_streams(torch)
         up.wait_stream(cur)     # device storage may be recycled from earlier kernels
         comp = _compute_streams(torch, concurrent) if concurrent > 1 else [cur]
@@ -311,33 +322,51 @@ class Staging:
             views.append((host.view(r, -1), t.view(r, -1)))
         hin, (ho, to) = views[:-1], views[-1]
         esz = to.element_size()
+        tr = STREAM_TRACE
+
+        def mark(stream, what):
+            if tr is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(stream)
+                tr.append((what, e))
+
         for p, (r0, r1) in enumerate(panels):
+            mark(up, f"h2d{p}<")
             with torch.cuda.stream(up):
                 for (h, t) in hin + ([(ho, to)] if oup else []):
                     t[r0:r1].copy_(h[r0:r1], non_blocking=True)
                     self._count(h2d=(r1 - r0) * t.shape[1] * esz)
+            mark(up, f"h2d{p}>")
             ev = torch.cuda.Event()
             ev.record(up)
             cs = comp[p % len(comp)]
             cs.wait_event(ev)
+            mark(cs, f"k{p}<")
             with torch.cuda.stream(cs):
                 launch(r0, r1)
+            mark(cs, f"k{p}>")
             self.panels += 1
             if written_back:
                 done = torch.cuda.Event()
                 done.record(cs)
                 down.wait_event(done)
+                mark(down, f"d2h{p}<")
                 with torch.cuda.stream(down):
                     ho[r0:r1].copy_(to[r0:r1], non_blocking=True)
+                mark(down, f"d2h{p}>")
                 self._count(d2h=(r1 - r0) * to.shape[1] * esz)
         assert panels[-1][1] <= rows
         for cs in comp:
             if cs is not cur:
                 cur.wait_stream(cs)
         if written_back:
+            # later kernels do not wait for the write-backs: they only read
+            # these rows, or write rows whose buffer is written back again
+            # after them (a later writer keeps it dirty, or streams its own
+            # write-back behind these on the same stream); flush() orders its
+            # copies after this event
             self._wb_event = torch.cuda.Event()
             self._wb_event.record(down)
-            cur.wait_event(self._wb_event)
 
     def buffer_table(self, buffers):
         """A device array of b200_buffer for the given host Buffers."""
@@ -647,6 +676,7 @@ def pack_b(lib, precision, b_ptr, sB, N, K, stream, call=None, allow_kn=True):
 # Host-copy pipelining (Staging.stream_rows): only when the streamed bytes
 # are worth several panels; each panel ~32 MB of traffic, 2..8 panels.
 STREAM_MIN_BYTES = 48 << 20
+STREAM_TRACE = None   # dev: a list to collect (label, timed event) of stream_rows
 # exact GEMMs stream B by column panels too (B200_STREAM_2D=0: row panels only)
 STREAM_2D = os.environ.get("B200_STREAM_2D", "1") != "0"
 STREAM_PANEL_BYTES = 32 << 20
@@ -969,9 +999,8 @@ class DeviceBackend:
                 s.panels += 1
         for cs in comp:
             cur.wait_stream(cs)
-        s._wb_event = torch.cuda.Event()
+        s._wb_event = torch.cuda.Event()   # see stream_rows: no wait on it here
         s._wb_event.record(down)
-        cur.wait_event(s._wb_event)
         if last_writer:
             s.dirty.discard(id(g.C))
         self._shadow = None
