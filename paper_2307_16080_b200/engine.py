@@ -44,6 +44,16 @@ from .lift import (ALLOC, BINF, BINI, CALL, CAST, CMPF, CMPI, CONST, DEALLOC, IF
                    RETURN_GPU, STORE, Launch, Unsupported, evaluate, lift_region)
 from .runtime import DeviceBackend
 
+
+def _vm_reg_limit():
+    """Register limit of the tier VM programs run on: none when the native
+    tier is on (native.py: registers become scalars), else the interpreter's
+    register file (csrc/vm.cu)."""
+    from . import native
+
+    return None if native.available() else vmcode.MAX_REGS
+
+
 ENGINE_NAME = "b200"
 
 # Execution knobs.  Process-wide defaults come from the environment and
@@ -365,7 +375,8 @@ class _Run:
         # generic tier: the device tape VM (runs in order after queued plans)
         count = st is None
         try:
-            prog = vmcode.encode(r, links, remainder, band, count, checked=not safe)
+            prog = vmcode.encode(r, links, remainder, band, count, checked=not safe,
+                                 max_regs=_vm_reg_limit())
         except Unsupported as exc:
             self.flush_pending()
             raise E.ModeUnsupported(f"b200 engine: {exc}") from None
@@ -382,6 +393,12 @@ class _Run:
         """Execute a VM plan after the queued plans; tally; raise its fault."""
         self.flush_pending({id(r.buffers[slot]) for slot in plan.written})
         prog = plan.item
+        limit = _vm_reg_limit()
+        if limit is not None and prog.n_regs > limit:
+            # a cached plan encoded for the native tier, which is now off
+            raise _errors().ModeUnsupported(
+                f"b200 engine: region needs {prog.n_regs} VM registers (max {limit} without "
+                f"the native tier)")
         dev_tally, fault = self.be.vm(r, prog, checked=plan.checked)
         if fault is not None:
             self.be.flush()

@@ -142,7 +142,8 @@ def record_region(region, accesses, labels, cap=1 << 20):
     links, remainder = analysis.chain_of(region)
     band = [v.id for v in par.vars]
     checked = not analysis.statically_in_bounds(region, accesses)
-    prog = vmcode.encode(region, links, remainder, band, False, checked=checked)
+    prog = vmcode.encode(region, links, remainder, band, False, checked=checked,
+                         max_regs=None)   # the recorder is always native code
     env_regs = [v for v in region.env if region.kind[v] != "buf"]
     src, name, _ = native.vm_source(prog, region.buffers, env_regs, record=True)
     fn = jit.compile_kernel(src, name)

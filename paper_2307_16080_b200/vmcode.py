@@ -234,12 +234,14 @@ class _Enc:
         self.w[patch] = len(self.w)
 
 
-def encode(region, links, remainder, band_ids, count, checked):
+def encode(region, links, remainder, band_ids, count, checked, max_regs=MAX_REGS):
     """Build the VM program for ``region`` with ``band_ids`` bound per thread.
 
     ``links``/``remainder`` come from analysis.chain_of.  Chain levels are
     emitted untagged (their counts are added analytically); the remainder is
-    tagged when ``count`` is set.
+    tagged when ``count`` is set.  ``max_regs``: the register file of the
+    tier that will run it — the interpreter's MAX_REGS, or None for the
+    native tier (native.py: registers become scalars, no limit).
     """
     e = _Enc(region, band_ids, count, checked)
 
@@ -274,8 +276,9 @@ def encode(region, links, remainder, band_ids, count, checked):
     e.head(V_END, None)
     p = e.p
     p.n_regs = e.n_regs
-    if p.n_regs > MAX_REGS:
-        raise Unsupported(f"region needs {p.n_regs} VM registers (max {MAX_REGS})")
+    if max_regs is not None and p.n_regs > max_regs:
+        raise Unsupported(f"region needs {p.n_regs} VM registers (max {max_regs} without "
+                          f"the native tier)")
     # initial register images: environment scalars
     for v, val in region.env.items():
         kind = region.kind[v]

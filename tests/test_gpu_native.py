@@ -57,3 +57,50 @@ def test_kernels_load_from_the_disk_cache(tmp_path, monkeypatch):
     assert t_got == t_want
     for g, w in zip(got, want):
         assert g.data.tobytes() == w.data.tobytes()
+
+
+def _wide_kernel(n_ops=320):
+    """A triangle nest (not a map or contraction: the VM tier) whose body is
+    a chain of ``n_ops`` float operations, each a new SSA value: over the
+    interpreter's 256-register file."""
+    import bench_kernels as bk
+
+    body = ["            v0 = a[j]"]
+    for k in range(1, n_ops):
+        op = "*" if k % 2 else "+"
+        rhs = "constant(1.0009765625, F32)" if k % 2 else f"v{k // 2}"
+        body.append(f"            v{k} = v{k - 1} {op} {rhs}")
+    src = ("@staged\n"
+           "def wide(a: MemRef[(24,), F32], b: MemRef[(24,), F32]):\n"
+           "    for i in range(24):\n"
+           "        for j in range(i):\n" + "\n".join(body) + "\n"
+           f"            b[i] = b[i] + v{n_ops - 1}\n")
+    return bk._capture_from_source(src, "wide", {}, n_ops)
+
+
+def test_regions_over_the_interpreter_register_file_run_natively():
+    """VERDICT r1 'region shapes the reference runs but the engine rejects':
+    a body needing more than the interpreter's 256 VM registers runs on the
+    native tier (registers become scalars), bit-identical to the oracle with
+    an identical tally; with the native tier off it is ModeUnsupported."""
+    import oracle
+    import paper_2307_16080_b200 as b2
+    from paper_2307_16080_b200 import native, vmcode
+    from staircase import errors as E
+
+    fn = _wide_kernel()
+    oracle.build()
+    _, want, t_want, _ = harness.run_engine(oracle, fn, None, "sequential", 3)
+    _, got, t_got, _ = harness.run_engine(b2.engine, fn, None, "sequential", 3)
+    assert t_got == t_want
+    for g, w in zip(got, want):
+        assert g.data.tobytes() == w.data.tobytes()
+    assert any(p[0] == "vm" for p in b2.engine.last_plan), b2.engine.last_plan
+    saved = native.ENABLED
+    native.ENABLED = False
+    try:
+        with pytest.raises(E.ModeUnsupported, match="VM registers"):
+            harness.run_engine(b2.engine, fn, None, "sequential", 3)
+    finally:
+        native.ENABLED = saved
+    assert vmcode.MAX_REGS == 256
