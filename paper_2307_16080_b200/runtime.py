@@ -963,8 +963,17 @@ class DeviceBackend:
                                   P(hA.data_ptr() + esz * (r0 * K + k0)), K * esz,
                                   (k1 - k0) * esz, r1 - r0, 1, upp), "b200_copy2d")
 
+        tr = STREAM_TRACE
+
+        def mark(stream, what):
+            if tr is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(stream)
+                tr.append((what, e))
+
         for j, (c0, c1) in enumerate(cols):
             for r0, r1 in rows:
+                mark(up, f"h2d C{r0 // ms},{j}<")
                 if not init:
                     block(tC, hC, c0, c1, r0, r1, 1, upp)
                     s._count(h2d=(r1 - r0) * (c1 - c0) * esz)
@@ -978,9 +987,11 @@ class DeviceBackend:
                     if r0 == rows[0][0]:   # B's column panel j, slice by slice
                         block(tB, hB, c0, c1, k0, k1, 1, upp)
                         s._count(h2d=(k1 - k0) * (c1 - c0) * esz)
+                    mark(up, f"h2d {r0 // ms},{j},k{si}>")
                     ev = torch.cuda.Event()
                     ev.record(up)
                     cs.wait_event(ev)
+                    mark(cs, f"gemm {r0 // ms},{j},k{si}<")
                     first, last = si == 0, si == len(ks) - 1
                     with torch.cuda.stream(cs):
                         bp = (bias_t.data_ptr() + esz * (bias_base + c0 * bias_stride)
@@ -990,11 +1001,14 @@ class DeviceBackend:
                                   1, r1 - r0, c1 - c0, k1 - k0, init if first else 0,
                                   init_value, P(bp) if bp else None, bias_stride, 128, 128,
                                   ctypes.c_void_p(cs.cuda_stream))
+                mark(cs, f"gemm {r0 // ms},{j}>")
                 with torch.cuda.stream(cs):
                     done = torch.cuda.Event()
                     done.record(cs)
                 down.wait_event(done)
+                mark(down, f"d2h {r0 // ms},{j}<")
                 block(hC, tC, c0, c1, r0, r1, 2, downp)
+                mark(down, f"d2h {r0 // ms},{j}>")
                 s._count(d2h=(r1 - r0) * (c1 - c0) * esz)
                 s.panels += 1
         for cs in comp:

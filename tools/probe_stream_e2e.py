@@ -50,7 +50,10 @@ def main():
         q = 0
         a_done = set()
         b_done = set()
-        if os.environ.get("ORDER") == "zig":
+        if os.environ.get("ORDER") == "row":
+            # each row panel's blocks across every column panel in turn
+            order = [(i, j) for i in range(mp) for j in range(np_)]
+        elif os.environ.get("ORDER") == "zig":
             # pairs of row panels sweep every column panel before the next pair
             order = [(i, j) for i0 in range(0, mp, 2) for j in range(np_)
                      for i in range(i0, min(mp, i0 + 2))]
