@@ -452,23 +452,37 @@ __global__ void __launch_bounds__(kThreads, 2) gemm_exact_full_kernel(Args<float
 constexpr int TSTAGES = 3;
 constexpr size_t kTmaStageA = (size_t)FBM * FBK * 4;   // 16 KB
 constexpr size_t kTmaStageB = (size_t)FBK * FBN * 4;   // 16 KB
-constexpr size_t kTmaSmem = 1024 + TSTAGES * (kTmaStageA + kTmaStageB) + 64;
 
-template <int AK, int UNR = 2, bool EAGER = false>
-__global__ void __launch_bounds__(kThreads, 2)
+// Shared memory of the TMA kernel with an MI x NJ micro-tile per thread (a
+// 16 MI x 16 NJ CTA tile) and STG stages.
+constexpr size_t tma_smem(int mi, int nj, int stg) {
+  return 1024 + (size_t)stg * ((size_t)16 * mi * FBK * 4 + (size_t)FBK * 16 * nj * 4) + 64;
+}
+constexpr size_t kTmaSmem = tma_smem(8, 8, TSTAGES);
+
+// MI x NJ = 8 x 8 is the 128 x 128 CTA tile of untiled and (8, 8)-tiled
+// nests; 4 x 16 (64 x 256) and 16 x 4 (256 x 64) are the tiles runtime.cta_tile
+// gives (4, 16)- and (16, 4)-tiled ones.  Thread (tx, ty) owns rows
+// 64 (i / 4) + 4 ty + i % 4 and columns 64 (j / 4) + 4 tx + j % 4: 16-byte
+// shared loads, conflict-free across a warp.  The 40 KB stages of the
+// non-square tiles come two per CTA (two CTAs per SM).
+template <int AK, int UNR = 2, bool EAGER = false, int MI = 8, int NJ = 8, int STG = TSTAGES>
+__global__ void __launch_bounds__(kThreads, MI * NJ >= 64 ? 2 : 4)
     gemm_exact_tma_kernel(const __grid_constant__ CUtensorMap tma_a,
                           const __grid_constant__ CUtensorMap tma_b, Args<float, Strided> g) {
   using namespace b200tc;
+  constexpr int BM = 16 * MI, BN = 16 * NJ;
+  constexpr size_t SA = (size_t)BM * FBK * 4, SB = (size_t)FBK * BN * 4;
   extern __shared__ __align__(1024) unsigned char smem_dyn[];
   const uint32_t base = (smem_u32(smem_dyn) + 1023u) & ~1023u;
   unsigned char *gbase = smem_dyn + (base - smem_u32(smem_dyn));
   const float *As = reinterpret_cast<const float *>(gbase);
-  const float *Bs = reinterpret_cast<const float *>(gbase + TSTAGES * kTmaStageA);
-  const uint32_t sA0 = base, sB0 = base + (uint32_t)(TSTAGES * kTmaStageA);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + TSTAGES * (kTmaStageA + kTmaStageB));
+  const float *Bs = reinterpret_cast<const float *>(gbase + STG * SA);
+  const uint32_t sA0 = base, sB0 = base + (uint32_t)(STG * SA);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + STG * (SA + SB));
   const uint32_t bar0 = smem_u32(bars);
   auto full = [&](int st) { return bar0 + 8u * st; };
-  auto empty = [&](int st) { return bar0 + 8u * (TSTAGES + st); };
+  auto empty = [&](int st) { return bar0 + 8u * (STG + st); };
 
   // grouped raster: consecutive CTAs walk GROUP_M tile rows across all tile
   // columns, so a wave touches a few A panels and reuses B panels from L2.
@@ -476,25 +490,23 @@ __global__ void __launch_bounds__(kThreads, 2)
   // GROUP_M 8: 433, 16: 364, 32: 530 (A, B and C once: 192); compute-bound
   // either way (31.4 TFLOP/s for all of them)
   constexpr int64_t GROUP_M = 16;
-  const int64_t mt = g.M / FBM, nt = g.N / FBN;
+  const int64_t mt = g.M / BM, nt = g.N / BN;
   const int64_t tl = blockIdx.x;
   const int64_t first_m = (tl / (GROUP_M * nt)) * GROUP_M;
   const int64_t gm = mt - first_m < GROUP_M ? mt - first_m : GROUP_M;
   const int64_t tin = tl % (GROUP_M * nt);
-  const int64_t m0 = (first_m + tin % gm) * FBM, n0 = (tin / gm) * FBN;
+  const int64_t m0 = (first_m + tin % gm) * BM, n0 = (tin / gm) * BN;
   const int t = threadIdx.x, lane = t % 32;
   const int tx = t % 16, ty = t / 16;
   const int64_t ktiles = g.K / FBK;
   auto issue = [&](int64_t kt) {
-    const int st = (int)(kt % TSTAGES);
-    mbar_expect_tx(full(st), (uint32_t)(kTmaStageA + kTmaStageB));
-    tma_load_2d(&tma_a, full(st), sA0 + st * (uint32_t)kTmaStageA, (int32_t)(kt * FBK),
-                (int32_t)m0);
-    tma_load_2d(&tma_b, full(st), sB0 + st * (uint32_t)kTmaStageB, (int32_t)n0,
-                (int32_t)(kt * FBK));
+    const int st = (int)(kt % STG);
+    mbar_expect_tx(full(st), (uint32_t)(SA + SB));
+    tma_load_2d(&tma_a, full(st), sA0 + st * (uint32_t)SA, (int32_t)(kt * FBK), (int32_t)m0);
+    tma_load_2d(&tma_b, full(st), sB0 + st * (uint32_t)SB, (int32_t)n0, (int32_t)(kt * FBK));
   };
   if (t == 0) {
-    for (int st = 0; st < TSTAGES; ++st) {
+    for (int st = 0; st < STG; ++st) {
       mbar_init(full(st), 1);
       mbar_init(empty(st), kThreads / 32);
     }
@@ -502,43 +514,44 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
   __syncthreads();
   if (t == 0)
-    for (int64_t kt = 0; kt < TSTAGES && kt < ktiles; ++kt) issue(kt);
+    for (int64_t kt = 0; kt < STG && kt < ktiles; ++kt) issue(kt);
 
-  float acc[8][8];
+  auto row = [&](int i) { return (i >> 2) * 64 + ty * 4 + (i & 3); };
+  auto col = [&](int j) { return (j >> 2) * 64 + tx * 4 + (j & 3); };
+  float acc[MI][NJ];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int64_t m = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+  for (int i = 0; i < MI; ++i) {
+    const int64_t m = m0 + row(i);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int64_t n = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+    for (int j = 0; j < NJ; ++j) {
+      const int64_t n = n0 + col(j);
       acc[i][j] = g.init ? g.init_value : g.C[g.ad.c(m, n)];
     }
   }
-  const int arow = ty * 4, bcol = tx * 4;
-  // stage / phase counters instead of kt % TSTAGES (a 64-bit division on the
+  // stage / phase counters instead of kt % STG (a 64-bit division on the
   // integer pipe the FMULs / FADDs share)
-  int st = 0, pst = TSTAGES - 1;
+  int st = 0, pst = STG - 1;
   uint32_t ph = 0, pph = 1;
   const int nk = (int)ktiles;
 #pragma unroll 1
   for (int kt = 0; kt < nk; ++kt) {
     // thread 0 refills the stage every warp released one chunk ago (chunk
-    // kt - 1 -> kt + TSTAGES - 1): waiting one chunk late lets warp 0 run a
+    // kt - 1 -> kt + STG - 1): waiting one chunk late lets warp 0 run a
     // chunk ahead of the slowest warp instead of stalling on it
     if (EAGER) {
-    } else if (t == 0 && kt > 0 && kt - 1 + TSTAGES < nk) {
+    } else if (t == 0 && kt > 0 && kt - 1 + STG < nk) {
       mbar_wait(empty(pst), pph);
-      issue(kt - 1 + TSTAGES);
+      issue(kt - 1 + STG);
     }
     mbar_wait(full(st), ph);
-    const float *as = As + st * (kTmaStageA / 4);
-    const float *bs = Bs + st * (kTmaStageB / 4);
+    const float *as = As + st * (SA / 4);
+    const float *bs = Bs + st * (SB / 4);
 #pragma unroll UNR
     for (int kq = 0; kq < FBK; kq += AK) {
-      float a[8][AK];
+      float a[MI][AK];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float *p = as + (i < 4 ? arow + i : 64 + arow + i - 4) * FBK + kq;
+      for (int i = 0; i < MI; ++i) {
+        const float *p = as + row(i) * FBK + kq;
         if constexpr (AK == 4) {
           const float4 v = *reinterpret_cast<const float4 *>(p);
           a[i][0] = v.x, a[i][1] = v.y, a[i][2] = v.z, a[i][3] = v.w;
@@ -549,32 +562,35 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
 #pragma unroll
       for (int u = 0; u < AK; ++u) {
-        const float4 b0 = *reinterpret_cast<const float4 *>(bs + (kq + u) * FBN + bcol);
-        const float4 b1 = *reinterpret_cast<const float4 *>(bs + (kq + u) * FBN + 64 + bcol);
-        const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+        float b[NJ];
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+        for (int q = 0; q < NJ / 4; ++q) {
+          const float4 v = *reinterpret_cast<const float4 *>(bs + (kq + u) * BN + 64 * q + tx * 4);
+          b[4 * q] = v.x, b[4 * q + 1] = v.y, b[4 * q + 2] = v.z, b[4 * q + 3] = v.w;
+        }
 #pragma unroll
-          for (int j = 0; j < 8; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(a[i][u], b[j]));
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(a[i][u], b[j]));
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty(st));
-    if (EAGER && t == 0 && kt + TSTAGES < nk) {
+    if (EAGER && t == 0 && kt + STG < nk) {
       mbar_wait(empty(st), ph);   // every warp is done with this stage
-      issue(kt + TSTAGES);
+      issue(kt + STG);
     }
     pst = st;
     pph = ph;
-    if (++st == TSTAGES) { st = 0; ph ^= 1; }
+    if (++st == STG) { st = 0; ph ^= 1; }
   }
 
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int64_t m = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+  for (int i = 0; i < MI; ++i) {
+    const int64_t m = m0 + row(i);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int64_t n = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+    for (int j = 0; j < NJ; ++j) {
+      const int64_t n = n0 + col(j);
       float v = acc[i][j];
       if (g.bias) v = __fadd_rn(v, __ldg(g.bias + n * g.bias_stride));
       g.C[g.ad.c(m, n)] = v;
@@ -582,17 +598,18 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
 }
 
-bool make_exact_maps(CUtensorMap *ma, CUtensorMap *mb, const Args<float, Strided> &g) {
+bool make_exact_maps(CUtensorMap *ma, CUtensorMap *mb, const Args<float, Strided> &g,
+                     int bm = FBM, int bn = FBN) {
   using namespace b200tc;
   EncodeTiled enc = get_encode();
   if (!enc) return false;
   cuuint32_t estr[2] = {1, 1};
   cuuint64_t da[2] = {(cuuint64_t)g.K, (cuuint64_t)g.M};
   cuuint64_t sa[1] = {(cuuint64_t)(g.ad.sAm * 4)};
-  cuuint32_t ba[2] = {(cuuint32_t)FBK, (cuuint32_t)FBM};
+  cuuint32_t ba[2] = {(cuuint32_t)FBK, (cuuint32_t)bm};
   cuuint64_t db[2] = {(cuuint64_t)g.N, (cuuint64_t)g.K};
   cuuint64_t sb[1] = {(cuuint64_t)(g.ad.sBk * 4)};
-  cuuint32_t bb[2] = {(cuuint32_t)FBN, (cuuint32_t)FBK};
+  cuuint32_t bb[2] = {(cuuint32_t)bn, (cuuint32_t)FBK};
   return enc(ma, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(g.A), da, sa, ba, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
@@ -603,34 +620,41 @@ bool make_exact_maps(CUtensorMap *ma, CUtensorMap *mb, const Args<float, Strided
              CUDA_SUCCESS;
 }
 
-int launch_tma(const Args<float, Strided> &g, void *stream) {
+// One whole-tile TMA launch of the MI x NJ kernel (grid = the tiles), or 1
+// when its tensor maps do not apply (the caller falls back).
+template <int AK, int MI, int NJ, int STG, bool EAGER = false, int UNR = 2>
+int launch_tma_shape(const Args<float, Strided> &g, void *stream) {
+  constexpr int BM = 16 * MI, BN = 16 * NJ;
   CUtensorMap ma, mb;
-  if (!make_exact_maps(&ma, &mb, g)) return 1;   // not applicable: the caller falls back
-  // (measured at 4096^3: <AK 4, unroll 2> 31.4 TFLOP/s, <2, 2> 31.3, <4, 4>
-  // 29.9 — it spills)
-  const char *ev = getenv("B200_GEMM_EXACT_EAGER");   // dev A/B: refill right after release
-  auto k = ev && ev[0] == '1' ? gemm_exact_tma_kernel<4, 2, true> : gemm_exact_tma_kernel<4, 2>;
+  if (!make_exact_maps(&ma, &mb, g, BM, BN)) return 1;
+  auto k = gemm_exact_tma_kernel<AK, UNR, EAGER, MI, NJ, STG>;
+  constexpr size_t smem = tma_smem(MI, NJ, STG);
+  static_assert((MI * NJ >= 64 ? 2 : 4) * smem <= 232448, "CTAs per SM");
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemm_exact_tma_kernel<4, 2>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
-    cudaFuncSetAttribute(gemm_exact_tma_kernel<4, 2, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  const int64_t tiles = (g.M / FBM) * (g.N / FBN);
+  const int64_t tiles = (g.M / BM) * (g.N / BN);
   if (tiles >= (int64_t(1) << 31)) return 1;
-
-  k<<<(unsigned)tiles, kThreads, kTmaSmem, static_cast<cudaStream_t>(stream)>>>(ma, mb, g);
+  k<<<(unsigned)tiles, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(ma, mb, g);
   return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ELAUNCH;
 }
 
-inline bool full_ok(const Args<float, Strided> &g) {
+int launch_tma(const Args<float, Strided> &g, void *stream) {
+  // (measured at 4096^3: <AK 4, unroll 2> 31.4 TFLOP/s, <2, 2> 31.3, <4, 4>
+  // 29.9 — it spills)
+  const char *ev = getenv("B200_GEMM_EXACT_EAGER");   // dev A/B: refill right after release
+  if (ev && ev[0] == '1') return launch_tma_shape<4, 8, 8, TSTAGES, true>(g, stream);
+  return launch_tma_shape<4, 8, 8, TSTAGES>(g, stream);
+}
+
+inline bool full_ok(const Args<float, Strided> &g, int bm = FBM, int bn = FBN) {
   const auto &a = g.ad;
-  return a.sAk == 1 && a.sBn == 1 && g.M % FBM == 0 && g.N % FBN == 0 && g.K % FBK == 0 &&
+  return a.sAk == 1 && a.sBn == 1 && g.M % bm == 0 && g.N % bn == 0 && g.K % FBK == 0 &&
          g.K > 0 && a.sAm % 4 == 0 && a.sBk % 4 == 0 &&
          (reinterpret_cast<uintptr_t>(g.A) & 15) == 0 &&
-         (reinterpret_cast<uintptr_t>(g.B) & 15) == 0 && g.M / FBM <= 65535;
+         (reinterpret_cast<uintptr_t>(g.B) & 15) == 0 && g.M / bm <= 65535;
 }
 
 int launch_full(const Args<float, Strided> &g, void *stream) {
@@ -767,6 +791,23 @@ int launch_cta(const Args<float, Strided> &g, int cta_m, int cta_n, void *stream
   if (cta_m == 128 && cta_n == 128)
     return vec ? launch_tile<float, Strided, 128, 128, 8, 8, true>(g, stream)
                : launch_tile<float, Strided, 128, 128, 8, 8>(g, stream);
+  // whole-tile shapes: the TMA kernel with a 4 x 16 / 16 x 4 micro-tile
+  // (round 2; the general kernel measured 26.8 / 24.9 TFLOP/s at 4096^3)
+  const bool tma = !getenv("B200_GEMM_EXACT_OLD");
+  if (cta_m == 64 && cta_n == 256 && tma && g.ntn == 0 && full_ok(g, 64, 256)) {
+    const int rc = launch_tma_shape<4, 4, 16, 2>(g, stream);   // 31.8 TFLOP/s
+    if (rc != 1) return rc;
+  }
+  if (cta_m == 256 && cta_n == 64 && tma && g.ntn == 0 && full_ok(g, 256, 64)) {
+    // <AK 2, unroll 1>: 29.5 TFLOP/s (<1, 1> 28.8, <2, 2> 27.6: a 16-row
+    // micro-tile's A operands crowd the 128 registers)
+    const int rc = launch_tma_shape<2, 16, 4, 2, false, 1>(g, stream);
+    if (rc != 1) return rc;
+  }
+  if (cta_m == 64 && cta_n == 64 && tma && g.ntn == 0 && full_ok(g, 64, 64)) {
+    const int rc = launch_tma_shape<4, 4, 4, 3>(g, stream);   // four CTAs per SM
+    if (rc != 1) return rc;
+  }
   if (cta_m == 64 && cta_n == 256)
     return vec ? launch_tile<float, Strided, 64, 256, 8, 8, true>(g, stream)
                : launch_tile<float, Strided, 64, 256, 8, 8>(g, stream);
