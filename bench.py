@@ -944,7 +944,8 @@ def run_ours(args, rank, world, local):
     if auto:
         if world == 1:
             for prec, tiles in (("f32x3", None), ("bf16", None), ("tf32", None),
-                                ("bf16", (8, 8)), ("bf16", (4, 16)), ("exact", (8, 8))):
+                                ("bf16", (8, 8)), ("bf16", (4, 16)), ("exact", (8, 8)),
+                                ("exact", (4, 16))):
                 wl = Workload("mm", tiles)
                 r = measure(wl, prec, rank, world, local, with_cpu=False, **k)
                 if r is not None:
