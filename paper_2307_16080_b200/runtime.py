@@ -845,7 +845,7 @@ class DeviceBackend:
                         _gemm_rows(g.B, g.offB, g.sB, g.K, g.N) == (0, g.K) and
                         self._owned(g.B, 0, g.K) and g.N % 256 == 0):
                     return self._gemm_streamed_2d(g, init, init_value, bias, bias_base,
-                                                  bias_stride, last_writer)
+                                                  bias_stride, last_writer, cta=cta)
                 return self._gemm_streamed(g, precision, panels, stream_a, init, init_value,
                                            bias_ptr, bias_stride, shadow_out, shadow_in,
                                            last_writer, cta, crows[0],
@@ -892,7 +892,8 @@ class DeviceBackend:
         warnings.warn(msg, PrecisionFallback, stacklevel=3)
 
     def _gemm_streamed_2d(self, g, init, init_value, bias, bias_base, bias_stride,
-                          last_writer, mpanels=4, npanels=2, concurrent=3, kslices=4):
+                          last_writer, mpanels=4, npanels=2, concurrent=3, kslices=4,
+                          cta=None):
         """Exact C (+)= A.B with A, B and C streamed in blocks: B in column
         panels, A in row panels, C in (row, column) blocks, and each block's
         contraction in `kslices` K slices, so a block's first slice computes
@@ -951,6 +952,11 @@ class DeviceBackend:
                                   P(src.data_ptr() + esz * (r0 * N + c0)), N * esz,
                                   (c1 - c0) * esz, r1 - r0, kind, stream), "b200_copy2d")
 
+        # the nest's CTA tile (its tile sizes, cta_tile) when the blocks are
+        # whole tiles of it, else the 128 x 128 whole-tile kernel
+        tm, tn = cta if cta is not None else (128, 128)
+        if any((r1 - r0) % tm for r0, r1 in rows) or any((c1 - c0) % tn for c0, c1 in cols):
+            tm, tn = 128, 128
         # K slices: multiples of 32 (the whole-tile kernel's stage depth)
         kl = -(-K // kslices)
         kl = -(-kl // 32) * 32
@@ -999,7 +1005,7 @@ class DeviceBackend:
                         self.call("b200_gemm_f32_exact_tiled", P(tA[r0, k0:].data_ptr()), K, 1,
                                   P(tB[k0, c0:].data_ptr()), N, 1, P(tC[r0, c0:].data_ptr()), N,
                                   1, r1 - r0, c1 - c0, k1 - k0, init if first else 0,
-                                  init_value, P(bp) if bp else None, bias_stride, 128, 128,
+                                  init_value, P(bp) if bp else None, bias_stride, tm, tn,
                                   ctypes.c_void_p(cs.cuda_stream))
                 mark(cs, f"gemm {r0 // ms},{j}>")
                 with torch.cuda.stream(cs):

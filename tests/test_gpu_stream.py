@@ -53,14 +53,14 @@ def _gemm_then_vm():
     return bk._capture_from_source(GEMM_THEN_VM, "gemm_then_vm", {}, "stream")
 
 
-def _run(fn, precision, stream, monkeypatch):
+def _run(fn, precision, stream, monkeypatch, pipeline=None):
     import paper_2307_16080_b200 as b2
     from paper_2307_16080_b200 import engine, runtime
 
     monkeypatch.setattr(runtime, "STREAM_MIN_BYTES", 1)
     monkeypatch.setattr(runtime, "STREAM_PANEL_BYTES", 1 << 12)
     with engine.using(precision=precision, stream_io=stream):
-        _, bufs, tally, _ = harness.run_engine(b2.engine, fn, None, "sequential", 5)
+        _, bufs, tally, _ = harness.run_engine(b2.engine, fn, pipeline, "sequential", 5)
     return bufs, tally, list(engine.last_plan), engine.last_staging.panels
 
 
@@ -146,3 +146,18 @@ def test_block_streamed_exact_gemm_equals_row_panels(name, shape, monkeypatch):
     assert plan == plan_want and t_blocks == t_rows == t_want
     for g, r, w in zip(blocks, rows, want):
         assert g.data.tobytes() == r.data.tobytes() == w.data.tobytes()
+
+
+@pytest.mark.parametrize("tiles", ["tile88", "tile416"])
+def test_block_streamed_tiled_gemm_uses_its_cta_tile(tiles, monkeypatch):
+    """A reference-tiled matmul streamed in blocks runs each block on the CTA
+    tile its tile sizes select (plan label), bit-identical to the unstreamed
+    run, tally included."""
+    fn = _fn("mm1024")
+    pipe = {"tile88": harness.TILE88, "tile416": harness.TILE416}[tiles]
+    want, t_want, plan_want, _ = _run(fn, "exact", False, monkeypatch, pipe)
+    got, t_got, plan, panels = _run(fn, "exact", True, monkeypatch, pipe)
+    assert panels >= 2 and plan == plan_want and t_got == t_want, (plan, plan_want)
+    assert ("cta64x256" if tiles == "tile416" else "cta128x128") in str(plan), plan
+    for g, w in zip(got, want):
+        assert g.data.tobytes() == w.data.tobytes()
