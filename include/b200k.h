@@ -100,8 +100,10 @@ int b200_gemm_f32_exact(const float *A, int64_t sAm, int64_t sAk,
  * sizes of a tiled matmul nest (reference passes/tiling.py:56-80, whose
  * outer loop gpu-map sends to blocks: passes/gpumap.py:22-34); supported
  * shapes 128x128, 64x256, 256x64, 64x64, 32x32 (B200_EUNSUPPORTED
- * otherwise).  Results are identical for every tile: each output's k-chain
- * is the same.
+ * otherwise); operands that tile whole (unit-stride, 16-byte aligned rows,
+ * M / N multiples of the tile, K of 32) run the TMA-fed kernel with that
+ * CTA tile, anything else the general tiled kernel.  Results are identical
+ * for every tile: each output's k-chain is the same.
  */
 int b200_gemm_f32_exact_tiled(const float *A, int64_t sAm, int64_t sAk,
                               const float *B, int64_t sBk, int64_t sBn,
