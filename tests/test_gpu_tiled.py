@@ -22,7 +22,9 @@ import tcbound
 pytestmark = pytest.mark.gpu
 
 SAMPLES = 96
-TILES = {"8x8": (harness.TILE88, (8, 8)), "4x16": (harness.TILE416, (4, 16))}
+TILES = {"8x8": (harness.TILE88, (8, 8)), "4x16": (harness.TILE416, (4, 16)),
+         "16x4": (harness._spec("scf-parallel-loop-tiling{sizes=[16, 4]}"), (16, 4)),
+         "2x2": (harness._spec("scf-parallel-loop-tiling{sizes=[2, 2]}"), (2, 2))}
 
 
 def _inputs(fn, seed=0):
@@ -66,8 +68,9 @@ def _plan_cta(plan):
     return notes
 
 
-@pytest.mark.parametrize("precision", ["exact", "bf16", "tf32"])
-@pytest.mark.parametrize("tile", ["8x8", "4x16"])
+@pytest.mark.parametrize("precision,tile", [(p, t) for p in ("exact", "bf16", "tf32")
+                                            for t in ("8x8", "4x16")] +
+                         [("exact", "16x4"), ("exact", "2x2")])
 def test_tiled_matmul_4096(tile, precision):
     import bench_kernels as bk
     from paper_2307_16080_b200.runtime import cta_tile
