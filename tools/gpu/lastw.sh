@@ -1,3 +1,4 @@
+# Measured a last-warp-refill variant (B200_GEMM_EXACT_EAGER=2) that was not kept.
 for i in 1 2 3; do
 echo "deferred:"; python tools/probe_exact.py
 echo "last-warp:"; B200_GEMM_EXACT_EAGER=2 python tools/probe_exact.py

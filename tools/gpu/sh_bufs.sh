@@ -1,3 +1,5 @@
+# A/B against ab/libold.so, a build of the previous source made for the measurement
+# (git stash; build; cp paper_2307_16080_b200/libb200k.so ab/libold.so); ab/ is not tracked.
 timeout 900 python -m pytest tests/test_gpu_tc.py tests/test_gpu_fullsize.py tests/test_gpu_tiled.py -x -q -p no:cacheprovider > gpurun_out/sh_tests.log 2>&1; echo "pytest exit $?"; tail -2 gpurun_out/sh_tests.log
 for i in 1 2; do for lib in new old; do
 if [ $lib = old ]; then export B200_LIB=$PWD/ab/libold.so; else unset B200_LIB; fi
