@@ -119,12 +119,6 @@ def _device():
         return -1
 
 
-def _flit(v):
-    """Bit-exact f32 literal."""
-    bits = struct.unpack("<I", struct.pack("<f", v))[0]
-    return f"__int_as_float(0x{bits:08x})"
-
-
 _FOPS = ["__fadd_rn", "__fsub_rn", "__fmul_rn", "__fdiv_rn"]
 
 
@@ -157,6 +151,12 @@ def map_source(m):
         L.append(f"    const long long o{k} = {' + '.join(terms) if terms else '0'};")
     T = "float4" if vec else "float"
     lanes = ["x", "y", "z", "w"] if vec else [None]
+    # constants come from a __constant__ table, not immediates: ptxas folds
+    # an f32 op of two immediates without round-to-nearest-even at an exact
+    # tie (0x3f065226 - 0x4027a8c1 folded to 0xc0061437; the hardware FADD,
+    # like the reference's per-op rounding, gives 0xc0061438), and the table
+    # is mutable module memory, so nothing folds through it
+    kc = []
     pc = 0
     while pc < len(m.prog):
         w = m.prog[pc]
@@ -171,7 +171,8 @@ def map_source(m):
                 L.append(f"    const float r{dst} = p{a}[o{a}];")
             pc += 1
         elif op == 1:  # CF
-            c = _flit(m.consts[a])
+            kc.append(struct.unpack("<I", struct.pack("<f", m.consts[a]))[0])
+            c = f"__int_as_float(KC[{len(kc) - 1}])"
             L.append(f"    const {T} r{dst} = " +
                      (f"make_float4({c}, {c}, {c}, {c});" if vec else f"{c};"))
             pc += 1
@@ -190,6 +191,9 @@ def map_source(m):
                 L.append(f"    p{a}[o{a}] = r{dst};")
             pc += 1
     L += ["  }", "}"]
+    if kc:
+        L.insert(0, "__constant__ unsigned int KC[%d] = {%s};" % (
+            len(kc), ", ".join(f"0x{v:08x}u" for v in kc)))
     return "\n".join(L) + "\n", name, total
 
 

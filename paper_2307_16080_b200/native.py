@@ -176,6 +176,29 @@ def vm_source(prog, buffers, env_regs, record=False):
             env.append((reg, k))
         else:
             consts.append((reg, val))
+    # Constants that reach a float operation are read from a __constant__
+    # table instead of embedded: ptxas folds an f32 sub.rn of two immediates
+    # without round-to-nearest-even at an exact tie (measured: 0x3f065226 -
+    # 0x4027a8c1 folded to 0xc0061437, the hardware FADD gives 0xc0061438),
+    # and the reference rounds every operation at run time.  The table is
+    # mutable module memory, so nothing can fold through it.  Integer
+    # constants (bounds, strides) stay literal for the optimiser.
+    fregs = set()
+    for _, op, _, _, a in insts:
+        if op == V_BINF:
+            fregs.update(a[1:3])
+    grew = True
+    while grew:   # through register copies
+        grew = False
+        for _, op, _, _, a in insts:
+            if op == V_MOV and a[0] in fregs and a[1] not in fregs:
+                fregs.add(a[1])
+                grew = True
+    table = []
+
+    def kslot(val):
+        table.append(val & 0xFFFFFFFFFFFFFFFF)
+        return len(table) - 1
 
     if record:
         L = [_PRELUDE, _RECORD,
@@ -198,7 +221,10 @@ def vm_source(prog, buffers, env_regs, record=False):
     if record:
         L.append("    i64 seq = 0;")
     for reg, val in consts:
-        L.append(f"    R{reg} = 0x{val & 0xFFFFFFFFFFFFFFFF:x}ULL;")
+        if reg in fregs:
+            L.append(f"    R{reg} = KC[{kslot(val)}];")
+        else:
+            L.append(f"    R{reg} = 0x{val & 0xFFFFFFFFFFFFFFFF:x}ULL;")
     for reg, _ in env:
         L.append(f"    R{reg} = E{reg};")
     if prog.band:
@@ -211,7 +237,10 @@ def vm_source(prog, buffers, env_regs, record=False):
             line.append(f"L{pc}:;")
         if count and tag >= 0:
             line.append(f"c{tag}++;")
-        line.append(_stmt(pc, op, fl, a, buffers, count, record))
+        if op == V_CONST and a[0] in fregs:
+            line.append(f"R{a[0]} = KC[{kslot(_u64(a[1], a[2]))}];")
+        else:
+            line.append(_stmt(pc, op, fl, a, buffers, count, record))
         L.append("    " + " ".join(line))
     L.append("  next_point:;")
     L.append("  }")
@@ -225,6 +254,10 @@ def vm_source(prog, buffers, env_regs, record=False):
                      f"if (lane == 0 && v) atomicAdd(&TALLY[{i}], v); }}")
         L.append("  }")
     L.append("}")
+    if table:
+        at = next(i for i, x in enumerate(L) if x.startswith('extern "C" __global__'))
+        L.insert(at, "__constant__ unsigned long long KC[%d] = {%s};" % (
+            len(table), ", ".join(f"0x{v:x}ULL" for v in table)))
     return "\n".join(L) + "\n", name, env
 
 

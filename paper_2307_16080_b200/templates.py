@@ -317,11 +317,21 @@ def conv_view(region, g, dtypes=("f32",)):
         if lb != 0 and ((offC.t.get(v.id, 0), offA.t.get(v.id, 0)) != (sc[0], sa[0]) or
                         st != 1 or lb != n0):
             return None
-    # classify each variable by its coefficient signature
+    # classify each variable by its coefficient signature.  Size-1
+    # dimensions make signatures coincide (e.g. a 1x1 filter over one output
+    # row: the input's channel and row strides are both W), so a variable
+    # takes the first role, in nest order, whose signature matches and whose
+    # dimension its index range fits (the shape checks below confirm it)
+    def fits(v, extent):
+        lb, st, t = g.stat(v)
+        return lb + st * (t - 1) < extent
+
     roles = {}
+    m_roles = (((sc[0], sa[0]), "n", C.shape[0]), ((sc[2], sa[2]), "ho", C.shape[2]),
+               ((sc[3], sa[3]), "wo", C.shape[3]))
     for v in g.m_vars:
         sig = (offC.t.get(v.id, 0), offA.t.get(v.id, 0))
-        role = {(sc[0], sa[0]): "n", (sc[2], sa[2]): "ho", (sc[3], sa[3]): "wo"}.get(sig)
+        role = next((r for sg, r, ext in m_roles if sg == sig and fits(v, ext)), None)
         if role is None:
             return None
         roles.setdefault(role, []).append(v)
@@ -329,10 +339,13 @@ def conv_view(region, g, dtypes=("f32",)):
         if (offC.t.get(v.id, 0), offB.t.get(v.id, 0)) != (sc[1], sb[0]):
             return None
         roles.setdefault("co", []).append(v)
+    k_roles = (((sa[1], sb[1]), "ci", B.shape[1]), ((sa[2], sb[2]), "ki", B.shape[2]),
+               ((sa[3], sb[3]), "kj", B.shape[3]))
     for v in g.k_vars:
         sig = (offA.t.get(v.id, 0), offB.t.get(v.id, 0))
-        role = {(sa[1], sb[1]): "ci", (sa[2], sb[2]): "ki", (sa[3], sb[3]): "kj"}.get(sig)
-        if role is None or role in roles:
+        role = next((r for sg, r, ext in k_roles
+                     if sg == sig and r not in roles and fits(v, ext)), None)
+        if role is None:
             return None
         if g.stat(v)[1] != 1:
             return None

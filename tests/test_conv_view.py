@@ -92,3 +92,23 @@ def test_batch_shard_conv_is_a_conv(rank, world, rows, monkeypatch):
     cv = templates.conv_view(None, g, ("f32",))
     assert cv is not None
     assert (cv.n0, cv.nb, cv.c, cv.f, cv.ho, cv.wo) == (rows[0], rows[1] - rows[0], 16, 8, 32, 32)
+
+
+@pytest.mark.parametrize("shape", [(16, 1, 5, 1, 1), (70, 1, 34, 1, 1), (16, 3, 1, 1, 1),
+                                   (8, 1, 1, 1, 1), (16, 1, 1, 3, 3)])
+def test_size_one_dimensions_are_still_a_conv(shape, monkeypatch):
+    """One output row and a 1x1 filter make the input's channel and row
+    strides equal (both W), so two roles share a coefficient signature; the
+    variable still takes the role its index range fits (found by the
+    extended random-shape run: these nests had fallen back to the exact
+    contraction at bf16)."""
+    import test_gpu_conv as tg
+    from paper_2307_16080_b200 import templates
+
+    c, ho, wo, kh, kw = shape
+    fn = tg._conv_kernel(3, c, 64, ho, wo, kh, kw)
+    (g,) = _capture_matches(fn, None, monkeypatch)
+    cv = templates.conv_view(None, g, ("f32",))
+    assert cv is not None
+    assert (cv.nb, cv.c, cv.f, cv.ho, cv.wo, cv.kh, cv.kw) == (3, c, 64, ho, wo, kh, kw)
+    assert cv.k_order[0] == "ci"
