@@ -1121,7 +1121,8 @@ namespace {
 int pack_input(const float *src, const int64_t *sstr, void *dst, int64_t nb, int64_t c,
                int64_t h, int64_t w, int64_t cp, cudaStream_t stream, WPack wp, bool *wp_done) {
   *wp_done = false;
-  if (nb <= 0 || h <= 0 || w <= 0 || cp < c || cp % 64 || w > PACK_MAXW) return B200_EINVAL;
+  if (nb == 0) return B200_OK;   // an empty batch shard: nothing to convert
+  if (nb < 0 || h <= 0 || w <= 0 || cp < c || cp % 64 || w > PACK_MAXW) return B200_EINVAL;
   // rows contiguous (h stride = W * w stride): one line per image plane
   const bool plane = sstr[2] == w * sstr[3];
   const int lines_per_img = plane ? 1 : (int)h;
@@ -1262,8 +1263,9 @@ extern "C" int b200_conv2d_tc(const void *in_nhwc, const void *wt, float *out,
                               int64_t wp, int64_t f, int64_t ho, int64_t wo, int64_t kh,
                               int64_t kw, int32_t init, float init_value, void *stream) {
   if (cp % 64 || ho <= 0 || wo <= 0 || kh <= 0 || kw <= 0 || ho + kh - 1 > hp ||
-      wo + kw - 1 > wp)
+      wo + kw - 1 > wp || nb < 0)
     return B200_EINVAL;
+  if (nb == 0) return B200_OK;   // an empty batch shard (shard.py)
   ConvGeo g;
   if (!conv_geo(g, out_strides, nb, cp, hp, wp, f, ho, wo, kh, kw, init, init_value))
     return B200_EUNSUPPORTED;
@@ -1286,8 +1288,9 @@ extern "C" int b200_conv2d_tc_fused(const float *in, const int64_t *in_strides, 
                                     int64_t wo, int64_t kh, int64_t kw, int32_t init,
                                     float init_value, void *stream) {
   if (c <= 0 || ho <= 0 || wo <= 0 || kh <= 0 || kw <= 0 || ho + kh - 1 > hp ||
-      wo + kw - 1 > wp)
+      wo + kw - 1 > wp || nb < 0)
     return B200_EINVAL;
+  if (nb == 0) return B200_OK;   // an empty batch shard (shard.py)
   const int64_t cp = (c + 63) / 64 * 64;
   ConvGeo g;
   if (!conv_geo(g, out_strides, nb, cp, hp, wp, f, ho, wo, kh, kw, init, init_value))

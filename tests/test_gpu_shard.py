@@ -117,3 +117,16 @@ def test_conv_shard_exact_matches_reference_chain():
     assert np.array_equal(O[n, f, h, w].view(np.int32), c.view(np.int32))
     # rows outside the shard were not touched
     assert np.array_equal(O[:8], O0[:8]) and np.array_equal(O[12:], O0[12:])
+
+
+@pytest.mark.parametrize("nb,world", [(13, 4), (7, 3), (3, 5)])
+@pytest.mark.parametrize("precision", ["exact", "bf16"])
+def test_conv_uneven_and_empty_shards(nb, world, precision):
+    """Batches the world does not divide, and more ranks than images (the
+    reference's chunking [total w / W, total (w + 1) / W) leaves some ranks
+    no rows): the union is still the unsharded run, bit for bit."""
+    import bench_kernels as bk
+
+    fn = bk.make_conv(nb)
+    got, want = _union(fn, world, precision)
+    assert got[2].tobytes() == want[2].tobytes()

@@ -46,7 +46,7 @@ def _sharded_union(fn, world, seed=3):
     return out, rows_seen
 
 
-@pytest.mark.parametrize("world", [1, 2, 3, 4])
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 7])   # 7 > 4 images: empty shards
 @pytest.mark.parametrize("fn", [corpus.conv_mid, corpus.matmul_t, corpus.conv_f32],
                          ids=["conv_mid", "matmul_t", "conv_f32"])
 def test_union_of_shards_is_the_unsharded_run(fn, world, oracle_engine):
