@@ -18,6 +18,7 @@ pytestmark = pytest.mark.gpu
 
 # B200_RANDOM_SCALE=k runs k times as many seeds (extended stress runs)
 SCALE = max(1, int(os.environ.get("B200_RANDOM_SCALE", "1")))
+OFFSET = int(os.environ.get("B200_RANDOM_OFFSET", "0"))   # a fresh range of seeds
 
 MM = '''
 @staged
@@ -63,7 +64,7 @@ def _both(fn, seed):
     return got, t_got, want, t_want, plan
 
 
-@pytest.mark.parametrize("seed", range(30 * SCALE))
+@pytest.mark.parametrize("seed", range(OFFSET, OFFSET + 30 * SCALE))
 def test_random_matmul_exact(seed):
     shp = _mm_shape(seed)
     fn = bk._capture_from_source(MM.format(**shp), "mm_r", {}, "_".join(map(str, shp.values())))
@@ -73,7 +74,7 @@ def test_random_matmul_exact(seed):
         assert g.data.tobytes() == w.data.tobytes(), (shp, plan)
 
 
-@pytest.mark.parametrize("seed", range(30 * SCALE))
+@pytest.mark.parametrize("seed", range(OFFSET, OFFSET + 30 * SCALE))
 def test_random_conv_exact(seed):
     shp = _conv_shape(seed)
     fn = bk._capture_from_source(CONV.format(**shp), "conv_r", {},
@@ -84,7 +85,7 @@ def test_random_conv_exact(seed):
         assert g.data.tobytes() == w.data.tobytes(), (shp, plan)
 
 
-@pytest.mark.parametrize("seed", range(16 * SCALE))
+@pytest.mark.parametrize("seed", range(OFFSET, OFFSET + 16 * SCALE))
 def test_random_matmul_bf16_within_bound(seed):
     """bf16 precision on bf16-representable inputs: every output within
     2 K 2^-24 sum|a b| + 4 2^-24 |want| of the float64 result."""
@@ -117,7 +118,7 @@ def test_random_matmul_bf16_within_bound(seed):
     assert (np.abs(got - want) <= bound).all(), (shp, b2.engine.last_plan)
 
 
-@pytest.mark.parametrize("seed", range(20 * SCALE))
+@pytest.mark.parametrize("seed", range(OFFSET, OFFSET + 20 * SCALE))
 def test_random_tile_unroll_pipelines_exact(seed):
     """The sweep's knobs on random nests: random tile sizes (tiling applies
     only where they divide the trip counts) and unroll factors on random
@@ -167,7 +168,7 @@ def ew_r(a: MemRef[({rows}, {cols}), F32], b: MemRef[({rows}, {cols}), F32],
 
 
 @pytest.mark.parametrize("jit_on", [True, False], ids=["nvrtc", "map_f32"])
-@pytest.mark.parametrize("seed", range(20 * SCALE))
+@pytest.mark.parametrize("seed", range(OFFSET, OFFSET + 20 * SCALE))
 def test_random_elementwise_exact(seed, jit_on, monkeypatch):
     """Random f32 expression trees (+ - * / and constants, depth <= 3) over
     random shapes, as pointwise NVRTC kernels: bit-identical to the oracle
@@ -227,7 +228,7 @@ def irr_r(a: MemRef[({n}, {n}), F32], b: MemRef[({n}, {n}), F32]):{body}
 
 
 @pytest.mark.parametrize("native", [True, False], ids=["native", "interpreter"])
-@pytest.mark.parametrize("seed", range(15 * SCALE))
+@pytest.mark.parametrize("seed", range(OFFSET, OFFSET + 15 * SCALE))
 def test_random_irregular_nests_exact(seed, native, monkeypatch):
     """Nests no template matches (triangular bounds, loop-carried updates,
     data-dependent branches) run as NVRTC-specialised VM programs — or, with
@@ -275,7 +276,7 @@ def test_exact_gemm_balanced_last_round(shape, monkeypatch):
     assert np.array_equal(got.view(np.int32), want.view(np.int32))
 
 
-@pytest.mark.parametrize("seed", range(12 * SCALE))
+@pytest.mark.parametrize("seed", range(OFFSET, OFFSET + 12 * SCALE))
 def test_random_conv_bf16_within_bound(seed):
     """The tensor-core conv (F in {32, 64, 128}; 1x1, 3x3, 5x5; random
     batch, channels and sizes) on bf16-representable inputs: every output
